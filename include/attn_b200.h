@@ -1,0 +1,112 @@
+/*
+ * attn_b200 — C ABI of the B200 (sm_100a) attention-template kernels.
+ *
+ * This is the drop-in boundary for the hot path of the attnforge reference (AttentionEngine,
+ * arXiv 2502.15349).  Each entry point replaces one reference executor; the host lowering
+ * (paper_2502_15349_b200/plan.py) turns an AttentionSpec into the descriptor structs below.
+ * Plain pointers and sizes only: device pointers are CUDA global-memory addresses, `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  All calls are stream-ordered and asynchronous;
+ * outputs are caller-allocated.  Nothing here owns memory between calls.
+ *
+ * Status codes mirror attnforge/errors.py kinds (errors.py:30-82): AF_ERR_INPUT* map to
+ * InputError subclasses (CLI exit 2), AF_ERR_UNSUPPORTED / AF_ERR_NAN to SemanticError (exit 1).
+ */
+#ifndef ATTN_B200_H_
+#define ATTN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py kinds) ---- */
+enum {
+  AF_OK = 0,
+  AF_ERR_INPUT = 1,          /* InputError            kind "input"          */
+  AF_ERR_SHAPE = 2,          /* ShapeError            kind "shape-mismatch" */
+  AF_ERR_UNSUPPORTED = 3,    /* UnsupportedError      kind "unsupported"    */
+  AF_ERR_NAN = 4,            /* NanError              kind "nan-in-output"  */
+  AF_ERR_CUDA = 5,           /* launch / driver failure (no reference analogue) */
+};
+
+/* ---- parallel template (attention.py:389-449, engine.py:423-505) ---- */
+enum { AF_FAMILY_SOFTMAX = 0, AF_FAMILY_ELEMENTWISE = 1 };
+enum { AF_ACT_IDENTITY = 0, AF_ACT_SIGMOID = 1, AF_ACT_RELU = 2 };
+enum { AF_DTYPE_BF16 = 0, AF_DTYPE_F32 = 1 };
+
+typedef struct af_parallel_desc {
+  int32_t batch, heads_q, heads_kv, seq_q, seq_k, d_qk, d_v;
+  int32_t dtype;             /* AF_DTYPE_BF16 (tcgen05 path) or AF_DTYPE_F32 (exact FFMA path) */
+  /* element strides [b, h, s, d] of q, k, v, o (d stride must be 1) */
+  int64_t q_stride[4], k_stride[4], v_stride[4], o_stride[4];
+  int32_t family;            /* AF_FAMILY_*: classified online_func / score_mod hook family */
+  int32_t act;               /* AF_ACT_*: elementwise score activation (elementwise family) */
+  float scale;               /* q_mod scale folded into scores, e.g. 1/sqrt(d_qk)          */
+  int32_t causal;            /* band mask from mask_mod: keep j <= i + diag_offset         */
+  int32_t diag_offset;
+  int32_t window;            /* >0: also keep only i + diag_offset - j < window            */
+  const float* slope;        /* elementwise family: z -= slope[h] * (i - j); may be NULL     */
+  float bias;                /* elementwise family: z += bias                               */
+} af_parallel_desc;
+
+/* O = template_forward(q, k, v); lse[b,h,i] = log-sum-exp of row i (softmax family, may be NULL).
+ * Replaces engine.run_tiled_parallel (engine.py:423) / lowering.ExecutablePlan.run (lowering.py:857). */
+int af_parallel_fwd(const af_parallel_desc* desc, const void* q, const void* k, const void* v,
+                    void* o, float* lse, void* stream);
+
+/* Bytes of device scratch af_parallel_bwd needs (fp32 dQ accumulator + row statistics). */
+size_t af_parallel_bwd_workspace(const af_parallel_desc* desc);
+
+/* VJP of af_parallel_fwd for cotangent dO (bf16).  dq/dk/dv use the q/k/v strides of desc; dk/dv
+ * are summed over the query heads of each GQA group.  Replaces engine.autodiff_grads
+ * (engine.py:630) over attention.build_parallel (attention.py:389) with seed dO. */
+int af_parallel_bwd(const af_parallel_desc* desc, const void* q, const void* k, const void* v,
+                    const void* o, const float* lse, const void* dout, void* dq, void* dk,
+                    void* dv, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- linear / recurrent template (attention.py:455-511, engine.py:525-616) ---- */
+typedef struct af_linear_desc {
+  int32_t batch, heads, seq, d_k, d_v;
+  int32_t chunk;             /* chunk length of the intra/inter decomposition (64) */
+  float q_scale;             /* q_mod scale (e.g. 1/sqrt(d_k)); 1 when absent       */
+  /* element strides [b, h, s, d] of q, k, v, o */
+  int64_t q_stride[4], k_stride[4], v_stride[4], o_stride[4];
+} af_linear_desc;
+
+/* o_t = q_t h_t,  h_t = a_t h_{t-1} + k_t^T v_t  with log a_t = log_decay[b,h,t] (fp32 [B,H,S]).
+ * k is the already-modified key (k_mod applied).  final_state (fp32 [B,H,Dk,Dv]) may be NULL.
+ * Replaces engine.run_chunk_recurrent (engine.py:554). */
+int af_linear_fwd(const af_linear_desc* desc, const void* q, const void* k, const void* v,
+                  const float* log_decay, void* o, float* final_state, void* stream);
+
+size_t af_linear_bwd_workspace(const af_linear_desc* desc);
+
+/* VJP of af_linear_fwd for cotangent dO: dq, dk, dv (bf16) and d log_decay (fp32 [B,H,S]). */
+int af_linear_bwd(const af_linear_desc* desc, const void* q, const void* k, const void* v,
+                  const float* log_decay, const void* dout, void* dq, void* dk, void* dv,
+                  float* dlog_decay, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- MLA decode (softmax over a shared latent cache; V = first d_v columns of K) ---- */
+typedef struct af_mla_desc {
+  int32_t batch, heads, seq_k, d_qk, d_v;
+  float scale;
+} af_mla_desc;
+
+size_t af_mla_decode_workspace(const af_mla_desc* desc);
+
+/* q [B, H, d_qk] bf16, kv [B, seq_k, d_qk] bf16 -> o [B, H, d_v] bf16, lse [B, H] fp32.
+ * Replaces engine.run_tiled_parallel with seq_q = 1 (test_engine.py:224-230). */
+int af_mla_decode(const af_mla_desc* desc, const void* q, const void* kv, void* o, float* lse,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- diagnostics ---- */
+const char* af_status_string(int status);
+const char* af_last_error(void);      /* thread-local message of the last failing call */
+int af_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ATTN_B200_H_ */

@@ -1,0 +1,90 @@
+"""Ahead-of-time build of the sm_100a C-ABI library (``_lib/libattn_b200.so``).
+
+Every ``csrc/*.cu`` translation unit is compiled with
+``nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo`` in parallel and linked into one shared
+object in-tree, so the built artefact travels with the repository snapshot to the GPU box.
+"""
+
+from __future__ import annotations
+
+import concurrent.futures as cf
+import hashlib
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+OUT = PKG / "_lib"
+LIB = OUT / "libattn_b200.so"
+INCLUDE = PKG.parent / "include"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+         "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found; the sm_100a library cannot be built")
+
+
+def _sources() -> list[Path]:
+    return sorted(CSRC.glob("*.cu"))
+
+
+def _headers() -> list[Path]:
+    return sorted(list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list(INCLUDE.glob("*.h")))
+
+
+def _digest(src: Path) -> str:
+    h = hashlib.sha256()
+    for p in [src, *_headers()]:
+        h.update(p.read_bytes())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+def _compile(src: Path) -> Path:
+    obj = OUT / "obj" / f"{src.stem}.{_digest(src)}.o"
+    if obj.exists():
+        return obj
+    obj.parent.mkdir(parents=True, exist_ok=True)
+    for stale in obj.parent.glob(f"{src.stem}.*.o"):
+        stale.unlink()
+    cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj) + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stderr}")
+    os.replace(str(obj) + ".tmp", obj)
+    return obj
+
+
+def build_library(verbose: bool = False, jobs: int | None = None) -> Path:
+    """Compile (incrementally) and link the C-ABI library; returns its path."""
+    OUT.mkdir(parents=True, exist_ok=True)
+    srcs = _sources()
+    jobs = jobs or min(len(srcs), os.cpu_count() or 4)
+    with cf.ThreadPoolExecutor(jobs) as ex:
+        objs = list(ex.map(_compile, srcs))
+    stamp = hashlib.sha256("".join(sorted(o.name for o in objs)).encode()).hexdigest()[:16]
+    stamp_file = OUT / "libattn_b200.stamp"
+    if LIB.exists() and stamp_file.exists() and stamp_file.read_text() == stamp:
+        return LIB
+    cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB) + ".tmp", *map(str, objs), "-lcudart_static",
+           "-ldl", "-lrt", "-lpthread"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    os.replace(str(LIB) + ".tmp", LIB)
+    stamp_file.write_text(stamp)
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+if __name__ == "__main__":
+    build_library(verbose=True)

@@ -1,0 +1,399 @@
+// K1 — parallel-template forward on sm_100a.
+//
+// Replaces the arithmetic of attnforge `engine.run_tiled_parallel` (engine.py:423-505): per query
+// block the online row-normalisation protocol carries row scales across key blocks and rescales
+// the accumulator (engine.py:481-489); the epilogue divides by the row sum (attention.py:569).
+//
+// Shape of the kernel (one CTA per SM, 10 warps):
+//   warps 0-3  : "row" warpgroup for query tile 0 (rows q0 .. q0+127)
+//   warps 4-7  : "row" warpgroup for query tile 1 (rows q0+128 .. q0+255)
+//   warp  8    : TMA producer (Q once, then a K/V ring of kStages)
+//   warp  9    : TMEM allocator + single-thread tcgen05.mma issuer
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+DV) O1 [256+DV, 256+2DV).
+// S_t = Q_t K^T lands in TMEM (fp32), the row warpgroup pulls one score row per thread
+// (tcgen05.ld 32x32b), applies the hook epilogue in registers, writes P back into the S columns as
+// packed bf16, and the MMA warp consumes P straight from TMEM (A-from-TMEM) for O_t += P V.
+// The two query tiles ping-pong so the tensor pipe runs tile 1's MMAs while tile 0's row math runs.
+#pragma once
+#include <cuda.h>
+#include "params.h"
+#include "sm100.cuh"
+
+namespace af {
+
+constexpr int kBlockM = 128;  // query rows per tile (TMEM lanes)
+constexpr int kBlockN = 128;  // keys per block
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+template <int D, int DV, int kStages>
+struct FwdSmem {
+  static constexpr int kQBytes = kBlockM * D * 2;
+  static constexpr int kKBytes = kBlockN * D * 2;
+  static constexpr int kVBytes = kBlockN * DV * 2;
+  static constexpr int kQOff = 0;
+  static constexpr int kKOff = kQOff + 2 * kQBytes;
+  static constexpr int kVOff = kKOff + kStages * kKBytes;
+  static constexpr int kBarOff = kVOff + kStages * kVBytes;
+  // barriers: q_full, k_full[S], k_empty[S], v_full[S], v_empty[S], s_full[2], p_full[2], o_done[2]
+  static constexpr int kNumBars = 1 + 4 * kStages + 6;
+  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
+  static constexpr int kTotal = kTmemSlotOff + 16 + 1024;  // + alignment slack
+};
+
+struct TileBand {
+  int jb_lo, jb_hi;  // key-block range [jb_lo, jb_hi)
+};
+
+// Range of key blocks any row in [r0, r1) can see under the band mask.
+__host__ __device__ inline TileBand key_band(const MaskParams& m, int r0, int r1, int seq_k) {
+  int hi = seq_k;
+  if (m.causal) hi = min(hi, r1 - 1 + m.diag_offset + 1);
+  int lo = 0;
+  if (m.window > 0) lo = max(0, r0 + m.diag_offset - m.window + 1);
+  TileBand b;
+  if (hi <= lo) {
+    b.jb_lo = 0;
+    b.jb_hi = 0;
+  } else {
+    b.jb_lo = lo / kBlockN;
+    b.jb_hi = (hi + kBlockN - 1) / kBlockN;
+  }
+  return b;
+}
+
+// True when every (i, j) of the block is kept by the band mask and in bounds.
+AF_DEVICE bool block_fully_kept(const MaskParams& m, int r0, int c0, int seq_k) {
+  if (c0 + kBlockN > seq_k) return false;
+  if (m.causal && c0 + kBlockN - 1 > r0 + m.diag_offset) return false;
+  if (m.window > 0 && (r0 + kBlockM - 1) + m.diag_offset - c0 >= m.window) return false;
+  return true;
+}
+AF_DEVICE bool kept(const MaskParams& m, int i, int j, int seq_k) {
+  bool k = j < seq_k;
+  if (m.causal) k = k && (j <= i + m.diag_offset);
+  if (m.window > 0) k = k && (i + m.diag_offset - j < m.window);
+  return k;
+}
+
+template <int kAct>
+AF_DEVICE float apply_act(float z) {
+  if constexpr (kAct == kActSigmoid) {
+    return __frcp_rn(1.0f + ex2(-z * kLog2e));
+  } else if constexpr (kAct == kActRelu) {
+    return fmaxf(z, 0.0f);
+  } else {
+    return z;
+  }
+}
+
+template <int D, int DV, int kFamily, int kAct, int kStages>
+__global__ void __launch_bounds__(320, 1)
+    parallel_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
+                        const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const ParallelFwdParams p) {
+  using L = FwdSmem<D, DV, kStages>;
+  static_assert(D % 64 == 0 && DV % 64 == 0 && D <= 256 && DV <= 128, "tile dims");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sQ = smem + L::kQOff;
+  uint8_t* sK = smem + L::kKOff;
+  uint8_t* sV = smem + L::kVOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + kStages;
+  uint64_t* v_full = k_empty + kStages;
+  uint64_t* v_empty = v_full + kStages;
+  uint64_t* s_full = v_empty + kStages;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
+
+  const int warp = static_cast<int>(warp_id());
+  const int q_blocks = (p.seq_q + 2 * kBlockM - 1) / (2 * kBlockM);
+  // Heaviest (latest) query blocks first: causal work grows with the block index.
+  const int qb = p.mask.causal ? (q_blocks - 1 - static_cast<int>(blockIdx.x))
+                               : static_cast<int>(blockIdx.x);
+  const int bh = blockIdx.y;
+  const int b = bh / p.heads_q;
+  const int h = bh % p.heads_q;
+  const int hk = h / (p.heads_q / p.heads_kv);
+  const int q0 = qb * 2 * kBlockM;
+  const int q_end = min(p.seq_q, q0 + 2 * kBlockM);
+  const TileBand band = key_band(p.mask, q0, q_end, p.seq_k);
+  const int nk = band.jb_hi - band.jb_lo;
+
+  if (warp == 8 && lane_id() == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 4);  // one arrival per row warp
+      mbar_init(&o_done[t], 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ───────────── TMA producer ─────────────
+    if (elect_one() && nk > 0) {
+      mbar_expect_tx(q_full, 2 * L::kQBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_4d(sQ + t * L::kQBytes + c * (kBlockM * 128), &tm_q, q_full, c * 64,
+                      q0 + t * kBlockM, h, b);
+      for (int n = 0; n < nk; ++n) {
+        const int s = n % kStages;
+        const uint32_t ph = (n / kStages) & 1;
+        const int kv0 = (band.jb_lo + n) * kBlockN;
+        mbar_wait(&k_empty[s], ph ^ 1);
+        mbar_expect_tx(&k_full[s], L::kKBytes);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_4d_hint(sK + s * L::kKBytes + c * (kBlockN * 128), &tm_k, &k_full[s], c * 64,
+                           kv0, hk, b, kEvictLast);
+        mbar_wait(&v_empty[s], ph ^ 1);
+        mbar_expect_tx(&v_full[s], L::kVBytes);
+        for (int c = 0; c < DV / 64; ++c)
+          tma_load_4d_hint(sV + s * L::kVBytes + c * (kBlockN * 128), &tm_v, &v_full[s], c * 64,
+                           kv0, hk, b, kEvictLast);
+      }
+    }
+  } else if (warp == 9) {
+    // ───────────── MMA issuer ─────────────
+    if (elect_one() && nk > 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(kBlockM, kBlockN, false, false);
+      constexpr uint32_t idesc_o = make_idesc_bf16(kBlockM, DV, false, true);
+      const uint32_t sq_addr = smem_u32(sQ);
+      const uint32_t sk_addr = smem_u32(sK);
+      const uint32_t sv_addr = smem_u32(sV);
+      auto issue_s = [&](int t, int n) {
+        const int s = n % kStages;
+        const uint32_t d_tmem = tmem + t * kBlockN;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk / 4) * (kBlockM * 128) + (kk % 4) * 32;
+          const uint64_t a = make_sdesc(sq_addr + t * L::kQBytes + off, 0, 1024);
+          const uint64_t bdesc = make_sdesc(sk_addr + s * L::kKBytes + (kk / 4) * (kBlockN * 128) +
+                                                (kk % 4) * 32,
+                                            0, 1024);
+          mma_ss(d_tmem, a, bdesc, idesc_s, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int n) {
+        const int s = n % kStages;
+        const uint32_t d_tmem = tmem + 2 * kBlockN + t * DV;
+        const uint32_t p_tmem = tmem + t * kBlockN;
+#pragma unroll
+        for (int kk = 0; kk < kBlockN / 16; ++kk) {
+          const uint64_t bdesc =
+              make_sdesc(sv_addr + s * L::kVBytes + kk * 16 * 128, kBlockN * 128, 1024);
+          mma_ts(d_tmem, p_tmem + kk * 8, bdesc, idesc_o, (n > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&o_done[t]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      mma_commit(&k_empty[0]);
+      for (int n = 0; n < nk; ++n) {
+        const int s = n % kStages;
+        const uint32_t ph = (n / kStages) & 1;
+        const bool more = n + 1 < nk;
+        const int s1 = (n + 1) % kStages;
+        const uint32_t ph1 = ((n + 1) / kStages) & 1;
+        mbar_wait(&v_full[s], ph);
+        mbar_wait(&p_full[0], n & 1);
+        tc_fence_after();
+        issue_pv(0, n);
+        if (more) {
+          mbar_wait(&k_full[s1], ph1);
+          tc_fence_after();
+          issue_s(0, n + 1);
+        }
+        mbar_wait(&p_full[1], n & 1);
+        tc_fence_after();
+        issue_pv(1, n);
+        mma_commit(&v_empty[s]);
+        if (more) {
+          issue_s(1, n + 1);
+          mma_commit(&k_empty[s1]);
+        }
+      }
+    }
+  } else {
+    // ───────────── row warpgroups (hook epilogue) ─────────────
+    const int t = warp / 4;                  // query tile
+    const int wq = warp % 4;                 // TMEM lane quarter
+    const int row = wq * 32 + static_cast<int>(lane_id());
+    const int i = q0 + t * kBlockM + row;    // absolute query index
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t s_tmem = tmem + lane_base + t * kBlockN;
+    const uint32_t o_tmem = tmem + lane_base + 2 * kBlockN + t * DV;
+    const int r0 = q0 + t * kBlockM;
+
+    float m_run = -INFINITY;  // running max, log2-scaled units
+    float l_run = 0.0f;
+    float slope = 0.0f;
+    if constexpr (kFamily == kFamilyElementwise) {
+      if (p.slope != nullptr) slope = p.slope[h];
+    }
+    const float fi = static_cast<float>(i);
+
+    for (int n = 0; n < nk; ++n) {
+      const int c0 = (band.jb_lo + n) * kBlockN;
+      mbar_wait(&s_full[t], n & 1);
+      tc_fence_after();
+      uint32_t sr[kBlockN];
+#pragma unroll
+      for (int c = 0; c < kBlockN / 32; ++c)
+        tmem_ld32(s_tmem + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      tmem_ld_wait();
+      float* s = reinterpret_cast<float*>(sr);
+      const bool full = block_fully_kept(p.mask, r0, c0, p.seq_k);
+
+      if constexpr (kFamily == kFamilySoftmax) {
+        float bmax = -INFINITY;
+        if (full) {
+#pragma unroll
+          for (int c = 0; c < kBlockN; ++c) {
+            s[c] *= p.scale_log2;
+            bmax = fmaxf(bmax, s[c]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < kBlockN; ++c) {
+            s[c] = kept(p.mask, i, c0 + c, p.seq_k) ? s[c] * p.scale_log2 : -INFINITY;
+            bmax = fmaxf(bmax, s[c]);
+          }
+        }
+        const float m_new = fmaxf(m_run, bmax);
+        // Lazy rescale: keep the stale max unless the new one exceeds it by more than 2^8.
+        const bool need = (m_new - m_run) > 8.0f;
+        float factor = 1.0f;
+        if (need) {
+          factor = (m_run == -INFINITY) ? 0.0f : ex2(m_run - m_new);
+          m_run = m_new;
+        }
+        const float m_use = (m_run == -INFINITY) ? 0.0f : m_run;
+        float lsum = 0.0f;
+        uint32_t pk[kBlockN / 2];
+#pragma unroll
+        for (int c = 0; c < kBlockN; c += 2) {
+          const float e0 = ex2(s[c] - m_use);
+          const float e1 = ex2(s[c + 1] - m_use);
+          lsum += e0 + e1;
+          pk[c / 2] = pack_bf16(e0, e1);
+        }
+        l_run = l_run * factor + lsum;
+#pragma unroll
+        for (int c = 0; c < kBlockN / 64; ++c)
+          tmem_st32(s_tmem + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+        tmem_st_wait();
+        // Correction of the O accumulator (only rows whose max moved by > 2^8).
+        if (n > 0 && __any_sync(0xffffffffu, need)) {
+          mbar_wait(&o_done[t], (n - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < DV / 32; ++c) {
+            uint32_t orr[32];
+            tmem_ld32(o_tmem + c * 32, orr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              orr[e] = __float_as_uint(__uint_as_float(orr[e]) * factor);
+            tmem_st32(o_tmem + c * 32, orr);
+          }
+          tmem_st_wait();
+        }
+      } else {
+        uint32_t pk[kBlockN / 2];
+        const float bias = p.bias + slope * static_cast<float>(c0) - slope * fi;
+#pragma unroll
+        for (int c = 0; c < kBlockN; c += 2) {
+          float z0 = s[c] * p.scale + bias + slope * static_cast<float>(c);
+          float z1 = s[c + 1] * p.scale + bias + slope * static_cast<float>(c + 1);
+          float e0 = apply_act<kAct>(z0);
+          float e1 = apply_act<kAct>(z1);
+          if (!full) {
+            if (!kept(p.mask, i, c0 + c, p.seq_k)) e0 = 0.0f;
+            if (!kept(p.mask, i, c0 + c + 1, p.seq_k)) e1 = 0.0f;
+          }
+          pk[c / 2] = pack_bf16(e0, e1);
+        }
+#pragma unroll
+        for (int c = 0; c < kBlockN / 64; ++c)
+          tmem_st32(s_tmem + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&p_full[t]);
+    }
+
+    // ───────────── epilogue: O / l, LSE ─────────────
+    float inv = 1.0f;
+    if constexpr (kFamily == kFamilySoftmax) inv = (l_run == 0.0f) ? 0.0f : 1.0f / l_run;
+    if (nk > 0) {
+      mbar_wait(&o_done[t], (nk - 1) & 1);
+      tc_fence_after();
+    }
+    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_stride_b +
+                          h * p.o_stride_h + static_cast<int64_t>(i) * p.o_stride_s;
+#pragma unroll
+    for (int c = 0; c < DV / 32; ++c) {
+      uint32_t orr[32];
+      if (nk > 0) {
+        tmem_ld32(o_tmem + c * 32, orr);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) orr[e] = 0u;
+      }
+      if (i < p.seq_q) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(orr[v * 8 + 0]) * inv, __uint_as_float(orr[v * 8 + 1]) * inv);
+          w.y = pack_bf16(__uint_as_float(orr[v * 8 + 2]) * inv, __uint_as_float(orr[v * 8 + 3]) * inv);
+          w.z = pack_bf16(__uint_as_float(orr[v * 8 + 4]) * inv, __uint_as_float(orr[v * 8 + 5]) * inv);
+          w.w = pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv);
+          dst[v] = w;
+        }
+      }
+    }
+    if constexpr (kFamily == kFamilySoftmax) {
+      if (p.lse != nullptr && i < p.seq_q) {
+        const float lse = (l_run == 0.0f) ? -INFINITY : (m_run * kLn2 + logf(l_run));
+        p.lse[(static_cast<int64_t>(b) * p.heads_q + h) * p.seq_q + i] = lse;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace af
