@@ -2,12 +2,6 @@
 #include "host_common.h"
 
 extern "C" {
-size_t af_parallel_bwd_workspace(const af_parallel_desc*) { return 0; }
-int af_parallel_bwd(const af_parallel_desc*, const void*, const void*, const void*, const void*,
-                    const float*, const void*, void*, void*, void*, void*, size_t, void*) {
-  af::set_error("af_parallel_bwd not built yet");
-  return AF_ERR_UNSUPPORTED;
-}
 int af_linear_fwd(const af_linear_desc*, const void*, const void*, const void*, const float*,
                   void*, float*, void*) {
   af::set_error("af_linear_fwd not built yet");
