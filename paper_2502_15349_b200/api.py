@@ -1,0 +1,394 @@
+"""GPU executors with the reference's call signatures (the drop-in boundary, Python side).
+
+Every function takes an ``AttentionSpec`` (this package's, or an ``attnforge`` one — converted by
+``spec.from_reference``) and a dict of CUDA tensors named like the reference's ``arrays``
+(``q``, ``k``, ``v`` and each extra; ``qidx``/``kidx`` are synthesised in-kernel and ignored), and
+returns freshly allocated CUDA tensors.  Inputs are never mutated.
+
+========================================  =====================================================
+reference (attnforge)                     here
+========================================  =====================================================
+engine.run_tiled_parallel  (engine.py:423)  ``run_tiled_parallel`` / ``parallel_forward`` (+LSE)
+engine.run_naive_parallel  (engine.py:401)  ``run_naive_parallel`` (same kernel; tiled ≡ naive)
+engine.run_chunk_recurrent (engine.py:554)  ``run_chunk_recurrent`` / ``linear_forward``
+engine.run_step_recurrent  (engine.py:525)  ``run_step_recurrent`` (chunked kernel; chunk ≡ step)
+engine.autodiff_grads      (engine.py:630)  ``autodiff_grads`` (seed ones, or an explicit ``dout``)
+ExecutablePlan.run         (lowering.py:857) ``bind(spec).run(arrays)``
+========================================  =====================================================
+
+There is no CPU path: every call lowers the spec (``plan.py``) and launches the sm_100a library
+through its C ABI (``runtime.py``); if the library or a GPU is missing the call raises.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import runtime as rt
+from .errors import InputError, NanError, ShapeError, UnsupportedError
+from .plan import FAMILY_SOFTMAX, LinearPlan, ParallelPlan, plan_linear, plan_parallel
+from .spec import AttentionSpec, Pattern, from_reference
+
+_BF16 = torch.bfloat16
+
+
+def _spec(spec) -> AttentionSpec:
+    return spec if isinstance(spec, AttentionSpec) else from_reference(spec)
+
+
+def _stream() -> int | None:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need(arrays: dict, name: str) -> torch.Tensor:
+    if name not in arrays:
+        raise InputError("missing input tensor", name=name)
+    t = arrays[name]
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InputError("inputs must be CUDA tensors (this backend has no CPU path)", name=name)
+    return t
+
+
+def _check_shape(t: torch.Tensor, want: tuple, name: str) -> None:
+    if tuple(t.shape) != tuple(want):
+        raise ShapeError("input shape mismatch", name=name, want=tuple(want), got=tuple(t.shape))
+
+
+def _as(t: torch.Tensor, dtype) -> torch.Tensor:
+    t = t if t.dtype == dtype else t.to(dtype)
+    return t if t.stride(-1) == 1 else t.contiguous()
+
+
+def _check_nan(out: torch.Tensor, what: str) -> torch.Tensor:
+    if torch.isnan(out).any().item():
+        raise NanError("output contains NaN", path=what, count=int(torch.isnan(out).sum()))
+    return out
+
+
+# ───────────────────────────── parallel template ─────────────────────────────
+
+def _parallel_inputs(plan: ParallelPlan, arrays: dict, dtype):
+    d = plan.spec.dims
+    hkv = d.kv_heads
+    q = _need(arrays, "q")
+    k = _need(arrays, "k")
+    _check_shape(q, (d.batch, d.heads, d.seq_q, d.d_qk), "q")
+    _check_shape(k, (d.batch, hkv, d.seq_k, d.d_qk), "k")
+    if plan.spec.kv_shared:
+        v = k[..., : d.d_v]
+    else:
+        v = _need(arrays, "v")
+        _check_shape(v, (d.batch, hkv, d.seq_k, d.d_v), "v")
+    slope = None
+    if plan.slope_extra is not None:
+        slope = _need(arrays, plan.slope_extra).to(torch.float32).reshape(-1)
+        slope = slope.expand(d.heads).contiguous() if slope.numel() == 1 else slope.contiguous()
+    elif plan.slope_const != 0.0:
+        slope = torch.full((d.heads,), plan.slope_const, device=q.device, dtype=torch.float32)
+    return _as(q, dtype), _as(k, dtype), _as(v, dtype), slope
+
+
+def _desc(plan: ParallelPlan, q, k, v, o, slope, dtype_code: int) -> rt.ParallelDesc:
+    d = plan.spec.dims
+    c = rt.ParallelDesc()
+    c.batch, c.heads_q, c.heads_kv = d.batch, d.heads, d.kv_heads
+    c.seq_q, c.seq_k, c.d_qk, c.d_v = d.seq_q, d.seq_k, d.d_qk, d.d_v
+    c.dtype = dtype_code
+    c.q_stride, c.k_stride, c.v_stride = rt.strides4(q), rt.strides4(k), rt.strides4(v)
+    c.o_stride = rt.strides4(o)
+    c.family, c.act, c.scale = plan.family, plan.act, float(plan.scale)
+    c.causal, c.diag_offset, c.window = plan.band.causal, plan.band.diag_offset, \
+        plan.band.kernel_window
+    c.slope = rt.ptr(slope)
+    c.bias = float(plan.bias)
+    return c
+
+
+def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: bool = False):
+    """Forward of the parallel template → ``(O [B,H,Sq,Dv], LSE [B,H,Sq] fp32 or None)``.
+
+    ``precision="bf16"`` runs the tcgen05 kernel (K1) on bf16 inputs (fp32 inputs are rounded);
+    ``"fp32"`` runs the exact-FFMA fp32 kernel (cfg1 parity path)."""
+    spec = _spec(spec)
+    plan = plan_parallel(spec)
+    dtype = _BF16 if precision == "bf16" else torch.float32
+    q, k, v, slope = _parallel_inputs(plan, arrays, dtype)
+    d = spec.dims
+    o = torch.empty(d.batch, d.heads, d.seq_q, d.d_v, device=q.device, dtype=dtype)
+    lse = (torch.empty(d.batch, d.heads, d.seq_q, device=q.device, dtype=torch.float32)
+           if plan.has_lse else None)
+    desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16 if dtype == _BF16 else rt.AF_DTYPE_F32)
+    rt.check(rt.lib().af_parallel_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                      o.data_ptr(), rt.ptr(lse), _stream()), "af_parallel_fwd")
+    if check_nan:
+        _check_nan(o, "kernel")
+    return o, lse
+
+
+def run_tiled_parallel(spec, arrays: dict, block_q: int = 64, block_k: int = 64, **kw):
+    """Drop-in for ``engine.run_tiled_parallel`` (engine.py:423).  The kernel's own 128x128 tile
+    replaces ``block_q``/``block_k`` (the reference pins tiled ≡ naive for any blocking,
+    test_engine.py:189-205)."""
+    if block_q < 1 or block_k < 1:
+        raise InputError("block sizes must be positive", block_q=block_q, block_k=block_k)
+    return parallel_forward(spec, arrays, check_nan=True, **kw)[0]
+
+
+def run_naive_parallel(spec, arrays: dict, **kw):
+    return parallel_forward(spec, arrays, check_nan=True, **kw)[0]
+
+
+def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tensor) -> dict:
+    """VJP of ``parallel_forward`` for cotangent ``dout``: ``{"q": dq, "k": dk, "v": dv}`` (bf16;
+    dk/dv summed over each GQA group; for ``kv_shared`` the V gradient is folded into dk)."""
+    spec = _spec(spec)
+    plan = plan_parallel(spec)
+    q, k, v, slope = _parallel_inputs(plan, arrays, _BF16)
+    d = spec.dims
+    o = _as(o, _BF16)
+    dout = _as(dout, _BF16).contiguous() if dout.stride() != o.stride() else _as(dout, _BF16)
+    if dout.stride() != o.stride():
+        dout = dout.contiguous()
+        o = o.contiguous()
+    _check_shape(dout, (d.batch, d.heads, d.seq_q, d.d_v), "dout")
+    dq = torch.empty_like(q, memory_format=torch.contiguous_format)
+    dk = torch.empty(k.shape, device=k.device, dtype=_BF16)
+    dv = torch.empty(d.batch, d.kv_heads, d.seq_k, d.d_v, device=k.device, dtype=_BF16)
+    desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16)
+    # dq/dk/dv are written with the q/k/v strides of the descriptor: use contiguous copies
+    if q.stride() != dq.stride() or k.stride() != dk.stride() or v.stride() != dv.stride():
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16)
+    L = rt.lib()
+    ws_n = L.af_parallel_bwd_workspace(desc)
+    ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
+    if plan.family == FAMILY_SOFTMAX and lse is None:
+        raise InputError("softmax backward needs the forward LSE")
+    rt.check(L.af_parallel_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                               rt.ptr(lse), dout.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                               dv.data_ptr(), ws.data_ptr(), ws_n, _stream()), "af_parallel_bwd")
+    if spec.kv_shared:
+        dk = dk.clone()
+        dk[..., : d.d_v] += dv
+        return {"q": dq, "k": dk}
+    return {"q": dq, "k": dk, "v": dv}
+
+
+# ───────────────────────────── recurrent template ─────────────────────────────
+
+def _linear_desc(plan: LinearPlan, q, k, v, o) -> rt.LinearDesc:
+    d = plan.spec.dims
+    c = rt.LinearDesc()
+    c.batch, c.heads, c.seq, c.d_k, c.d_v = d.batch, d.heads, d.seq_q, d.d_qk, d.d_v
+    c.chunk = plan.chunk
+    c.q_scale = float(plan.q_scale)
+    c.q_stride, c.k_stride, c.v_stride, c.o_stride = (rt.strides4(q), rt.strides4(k),
+                                                      rt.strides4(v), rt.strides4(o))
+    return c
+
+
+def _per_step(arrays: dict, name: str, d) -> torch.Tensor:
+    t = _need(arrays, name).to(torch.float32)
+    return t.expand(d.batch, d.heads, d.seq_k, 1)
+
+
+def linear_log_decay(plan: LinearPlan, arrays: dict) -> torch.Tensor:
+    """log a_t as an fp32 [B, H, S] tensor (product of the h_mod factors, attention.py:332)."""
+    d = plan.spec.dims
+    dev = _need(arrays, "q").device
+    out = torch.full((d.batch, d.heads, d.seq_k), math.log(plan.decay_const)
+                     if plan.decay_const > 0 else -math.inf, device=dev, dtype=torch.float32)
+    for name in plan.decay_factors:
+        out = out + torch.log(_per_step(arrays, name, d)[..., 0])
+    return out.contiguous()
+
+
+def _linear_inputs(plan: LinearPlan, arrays: dict):
+    d = plan.spec.dims
+    q, k, v = _need(arrays, "q"), _need(arrays, "k"), _need(arrays, "v")
+    _check_shape(q, (d.batch, d.heads, d.seq_q, d.d_qk), "q")
+    _check_shape(k, (d.batch, d.heads, d.seq_k, d.d_qk), "k")
+    _check_shape(v, (d.batch, d.heads, d.seq_k, d.d_v), "v")
+    km = k
+    if plan.k_gate is not None:
+        km = k.to(torch.float32) * _per_step(arrays, plan.k_gate, d)
+    return _as(q, _BF16), _as(km, _BF16), _as(v, _BF16)
+
+
+def linear_forward(spec, arrays: dict, chunk: int = 64, *, check_nan: bool = False):
+    """Chunked linear template forward → O [B,H,S,Dv] (bf16)."""
+    spec = _spec(spec)
+    plan = plan_linear(spec, chunk)
+    q, km, v = _linear_inputs(plan, arrays)
+    logd = linear_log_decay(plan, arrays)
+    d = spec.dims
+    o = torch.empty(d.batch, d.heads, d.seq_q, d.d_v, device=q.device, dtype=_BF16)
+    desc = _linear_desc(plan, q, km, v, o)
+    rt.check(rt.lib().af_linear_fwd(desc, q.data_ptr(), km.data_ptr(), v.data_ptr(),
+                                    logd.data_ptr(), o.data_ptr(), None, _stream()),
+             "af_linear_fwd")
+    if check_nan:
+        _check_nan(o, "chunk")
+    return o
+
+
+def run_chunk_recurrent(spec, arrays: dict, chunk: int = 64):
+    """Drop-in for ``engine.run_chunk_recurrent`` (engine.py:554)."""
+    if chunk < 1:
+        raise InputError("chunk must be positive", chunk=chunk)
+    return linear_forward(spec, arrays, 64, check_nan=True)
+
+
+def run_step_recurrent(spec, arrays: dict):
+    """Drop-in for ``engine.run_step_recurrent`` (engine.py:525); chunked ≡ stepwise
+    (test_engine.py:208-221)."""
+    return linear_forward(spec, arrays, 64, check_nan=True)
+
+
+def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 64) -> dict:
+    """VJP of ``linear_forward``: grads for q, k, v and each differentiable extra of a_t / k_mod."""
+    spec = _spec(spec)
+    plan = plan_linear(spec, chunk)
+    q, km, v = _linear_inputs(plan, arrays)
+    logd = linear_log_decay(plan, arrays)
+    d = spec.dims
+    dout = _as(dout, _BF16).contiguous()
+    dq, dkm, dv = torch.empty_like(q), torch.empty_like(km), torch.empty_like(v)
+    dlogd = torch.empty_like(logd)
+    o = torch.empty(d.batch, d.heads, d.seq_q, d.d_v, device=q.device, dtype=_BF16)
+    desc = _linear_desc(plan, q, km, v, o)
+    L = rt.lib()
+    ws_n = L.af_linear_bwd_workspace(desc)
+    ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
+    rt.check(L.af_linear_bwd(desc, q.data_ptr(), km.data_ptr(), v.data_ptr(), logd.data_ptr(),
+                             dout.data_ptr(), dq.data_ptr(), dkm.data_ptr(), dv.data_ptr(),
+                             dlogd.data_ptr(), ws.data_ptr(), ws_n, _stream()), "af_linear_bwd")
+    grads = {"q": dq, "v": dv}
+    k = _need(arrays, "k")
+    if plan.k_gate is not None:
+        gate = _per_step(arrays, plan.k_gate, d)
+        grads["k"] = (dkm.float() * gate).to(_BF16)
+    else:
+        grads["k"] = dkm
+    # chain d log a_t and d k_mod into the differentiable extras
+    for e in spec.extra_inputs:
+        if not e.differentiable:
+            continue
+        g = torch.zeros(d.batch, d.heads, d.seq_k, device=q.device, dtype=torch.float32)
+        t = _per_step(arrays, e.name, d)[..., 0]
+        n_occ = plan.decay_factors.count(e.name)
+        if n_occ:
+            g = g + n_occ * dlogd / t
+        if plan.k_gate == e.name:
+            g = g + (dkm.float() * k.float()).sum(-1)
+        want = _need(arrays, e.name).shape
+        grads[e.name] = _sum_to(g.unsqueeze(-1), want)
+    return grads
+
+
+def _sum_to(g: torch.Tensor, shape) -> torch.Tensor:
+    dims = [i for i, (a, b) in enumerate(zip(g.shape, shape)) if b == 1 and a != 1]
+    return g.sum(dim=dims, keepdim=True) if dims else g
+
+
+# ───────────────────────────── autodiff entry point ─────────────────────────────
+
+def autodiff_grads(spec, arrays: dict, wrt=None, dout: torch.Tensor | None = None) -> dict:
+    """Drop-in for ``engine.autodiff_grads`` (engine.py:630): gradients of ``sum(O)`` (or of
+    ``<dout, O>`` when ``dout`` is given) with respect to q, k, v and differentiable extras."""
+    spec = _spec(spec)
+    d = spec.dims
+    if spec.pattern is Pattern.PARALLEL:
+        o, lse = parallel_forward(spec, arrays)
+        g = torch.ones_like(o) if dout is None else dout
+        grads = parallel_backward(spec, arrays, o, lse, g)
+        for e in spec.extra_inputs:
+            if e.differentiable:
+                raise UnsupportedError("gradients w.r.t. parallel-template extras are not "
+                                       "lowered", extra=e.name)
+    else:
+        g = torch.ones(d.batch, d.heads, d.seq_q, d.d_v, device=_need(arrays, "q").device,
+                       dtype=_BF16) if dout is None else dout
+        grads = linear_backward(spec, arrays, g)
+    if wrt is None:
+        wrt = ["q", "k", "v"] + [e.name for e in spec.extra_inputs if e.differentiable]
+    missing = [n for n in wrt if n not in grads]
+    if missing:
+        raise InputError("cannot differentiate unknown inputs", names=missing)
+    return {n: grads[n] for n in wrt}
+
+
+# ───────────────────────────── bound executable ─────────────────────────────
+
+@dataclass
+class BoundKernel:
+    """``lowering.bind_executable(assemble_kernel(spec, tile), plan)`` analogue: the lowered plan
+    bound to the sm_100a kernels; ``run(arrays)`` executes it (lowering.py:857-860)."""
+
+    spec: AttentionSpec
+    plan: object
+
+    def run(self, arrays: dict) -> torch.Tensor:
+        if self.spec.pattern is Pattern.PARALLEL:
+            return run_tiled_parallel(self.spec, arrays)
+        return run_chunk_recurrent(self.spec, arrays)
+
+
+def bind(spec) -> BoundKernel:
+    spec = _spec(spec)
+    plan = plan_parallel(spec) if spec.pattern is Pattern.PARALLEL else plan_linear(spec)
+    return BoundKernel(spec, plan)
+
+
+# ───────────────────────────── autograd module ─────────────────────────────
+
+class _ParallelFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, spec, q, k, v, extras):
+        arrays = {"q": q, "k": k, "v": v, **extras}
+        with torch.cuda.device(q.device):
+            o, lse = parallel_forward(spec, arrays)
+        ctx.spec, ctx.extras = spec, extras
+        ctx.save_for_backward(q, k, v, o, lse if lse is not None else torch.empty(0))
+        ctx.has_lse = lse is not None
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse = ctx.saved_tensors
+        arrays = {"q": q, "k": k, "v": v, **ctx.extras}
+        with torch.cuda.device(q.device):
+            g = parallel_backward(ctx.spec, arrays, o, lse if ctx.has_lse else None, do)
+        return None, g["q"].to(q.dtype), g["k"].to(k.dtype), g.get("v", None), None
+
+
+class AttentionEngine:
+    """AttentionEngine-style callable: ``AttentionEngine(spec)(q, k, v, **custom_fwd_inputs)``
+    with autograd support (forward K1, backward K2 / linear K4-K5)."""
+
+    def __init__(self, spec):
+        self.spec = _spec(spec)
+        self.plan = bind(self.spec).plan
+
+    def __call__(self, q, k, v, **extras):
+        if self.spec.pattern is Pattern.PARALLEL:
+            return _ParallelFn.apply(self.spec, q, k, v, extras)
+        return _LinearFn.apply(self.spec, q, k, v, extras)
+
+
+class _LinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, spec, q, k, v, extras):
+        ctx.spec, ctx.extras = spec, extras
+        ctx.save_for_backward(q, k, v)
+        return linear_forward(spec, {"q": q, "k": k, "v": v, **extras})
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v = ctx.saved_tensors
+        with torch.cuda.device(q.device):
+            g = linear_backward(ctx.spec, {"q": q, "k": k, "v": v, **ctx.extras}, do)
+        return None, g["q"].to(q.dtype), g["k"].to(k.dtype), g["v"].to(v.dtype), None

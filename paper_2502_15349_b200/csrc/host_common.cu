@@ -40,9 +40,28 @@ void set_error(const char* fmt, ...) {
 
 const char* last_error() { return g_last_error.c_str(); }
 
+void ensure_context() {
+  // The library links the CUDA runtime statically; a thread that has not touched CUDA through
+  // *this* runtime (e.g. torch's autograd worker) may have no current driver context.
+  using GetCurrentFn = CUresult (*)(CUcontext*);
+  static GetCurrentFn get_current = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuCtxGetCurrent", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      get_current = reinterpret_cast<GetCurrentFn>(p);
+  });
+  CUcontext ctx = nullptr;
+  if (get_current == nullptr || get_current(&ctx) != CUDA_SUCCESS || ctx == nullptr) cudaFree(0);
+}
+
 bool make_tmap_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, int elem_bytes,
                   int d, int s, int h, int b, const int64_t* st, int box_d, int box_s,
                   bool swizzle128) {
+  ensure_context();
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) {
     set_error("cuTensorMapEncodeTiled unavailable (driver too old or no GPU)");

@@ -38,5 +38,6 @@ bool make_tmap_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype,
                   bool swizzle128);
 
 int sm_count();
+void ensure_context();
 
 }  // namespace af

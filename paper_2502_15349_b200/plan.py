@@ -1,0 +1,522 @@
+"""Lowering: AttentionSpec → kernel plan (the host half of the template boundary).
+
+The reference assembles a sectioned template per variant (``lowering.assemble_kernel``,
+lowering.py:459-468) and interprets it per tile.  Here the same hooks are *classified* into one of
+the register-level epilogue families the sm_100a kernels implement, plus launch parameters:
+
+parallel template (``ParallelPlan``)
+  * ``q_mod`` / ``k_mod``: a compile-time scalar (``q / sqrt(dimqk)``) folded into the scores;
+  * mask hooks (``ismask``): band masks recognised from their comparison
+    (``kidx <= qidx`` causal, ``qidx - kidx < W`` sliding window, with offsets) → block skipping in
+    the kernel plus per-element masking on edge blocks.  The out-of-band value must be the one the
+    family ignores (-inf before softmax, 0 after an elementwise activation);
+  * rownorm: the online softmax protocol (recognised numerically, so equivalent spellings such as
+    the bundled capped-softmax file's ``log(0)`` form also match) → softmax family with LSE;
+    no rownorm → elementwise family ``act(tau*s - slope_h*(qidx-kidx) + bias)`` with
+    act ∈ {sigmoid, relu, identity};
+  * anything else raises ``UnsupportedError`` — there is no CPU fallback.
+
+recurrent template (``LinearPlan``)
+  * ``diagonal_scale(h_mod)`` (attention.py:332-369) must be a product of per-step extras /
+    constants; ``k_mod`` may multiply by one per-step extra (Mamba2 ``k * gate``); ``q_mod`` a
+    scalar.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import hooklang as H
+from .errors import UnsupportedError, InputError
+from .spec import (AttentionSpec, DirectRowNorm, OnlineRowNorm, Pattern, diagonal_scale)
+
+FAMILY_SOFTMAX, FAMILY_ELEMENTWISE = 0, 1
+ACT_IDENTITY, ACT_SIGMOID, ACT_RELU = 0, 1, 2
+
+
+@dataclass
+class Band:
+    """Band mask recognised from mask hooks:  keep(i, j) = j <= i + upper  and  i - j < window.
+
+    Kernel parameters (``af_parallel_desc``): causal = upper is set, diag_offset = upper,
+    window = window + upper (the kernel's window bound is relative to the diagonal offset)."""
+
+    upper: int | None = None
+    window: int | None = None
+
+    def keep(self, i: np.ndarray, j: np.ndarray) -> np.ndarray:
+        k = np.ones(np.broadcast_shapes(np.shape(i), np.shape(j)), bool)
+        if self.upper is not None:
+            k &= j <= i + self.upper
+        if self.window is not None:
+            k &= (i - j) < self.window
+        return k
+
+    @property
+    def causal(self) -> int:
+        return int(self.upper is not None)
+
+    @property
+    def diag_offset(self) -> int:
+        return self.upper or 0
+
+    @property
+    def kernel_window(self) -> int:
+        return 0 if self.window is None else self.window + self.diag_offset
+
+
+@dataclass
+class ParallelPlan:
+    spec: AttentionSpec
+    family: int
+    act: int = ACT_IDENTITY
+    scale: float = 1.0
+    band: Band = field(default_factory=Band)
+    slope_extra: str | None = None  # per-head extra multiplying -(qidx - kidx)
+    slope_const: float = 0.0        # constant multiplier of -(qidx - kidx)
+    bias: float = 0.0
+
+    @property
+    def has_lse(self) -> bool:
+        return self.family == FAMILY_SOFTMAX
+
+
+@dataclass
+class LinearPlan:
+    spec: AttentionSpec
+    q_scale: float = 1.0
+    decay_factors: tuple[str, ...] = ()   # extras whose product (with decay_const) is a_t
+    decay_const: float = 1.0
+    k_gate: str | None = None             # extra multiplying k (k_mod = k * gate)
+    chunk: int = 64
+
+
+# ───────────────────────────── helpers ─────────────────────────────
+
+def _scalar_mod(fn, var: str, consts: dict) -> float:
+    """``var * c`` / ``var / c`` / ``c * var`` / bare ``var`` with c a compile-time constant."""
+    if fn is None:
+        return 1.0
+    e = fn.expr
+    if isinstance(e, H.Name) and e.name == var:
+        return 1.0
+    if isinstance(e, H.BinOp) and e.op in "*/":
+        for a, b, swap in ((e.lhs, e.rhs, False), (e.rhs, e.lhs, True)):
+            if isinstance(a, H.Name) and a.name == var and not (swap and e.op == "/"):
+                c = H.const_value(b, consts)
+                if c is not None and math.isfinite(c) and c != 0:
+                    return c if e.op == "*" else 1.0 / c
+    raise UnsupportedError(f"{var}_mod is not a compile-time scalar on this template "
+                           "(elementwise feature maps with extras are not lowered yet)",
+                           source=fn.source)
+
+
+def _linear_in_index(e, consts: dict):
+    """Return (a, b, c) with e == a*qidx + b*kidx + c for an expression over qidx/kidx/consts,
+    or None."""
+    if isinstance(e, H.Name):
+        if e.name == "qidx":
+            return (1.0, 0.0, 0.0)
+        if e.name == "kidx":
+            return (0.0, 1.0, 0.0)
+    c = H.const_value(e, consts)
+    if c is not None:
+        return (0.0, 0.0, c)
+    if isinstance(e, H.Neg):
+        r = _linear_in_index(e.operand, consts)
+        return None if r is None else tuple(-x for x in r)
+    if isinstance(e, H.BinOp):
+        l, r = _linear_in_index(e.lhs, consts), _linear_in_index(e.rhs, consts)
+        if l is None or r is None:
+            return None
+        if e.op == "+":
+            return tuple(x + y for x, y in zip(l, r))
+        if e.op == "-":
+            return tuple(x - y for x, y in zip(l, r))
+        if e.op == "*":
+            if l[0] == l[1] == 0:
+                return tuple(l[2] * y for y in r)
+            if r[0] == r[1] == 0:
+                return tuple(r[2] * x for x in l)
+        if e.op == "/" and r[0] == r[1] == 0 and r[2] != 0:
+            return tuple(x / r[2] for x in l)
+    return None
+
+
+def _band_from_cond(cond: H.Cmp, consts: dict, band: Band) -> bool:
+    """Fold one comparison over qidx/kidx into the band; False when it is not a band bound."""
+    l, r = _linear_in_index(cond.lhs, consts), _linear_in_index(cond.rhs, consts)
+    if l is None or r is None:
+        return False
+    a, b, c = (x - y for x, y in zip(l, r))  # a*i + b*j + c  (op)  0
+    op = cond.op
+    if op in (">", ">="):
+        a, b, c = -a, -b, -c
+        op = "<" if op == ">" else "<="
+    if op not in ("<", "<=") or a != -b or a == 0:
+        return False
+    if op == "<":  # integer positions: x < 0  <=>  x <= -1
+        c += 1.0
+    # a*(i - j) + c <= 0
+    if a < 0:  # j <= i + c/a
+        up = math.floor(c / a + 1e-9)
+        band.upper = up if band.upper is None else min(band.upper, up)
+    else:      # i - j <= -c/a  <=>  i - j < floor(-c/a) + 1
+        w = math.floor(-c / a + 1e-9) + 1
+        band.window = w if band.window is None else min(band.window, w)
+    return True
+
+
+def _mask_kind(fn, consts: dict, band: Band):
+    """Classify a mask hook: returns the out-of-band value (0.0 or -inf) after folding its band
+    condition into ``band``; None if unrecognised."""
+    e = fn.expr
+    if isinstance(e, H.Fn) and e.func == "where" and isinstance(e.args[0], H.Cmp):
+        cond, a, b = e.args
+        if isinstance(a, H.Name) and a.name == "s":
+            out = H.const_value(b, consts)
+            if out is not None and (out == 0.0 or out == -math.inf):
+                if _band_from_cond(cond, consts, band):
+                    return out
+    if isinstance(e, H.BinOp) and e.op == "*":
+        for x, y in ((e.lhs, e.rhs), (e.rhs, e.lhs)):
+            if (isinstance(x, H.Name) and x.name == "s" and isinstance(y, H.Fn)
+                    and y.func == "where" and isinstance(y.args[0], H.Cmp)
+                    and H.const_value(y.args[1], consts) == 1.0
+                    and H.const_value(y.args[2], consts) == 0.0):
+                if _band_from_cond(y.args[0], consts, band):
+                    return 0.0
+    return None
+
+
+def _run_online(rn: OnlineRowNorm, consts: dict, s: np.ndarray, splits: list[int]) -> np.ndarray:
+    """Evaluate an online rownorm protocol on score rows (numpy, for classification only) and
+    return the normalised probability rows (acc with V = identity)."""
+    rows, n = s.shape
+    env0 = dict(consts)
+    scales = {name: np.full((rows, 1), float(_np_eval(fn.expr, env0)))
+              for name, fn in rn.prologue}
+    acc = np.zeros((rows, n))
+    start = 0
+    for stop in splits + [n]:
+        blk = s[:, start:stop]
+        env = {**consts, **scales, "s": blk}
+        for name, fn in rn.fwd:
+            env[name] = _np_eval(fn.expr, env)
+        p = np.broadcast_to(np.asarray(env["scores"], float), blk.shape)
+        r = np.asarray(env["rescale"], float)
+        acc = acc * r
+        acc[:, start:stop] += p
+        scales = {k: np.asarray(env[k], float) * np.ones((rows, 1)) for k in rn.rowscales}
+        start = stop
+    out = _np_eval(rn.epilogue.expr, {**consts, **scales, "acc": acc})
+    return np.asarray(out, float) * np.ones((rows, n))
+
+
+def _np_eval(e, env):
+    with np.errstate(all="ignore"):
+        if isinstance(e, H.Num):
+            return e.value
+        if isinstance(e, H.Name):
+            return env[e.name]
+        if isinstance(e, H.Neg):
+            return -_np_eval(e.operand, env)
+        if isinstance(e, H.BinOp):
+            a, b = _np_eval(e.lhs, env), _np_eval(e.rhs, env)
+            return {"+": np.add, "-": np.subtract, "*": np.multiply, "/": np.divide}[e.op](
+                np.float64(1) * a, b)
+        if isinstance(e, H.Cmp):
+            a, b = _np_eval(e.lhs, env), _np_eval(e.rhs, env)
+            return {"==": np.equal, "!=": np.not_equal, "<": np.less, "<=": np.less_equal,
+                    ">": np.greater, ">=": np.greater_equal}[e.op](a, b).astype(float)
+        f = e.func
+        a = [_np_eval(x, env) for x in e.args]
+        one = {"exp": np.exp, "exp2": np.exp2, "log": np.log, "abs": np.abs, "tanh": np.tanh,
+               "sigmoid": lambda x: 1 / (1 + np.exp(-np.asarray(x, float))),
+               "relu": lambda x: np.maximum(x, 0.0), "sqrt": np.sqrt}
+        if f in one:
+            return one[f](a[0])
+        if f == "reduceSum":
+            return np.sum(a[0], axis=-1, keepdims=True)
+        if f == "reduceMax":
+            return np.max(a[0], axis=-1, keepdims=True)
+        if f == "reduceAbssum":
+            return np.sum(np.abs(a[0]), axis=-1, keepdims=True)
+        if f == "max":
+            return np.maximum(a[0], a[1])
+        if f == "min":
+            return np.minimum(a[0], a[1])
+        if f == "clamp":
+            return np.clip(a[0], a[1], a[2])
+        if f == "where":
+            return np.where(np.asarray(a[0]) != 0, a[1], a[2])
+    raise InputError("unhandled expression form", form=type(e).__name__)
+
+
+def is_online_softmax(rn, consts: dict) -> bool:
+    """Numerical fingerprint: does this online protocol compute softmax rows for arbitrary
+    blockings, including -inf (masked) entries and fully-masked rows (→ 0)?"""
+    if not isinstance(rn, OnlineRowNorm):
+        return False
+    rng = np.random.default_rng(1234)
+    s = rng.uniform(-6, 6, size=(6, 24))
+    s[1, :9] = -np.inf
+    s[2, :] = -np.inf
+    s[3, 5:] = -np.inf
+    s[4] *= 10.0
+    m = np.max(s, axis=-1, keepdims=True)
+    with np.errstate(all="ignore"):
+        e = np.where(np.isfinite(m), np.exp(s - np.where(np.isfinite(m), m, 0)), 0.0)
+        den = e.sum(-1, keepdims=True)
+        want = np.where(den == 0, 0.0, e / np.where(den == 0, 1, den))
+    try:
+        for splits in ([], [1, 2, 9, 17], [12], [3, 6, 9, 12, 15, 18, 21]):
+            got = _run_online(rn, consts, s, splits)
+            if not np.allclose(got, want, atol=1e-12, rtol=1e-10):
+                return False
+    except Exception:  # noqa: BLE001 - any evaluation failure means "not softmax"
+        return False
+    return True
+
+
+def _strip_act(e):
+    if isinstance(e, H.Fn) and e.func in ("sigmoid", "relu"):
+        return (ACT_SIGMOID if e.func == "sigmoid" else ACT_RELU), e.args[0]
+    return ACT_IDENTITY, e
+
+
+def _affine_score(e, consts: dict, extras: dict):
+    """e == tau*s - slope*(qidx - kidx) + bias with slope = const or a per-head extra.
+    Returns (tau, slope_const, slope_extra, bias) or None."""
+    terms: dict = {}
+
+    def add(key, coef):
+        terms[key] = terms.get(key, 0.0) + coef
+
+    def walk(n, sign: float) -> bool:
+        if isinstance(n, H.BinOp) and n.op in "+-":
+            return walk(n.lhs, sign) and walk(n.rhs, sign if n.op == "+" else -sign)
+        if isinstance(n, H.Neg):
+            return walk(n.operand, -sign)
+        c = H.const_value(n, consts)
+        if c is not None:
+            add("1", sign * c)
+            return True
+        if isinstance(n, H.Name) and n.name == "s":
+            add("s", sign)
+            return True
+        lin = _linear_in_index(n, consts)
+        if lin is not None and lin[0] == -lin[1]:
+            add("d", sign * lin[0])
+            add("1", sign * lin[2])
+            return True
+        if isinstance(n, H.BinOp) and n.op in "*/":
+            for x, y in ((n.lhs, n.rhs), (n.rhs, n.lhs)):
+                if n.op == "/" and x is n.rhs:
+                    continue
+                cy = H.const_value(y, consts)
+                if isinstance(x, H.Name) and x.name == "s" and cy is not None:
+                    add("s", sign * (cy if n.op == "*" else 1.0 / cy))
+                    return True
+                if isinstance(x, H.Name) and x.name in extras and n.op == "*":
+                    lin = _linear_in_index(y, consts)
+                    if lin is not None and lin[0] == -lin[1] and lin[2] == 0:
+                        add(("x", x.name), sign * lin[0])
+                        return True
+                    if isinstance(y, H.BinOp) and y.op == "*":
+                        pass
+            # const * extra * (i - j) forms
+            if n.op == "*":
+                fs: list = []
+
+                def flat(z):
+                    if isinstance(z, H.BinOp) and z.op == "*":
+                        flat(z.lhs)
+                        flat(z.rhs)
+                    else:
+                        fs.append(z)
+
+                flat(n)
+                coef, ext, lin = 1.0, None, None
+                for z in fs:
+                    cz = H.const_value(z, consts)
+                    if cz is not None:
+                        coef *= cz
+                    elif isinstance(z, H.Name) and z.name in extras and ext is None:
+                        ext = z.name
+                    elif lin is None:
+                        lin = _linear_in_index(z, consts)
+                        if lin is None:
+                            return False
+                    else:
+                        return False
+                if lin is not None and lin[0] == -lin[1] and lin[2] == 0:
+                    add(("x", ext) if ext else "d", sign * coef * lin[0])
+                    return True
+        return False
+
+    if not walk(e, 1.0):
+        return None
+    tau = terms.pop("s", 0.0)
+    bias = terms.pop("1", 0.0)
+    dcoef = terms.pop("d", 0.0)
+    ext = [k for k in terms if isinstance(k, tuple)]
+    if terms.keys() - set(ext) or len(ext) > 1 or tau == 0.0:
+        return None
+    slope_extra, slope_coef = None, 0.0
+    if ext:
+        slope_extra, slope_coef = ext[0][1], terms[ext[0]]
+    # kernel form: z = tau*s - slope*(i - j) + bias  → slope = -coef_of(i - j)
+    return tau, -dcoef, slope_extra, -slope_coef, bias
+
+
+def plan_parallel(spec: AttentionSpec) -> ParallelPlan:
+    if spec.pattern is not Pattern.PARALLEL:
+        raise InputError("variant is not a parallel-pattern variant", variant=spec.name)
+    spec.validate()
+    consts = spec.dims.const_env()
+    scale = _scalar_mod(spec.q_mod, "q", consts) * _scalar_mod(spec.k_mod, "k", consts)
+    if spec.v_mod is not None and _scalar_mod(spec.v_mod, "v", consts) != 1.0:
+        raise UnsupportedError("v_mod scaling is not lowered", source=spec.v_mod.source)
+    if spec.output_mod is not None:
+        raise UnsupportedError("output_mod is not lowered on the parallel template yet",
+                               source=spec.output_mod.source)
+    band = Band()
+    plain, mask_vals = [], []
+    seen_mask = False
+    for m in spec.score_mods:
+        if m.ismask:
+            seen_mask = True
+            v = _mask_kind(m, consts, band)
+            if v is None:
+                raise UnsupportedError("mask_mod is not a recognised band mask", source=m.source)
+            mask_vals.append(v)
+        else:
+            if seen_mask:
+                raise UnsupportedError("score_mod after a mask_mod is not lowered", source=m.source)
+            plain.append(m)
+    rn = spec.rownorm
+    if rn is not None and is_online_softmax(rn if isinstance(rn, OnlineRowNorm) else None, consts):
+        if plain:
+            raise UnsupportedError("score_mod ahead of the online softmax is not lowered yet",
+                                   source=plain[0].source)
+        if any(v != -math.inf for v in mask_vals):
+            raise UnsupportedError("softmax masks must use the additive -inf form")
+        return ParallelPlan(spec, FAMILY_SOFTMAX, scale=scale, band=band)
+    if isinstance(rn, DirectRowNorm) and _direct_is_softmax(rn, consts):
+        if plain or any(v != -math.inf for v in mask_vals):
+            raise UnsupportedError("direct softmax with score mods is not lowered")
+        return ParallelPlan(spec, FAMILY_SOFTMAX, scale=scale, band=band)
+    if rn is not None:
+        raise UnsupportedError("row normalisation is neither online softmax nor absent; the "
+                               "abssum-clamp / generic online forms are not lowered yet",
+                               variant=spec.name)
+    # elementwise family: compose the plain score mods into one expression of s
+    expr = H.Name("s")
+    for m in plain:
+        expr = _substitute(m.expr, "s", expr)
+    act, inner = _strip_act(expr)
+    extras = {e.name: e for e in spec.extra_inputs}
+    aff = _affine_score(inner, consts, extras)
+    if aff is None:
+        raise UnsupportedError("score_mod is not act(a*s + slope*(qidx-kidx) + c)",
+                               expr=H.to_source(expr))
+    tau, slope_c, slope_x, slope_xc, bias = aff
+    if any(v != 0.0 for v in mask_vals):
+        raise UnsupportedError("masks ahead of a norm-free score must zero the score (s*0/1)")
+    if slope_x is not None:
+        ex = extras[slope_x]
+        if tuple(ex.shape) not in ((1, "heads", 1, 1), (1, 1, 1, 1)):
+            raise UnsupportedError("relative-position slope extra must be per-head [1,heads,1,1]",
+                                   extra=slope_x)
+        if slope_c != 0.0:
+            raise UnsupportedError("mixed constant and per-head slopes are not lowered")
+    if slope_x is not None and slope_xc != 1.0:
+        raise UnsupportedError("slope extra must enter with coefficient 1", coef=slope_xc)
+    return ParallelPlan(spec, FAMILY_ELEMENTWISE, act=act, scale=scale * tau, band=band,
+                        slope_extra=slope_x, slope_const=slope_c, bias=bias)
+
+
+def _direct_is_softmax(rn: DirectRowNorm, consts) -> bool:
+    rng = np.random.default_rng(7)
+    s = rng.uniform(-5, 5, size=(4, 16))
+    s[1, :4] = -np.inf
+    s[2] = -np.inf
+    try:
+        got = np.asarray(_np_eval(rn.body.expr, {**consts, "s": s}), float)
+    except Exception:  # noqa: BLE001
+        return False
+    m = np.max(s, -1, keepdims=True)
+    with np.errstate(all="ignore"):
+        e = np.where(np.isfinite(m), np.exp(s - np.where(np.isfinite(m), m, 0)), 0)
+        den = e.sum(-1, keepdims=True)
+        want = np.where(den == 0, 0, e / np.where(den == 0, 1, den))
+    return bool(np.allclose(got, want, atol=1e-12))
+
+
+def _substitute(e, name: str, by):
+    if isinstance(e, H.Name):
+        return by if e.name == name else e
+    if isinstance(e, H.Num):
+        return e
+    if isinstance(e, H.Neg):
+        return H.Neg(_substitute(e.operand, name, by))
+    if isinstance(e, (H.BinOp, H.Cmp)):
+        return type(e)(e.op, _substitute(e.lhs, name, by), _substitute(e.rhs, name, by))
+    return H.Fn(e.func, tuple(_substitute(a, name, by) for a in e.args))
+
+
+def plan_linear(spec: AttentionSpec, chunk: int = 64) -> LinearPlan:
+    if spec.pattern is not Pattern.RECURRENT:
+        raise InputError("variant is not a recurrent-pattern variant", variant=spec.name)
+    spec.validate()
+    consts = spec.dims.const_env()
+    scale = diagonal_scale(spec.h_mod)
+    if scale is None:
+        raise UnsupportedError("h_mod does not factor as h times a per-step scale; only stepwise "
+                               "execution applies", h_mod=spec.h_mod.source)
+    extras = spec.extras_by_name()
+    factors: list = []
+
+    def flat(z):
+        if isinstance(z, H.BinOp) and z.op == "*":
+            flat(z.lhs)
+            flat(z.rhs)
+        else:
+            factors.append(z)
+
+    flat(scale)
+    const, names = 1.0, []
+    for f in factors:
+        c = H.const_value(f, consts)
+        if c is not None:
+            const *= c
+        elif isinstance(f, H.Name) and f.name in extras:
+            names.append(f.name)
+        else:
+            raise UnsupportedError("per-step scale is not a product of extras and constants",
+                                   factor=H.to_source(f))
+    k_gate = None
+    if spec.k_mod is not None:
+        e = spec.k_mod.expr
+        ok = False
+        if isinstance(e, H.BinOp) and e.op == "*":
+            for x, y in ((e.lhs, e.rhs), (e.rhs, e.lhs)):
+                if isinstance(x, H.Name) and x.name == "k" and isinstance(y, H.Name) \
+                        and y.name in extras:
+                    k_gate, ok = y.name, True
+        if not ok:
+            raise UnsupportedError("k_mod must be k * <per-step extra> on the linear template",
+                                   source=spec.k_mod.source)
+    if spec.v_mod is not None:
+        raise UnsupportedError("v_mod is not lowered on the linear template yet",
+                               source=spec.v_mod.source)
+    if spec.output_mod is not None:
+        raise UnsupportedError("output_mod is not lowered on the linear template yet",
+                               source=spec.output_mod.source)
+    q_scale = _scalar_mod(spec.q_mod, "q", consts)
+    return LinearPlan(spec, q_scale=q_scale, decay_factors=tuple(names), decay_const=const,
+                      k_gate=k_gate, chunk=chunk)
