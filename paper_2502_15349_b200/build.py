@@ -23,6 +23,7 @@ INCLUDE = PKG.parent / "include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+FLAGS += os.environ.get("AF_EXTRA_NVCC_FLAGS", "").split()  # developer ablations only
 
 
 def nvcc() -> str:

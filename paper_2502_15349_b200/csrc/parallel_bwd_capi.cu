@@ -21,7 +21,7 @@ int launch_bwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorM
     attr_done = true;
   }
   dim3 grid((d->seq_k + kBlockN - 1) / kBlockN, d->batch * d->heads_kv);
-  kern<<<grid, 320, L::kTotal, stream>>>(tq, tk, tv, tdo, p, lse2, delta, seq_q_pad);
+  kern<<<grid, 512, L::kTotal, stream>>>(tq, tk, tv, tdo, p, lse2, delta, seq_q_pad);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
 }
@@ -124,3 +124,9 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
   }
   return AF_OK;
 }
+
+#ifdef AF_TRACE
+extern "C" int af_debug_trace_read(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, af::g_af_trace, sizeof(af::g_af_trace)));
+}
+#endif
