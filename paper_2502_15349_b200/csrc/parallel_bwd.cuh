@@ -1,24 +1,25 @@
-// K2 — parallel-template backward on sm_100a.
+// K2 — parallel-template backward on sm_100a: two atomic-free kernels.
 //
 // Computes the VJP of K1 for a cotangent dO, i.e. what attnforge obtains by differentiating the
-// dense pattern graph (attention.derive_backward, attention.py:529-550, adjoint rules
+// dense pattern graph (attention.derive_backward, attention.py:529-550; adjoint rules
 // graph.py:481-569) — restated in closed form:
 //   softmax family     : P = exp(s - LSE), dV = P^T dO, dP = dO V^T, dS = P o (dP - D),
 //                        D_i = sum_d dO_id O_id
 //   elementwise family : P = act(z), dV = P^T dO, dP = dO V^T, dS = dP o act'(z) o mask
 //   both               : dQ = tau dS K, dK = tau dS^T Q   (tau = q_mod scale)
-// One CTA owns one 128-row key tile of one KV head and loops over every query head of its GQA
-// group and every query tile the band mask lets it see, so dK/dV accumulate in TMEM and need no
-// cross-CTA reduction.  dQ partial tiles are reduced into an fp32 accumulator in global memory.
 //
-// Warp roles (512 threads, <= 128 registers each):
-//   warps 0-7  : key-row warps, two per TMEM lane quarter; warp w owns key row (w%4)*32+lane and
-//                query columns [64*(w/4), 64*(w/4)+64): P^T, dS^T, then the dV (w<4) / dK store
-//   warps 8-11 : dQ drain (TMEM -> registers, release TMEM, fp32 red.add into dq_accum)
-//   warp  12   : TMA producer: K, V once; ring of (Q, dO, LSE, D) per query tile
-//   warp  13   : TMEM allocator + tcgen05.mma issuer            (warps 14-15 idle)
-// TMEM: [0,128) S^T -> P^T(bf16) | [128,256) dP^T -> dS^T(bf16) -> dQ | [256,256+DV) dV | dK
-// Packed bf16 P^T / dS^T of query columns [0,64) land in packed columns [0,32) of their region
+// K2a (key-tile stationary) accumulates dK, dV of one 128-row key tile in TMEM over every query
+// head of its GQA group and every visible query tile: S^T = K Q^T, dP^T = V dO^T (SS MMAs),
+// dV += P^T dO, dK += dS^T Q (A operand = packed bf16 P^T / dS^T straight from TMEM).
+// K2b (query-tile stationary) accumulates dQ of one 128-row query tile in TMEM over the visible key
+// tiles: S = Q K^T, dP = dO V^T, dQ += dS K, with Q and dO parked in TMEM as the A operands.
+// No cross-CTA reduction exists, so results are bitwise deterministic (the reference's own
+// determinism contract) at the price of recomputing S and dP in K2b.
+//
+// Both kernels: 320 threads.  warps 0-7 = row warps (two per TMEM lane quarter; warp w owns TMEM
+// lane (w%4)*32+lane and columns [64*(w/4), 64*(w/4)+64) of the 128-wide score tile), warp 8 =
+// TMA producer, warp 9 = TMEM allocator + single-thread tcgen05.mma issuer.
+// Packed bf16 P / dS of score columns [0,64) land in packed columns [0,32) of their TMEM region
 // and those of [64,128) in [64,96), so each warp only overwrites columns it alone has read.
 #pragma once
 #include <cuda.h>
@@ -28,39 +29,8 @@
 
 namespace af {
 
-#ifdef AF_TRACE
-// Developer timeline of one CTA (blockIdx 0,0): g_af_trace[event][iteration] = clock64().
-__device__ long long g_af_trace[16][512];
-#define AF_T(ev, n)                                                              \
-  do {                                                                           \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && (n) < 512) g_af_trace[ev][n] = clock64(); \
-  } while (0)
-#else
-#define AF_T(ev, n) \
-  do {              \
-  } while (0)
-#endif
-
-template <int D, int DV>
-struct BwdSmem {
-  static constexpr int kStages = 2;
-  static constexpr int kKBytes = kBlockN * D * 2;
-  static constexpr int kVBytes = kBlockN * DV * 2;
-  static constexpr int kQBytes = kBlockM * D * 2;
-  static constexpr int kOBytes = kBlockM * DV * 2;
-  static constexpr int kKOff = 0;
-  static constexpr int kVOff = kKOff + kKBytes;
-  static constexpr int kQOff = kVOff + kVBytes;
-  static constexpr int kOOff = kQOff + kStages * kQBytes;
-  static constexpr int kDSOff = kOOff + kStages * kOBytes;
-  static constexpr int kLseOff = kDSOff + kBlockM * kBlockN * 2;
-  static constexpr int kDeltaOff = kLseOff + kStages * kBlockM * 4;
-  static constexpr int kBarOff = kDeltaOff + kStages * kBlockM * 4;
-  // kv_full, full[2], empty[2], s_full, dp_full, p_ready, ds_ready, dq_full, dq_free, acc_full
-  static constexpr int kNumBars = 1 + 2 * kStages + 7;
-  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
-  static constexpr int kTotal = kTmemSlotOff + 16;
-};
+// packed (bf16x2) TMEM column of the k-th 16-wide K slice of a P / dS A operand
+AF_DEVICE uint32_t split_col(int kk) { return kk < 4 ? kk * 8 : 64 + (kk - 4) * 8; }
 
 // Query-row range a key tile [k0, k0+128) is visible from under the band mask.
 __host__ __device__ inline void query_band(const MaskParams& m, int k0, int seq_q, int& lo,
@@ -71,39 +41,90 @@ __host__ __device__ inline void query_band(const MaskParams& m, int k0, int seq_
   if (m.window > 0) hi = min(seq_q, k0 + kBlockN - 1 - m.diag_offset + m.window);
 }
 
-AF_DEVICE bool block_fully_kept_t(const MaskParams& m, int q0, int k0, int seq_q, int seq_k) {
+AF_DEVICE bool tile_fully_kept(const MaskParams& m, int q0, int k0, int seq_q, int seq_k) {
   if (q0 + kBlockM > seq_q) return false;
   return block_fully_kept(m, q0, k0, seq_k);
 }
 
-template <int kAct>
-AF_DEVICE float act_grad(float z, float a) {  // a = act(z)
-  if constexpr (kAct == kActSigmoid) {
-    return a * (1.0f - a);
-  } else if constexpr (kAct == kActRelu) {
-    return z >= 0.0f ? 1.0f : 0.0f;  // ties route to the first max operand (graph.py:517-527)
-  } else {
-    return 1.0f;
+AF_DEVICE float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+AF_DEVICE float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+template <int N>
+AF_DEVICE void store_row_bf16(__nv_bfloat16* dst, const uint32_t (&r)[N], float mul) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int v = 0; v < N / 8; ++v) {
+    uint4 w;
+    w.x = pack_bf16(__uint_as_float(r[v * 8 + 0]) * mul, __uint_as_float(r[v * 8 + 1]) * mul);
+    w.y = pack_bf16(__uint_as_float(r[v * 8 + 2]) * mul, __uint_as_float(r[v * 8 + 3]) * mul);
+    w.z = pack_bf16(__uint_as_float(r[v * 8 + 4]) * mul, __uint_as_float(r[v * 8 + 5]) * mul);
+    w.w = pack_bf16(__uint_as_float(r[v * 8 + 6]) * mul, __uint_as_float(r[v * 8 + 7]) * mul);
+    d4[v] = w;
   }
 }
 
+// dS from packed P and fp32 dP for 32 columns (both families)
+template <int kFamily, int kAct, bool kRowDelta>
+AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float* del_col,
+                       float del_row, uint32_t gmask, uint32_t* dsk) {
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    const uint32_t w = pk[e / 2];
+    const float p0 = bf16_lo(w), p1 = bf16_hi(w);
+    const float dp0 = __uint_as_float(dr[e]), dp1 = __uint_as_float(dr[e + 1]);
+    float ds0, ds1;
+    if constexpr (kFamily == kFamilySoftmax) {
+      ds0 = p0 * (dp0 - (kRowDelta ? del_row : del_col[e]));
+      ds1 = p1 * (dp1 - (kRowDelta ? del_row : del_col[e + 1]));
+    } else if constexpr (kAct == kActSigmoid) {
+      ds0 = dp0 * p0 * (1.0f - p0);
+      ds1 = dp1 * p1 * (1.0f - p1);
+    } else {
+      ds0 = ((gmask >> e) & 1u) ? dp0 : 0.0f;
+      ds1 = ((gmask >> (e + 1)) & 1u) ? dp1 : 0.0f;
+    }
+    dsk[e / 2] = pack_bf16(ds0, ds1);
+  }
+}
+
+// ═══════════════════════════════ K2a: dK, dV ═══════════════════════════════
+
+template <int D, int DV>
+struct BwdKVSmem {
+  static constexpr int kStages = 2;
+  static constexpr int kKBytes = kBlockN * D * 2;
+  static constexpr int kVBytes = kBlockN * DV * 2;
+  static constexpr int kQBytes = kBlockM * D * 2;
+  static constexpr int kOBytes = kBlockM * DV * 2;
+  static constexpr int kKOff = 0;
+  static constexpr int kVOff = kKOff + kKBytes;
+  static constexpr int kQOff = kVOff + kVBytes;
+  static constexpr int kOOff = kQOff + kStages * kQBytes;
+  static constexpr int kLseOff = kOOff + kStages * kOBytes;
+  static constexpr int kDeltaOff = kLseOff + kStages * kBlockM * 4;
+  static constexpr int kBarOff = kDeltaOff + kStages * kBlockM * 4;
+  // kv_full, full[S], empty[S], s_full, dp_full, p_ready, ds_ready, acc_full
+  static constexpr int kNumBars = 1 + 2 * kStages + 5;
+  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
+  static constexpr int kTotal = kTmemSlotOff + 16;
+};
+
 template <int D, int DV, int kFamily, int kAct>
-__global__ void __launch_bounds__(512, 1)
-    parallel_bwd_kernel(const __grid_constant__ CUtensorMap tm_q,
-                        const __grid_constant__ CUtensorMap tm_k,
-                        const __grid_constant__ CUtensorMap tm_v,
-                        const __grid_constant__ CUtensorMap tm_do, const ParallelBwdParams p,
-                        const float* __restrict__ lse2, const float* __restrict__ delta,
-                        int seq_q_pad) {
-  using L = BwdSmem<D, DV>;
+__global__ void __launch_bounds__(320, 1)
+    parallel_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q,
+                             const __grid_constant__ CUtensorMap tm_k,
+                             const __grid_constant__ CUtensorMap tm_v,
+                             const __grid_constant__ CUtensorMap tm_do, const ParallelBwdParams p,
+                             const float* __restrict__ lse2, const float* __restrict__ delta,
+                             int seq_q_pad) {
+  using L = BwdKVSmem<D, DV>;
   constexpr int kStages = L::kStages;
   static_assert(D % 64 == 0 && DV % 64 == 0 && D + DV <= 256, "tile dims");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sK = smem + L::kKOff;
   uint8_t* sV = smem + L::kVOff;
   uint8_t* sQ = smem + L::kQOff;
-  uint8_t* sO = smem + L::kOOff;  // dO stages
-  uint8_t* sDS = smem + L::kDSOff;
+  uint8_t* sO = smem + L::kOOff;
   float* sLse = reinterpret_cast<float*>(smem + L::kLseOff);
   float* sDelta = reinterpret_cast<float*>(smem + L::kDeltaOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -114,9 +135,7 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* dp_full = s_full + 1;
   uint64_t* p_ready = dp_full + 1;
   uint64_t* ds_ready = p_ready + 1;
-  uint64_t* dq_full = ds_ready + 1;
-  uint64_t* dq_free = dq_full + 1;
-  uint64_t* acc_full = dq_free + 1;
+  uint64_t* acc_full = ds_ready + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -133,7 +152,7 @@ __global__ void __launch_bounds__(512, 1)
   const int tiles_per_head = qt_hi - qt_lo;
   const int niter = tiles_per_head * group;
 
-  if (warp == 12 && lane_id() == 0) {
+  if (warp == 8 && lane_id() == 0) {
     mbar_init(kv_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -143,21 +162,17 @@ __global__ void __launch_bounds__(512, 1)
     mbar_init(dp_full, 1);
     mbar_init(p_ready, 8);
     mbar_init(ds_ready, 8);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_free, 4);
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
-  if (warp == 13) tmem_alloc<512>(tmem_slot);
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + DV;
-  // packed (bf16x2) column of the k-th 16-query slice of P^T / dS^T
-  auto a_col = [](int kk) -> uint32_t { return kk < 4 ? kk * 8 : 64 + (kk - 4) * 8; };
 
-  if (warp == 12) {
+  if (warp == 8) {
     // ───────────── TMA producer ─────────────
     if (elect_one() && niter > 0) {
       mbar_expect_tx(kv_full, L::kKBytes + L::kVBytes);
@@ -165,13 +180,17 @@ __global__ void __launch_bounds__(512, 1)
         tma_load_4d(sK + c * (kBlockN * 128), &tm_k, kv_full, c * 64, k0, hk, b);
       for (int c = 0; c < DV / 64; ++c)
         tma_load_4d(sV + c * (kBlockN * 128), &tm_v, kv_full, c * 64, k0, hk, b);
+      int hi_ = 0, qt_ = 0;
       for (int n = 0; n < niter; ++n) {
         const int s = n % kStages;
         const uint32_t ph = (n / kStages) & 1;
-        const int h = hk * group + n / tiles_per_head;
-        const int q0 = (qt_lo + n % tiles_per_head) * kBlockM;
+        const int h = hk * group + hi_;
+        const int q0 = (qt_lo + qt_) * kBlockM;
+        if (++qt_ == tiles_per_head) {
+          qt_ = 0;
+          ++hi_;
+        }
         mbar_wait(&empty[s], ph ^ 1);
-        AF_T(10, n);
         mbar_expect_tx(&full[s], L::kQBytes + L::kOBytes + 2 * kBlockM * 4);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d_hint(sQ + s * L::kQBytes + c * (kBlockM * 128), &tm_q, &full[s], c * 64, q0,
@@ -192,18 +211,20 @@ __global__ void __launch_bounds__(512, 1)
             : "memory");
       }
     }
-  } else if (warp == 13) {
+  } else if (warp == 9) {
     // ───────────── MMA issuer ─────────────
     if (elect_one() && niter > 0) {
       constexpr uint32_t id_s = make_idesc_bf16(kBlockN, kBlockM, false, false);   // S^T = K Q^T
       constexpr uint32_t id_dp = make_idesc_bf16(kBlockN, kBlockM, false, false);  // dP^T = V dO^T
       constexpr uint32_t id_dv = make_idesc_bf16(kBlockN, DV, false, true);        // dV += P^T dO
       constexpr uint32_t id_dk = make_idesc_bf16(kBlockN, D, false, true);         // dK += dS^T Q
-      constexpr uint32_t id_dq = make_idesc_bf16(kBlockM, D, true, true);          // dQ = dS K
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), aQ = smem_u32(sQ), aO = smem_u32(sO);
-      const uint32_t aDS = smem_u32(sDS);
       auto kmajor = [](uint32_t base, int kk, int rows) {
         return make_sdesc(base + (kk / 4) * (rows * 128) + (kk % 4) * 32, 0, 1024);
+      };
+      auto wait_full = [&](int n) {
+        mbar_wait(&full[n % kStages], (n / kStages) & 1);
+        tc_fence_after();
       };
       auto issue_s = [&](int n) {
         const int s = n % kStages;
@@ -221,78 +242,48 @@ __global__ void __launch_bounds__(512, 1)
                  id_dp, kk > 0);
         mma_commit(dp_full);
       };
-      auto issue_dv = [&](int n) {  // dV += P^T dO  (A = P^T in TMEM, B = dO [q][dv] MN-major)
-        const int s = n % kStages;
-#pragma unroll
-        for (int kk = 0; kk < kBlockM / 16; ++kk)
-          mma_ts(tmem + kColDV, tmem + kColS + a_col(kk),
-                 make_sdesc(aO + s * L::kOBytes + kk * 16 * 128, kBlockM * 128, 1024), id_dv,
-                 (n > 0 || kk > 0));
-      };
-      auto wait_full = [&](int n) {
-        mbar_wait(&full[n % kStages], (n / kStages) & 1);
-        tc_fence_after();
-      };
-      // Issue order keeps the tensor pipe busy while the row warps and the dQ drain work:
-      //   S0 dP0 | dV0 S1 | dK0 dQ0 | dV1 dP1 S2 | dK1 dQ1 | dV2 dP2 S3 | ...
-      // TMEM reuse is safe because tcgen05.mma ops of one thread execute in issue order.
+      // S0 dP0 | dV0 S1 | dK0 dP1 | dV1 S2 | dK1 dP2 | ...   (in-order tcgen05 execution makes
+      // the TMEM reuse safe: S_{n+1} follows dV_n, which reads P^T_n; dP_{n+1} follows dK_n)
       mbar_wait(kv_full, 0);
       wait_full(0);
       issue_s(0);
       issue_dp(0);
-      mbar_wait(p_ready, 0);
-      tc_fence_after();
-      issue_dv(0);
-      if (niter > 1) {
-        wait_full(1);
-        issue_s(1);
-      }
       for (int n = 0; n < niter; ++n) {
         const int s = n % kStages;
-        // dK += dS^T Q ; dQ = dS K
-        mbar_wait(ds_ready, n & 1);
-        AF_T(0, n);
+        mbar_wait(p_ready, n & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kBlockM / 16; ++kk)
-          mma_ts(tmem + kColDK, tmem + kColDP + a_col(kk),
+          mma_ts(tmem + kColDV, tmem + kColS + split_col(kk),
+                 make_sdesc(aO + s * L::kOBytes + kk * 16 * 128, kBlockM * 128, 1024), id_dv,
+                 (n > 0 || kk > 0));
+        if (n + 1 < niter) {
+          wait_full(n + 1);
+          issue_s(n + 1);
+        }
+        mbar_wait(ds_ready, n & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kBlockM / 16; ++kk)
+          mma_ts(tmem + kColDK, tmem + kColDP + split_col(kk),
                  make_sdesc(aQ + s * L::kQBytes + kk * 16 * 128, kBlockM * 128, 1024), id_dk,
                  (n > 0 || kk > 0));
-#pragma unroll
-        for (int kk = 0; kk < kBlockN / 16; ++kk)
-          mma_ss(tmem + kColDP, make_sdesc(aDS + kk * 16 * 128, kBlockN * 128, 1024),
-                 make_sdesc(aK + kk * 16 * 128, kBlockN * 128, 1024), id_dq, kk > 0);
-        mma_commit(dq_full);
         mma_commit(&empty[s]);
-        if (n + 1 < niter) {
-          mbar_wait(p_ready, (n + 1) & 1);
-          AF_T(1, n + 1);
-          tc_fence_after();
-          issue_dv(n + 1);
-          mbar_wait(dq_free, n & 1);
-          AF_T(2, n + 1);
-          tc_fence_after();
-          issue_dp(n + 1);
-          if (n + 2 < niter) {
-            wait_full(n + 2);
-            AF_T(3, n + 2);
-            issue_s(n + 2);
-          }
-        }
+        if (n + 1 < niter) issue_dp(n + 1);
       }
       mma_commit(acc_full);
     }
-  } else if (warp < 8) {
+  } else {
     // ───────────── key-row warps ─────────────
     const int wq = warp % 4;
     const int half = warp / 4;
     const int row = wq * 32 + static_cast<int>(lane_id());
     const int j = k0 + row;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const int cb = half * 64;              // first query column owned by this warp
-    const uint32_t pcol = half * 64;       // packed destination column (see header)
+    const int cb = half * 64;
+    const uint32_t pcol = half * 64;
     const float fj = static_cast<float>(j);
-    int hi_ = 0, qt_ = 0;                  // (query head, query tile) of iteration n
+    int hi_ = 0, qt_ = 0;
     for (int n = 0; n < niter; ++n) {
       const int s = n % kStages;
       const int h = hk * group + hi_;
@@ -301,7 +292,7 @@ __global__ void __launch_bounds__(512, 1)
         qt_ = 0;
         ++hi_;
       }
-      const bool fullblk = block_fully_kept_t(p.mask, q0, k0, p.seq_q, p.seq_k);
+      const bool fullblk = tile_fully_kept(p.mask, q0, k0, p.seq_q, p.seq_k);
       float slope = 0.0f;
       if constexpr (kFamily == kFamilyElementwise) {
         if (p.slope != nullptr) slope = p.slope[h];
@@ -310,64 +301,69 @@ __global__ void __launch_bounds__(512, 1)
       const float* del_s = sDelta + s * kBlockM + cb;
 
       mbar_wait(s_full, n & 1);
-      if (threadIdx.x == 0) AF_T(4, n);
       tc_fence_after();
-      // P^T is kept as packed bf16 — exactly the operand the dV MMA consumes — and re-expanded
-      // for dS; this halves the live registers of the row warps.
       uint32_t pk[32];
-      uint32_t gmask[2];      // elementwise family: kept && act'(z) != 0 (relu / identity)
+      uint32_t gmask[2];
 #pragma unroll
       for (int c2 = 0; c2 < 2; ++c2) {
         uint32_t sr[32];
         tmem_ld32(tmem + lane_base + kColS + cb + c2 * 32, sr);
         tmem_ld_wait();
-        float pv[32];
         uint32_t bits = 0u;
         if constexpr (kFamily == kFamilySoftmax) {
           if (fullblk) {
 #pragma unroll
             for (int e = 0; e < 32; e += 4) {
               const float4 l4 = *reinterpret_cast<const float4*>(lse_s + c2 * 32 + e);
-              pv[e + 0] = ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x));
-              pv[e + 1] = ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y));
-              pv[e + 2] = ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z));
-              pv[e + 3] = ex2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w));
+              pk[c2 * 16 + e / 2] =
+                  pack_bf16(ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x)),
+                            ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y)));
+              pk[c2 * 16 + e / 2 + 1] =
+                  pack_bf16(ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z)),
+                            ex2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w)));
             }
           } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const int i = q0 + cb + c2 * 32 + e;
-              const bool keep = kept(p.mask, i, j, p.seq_k) && i < p.seq_q;
-              pv[e] = keep ? ex2(fmaf(__uint_as_float(sr[e]), p.scale_log2, -lse_s[c2 * 32 + e]))
-                           : 0.0f;
+            for (int e = 0; e < 32; e += 2) {
+              float pv[2];
+#pragma unroll
+              for (int x = 0; x < 2; ++x) {
+                const int i = q0 + cb + c2 * 32 + e + x;
+                const bool keep = kept(p.mask, i, j, p.seq_k) && i < p.seq_q;
+                pv[x] = keep ? ex2(fmaf(__uint_as_float(sr[e + x]), p.scale_log2,
+                                        -lse_s[c2 * 32 + e + x]))
+                             : 0.0f;
+              }
+              pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
             }
           }
         } else {
           const float zb = p.bias - slope * (static_cast<float>(q0 + cb + c2 * 32) - fj);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int i = q0 + cb + c2 * 32 + e;
-            const float z = fmaf(__uint_as_float(sr[e]), p.scale, zb - slope * static_cast<float>(e));
-            const bool keep = fullblk || (kept(p.mask, i, j, p.seq_k) && i < p.seq_q);
-            const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
-            bits |= (keep && g) ? (1u << e) : 0u;
-            pv[e] = keep ? apply_act<kAct>(z) : 0.0f;
+          for (int e = 0; e < 32; e += 2) {
+            float pv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              const int i = q0 + cb + c2 * 32 + e + x;
+              const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
+                                   zb - slope * static_cast<float>(e + x));
+              const bool keep = fullblk || (kept(p.mask, i, j, p.seq_k) && i < p.seq_q);
+              const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
+              bits |= (keep && g) ? (1u << (e + x)) : 0u;
+              pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
+            }
+            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
           }
         }
         gmask[c2] = bits;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) pk[c2 * 16 + e] = pack_bf16(pv[2 * e], pv[2 * e + 1]);
       }
       tmem_st32(tmem + lane_base + kColS + pcol, pk);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(p_ready);
-      if (threadIdx.x == 0) AF_T(5, n);
 
-      // dS^T = P^T o (dP^T - D)   |   dP^T o act'(z)
       mbar_wait(dp_full, n & 1);
-      if (threadIdx.x == 0) AF_T(6, n);
       tc_fence_after();
       uint32_t dsk[32];
 #pragma unroll
@@ -375,58 +371,20 @@ __global__ void __launch_bounds__(512, 1)
         uint32_t dr[32];
         tmem_ld32(tmem + lane_base + kColDP + cb + c2 * 32, dr);
         tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; e += 4) {
-          const float p0 = __uint_as_float(pk[c2 * 16 + e / 2] << 16);
-          const float p1 = __uint_as_float(pk[c2 * 16 + e / 2] & 0xFFFF0000u);
-          const float p2 = __uint_as_float(pk[c2 * 16 + e / 2 + 1] << 16);
-          const float p3 = __uint_as_float(pk[c2 * 16 + e / 2 + 1] & 0xFFFF0000u);
-          float ds[4];
-          if constexpr (kFamily == kFamilySoftmax) {
-            const float4 d4 = *reinterpret_cast<const float4*>(del_s + c2 * 32 + e);
-            ds[0] = p0 * (__uint_as_float(dr[e + 0]) - d4.x);
-            ds[1] = p1 * (__uint_as_float(dr[e + 1]) - d4.y);
-            ds[2] = p2 * (__uint_as_float(dr[e + 2]) - d4.z);
-            ds[3] = p3 * (__uint_as_float(dr[e + 3]) - d4.w);
-          } else if constexpr (kAct == kActSigmoid) {
-            ds[0] = __uint_as_float(dr[e + 0]) * p0 * (1.0f - p0);
-            ds[1] = __uint_as_float(dr[e + 1]) * p1 * (1.0f - p1);
-            ds[2] = __uint_as_float(dr[e + 2]) * p2 * (1.0f - p2);
-            ds[3] = __uint_as_float(dr[e + 3]) * p3 * (1.0f - p3);
-          } else {
-#pragma unroll
-            for (int x = 0; x < 4; ++x)
-              ds[x] = ((gmask[c2] >> (e + x)) & 1u) ? __uint_as_float(dr[e + x]) : 0.0f;
-          }
-          dsk[c2 * 16 + e / 2] = pack_bf16(ds[0], ds[1]);
-          dsk[c2 * 16 + e / 2 + 1] = pack_bf16(ds[2], ds[3]);
-        }
+        make_ds<kFamily, kAct, false>(pk + c2 * 16, dr, del_s + c2 * 32, 0.0f, gmask[c2],
+                                      dsk + c2 * 16);
       }
-      // dS^T into TMEM (A operand of dK) ...
       tmem_st32(tmem + lane_base + kColDP + pcol, dsk);
-      // ... and into shared memory as the MN-major A operand of dQ = dS K: query chunk `half`
-      // is [128 key rows][128 B] with 16-byte granules XOR-swizzled by (row % 8).
-      if (n > 0) mbar_wait(dq_full, (n - 1) & 1);  // dQ_{n-1} finished reading sDS
-      {
-        uint8_t* base = sDS + half * (kBlockN * 128) + row * 128;
-#pragma unroll
-        for (int g = 0; g < 8; ++g)
-          *reinterpret_cast<uint4*>(base + ((g ^ (row & 7)) * 16)) =
-              make_uint4(dsk[g * 4 + 0], dsk[g * 4 + 1], dsk[g * 4 + 2], dsk[g * 4 + 3]);
-      }
-      fence_proxy_async_smem();
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(ds_ready);
-      if (threadIdx.x == 0) AF_T(7, n);
     }
-    // ───────────── epilogue: warps 0-3 store dV, warps 4-7 store dK ─────────────
+    // ───────────── epilogue: warps 0-3 store dV rows, warps 4-7 store dK rows ─────────────
     if (niter > 0) {
       mbar_wait(acc_full, 0);
       tc_fence_after();
     }
-    // Every lane runs the warp-collective TMEM loads; only rows inside seq_k store.
     const bool live = j < p.seq_k;
     const int ncol = half == 0 ? DV : D;
     const uint32_t col0 = half == 0 ? kColDV : kColDK;
@@ -446,75 +404,309 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) r[e] = 0u;
       }
-      if (live) {
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(r[v * 8 + 0]) * mul, __uint_as_float(r[v * 8 + 1]) * mul);
-          w.y = pack_bf16(__uint_as_float(r[v * 8 + 2]) * mul, __uint_as_float(r[v * 8 + 3]) * mul);
-          w.z = pack_bf16(__uint_as_float(r[v * 8 + 4]) * mul, __uint_as_float(r[v * 8 + 5]) * mul);
-          w.w = pack_bf16(__uint_as_float(r[v * 8 + 6]) * mul, __uint_as_float(r[v * 8 + 7]) * mul);
-          d4[v] = w;
-        }
-      }
-    }
-  } else if (warp < 12) {
-    // ───────────── dQ drain warps 8-11 ─────────────
-    const int wq = warp % 4;
-    const int row = wq * 32 + static_cast<int>(lane_id());
-    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    for (int n = 0; n < niter; ++n) {
-      const int h = hk * group + n / tiles_per_head;
-      const int q0 = (qt_lo + n % tiles_per_head) * kBlockM;
-      mbar_wait(dq_full, n & 1);
-      if (threadIdx.x == 256) AF_T(8, n);
-      tc_fence_after();
-      float* dst = p.dq_accum + ((static_cast<int64_t>(b) * p.heads_q + h) * seq_q_pad + q0 + row) * D;
-      // Pull the tile out of TMEM in two 64-column halves; TMEM is released after the second
-      // half lands, and the reductions of both halves are issued from registers.
-      uint32_t r0[D / 2];
-#pragma unroll
-      for (int c = 0; c < D / 64; ++c)
-        tmem_ld32(tmem + lane_base + kColDP + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&r0[c * 32]));
-      tmem_ld_wait();
-#ifndef AF_ABLATE_DQ_RED
-#pragma unroll
-      for (int v = 0; v < D / 8; ++v)
-        atomicAdd(reinterpret_cast<float4*>(dst + v * 4),
-                  make_float4(__uint_as_float(r0[v * 4]), __uint_as_float(r0[v * 4 + 1]),
-                              __uint_as_float(r0[v * 4 + 2]), __uint_as_float(r0[v * 4 + 3])));
-#endif
-#pragma unroll
-      for (int c = 0; c < D / 64; ++c)
-        tmem_ld32(tmem + lane_base + kColDP + D / 2 + c * 32,
-                  *reinterpret_cast<uint32_t(*)[32]>(&r0[c * 32]));
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(dq_free);
-      if (threadIdx.x == 256) AF_T(9, n);
-#ifndef AF_ABLATE_DQ_RED
-#pragma unroll
-      for (int v = 0; v < D / 8; ++v)
-        atomicAdd(reinterpret_cast<float4*>(dst + D / 2 + v * 4),
-                  make_float4(__uint_as_float(r0[v * 4]), __uint_as_float(r0[v * 4 + 1]),
-                              __uint_as_float(r0[v * 4 + 2]), __uint_as_float(r0[v * 4 + 3])));
-#else
-      if (r0[0] == 0x7fffffffu) dst[0] = 1.0f;  // keep the loads live
-#endif
+      if (live) store_row_bf16<32>(dst + c * 32, r, mul);
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 13) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
 }
 
-// delta[b,h,i] = sum_d dO*O ; lse2 = LSE * log2(e) (padded rows: +inf -> P = 0, delta = 0)
+// ═══════════════════════════════ K2b: dQ ═══════════════════════════════
+
+template <int D, int DV>
+struct BwdQSmem {
+  static constexpr int kStages = 3;
+  static constexpr int kKBytes = kBlockN * D * 2;
+  static constexpr int kVBytes = kBlockN * DV * 2;
+  static constexpr int kKOff = 0;
+  static constexpr int kVOff = kKOff + kStages * kKBytes;
+  static constexpr int kBarOff = kVOff + kStages * kVBytes;
+  // full[S], empty[S], qa_ready, s_full, dp_full, ds_ready, acc_full
+  static constexpr int kNumBars = 2 * kStages + 5;
+  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
+  static constexpr int kTotal = kTmemSlotOff + 16;
+};
+
+// Load `W` packed bf16 words of one row (W*2 elements starting at src) into registers.
+template <int W>
+AF_DEVICE void load_row_words(const __nv_bfloat16* src, bool live, uint32_t (&w)[W]) {
+#pragma unroll
+  for (int v = 0; v < W / 4; ++v) {
+    const uint4 x = live ? *reinterpret_cast<const uint4*>(src + v * 8) : make_uint4(0, 0, 0, 0);
+    w[v * 4 + 0] = x.x;
+    w[v * 4 + 1] = x.y;
+    w[v * 4 + 2] = x.z;
+    w[v * 4 + 3] = x.w;
+  }
+}
+
+template <int D, int DV, int kFamily, int kAct>
+__global__ void __launch_bounds__(320, 1)
+    parallel_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_k,
+                           const __grid_constant__ CUtensorMap tm_v, const ParallelBwdParams p,
+                           const __nv_bfloat16* __restrict__ q,
+                           const __nv_bfloat16* __restrict__ dout, int64_t q_sb, int64_t q_sh,
+                           int64_t q_ss, int64_t do_sb, int64_t do_sh, int64_t do_ss,
+                           void* __restrict__ dq, const float* __restrict__ lse2,
+                           const float* __restrict__ delta, int seq_q_pad) {
+  using L = BwdQSmem<D, DV>;
+  constexpr int kStages = L::kStages;
+  static_assert(D % 64 == 0 && DV % 64 == 0 && D <= 128 && DV <= 128, "tile dims");
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sK = smem + L::kKOff;
+  uint8_t* sV = smem + L::kVOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStages;
+  uint64_t* qa_ready = empty + kStages;
+  uint64_t* s_full = qa_ready + 1;
+  uint64_t* dp_full = s_full + 1;
+  uint64_t* ds_ready = dp_full + 1;
+  uint64_t* acc_full = ds_ready + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
+
+  const int warp = static_cast<int>(warp_id());
+  const int q_tiles = (p.seq_q + kBlockM - 1) / kBlockM;
+  const int qt = p.mask.causal ? (q_tiles - 1 - static_cast<int>(blockIdx.x))
+                               : static_cast<int>(blockIdx.x);
+  const int bh = blockIdx.y;
+  const int b = bh / p.heads_q;
+  const int h = bh % p.heads_q;
+  const int hk = h / (p.heads_q / p.heads_kv);
+  const int q0 = qt * kBlockM;
+  const TileBand band = key_band(p.mask, q0, min(p.seq_q, q0 + kBlockM), p.seq_k);
+  const int nk = band.jb_hi - band.jb_lo;
+
+  if (warp == 8 && lane_id() == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(qa_ready, 8);
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(ds_ready, 8);
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // S [0,128) | dP [128,256) | dQ [256,256+D) | Q^A [384,384+D/2) | dO^A [448,448+DV/2)
+  constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColQA = 384, kColOA = 448;
+
+  if (warp == 8) {
+    // ───────────── TMA producer: K/V ring ─────────────
+    if (elect_one() && nk > 0) {
+      for (int n = 0; n < nk; ++n) {
+        const int s = n % kStages;
+        const uint32_t ph = (n / kStages) & 1;
+        const int kv0 = (band.jb_lo + n) * kBlockN;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], L::kKBytes + L::kVBytes);
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_4d_hint(sK + s * L::kKBytes + c * (kBlockN * 128), &tm_k, &full[s], c * 64,
+                           kv0, hk, b, kEvictLast);
+        for (int c = 0; c < DV / 64; ++c)
+          tma_load_4d_hint(sV + s * L::kVBytes + c * (kBlockN * 128), &tm_v, &full[s], c * 64,
+                           kv0, hk, b, kEvictLast);
+      }
+    }
+  } else if (warp == 9) {
+    // ───────────── MMA issuer ─────────────
+    if (elect_one() && nk > 0) {
+      constexpr uint32_t id_s = make_idesc_bf16(kBlockM, kBlockN, false, false);  // S = Q K^T
+      constexpr uint32_t id_dp = make_idesc_bf16(kBlockM, kBlockN, false, false); // dP = dO V^T
+      constexpr uint32_t id_dq = make_idesc_bf16(kBlockM, D, false, true);        // dQ += dS K
+      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
+      auto kmajor = [](uint32_t base, int kk, int rows) {
+        return make_sdesc(base + (kk / 4) * (rows * 128) + (kk % 4) * 32, 0, 1024);
+      };
+      auto issue_sdp = [&](int n) {
+        const int s = n % kStages;
+        mbar_wait(&full[s], (n / kStages) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ts(tmem + kColS, tmem + kColQA + kk * 8, kmajor(aK + s * L::kKBytes, kk, kBlockN),
+                 id_s, kk > 0);
+        mma_commit(s_full);
+#pragma unroll
+        for (int kk = 0; kk < DV / 16; ++kk)
+          mma_ts(tmem + kColDP, tmem + kColOA + kk * 8, kmajor(aV + s * L::kVBytes, kk, kBlockN),
+                 id_dp, kk > 0);
+        mma_commit(dp_full);
+      };
+      // S0 dP0 | dQ0 S1 dP1 | dQ1 S2 dP2 | ...  (S_{n+1} follows dQ_n, which reads dS_n)
+      mbar_wait(qa_ready, 0);
+      tc_fence_after();
+      issue_sdp(0);
+      for (int n = 0; n < nk; ++n) {
+        const int s = n % kStages;
+        mbar_wait(ds_ready, n & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kBlockN / 16; ++kk)
+          mma_ts(tmem + kColDQ, tmem + kColS + split_col(kk),
+                 make_sdesc(aK + s * L::kKBytes + kk * 16 * 128, kBlockN * 128, 1024), id_dq,
+                 (n > 0 || kk > 0));
+        mma_commit(&empty[s]);
+        if (n + 1 < nk) issue_sdp(n + 1);
+      }
+      mma_commit(acc_full);
+    }
+  } else {
+    // ───────────── query-row warps ─────────────
+    const int wq = warp % 4;
+    const int half = warp / 4;
+    const int row = wq * 32 + static_cast<int>(lane_id());
+    const int i = q0 + row;
+    const bool live = i < p.seq_q;
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const int cb = half * 64;
+    const uint32_t pcol = half * 64;
+    // Park this row's Q and dO (bf16) in TMEM as the K-major A operands: warp half h writes the
+    // packed words [h*D/4, (h+1)*D/4) of Q^A and [h*DV/4, ...) of dO^A.
+    {
+      const __nv_bfloat16* qrow =
+          q + b * q_sb + h * q_sh + static_cast<int64_t>(live ? i : 0) * q_ss + half * (D / 2);
+      const __nv_bfloat16* orow = dout + b * do_sb + h * do_sh +
+                                  static_cast<int64_t>(live ? i : 0) * do_ss + half * (DV / 2);
+      if constexpr (D == 128) {
+        uint32_t w[32];
+        load_row_words<32>(qrow, live, w);
+        tmem_st32(tmem + lane_base + kColQA + half * 32, w);
+      } else {
+        uint32_t w[16];
+        load_row_words<16>(qrow, live, w);
+        tmem_st16(tmem + lane_base + kColQA + half * 16, w);
+      }
+      if constexpr (DV == 128) {
+        uint32_t w[32];
+        load_row_words<32>(orow, live, w);
+        tmem_st32(tmem + lane_base + kColOA + half * 32, w);
+      } else {
+        uint32_t w[16];
+        load_row_words<16>(orow, live, w);
+        tmem_st16(tmem + lane_base + kColOA + half * 16, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(qa_ready);
+    }
+    const int64_t srow = (static_cast<int64_t>(b) * p.heads_q + h) * seq_q_pad + (live ? i : q0);
+    const float l2 = live ? lse2[srow] : INFINITY;  // +inf -> P = 0
+    const float dl = live ? delta[srow] : 0.0f;
+    float slope = 0.0f;
+    if constexpr (kFamily == kFamilyElementwise) {
+      if (p.slope != nullptr) slope = p.slope[h];
+    }
+    const float fi = static_cast<float>(i);
+    for (int n = 0; n < nk; ++n) {
+      const int c0 = (band.jb_lo + n) * kBlockN;
+      const bool fullblk = tile_fully_kept(p.mask, q0, c0, p.seq_q, p.seq_k);
+      mbar_wait(s_full, n & 1);
+      tc_fence_after();
+      uint32_t pk[32];
+      uint32_t gmask[2];
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        uint32_t sr[32];
+        tmem_ld32(tmem + lane_base + kColS + cb + c2 * 32, sr);
+        tmem_ld_wait();
+        uint32_t bits = 0u;
+        const int jb = c0 + cb + c2 * 32;
+        if constexpr (kFamily == kFamilySoftmax) {
+          if (fullblk) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 2)
+              pk[c2 * 16 + e / 2] =
+                  pack_bf16(ex2(fmaf(__uint_as_float(sr[e]), p.scale_log2, -l2)),
+                            ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l2)));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              const bool a0 = kept(p.mask, i, jb + e, p.seq_k);
+              const bool a1 = kept(p.mask, i, jb + e + 1, p.seq_k);
+              pk[c2 * 16 + e / 2] =
+                  pack_bf16(a0 ? ex2(fmaf(__uint_as_float(sr[e]), p.scale_log2, -l2)) : 0.0f,
+                            a1 ? ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l2)) : 0.0f);
+            }
+          }
+        } else {
+          const float zb = p.bias - slope * (fi - static_cast<float>(jb));
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float pv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
+                                   zb + slope * static_cast<float>(e + x));
+              const bool keep = live && (fullblk || kept(p.mask, i, jb + e + x, p.seq_k));
+              const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
+              bits |= (keep && g) ? (1u << (e + x)) : 0u;
+              pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
+            }
+            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+          }
+        }
+        gmask[c2] = bits;
+      }
+      mbar_wait(dp_full, n & 1);
+      tc_fence_after();
+      uint32_t dsk[32];
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        uint32_t dr[32];
+        tmem_ld32(tmem + lane_base + kColDP + cb + c2 * 32, dr);
+        tmem_ld_wait();
+        make_ds<kFamily, kAct, true>(pk + c2 * 16, dr, nullptr, dl, gmask[c2], dsk + c2 * 16);
+      }
+      // dS (packed) over this warp's own S columns: A operand of dQ += dS K
+      tmem_st32(tmem + lane_base + kColS + pcol, dsk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(ds_ready);
+    }
+    // ───────────── epilogue: dQ = tau * acc (bf16); each warp stores D/2 columns ─────────────
+    if (nk > 0) {
+      mbar_wait(acc_full, 0);
+      tc_fence_after();
+    }
+    __nv_bfloat16* dqrow = reinterpret_cast<__nv_bfloat16*>(dq) + b * q_sb + h * q_sh +
+                           static_cast<int64_t>(live ? i : 0) * q_ss + half * (D / 2);
+#pragma unroll 1
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t r[32];
+      if (nk > 0) {
+        tmem_ld32(tmem + lane_base + kColDQ + half * (D / 2) + c * 32, r);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) r[e] = 0u;
+      }
+      if (live) store_row_bf16<32>(dqrow + c * 32, r, p.scale);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// delta[b,h,i] = sum_d dO*O ; lse2 = LSE * log2(e) (padded / fully-masked rows: +inf -> P = 0)
 template <int DV>
 __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
                                       const __nv_bfloat16* __restrict__ dout,
@@ -526,9 +718,9 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
   // one warp per query row
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
+  if (gw >= total_rows) return;
   const int64_t bh = gw / seq_q_pad;
   const int i = static_cast<int>(gw % seq_q_pad);
-  if (gw >= total_rows) return;
   const int b = static_cast<int>(bh / heads), h = static_cast<int>(bh % heads);
   float acc = 0.0f;
   if (i < seq_q && family == kFamilySoftmax) {
@@ -537,43 +729,21 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
     for (int c = lane * 2; c < DV; c += 64) {
       const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(orow + c);
       const __nv_bfloat162 d = *reinterpret_cast<const __nv_bfloat162*>(drow + c);
-      acc += __bfloat162float(a.x) * __bfloat162float(d.x) + __bfloat162float(a.y) * __bfloat162float(d.y);
+      acc += __bfloat162float(a.x) * __bfloat162float(d.x) +
+             __bfloat162float(a.y) * __bfloat162float(d.y);
     }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) {
-    const int64_t idx = bh * seq_q_pad + i;
-    delta[idx] = acc;
+    delta[gw] = acc;
     float l = INFINITY;
     if (i < seq_q && family == kFamilySoftmax) {
       const float v = lse[(static_cast<int64_t>(b) * heads + h) * seq_q + i];
       l = (v == -INFINITY) ? INFINITY : v * kLog2e;  // fully-masked row: P = 0
     }
-    lse2[idx] = l;
+    lse2[gw] = l;
   }
-}
-
-// dq (bf16) = tau * dq_accum
-template <int D>
-__global__ void bwd_dq_convert_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dq,
-                                      int64_t sb, int64_t sh, int64_t ss, int heads, int seq_q,
-                                      int seq_q_pad, float tau, int64_t total_rows) {
-  const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t rowi = gt / (D / 8);
-  const int c = static_cast<int>(gt % (D / 8)) * 8;
-  if (rowi >= total_rows) return;
-  const int64_t bh = rowi / seq_q;
-  const int i = static_cast<int>(rowi % seq_q);
-  const int b = static_cast<int>(bh / heads), h = static_cast<int>(bh % heads);
-  const float4* src = reinterpret_cast<const float4*>(acc + (bh * seq_q_pad + i) * D + c);
-  const float4 x = src[0], y = src[1];
-  uint4 w;
-  w.x = pack_bf16(x.x * tau, x.y * tau);
-  w.y = pack_bf16(x.z * tau, x.w * tau);
-  w.z = pack_bf16(y.x * tau, y.y * tau);
-  w.w = pack_bf16(y.z * tau, y.w * tau);
-  *reinterpret_cast<uint4*>(dq + b * sb + h * sh + static_cast<int64_t>(i) * ss + c) = w;
 }
 
 }  // namespace af
