@@ -294,13 +294,13 @@ def run_gpu(args) -> None:
             "fwd_tflops": FWD_FLOPS / (fwd_ms * 1e-3) / 1e12, "bwd_tflops": bwd_tf,
             "e2e": {"value": world * STEP_FLOPS / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            "roofline": {"kernel": "K2 parallel backward (af_parallel_bwd: main kernel + row-stat "
-                                   "preprocess + dQ convert)",
+            "roofline": {"kernel": "K2 parallel backward (af_parallel_bwd: K2a dK/dV + K2b dQ + "
+                                   "row-stat preprocess)",
                          "bound": "tensor", "achieved": bwd_tf, "peak": pk["tflops_sustained"],
                          "unit": "TFLOP/s", "frac": bwd_tf / pk["tflops_sustained"],
                          "traffic": traffic,
                          "peak_source": f"{pk['source']} bf16_tflops_sustained"},
-            "gpu_launches": args.steps * 4,
+            "gpu_launches": args.steps * 4,  # K1 + preprocess + K2a + K2b per step
             "clocks": clk.summary(),
         }
         if cpu is not None:
