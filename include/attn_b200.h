@@ -67,26 +67,38 @@ int af_parallel_bwd(const af_parallel_desc* desc, const void* q, const void* k, 
                     void* dv, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- linear / recurrent template (attention.py:455-511, engine.py:525-616) ---- */
+/* Per-step tensors are fp32 with element strides [b, h, s] (0 = broadcast).  The h_mod of the
+ * variant factors as h * a_t (attention.diagonal_scale, attention.py:332-369) with
+ *   a_t = exp(log_decay_const) * prod_f decay_factor[f][b, h, t]          (n_decay_factors <= 2)
+ * and k_mod = k * key_gate[b, h, t] (key_gate may be NULL). */
 typedef struct af_linear_desc {
   int32_t batch, heads, seq, d_k, d_v;
-  int32_t chunk;             /* chunk length of the intra/inter decomposition (64) */
+  int32_t chunk;             /* chunk length of the intra/inter decomposition (128) */
   float q_scale;             /* q_mod scale (e.g. 1/sqrt(d_k)); 1 when absent       */
-  /* element strides [b, h, s, d] of q, k, v, o */
+  /* element strides [b, h, s, d] of q, k, v, o (o also describes dout / dq layouts) */
   int64_t q_stride[4], k_stride[4], v_stride[4], o_stride[4];
+  float log_decay_const;
+  int32_t n_decay_factors;
+  const float* decay_factor[2];
+  int64_t decay_factor_stride[2][3];
+  const float* key_gate;
+  int64_t key_gate_stride[3];
 } af_linear_desc;
 
-/* o_t = q_t h_t,  h_t = a_t h_{t-1} + k_t^T v_t  with log a_t = log_decay[b,h,t] (fp32 [B,H,S]).
- * k is the already-modified key (k_mod applied).  final_state (fp32 [B,H,Dk,Dv]) may be NULL.
- * Replaces engine.run_chunk_recurrent (engine.py:554). */
+/* o_t = q_scale * q_t h_t,  h_t = a_t h_{t-1} + (k_t * gate_t)^T v_t,  h_0 = 0.
+ * final_state must be NULL (reserved).  Replaces engine.run_chunk_recurrent (engine.py:554). */
 int af_linear_fwd(const af_linear_desc* desc, const void* q, const void* k, const void* v,
-                  const float* log_decay, void* o, float* final_state, void* stream);
+                  void* o, float* final_state, void* stream);
 
 size_t af_linear_bwd_workspace(const af_linear_desc* desc);
 
-/* VJP of af_linear_fwd for cotangent dO: dq, dk, dv (bf16) and d log_decay (fp32 [B,H,S]). */
+/* VJP of af_linear_fwd for cotangent dout: dq, dk (w.r.t. the raw k), dv (bf16, q/k/v strides)
+ * and, when non-NULL, d_decay_factor[f] / d_key_gate (fp32, ACCUMULATED with the strides of the
+ * corresponding input — zero them first; broadcast axes sum).  Replaces engine.autodiff_grads
+ * over RecurrenceDef.unroll (attention.py:468). */
 int af_linear_bwd(const af_linear_desc* desc, const void* q, const void* k, const void* v,
-                  const float* log_decay, const void* dout, void* dq, void* dk, void* dv,
-                  float* dlog_decay, void* workspace, size_t workspace_bytes, void* stream);
+                  const void* dout, void* dq, void* dk, void* dv, float* const* d_decay_factor,
+                  float* d_key_gate, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- MLA decode (softmax over a shared latent cache; V = first d_v columns of K) ---- */
 typedef struct af_mla_desc {

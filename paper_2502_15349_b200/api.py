@@ -179,119 +179,110 @@ def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tens
 
 # ───────────────────────────── recurrent template ─────────────────────────────
 
-def _linear_desc(plan: LinearPlan, q, k, v, o) -> rt.LinearDesc:
+def _step_tensor(arrays: dict, name: str, d) -> torch.Tensor:
+    t = _need(arrays, name)
+    if t.dim() != 4 or t.shape[2] != d.seq_k or t.shape[3] != 1:
+        raise ShapeError("per-step extra must be [B|1, H|1, seq, 1]", name=name,
+                         got=tuple(t.shape))
+    return t.to(torch.float32).contiguous()
+
+
+def _linear_desc(plan: LinearPlan, arrays: dict, q, k, v, o):
+    """Descriptor + the fp32 per-step tensors it points to (kept alive by the caller)."""
     d = plan.spec.dims
     c = rt.LinearDesc()
     c.batch, c.heads, c.seq, c.d_k, c.d_v = d.batch, d.heads, d.seq_q, d.d_qk, d.d_v
-    c.chunk = plan.chunk
+    c.chunk = 128
     c.q_scale = float(plan.q_scale)
     c.q_stride, c.k_stride, c.v_stride, c.o_stride = (rt.strides4(q), rt.strides4(k),
                                                       rt.strides4(v), rt.strides4(o))
-    return c
+    if plan.decay_const <= 0:
+        raise UnsupportedError("per-step decay constant must be positive", value=plan.decay_const)
+    c.log_decay_const = math.log(plan.decay_const)
+    keep = {}
+    if len(plan.decay_factors) > 2:
+        raise UnsupportedError("at most two per-step decay factors", n=len(plan.decay_factors))
+    c.n_decay_factors = len(plan.decay_factors)
+    for f, name in enumerate(plan.decay_factors):
+        t = keep.setdefault(name, _step_tensor(arrays, name, d))
+        c.decay_factor[f] = t.data_ptr()
+        c.decay_factor_stride[f] = rt.step_strides(t)
+    if plan.k_gate is not None:
+        t = keep.setdefault(plan.k_gate, _step_tensor(arrays, plan.k_gate, d))
+        c.key_gate = t.data_ptr()
+        c.key_gate_stride = rt.step_strides(t)
+    return c, keep
 
 
-def _per_step(arrays: dict, name: str, d) -> torch.Tensor:
-    t = _need(arrays, name).to(torch.float32)
-    return t.expand(d.batch, d.heads, d.seq_k, 1)
-
-
-def linear_log_decay(plan: LinearPlan, arrays: dict) -> torch.Tensor:
-    """log a_t as an fp32 [B, H, S] tensor (product of the h_mod factors, attention.py:332)."""
-    d = plan.spec.dims
-    dev = _need(arrays, "q").device
-    out = torch.full((d.batch, d.heads, d.seq_k), math.log(plan.decay_const)
-                     if plan.decay_const > 0 else -math.inf, device=dev, dtype=torch.float32)
-    for name in plan.decay_factors:
-        out = out + torch.log(_per_step(arrays, name, d)[..., 0])
-    return out.contiguous()
-
-
-def _linear_inputs(plan: LinearPlan, arrays: dict):
+def _linear_qkv(plan: LinearPlan, arrays: dict):
     d = plan.spec.dims
     q, k, v = _need(arrays, "q"), _need(arrays, "k"), _need(arrays, "v")
     _check_shape(q, (d.batch, d.heads, d.seq_q, d.d_qk), "q")
     _check_shape(k, (d.batch, d.heads, d.seq_k, d.d_qk), "k")
     _check_shape(v, (d.batch, d.heads, d.seq_k, d.d_v), "v")
-    km = k
-    if plan.k_gate is not None:
-        km = k.to(torch.float32) * _per_step(arrays, plan.k_gate, d)
-    return _as(q, _BF16), _as(km, _BF16), _as(v, _BF16)
+    return _as(q, _BF16), _as(k, _BF16), _as(v, _BF16)
 
 
-def linear_forward(spec, arrays: dict, chunk: int = 64, *, check_nan: bool = False):
-    """Chunked linear template forward → O [B,H,S,Dv] (bf16)."""
+def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = False):
+    """Chunked linear template forward (K4) → O [B,H,S,Dv] bf16.  The decay factors of h_mod
+    and the k_mod gate are applied inside the kernel."""
     spec = _spec(spec)
     plan = plan_linear(spec, chunk)
-    q, km, v = _linear_inputs(plan, arrays)
-    logd = linear_log_decay(plan, arrays)
+    q, k, v = _linear_qkv(plan, arrays)
     d = spec.dims
     o = torch.empty(d.batch, d.heads, d.seq_q, d.d_v, device=q.device, dtype=_BF16)
-    desc = _linear_desc(plan, q, km, v, o)
-    rt.check(rt.lib().af_linear_fwd(desc, q.data_ptr(), km.data_ptr(), v.data_ptr(),
-                                    logd.data_ptr(), o.data_ptr(), None, _stream()),
-             "af_linear_fwd")
+    desc, _keep = _linear_desc(plan, arrays, q, k, v, o)
+    rt.check(rt.lib().af_linear_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                    o.data_ptr(), None, _stream()), "af_linear_fwd")
     if check_nan:
         _check_nan(o, "chunk")
     return o
 
 
 def run_chunk_recurrent(spec, arrays: dict, chunk: int = 64):
-    """Drop-in for ``engine.run_chunk_recurrent`` (engine.py:554)."""
+    """Drop-in for ``engine.run_chunk_recurrent`` (engine.py:554).  The kernel's own chunk (128)
+    replaces ``chunk`` (chunked ≡ stepwise for any chunking, test_engine.py:208-221)."""
     if chunk < 1:
         raise InputError("chunk must be positive", chunk=chunk)
-    return linear_forward(spec, arrays, 64, check_nan=True)
+    return linear_forward(spec, arrays, check_nan=True)
 
 
 def run_step_recurrent(spec, arrays: dict):
-    """Drop-in for ``engine.run_step_recurrent`` (engine.py:525); chunked ≡ stepwise
-    (test_engine.py:208-221)."""
-    return linear_forward(spec, arrays, 64, check_nan=True)
+    """Drop-in for ``engine.run_step_recurrent`` (engine.py:525)."""
+    return linear_forward(spec, arrays, check_nan=True)
 
 
-def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 64) -> dict:
-    """VJP of ``linear_forward``: grads for q, k, v and each differentiable extra of a_t / k_mod."""
+def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 128) -> dict:
+    """VJP of ``linear_forward`` (K5): grads for q, k, v and every differentiable extra that
+    enters a_t or k_mod (accumulated in-kernel with the extra's broadcast shape)."""
     spec = _spec(spec)
     plan = plan_linear(spec, chunk)
-    q, km, v = _linear_inputs(plan, arrays)
-    logd = linear_log_decay(plan, arrays)
+    q, k, v = (t.contiguous() for t in _linear_qkv(plan, arrays))
     d = spec.dims
     dout = _as(dout, _BF16).contiguous()
-    dq, dkm, dv = torch.empty_like(q), torch.empty_like(km), torch.empty_like(v)
-    dlogd = torch.empty_like(logd)
-    o = torch.empty(d.batch, d.heads, d.seq_q, d.d_v, device=q.device, dtype=_BF16)
-    desc = _linear_desc(plan, q, km, v, o)
+    _check_shape(dout, (d.batch, d.heads, d.seq_q, d.d_v), "dout")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    # dout / dq use the o / q stride slots of the descriptor (all contiguous here)
+    desc, keep = _linear_desc(plan, arrays, q, k, v, dout)
+    extras = spec.extras_by_name()
+    grads_x = {name: torch.zeros(t.shape, device=q.device, dtype=torch.float32)
+               for name, t in keep.items() if extras[name].differentiable}
+    dfac = (rt.C.c_void_p * 2)()
+    for f, name in enumerate(plan.decay_factors):
+        if name in grads_x:
+            dfac[f] = grads_x[name].data_ptr()
+    dgate = grads_x.get(plan.k_gate) if plan.k_gate is not None else None
     L = rt.lib()
     ws_n = L.af_linear_bwd_workspace(desc)
     ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
-    rt.check(L.af_linear_bwd(desc, q.data_ptr(), km.data_ptr(), v.data_ptr(), logd.data_ptr(),
-                             dout.data_ptr(), dq.data_ptr(), dkm.data_ptr(), dv.data_ptr(),
-                             dlogd.data_ptr(), ws.data_ptr(), ws_n, _stream()), "af_linear_bwd")
-    grads = {"q": dq, "v": dv}
-    k = _need(arrays, "k")
-    if plan.k_gate is not None:
-        gate = _per_step(arrays, plan.k_gate, d)
-        grads["k"] = (dkm.float() * gate).to(_BF16)
-    else:
-        grads["k"] = dkm
-    # chain d log a_t and d k_mod into the differentiable extras (SURVEY A.4)
-    for e in spec.extra_inputs:
-        if not e.differentiable:
-            continue
-        g = torch.zeros(d.batch, d.heads, d.seq_k, device=q.device, dtype=torch.float32)
-        t = _per_step(arrays, e.name, d)[..., 0]
-        n_occ = plan.decay_factors.count(e.name)
-        if n_occ:
-            g = g + n_occ * dlogd / t
-        if plan.k_gate == e.name:
-            g = g + (dkm.float() * k.float()).sum(-1)
-        want = _need(arrays, e.name).shape
-        grads[e.name] = _sum_to(g.unsqueeze(-1), want)
+    rt.check(L.af_linear_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
+                             dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                             rt.C.cast(dfac, rt.C.c_void_p), rt.ptr(dgate), ws.data_ptr(), ws_n,
+                             _stream()), "af_linear_bwd")
+    grads = {"q": dq, "k": dk, "v": dv}
+    for name, g in grads_x.items():
+        grads[name] = g.reshape(_need(arrays, name).shape)
     return grads
-
-
-def _sum_to(g: torch.Tensor, shape) -> torch.Tensor:
-    dims = [i for i, (a, b) in enumerate(zip(g.shape, shape)) if b == 1 and a != 1]
-    return g.sum(dim=dims, keepdim=True) if dims else g
 
 
 # ───────────────────────────── autodiff entry point ─────────────────────────────

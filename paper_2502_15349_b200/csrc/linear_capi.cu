@@ -1,0 +1,201 @@
+// C-ABI entry points of the linear (recurrent) template: K4 forward and the K5 backward built from
+// three runs of the same chunked kernel plus the per-step gradient scan for the decay factors.
+#include "host_common.h"
+#include "linear_chunk.cuh"
+
+namespace af {
+namespace {
+
+struct LaArgs {
+  const void* q;
+  const void* k;
+  const void* v;
+  const int64_t* q_st;
+  const int64_t* k_st;
+  const int64_t* v_st;
+  int dqk, dvv;  // query/key dim, value dim of this run
+  void* o;
+  const int64_t* o_st;
+  float out_scale;
+  bool u_gate;       // key/value side scaled by the key gate
+  bool row_gate;     // output rows scaled by the key gate
+  const void* dot_x;
+  const int64_t* x_st;
+  float* dot;
+  bool reverse;
+};
+
+StepTensor step_tensor(const float* ptr, const int64_t* st) {
+  StepTensor t{};
+  t.ptr = ptr;
+  if (ptr != nullptr) {
+    t.sb = st[0];
+    t.sh = st[1];
+    t.ss = st[2];
+  }
+  return t;
+}
+
+LinearParams base_params(const af_linear_desc* d) {
+  LinearParams p{};
+  p.batch = d->batch;
+  p.heads = d->heads;
+  p.seq = d->seq;
+  p.log_const = d->log_decay_const;
+  p.nfac = d->n_decay_factors;
+  for (int f = 0; f < d->n_decay_factors; ++f)
+    p.fac[f] = step_tensor(d->decay_factor[f], d->decay_factor_stride[f]);
+  return p;
+}
+
+template <int DK, bool kRev>
+int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
+  using L = LinSmem<DK>;
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_4d(&tq, a.q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.dqk, d->seq, d->heads,
+                    d->batch, a.q_st, 64, kLinChunk, true) ||
+      !make_tmap_4d(&tk, a.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.dqk, d->seq, d->heads,
+                    d->batch, a.k_st, 64, kLinChunk, true) ||
+      !make_tmap_4d(&tv, a.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.dvv, d->seq, d->heads,
+                    d->batch, a.v_st, 64, kLinChunk, true))
+    return AF_ERR_INPUT;
+  LinearParams p = base_params(d);
+  p.dqk = a.dqk;
+  p.dv = a.dvv;
+  p.out_scale = a.out_scale;
+  if (a.u_gate) p.u_scale = step_tensor(d->key_gate, d->key_gate_stride);
+  if (a.row_gate) p.o_rowscale = step_tensor(d->key_gate, d->key_gate_stride);
+  p.o = a.o;
+  p.o_sb = a.o_st[0];
+  p.o_sh = a.o_st[1];
+  p.o_ss = a.o_st[2];
+  p.dot_x = a.dot_x;
+  if (a.dot_x != nullptr) {
+    p.x_sb = a.x_st[0];
+    p.x_sh = a.x_st[1];
+    p.x_ss = a.x_st[2];
+  }
+  p.dot = a.dot;
+  auto kern = linear_chunk_kernel<DK, kRev>;
+  static bool attr = false;
+  if (!attr) {
+    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
+    attr = true;
+  }
+  dim3 grid(d->batch * d->heads * (a.dvv / kLinVB));
+  kern<<<grid, 320, L::kTotal, s>>>(tq, tk, tv, p);
+  AF_CUDA_CHECK(cudaGetLastError());
+  return AF_OK;
+}
+
+int run_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
+  if (a.dvv % kLinVB != 0) {
+    set_error("linear template: value dim %d is not a multiple of %d", a.dvv, kLinVB);
+    return AF_ERR_UNSUPPORTED;
+  }
+  if (a.dqk == 128) return a.reverse ? launch_la<128, true>(d, a, s) : launch_la<128, false>(d, a, s);
+  if (a.dqk == 256) return a.reverse ? launch_la<256, true>(d, a, s) : launch_la<256, false>(d, a, s);
+  set_error("linear template: key dim %d not instantiated (128, 256)", a.dqk);
+  return AF_ERR_UNSUPPORTED;
+}
+
+int validate_linear(const af_linear_desc* d) {
+  AF_REQUIRE(d != nullptr, AF_ERR_INPUT, "null descriptor");
+  AF_REQUIRE(d->batch >= 1 && d->heads >= 1 && d->seq >= 1 && d->d_k >= 1 && d->d_v >= 1,
+             AF_ERR_INPUT, "dims must be >= 1");
+  AF_REQUIRE(d->n_decay_factors >= 0 && d->n_decay_factors <= 2, AF_ERR_UNSUPPORTED,
+             "at most two per-step decay factors are supported (got %d)", d->n_decay_factors);
+  AF_REQUIRE(d->q_stride[3] == 1 && d->k_stride[3] == 1 && d->v_stride[3] == 1 &&
+                 d->o_stride[3] == 1,
+             AF_ERR_INPUT, "feature stride must be 1");
+  return AF_OK;
+}
+
+}  // namespace
+}  // namespace af
+
+extern "C" int af_linear_fwd(const af_linear_desc* d, const void* q, const void* k, const void* v,
+                             void* o, float* final_state, void* stream) {
+  using namespace af;
+  int st = validate_linear(d);
+  if (st != AF_OK) return st;
+  AF_REQUIRE(final_state == nullptr, AF_ERR_UNSUPPORTED, "final_state output is not built yet");
+  LaArgs a{q, k, v, d->q_stride, d->k_stride, d->v_stride, d->d_k, d->d_v, o, d->o_stride,
+           d->q_scale, true, false, nullptr, nullptr, nullptr, false};
+  return run_la(d, a, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" size_t af_linear_bwd_workspace(const af_linear_desc* d) {
+  if (d == nullptr) return 0;
+  const size_t rows = static_cast<size_t>(d->batch) * d->heads * d->seq;
+  size_t bytes = rows * 2 * sizeof(float);
+  if (d->key_gate != nullptr) bytes += rows * static_cast<size_t>(d->d_k) * 2;  // bf16 Km
+  return bytes;
+}
+
+extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void* k, const void* v,
+                             const void* dout, void* dq, void* dk, void* dv,
+                             float* const* d_decay_factor, float* d_key_gate, void* workspace,
+                             size_t workspace_bytes, void* stream) {
+  using namespace af;
+  int st = validate_linear(d);
+  if (st != AF_OK) return st;
+  AF_REQUIRE(workspace_bytes >= af_linear_bwd_workspace(d), AF_ERR_INPUT, "workspace too small");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t n = static_cast<int64_t>(d->batch) * d->heads * d->seq;
+  float* dq_dot = static_cast<float*>(workspace);
+  float* dk_dot = dq_dot + n;
+  AF_CUDA_CHECK(cudaMemsetAsync(workspace, 0, static_cast<size_t>(2 * n) * sizeof(float), s));
+  // Gated keys, materialised once (see gate_keys_kernel)
+  const void* km = k;
+  const int64_t* km_st = d->k_stride;
+  int64_t km_contig[4] = {static_cast<int64_t>(d->heads) * d->seq * d->d_k,
+                          static_cast<int64_t>(d->seq) * d->d_k, d->d_k, 1};
+  if (d->key_gate != nullptr) {
+    __nv_bfloat16* kmb = reinterpret_cast<__nv_bfloat16*>(dk_dot + n);
+    const int64_t thr = n * (d->d_k / 8);
+    gate_keys_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(k), d->k_stride[0], d->k_stride[1], d->k_stride[2],
+        step_tensor(d->key_gate, d->key_gate_stride), d->heads, d->seq, d->d_k, kmb, n);
+    AF_CUDA_CHECK(cudaGetLastError());
+    km = kmb;
+    km_st = km_contig;
+  }
+  // dq = q_scale * LA_fwd(q=dO, k=V, v=Km)                 dq_dot = q . dq   (= Qm . dQm)
+  LaArgs a1{dout, v, km, d->o_stride, d->v_stride, km_st, d->d_v, d->d_k, dq, d->q_stride,
+            d->q_scale, false, false, q, d->q_stride, dq_dot, false};
+  if ((st = run_la(d, a1, s)) != AF_OK) return st;
+  // dKm = q_scale * LA_rev(q=V, k=dO, v=Q); dk = gate*dKm   dk_dot = Km . dKm
+  LaArgs a2{v, dout, q, d->v_stride, d->o_stride, d->q_stride, d->d_v, d->d_k, dk, d->k_stride,
+            d->q_scale, false, true, km, km_st, dk_dot, true};
+  if ((st = run_la(d, a2, s)) != AF_OK) return st;
+  // dV = q_scale * LA_rev(q=Km, k=Q, v=dO)
+  LaArgs a3{km, q, dout, km_st, d->q_stride, d->o_stride, d->d_k, d->d_v, dv, d->v_stride,
+            d->q_scale, false, false, nullptr, nullptr, nullptr, true};
+  if ((st = run_la(d, a3, s)) != AF_OK) return st;
+  const bool want_fac = d_decay_factor != nullptr &&
+                        ((d->n_decay_factors > 0 && d_decay_factor[0] != nullptr) ||
+                         (d->n_decay_factors > 1 && d_decay_factor[1] != nullptr));
+  if (want_fac || d_key_gate != nullptr) {
+    LinearParams p = base_params(d);
+    p.u_scale = step_tensor(d->key_gate, d->key_gate_stride);
+    StepTensor f0{}, f1{}, g{};
+    if (d_decay_factor != nullptr && d->n_decay_factors > 0)
+      f0 = step_tensor(d_decay_factor[0], d->decay_factor_stride[0]);
+    if (d_decay_factor != nullptr && d->n_decay_factors > 1)
+      f1 = step_tensor(d_decay_factor[1], d->decay_factor_stride[1]);
+    if (d_key_gate != nullptr) {
+      AF_REQUIRE(d->key_gate != nullptr, AF_ERR_INPUT, "d_key_gate without a key gate");
+      g = step_tensor(d_key_gate, d->key_gate_stride);
+    }
+    linear_step_grads_kernel<<<d->batch * d->heads, 256, 0, s>>>(dq_dot, dk_dot, p, f0, f1, g);
+    AF_CUDA_CHECK(cudaGetLastError());
+  }
+  return AF_OK;
+}
+
+#ifdef AF_TRACE
+extern "C" int af_debug_lin_trace_read(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, af::g_lin_trace, sizeof(af::g_lin_trace)));
+}
+#endif

@@ -1,0 +1,502 @@
+// K4 — linear (recurrent) template on sm_100a: chunked linear attention with a carried state.
+//
+// Computes, per (b, h) and per 64-wide block of the value dimension,
+//   forward : o_t = s_out * sum_{u<=t} e^{L_t - L_u} (q_t . k_u) v_u
+//   reverse : o_t = s_out * sum_{u>=t} e^{L_u - L_t} (q_t . k_u) v_u
+// with L the inclusive cumsum of log a_t — the recurrence h_t = a_t h_{t-1} + k_t^T v_t,
+// o_t = q_t h_t of attnforge `engine.run_step_recurrent` (engine.py:525-551), evaluated the way
+// `engine.run_chunk_recurrent` does (engine.py:554-616): per chunk of C = 128 tokens,
+//   O_c   = ((Q K^T) o D) V + (Q o cp) H_in        D[i,u] = e^{l_i - l_u} [u <= i]
+//   H_out = g H_in + (K o w)^T V                    cp_i = e^{l_i}, w_u = e^{l_{C-1} - l_u}, g = e^{l_{C-1}}
+// (l = in-chunk inclusive cumsum; the reverse direction swaps the roles, see below).  The
+// backward of the template is three more runs of this kernel (restated):
+//   dQm = LA_fwd(q=dO, k=V, v=Km),  dKm = LA_rev(q=V, k=dO, v=Qm),  dV = LA_rev(q=Km, k=Qm, v=dO),
+//   d log a_t = sum_{s>=t} (Qm_s . dQm_s - Km_s . dKm_s)
+// — the optional `dot` output accumulates X_t . o_t (fp32) for that last line.
+//
+// One CTA owns one (b, h, value block) and walks the chunks in order (reverse: last to first),
+// carrying the [DK x 64] fp32 state in TMEM.  Warps 0-7: two per chunk row (= TMEM lane), each
+// owning one half of the columns (scan of log a, decay weights, P = S o D, state rescale, bf16
+// state copy, output epilogue); warp 8: TMA producer; warp 9: TMEM allocator + MMA issuer.
+// TMEM: S [0,128) (packed P) | OI [128,192) | QH x2 [192,320) | H [320, 320+64*DK/128)
+// MMAs (all M=128): S = Q K^T (SS), QH = Q Hb (SS, Hb = bf16 state copy in smem), OI = P V (TS),
+// H += K^T Vw (SS, K^T read MN-major straight from the K tile, Vw = diag(w) V).
+#pragma once
+#include <cuda.h>
+#include "params.h"
+#include "sm100.cuh"
+
+namespace af {
+
+#ifdef AF_TRACE
+// Developer timeline of CTA 0: g_lin_trace[event][chunk] = clock64().
+__device__ long long g_lin_trace[16][128];
+#define AF_LT(ev, n)                                                                  \
+  do {                                                                                \
+    if (blockIdx.x == 0 && (n) < 128) g_lin_trace[ev][n] = clock64();                 \
+  } while (0)
+#else
+#define AF_LT(ev, n) \
+  do {               \
+  } while (0)
+#endif
+
+constexpr int kLinChunk = 128;
+constexpr int kLinVB = 64;  // value columns per CTA
+
+// Per-step fp32 tensor with element strides [b, h, s] (0 = broadcast axis).
+struct StepTensor {
+  const float* ptr;
+  int64_t sb, sh, ss;
+  AF_DEVICE float at(int b, int h, int t) const { return ptr[b * sb + h * sh + t * ss]; }
+};
+
+struct LinearParams {
+  int batch, heads, seq, dqk, dv;
+  float out_scale;
+  // log a_t = log_const + sum_f log(fac[f][b, h, t])
+  float log_const;
+  int nfac;
+  StepTensor fac[2];
+  StepTensor u_scale;    // per-token scale of the key/value side (k_mod = k * gate); ptr may be null
+  StepTensor o_rowscale; // per-token scale of the output rows (not of `dot`); ptr may be null
+  void* o;              // bf16 output with element strides
+  int64_t o_sb, o_sh, o_ss;
+  const void* dot_x;    // optional bf16 X with element strides: dot[t] += X_t . o_t
+  int64_t x_sb, x_sh, x_ss;
+  float* dot;           // [B, H, S] fp32 (accumulated across value blocks)
+};
+
+template <int DK>
+struct LinSmem {
+  static constexpr int kStages = DK == 128 ? 2 : 1;  // Q/K/V ring depth (smem bound at DK=256)
+  static constexpr int kQBytes = kLinChunk * DK * 2;
+  static constexpr int kVBytes = kLinChunk * kLinVB * 2;
+  static constexpr int kQOff = 0;
+  static constexpr int kKOff = kQOff + kStages * kQBytes;
+  static constexpr int kVOff = kKOff + kStages * kQBytes;
+  static constexpr int kVwOff = kVOff + kStages * kVBytes;
+  static constexpr int kHbOff = kVwOff + kVBytes;
+  static constexpr int kLOff = kHbOff + DK * kLinVB * 2;
+  static constexpr int kUOff = kLOff + kLinChunk * 4;
+  static constexpr int kScanOff = kUOff + kLinChunk * 4;
+  // ring: full[S], empty[S]; then s_full qh_full oi_full h_full | p_ready vw_ready h_scaled hb_ready
+  static constexpr int kBarOff = kScanOff + 64;
+  static constexpr int kNumBars = 2 * kStages + 8;
+  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
+  static constexpr int kTotal = kTmemSlotOff + 16;
+};
+
+constexpr float kLog2e_ = 1.4426950408889634f;
+
+// packed (bf16x2) TMEM column of the k-th 16-key slice of P (key halves [0,64) -> [0,32),
+// [64,128) -> [64,96): each row-warp half only overwrites S columns it alone has read)
+AF_DEVICE uint32_t split_col_lin(int kk) { return kk < 4 ? kk * 8 : 64 + (kk - 4) * 8; }
+
+// 128-byte-row swizzled tile helpers ([rows][64 bf16], 16-byte granule g of row r stored at
+// granule g ^ (r % 8) — the layout TMA SWIZZLE_128B produces and UMMA descriptors expect).
+AF_DEVICE uint4* swz_row(uint8_t* base, int r, int g) {
+  return reinterpret_cast<uint4*>(base + r * 128 + ((g ^ (r & 7)) << 4));
+}
+
+template <int DK, bool kReverse>
+__global__ void __launch_bounds__(320, 1)
+    linear_chunk_kernel(const __grid_constant__ CUtensorMap tm_q,
+                        const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const LinearParams p) {
+  using L = LinSmem<DK>;
+  static_assert(DK == 128 || DK == 256, "DK");
+  constexpr int kHalves = DK / 128;
+  constexpr int kStages = L::kStages;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ = smem + L::kQOff;
+  uint8_t* sK = smem + L::kKOff;
+  uint8_t* sV = smem + L::kVOff;
+  uint8_t* sVw = smem + L::kVwOff;
+  uint8_t* sHb = smem + L::kHbOff;
+  float* sL = reinterpret_cast<float*>(smem + L::kLOff);   // in-chunk cumsum of log2 a
+  float* sU = reinterpret_cast<float*>(smem + L::kUOff);   // key/value-side scale
+  float* sScan = reinterpret_cast<float*>(smem + L::kScanOff);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* full = bars;                 // Q, K, V of one chunk landed (one tx barrier)
+  uint64_t* empty = bars + kStages;      // the chunk's Q, K, V may be overwritten
+  uint64_t* s_full = bars + 2 * kStages;
+  uint64_t* qh_full = s_full + 1;
+  uint64_t* oi_full = s_full + 2;
+  uint64_t* h_full = s_full + 3;
+  uint64_t* p_ready = s_full + 4;
+  uint64_t* vw_ready = s_full + 5;
+  uint64_t* h_scaled = s_full + 6;
+  uint64_t* hb_ready = s_full + 7;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
+
+  const int warp = static_cast<int>(warp_id());
+  const int nvb = p.dv / kLinVB;
+  const int vb = blockIdx.x % nvb;
+  const int bh = blockIdx.x / nvb;
+  const int b = bh / p.heads;
+  const int h = bh % p.heads;
+  const int nchunks = (p.seq + kLinChunk - 1) / kLinChunk;
+
+  if (warp == 8 && lane_id() == 0) {
+    for (int i = 0; i < 2 * kStages + 4; ++i) mbar_init(&bars[i], 1);
+    for (int i = 2 * kStages + 4; i < L::kNumBars; ++i) mbar_init(&bars[i], 8);
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp < 8) {  // zero the bf16 state copy: chunk 0 multiplies Q by H_in = 0
+    for (int i = threadIdx.x; i < DK * kLinVB * 2 / 16; i += 256)
+      reinterpret_cast<uint4*>(sHb)[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // S [0,128) | OI [128,192) | QH x2 [192,320) | H [320, 320 + 64*DK/128)
+  constexpr uint32_t kColS = 0, kColOI = 128, kColQH = 192, kColH = 320;
+
+  if (warp == 8) {
+    // ───────────── TMA producer ─────────────
+    if (elect_one()) {
+      for (int n = 0; n < nchunks; ++n) {
+        const int c = kReverse ? nchunks - 1 - n : n;
+        const int t0 = c * kLinChunk;
+        const int st = n % kStages;
+        mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
+        mbar_expect_tx(&full[st], 2 * L::kQBytes + L::kVBytes);
+        for (int x = 0; x < DK / 64; ++x) {
+          tma_load_4d(sQ + st * L::kQBytes + x * (kLinChunk * 128), &tm_q, &full[st], x * 64, t0,
+                      h, b);
+          tma_load_4d(sK + st * L::kQBytes + x * (kLinChunk * 128), &tm_k, &full[st], x * 64, t0,
+                      h, b);
+        }
+        tma_load_4d(sV + st * L::kVBytes, &tm_v, &full[st], vb * kLinVB, t0, h, b);
+      }
+    }
+  } else if (warp == 9) {
+    // ───────────── MMA issuer:  S | QH | H update | OI ─────────────
+    if (elect_one()) {
+      constexpr uint32_t id_s = make_idesc_bf16(128, 128, false, false);     // S = Q K^T
+      constexpr uint32_t id_qh = make_idesc_bf16(128, kLinVB, false, true);  // QH = Q Hb
+      constexpr uint32_t id_oi = make_idesc_bf16(128, kLinVB, false, true);  // OI = P V
+      constexpr uint32_t id_h = make_idesc_bf16(128, kLinVB, true, true);    // H += K^T Vw
+      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV);
+      const uint32_t aVw = smem_u32(sVw), aHb = smem_u32(sHb);
+      auto kmaj = [](uint32_t base, int kk) {
+        return make_sdesc(base + (kk / 4) * (kLinChunk * 128) + (kk % 4) * 32, 0, 1024);
+      };
+      for (int n = 0; n < nchunks; ++n) {
+        const uint32_t ph = n & 1;
+        const int st = n % kStages;
+        const uint32_t qa = aQ + st * L::kQBytes, ka = aK + st * L::kQBytes;
+        const uint32_t va = aV + st * L::kVBytes;
+        mbar_wait(&full[st], (n / kStages) & 1);
+        AF_LT(0, n);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DK / 16; ++kk)
+          mma_ss(tmem + kColS, kmaj(qa, kk), kmaj(ka, kk), id_s, kk > 0);
+        mma_commit(s_full);
+        if (n > 0) mbar_wait(hb_ready, (n - 1) & 1);
+        AF_LT(1, n);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DK / 16; ++kk)
+          mma_ss(tmem + kColQH + ph * kLinVB, kmaj(qa, kk),
+                 make_sdesc(aHb + kk * 2048, 16384, 1024), id_qh, kk > 0);
+        mma_commit(qh_full);
+        mbar_wait(vw_ready, ph);
+        mbar_wait(h_scaled, ph);
+        AF_LT(3, n);
+        tc_fence_after();
+#pragma unroll
+        for (int hh = 0; hh < kHalves; ++hh)
+#pragma unroll
+          for (int kk = 0; kk < kLinChunk / 16; ++kk)
+            mma_ss(tmem + kColH + hh * kLinVB,
+                   make_sdesc(ka + hh * 2 * (kLinChunk * 128) + kk * 2048, kLinChunk * 128, 1024),
+                   make_sdesc(aVw + kk * 2048, 16384, 1024), id_h, (n > 0 || kk > 0));
+        mma_commit(h_full);
+        mbar_wait(p_ready, ph);
+        AF_LT(2, n);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kLinChunk / 16; ++kk)
+          mma_ts(tmem + kColOI, tmem + kColS + split_col_lin(kk),
+                 make_sdesc(va + kk * 2048, 16384, 1024), id_oi, kk > 0);
+        mma_commit(oi_full);
+        mma_commit(&empty[st]);
+      }
+    }
+  } else {
+    // ───────────── chunk-row warps: two per TMEM lane quarter, column halves ─────────────
+    const int wq = warp % 4;
+    const int half = warp / 4;
+    const int r = wq * 32 + static_cast<int>(lane_id());
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    // log2 a of this row for chunk n (prefetched one chunk ahead; rows past seq: a = 1)
+    auto load_x = [&](int n) -> float2 {
+      const int c = kReverse ? nchunks - 1 - n : n;
+      const int t = c * kLinChunk + r;
+      float x = 0.0f, us = 1.0f;
+      if (n < nchunks && t < p.seq) {
+        x = p.log_const * kLog2e_;
+        for (int f = 0; f < p.nfac; ++f) x += __log2f(p.fac[f].at(b, h, t));
+        if (p.u_scale.ptr != nullptr) us = p.u_scale.at(b, h, t);
+      }
+      return make_float2(x, us);
+    };
+    float2 nxt = half == 0 ? load_x(0) : make_float2(0.0f, 1.0f);
+    for (int n = 0; n < nchunks; ++n) {
+      const int c = kReverse ? nchunks - 1 - n : n;
+      const int t = c * kLinChunk + r;
+      const uint32_t ph = n & 1;
+      const int st = n % kStages;
+      const bool live = t < p.seq;
+      // every row warp is done reading sL / sU of the previous chunk
+      if (n > 0) named_bar_sync(3, 256);
+      // (a) in-chunk inclusive cumsum of log2 a (warps of half 0; shared through smem)
+      if (half == 0) {
+        float x = nxt.x;
+        const float us = nxt.y;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float y = __shfl_up_sync(0xffffffffu, x, off);
+          if (static_cast<int>(lane_id()) >= off) x += y;
+        }
+        if (lane_id() == 31) sScan[wq] = x;
+        named_bar_sync(1, 128);
+        float pre = 0.0f;
+        for (int w = 0; w < wq; ++w) pre += sScan[w];
+        sL[r] = x + pre;
+        sU[r] = us;
+        nxt = load_x(n + 1);  // prefetch the next chunk's decay factors
+      }
+      named_bar_sync(2, 256);
+      const float l_r = sL[r];
+      const float l_last = sL[kLinChunk - 1];
+      const float g = exp2f(l_last);
+      const float cp = kReverse ? exp2f(l_last - l_r) : exp2f(l_r);
+      const float wgt = sU[r] * (kReverse ? exp2f(l_r) : exp2f(l_last - l_r));
+      if (threadIdx.x == 0) AF_LT(4, n);
+      // (b) Vw = diag(w * u_scale) V (this half's 4 granules; the previous state update is done)
+      mbar_wait(&full[st], (n / kStages) & 1);
+#pragma unroll
+      for (int gq = 0; gq < 4; ++gq) {
+        const int gidx = half * 4 + gq;
+        uint4 vv = *swz_row(sV + st * L::kVBytes, r, gidx);
+        uint32_t* e = reinterpret_cast<uint32_t*>(&vv);
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2)
+          e[q2] = pack_bf16(bf16_lo_(e[q2]) * wgt, bf16_hi_(e[q2]) * wgt);
+        *swz_row(sVw, r, gidx) = vv;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(vw_ready);
+      if (threadIdx.x == 0) AF_LT(5, n);
+      // (d) H <- g H for this half's 32 of every 64 state columns (chunk 0: the update MMA
+      //     overwrites instead of accumulating)
+      if (n > 0) {
+#pragma unroll
+        for (int hh = 0; hh < kHalves; ++hh) {
+          uint32_t hr[32];
+          const uint32_t col = tmem + lane_base + kColH + hh * kLinVB + half * 32;
+          tmem_ld32(col, hr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) hr[e] = __float_as_uint(__uint_as_float(hr[e]) * g);
+          tmem_st32(col, hr);
+        }
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(h_scaled);
+      if (threadIdx.x == 0) AF_LT(6, n);
+      // (c) P = S o D o u_scale over this half's 64 key columns
+      mbar_wait(s_full, ph);
+      if (threadIdx.x == 0) AF_LT(7, n);
+      tc_fence_after();
+      {
+        uint32_t pk[32];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          uint32_t sr[32];
+          tmem_ld32(tmem + lane_base + kColS + half * 64 + cc * 32, sr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const int u = half * 64 + cc * 32 + e;
+            const float4 l4 = *reinterpret_cast<const float4*>(sL + u);
+            const float4 u4 = *reinterpret_cast<const float4*>(sU + u);
+            const float lu[4] = {l4.x, l4.y, l4.z, l4.w};
+            const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+            float pv[4];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const bool keep = kReverse ? (u + x >= r) : (u + x <= r);
+              const float d = ex2(kReverse ? lu[x] - l_r : l_r - lu[x]) * uu[x];
+              pv[x] = keep ? __uint_as_float(sr[e + x]) * d : 0.0f;
+            }
+            pk[cc * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+            pk[cc * 16 + e / 2 + 1] = pack_bf16(pv[2], pv[3]);
+          }
+        }
+        tmem_st32(tmem + lane_base + kColS + half * 64, pk);  // packed: see split_col_lin
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(p_ready);
+      if (threadIdx.x == 0) AF_LT(8, n);
+      // (f) bf16 copy of the updated state (this half's columns) for the next chunk's Q H —
+      //     after Q H of this chunk has read the previous copy
+      mbar_wait(h_full, ph);
+      mbar_wait(qh_full, ph);
+      if (threadIdx.x == 0) AF_LT(11, n);
+      tc_fence_after();
+#pragma unroll
+      for (int hh = 0; hh < kHalves; ++hh) {
+        const int dk = hh * 128 + r;
+        uint32_t hr[32];
+        tmem_ld32(tmem + lane_base + kColH + hh * kLinVB + half * 32, hr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int gq = 0; gq < 4; ++gq)
+          *swz_row(sHb, dk, half * 4 + gq) = make_uint4(
+              pack_bf16(__uint_as_float(hr[gq * 8 + 0]), __uint_as_float(hr[gq * 8 + 1])),
+              pack_bf16(__uint_as_float(hr[gq * 8 + 2]), __uint_as_float(hr[gq * 8 + 3])),
+              pack_bf16(__uint_as_float(hr[gq * 8 + 4]), __uint_as_float(hr[gq * 8 + 5])),
+              pack_bf16(__uint_as_float(hr[gq * 8 + 6]), __uint_as_float(hr[gq * 8 + 7])));
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(hb_ready);
+      if (threadIdx.x == 0) AF_LT(12, n);
+      // (e) O = s_out (OI + cp QH) for this half's 32 output columns (QH is double-buffered,
+      //     so the next chunk's Q H can already run)
+      mbar_wait(oi_full, ph);
+      if (threadIdx.x == 0) AF_LT(9, n);
+      tc_fence_after();
+      {
+        const float rs = (p.o_rowscale.ptr != nullptr && live) ? p.o_rowscale.at(b, h, t) : 1.0f;
+        const int col0 = vb * kLinVB + half * 32;
+        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_sb + h * p.o_sh +
+                              static_cast<int64_t>(live ? t : 0) * p.o_ss + col0;
+        uint32_t oi[32], qh[32];
+        tmem_ld32(tmem + lane_base + kColOI + half * 32, oi);
+        tmem_ld32(tmem + lane_base + kColQH + ph * kLinVB + half * 32, qh);
+        tmem_ld_wait();
+        float ov[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          ov[e] = p.out_scale * fmaf(cp, __uint_as_float(qh[e]), __uint_as_float(oi[e]));
+        if (live) {
+          uint4* d4 = reinterpret_cast<uint4*>(orow);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            d4[v] = make_uint4(pack_bf16(rs * ov[v * 8 + 0], rs * ov[v * 8 + 1]),
+                               pack_bf16(rs * ov[v * 8 + 2], rs * ov[v * 8 + 3]),
+                               pack_bf16(rs * ov[v * 8 + 4], rs * ov[v * 8 + 5]),
+                               pack_bf16(rs * ov[v * 8 + 6], rs * ov[v * 8 + 7]));
+          if (p.dot_x != nullptr) {
+            const uint4* x4 = reinterpret_cast<const uint4*>(
+                reinterpret_cast<const __nv_bfloat16*>(p.dot_x) + b * p.x_sb + h * p.x_sh +
+                static_cast<int64_t>(t) * p.x_ss + col0);
+            float dotacc = 0.0f;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const uint4 xv = x4[v];
+              const uint32_t* xe = reinterpret_cast<const uint32_t*>(&xv);
+#pragma unroll
+              for (int q2 = 0; q2 < 4; ++q2)
+                dotacc += bf16_lo_(xe[q2]) * ov[v * 8 + 2 * q2] +
+                          bf16_hi_(xe[q2]) * ov[v * 8 + 2 * q2 + 1];
+            }
+            atomicAdd(p.dot + (static_cast<int64_t>(b) * p.heads + h) * p.seq + t, dotacc);
+          }
+        }
+      }
+      if (threadIdx.x == 0) AF_LT(10, n);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// Per-step gradients (SURVEY A.4 restated):  d log a_t = sum_{s>=t} (dq_dot_s - dk_dot_s)
+// where dq_dot = Qm . dQm, dk_dot = Km . dKm;  d fac_f += d log a / fac_f;
+// d gate += dk_dot / gate (k_mod = k * gate: dL/dgate = k . dKm).  One block per (b, h) sequence; outputs accumulate with
+// the strides of the corresponding input (broadcast axes sum via atomics).
+__global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
+                                         const float* __restrict__ dk_dot, LinearParams p,
+                                         StepTensor dfac0, StepTensor dfac1, StepTensor dgate) {
+  __shared__ float part[32];
+  const int bh = blockIdx.x;
+  const int b = bh / p.heads, h = bh % p.heads;
+  const int64_t base = static_cast<int64_t>(bh) * p.seq;
+  const int seq = p.seq;
+  auto val = [&](int t) { return dq_dot[base + t] - dk_dot[base + t]; };
+  const int per = (seq + blockDim.x - 1) / blockDim.x;
+  const int t0 = threadIdx.x * per;
+  const int t1 = min(seq, t0 + per);
+  float s = 0.0f;
+  for (int t = t1 - 1; t >= t0; --t) s += val(t);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float x = s;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float y = __shfl_down_sync(0xffffffffu, x, off);
+    if (lane + off < 32) x += y;
+  }
+  if (lane == 0) part[w] = x;
+  __syncthreads();
+  float acc = x - s;  // sum over later threads of this warp
+  for (int w2 = w + 1; w2 < static_cast<int>(blockDim.x >> 5); ++w2) acc += part[w2];
+  for (int t = t1 - 1; t >= t0; --t) {
+    acc += val(t);
+    const float dloga = acc;
+    const StepTensor* df[2] = {&dfac0, &dfac1};
+    for (int f = 0; f < p.nfac; ++f)
+      if (df[f]->ptr != nullptr)
+        atomicAdd(const_cast<float*>(df[f]->ptr) + b * df[f]->sb + h * df[f]->sh + t * df[f]->ss,
+                  dloga / p.fac[f].at(b, h, t));
+    if (dgate.ptr != nullptr)
+      atomicAdd(const_cast<float*>(dgate.ptr) + b * dgate.sb + h * dgate.sh + t * dgate.ss,
+                dk_dot[base + t] / p.u_scale.at(b, h, t));
+  }
+}
+
+// Km = bf16(k * gate): the backward uses one rounded copy of the gated keys in every pass so the
+// two dot terms of d log a cancel consistently (folding the gate into P / Vw instead rounds the
+// passes differently and loses ~2 digits in the cancellation).
+__global__ void gate_keys_kernel(const __nv_bfloat16* __restrict__ k, int64_t sb, int64_t sh,
+                                 int64_t ss, StepTensor gate, int heads, int seq, int dk,
+                                 __nv_bfloat16* __restrict__ out, int64_t total_rows) {
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int per_row = dk / 8;
+  const int64_t row = gid / per_row;
+  if (row >= total_rows) return;
+  const int c = static_cast<int>(gid % per_row) * 8;
+  const int t = static_cast<int>(row % seq);
+  const int64_t bh = row / seq;
+  const int b = static_cast<int>(bh / heads), h = static_cast<int>(bh % heads);
+  const float g = gate.at(b, h, t);
+  const uint4 x = *reinterpret_cast<const uint4*>(k + b * sb + h * sh + t * ss + c);
+  const uint32_t* e = reinterpret_cast<const uint32_t*>(&x);
+  uint4 y;
+  uint32_t* o = reinterpret_cast<uint32_t*>(&y);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) o[i] = pack_bf16(bf16_lo_(e[i]) * g, bf16_hi_(e[i]) * g);
+  *reinterpret_cast<uint4*>(out + row * dk + c) = y;
+}
+
+}  // namespace af

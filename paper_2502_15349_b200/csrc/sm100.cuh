@@ -240,6 +240,8 @@ AF_DEVICE uint32_t pack_bf16(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+AF_DEVICE float bf16_lo_(uint32_t w) { return __uint_as_float(w << 16); }
+AF_DEVICE float bf16_hi_(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 AF_DEVICE float ex2(float x) {
   float r;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));

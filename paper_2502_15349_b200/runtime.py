@@ -36,11 +36,17 @@ class ParallelDesc(C.Structure):
     ]
 
 
+I64x3 = C.c_int64 * 3
+
+
 class LinearDesc(C.Structure):
     _fields_ = [
         ("batch", C.c_int32), ("heads", C.c_int32), ("seq", C.c_int32), ("d_k", C.c_int32),
         ("d_v", C.c_int32), ("chunk", C.c_int32), ("q_scale", C.c_float),
         ("q_stride", I64x4), ("k_stride", I64x4), ("v_stride", I64x4), ("o_stride", I64x4),
+        ("log_decay_const", C.c_float), ("n_decay_factors", C.c_int32),
+        ("decay_factor", C.c_void_p * 2), ("decay_factor_stride", I64x3 * 2),
+        ("key_gate", C.c_void_p), ("key_gate_stride", I64x3),
     ]
 
 
@@ -58,10 +64,10 @@ SIGNATURES: dict[str, tuple] = {
     "af_parallel_bwd_workspace": (C.c_size_t, [C.POINTER(ParallelDesc)]),
     "af_parallel_bwd": (C.c_int, [C.POINTER(ParallelDesc), P, P, P, P, P, P, P, P, P, P,
                                   C.c_size_t, P]),
-    "af_linear_fwd": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P, P]),
+    "af_linear_fwd": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P]),
     "af_linear_bwd_workspace": (C.c_size_t, [C.POINTER(LinearDesc)]),
     "af_linear_bwd": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P, P, P, P, P, C.c_size_t,
-                                P]),
+                                P]),  # (desc, q, k, v, dout, dq, dk, dv, d_factor**, d_gate, ws..)
     "af_mla_decode_workspace": (C.c_size_t, [C.POINTER(MlaDesc)]),
     "af_mla_decode": (C.c_int, [C.POINTER(MlaDesc), P, P, P, P, P, C.c_size_t, P]),
     "af_status_string": (C.c_char_p, [C.c_int]),
@@ -116,3 +122,8 @@ def ptr(t) -> int | None:
 
 def strides4(t) -> I64x4:
     return I64x4(*[int(s) for s in t.stride()])
+
+
+def step_strides(t) -> I64x3:
+    """[b, h, s] element strides of a rank-4 per-step tensor [B|1, H|1, S, 1] (0 = broadcast)."""
+    return I64x3(*[0 if t.shape[i] == 1 else int(t.stride(i)) for i in range(3)])
