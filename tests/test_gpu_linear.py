@@ -1,0 +1,88 @@
+"""Parity of the sm_100a linear template (K4 forward, K5 backward) against the float64 oracle
+(oracle pinned to the reference's step/chunk executors and unrolled
+autodiff in tests/test_oracle_golden.py).  Tolerance: normwise <= 2e-2 for O and
+every gradient, no max-abs bound (RetNet gamma ~ 1 makes |O| large)."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import recurrent as OR
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2502_15349_b200 as af  # noqa: E402
+from paper_2502_15349_b200 import spec as S  # noqa: E402
+
+
+def to_dev(arrays):
+    return {k: torch.tensor(np.ascontiguousarray(v), device="cuda").to(
+        torch.bfloat16 if k in ("q", "k", "v") else torch.float32) for k, v in arrays.items()}
+
+
+def rounded(arrays):
+    out = dict(arrays)
+    for k in ("q", "k", "v"):
+        out[k] = torch.tensor(arrays[k]).to(torch.bfloat16).double().numpy()
+    return out
+
+
+def nw(got, want):
+    got = np.asarray(got, np.float64).reshape(np.shape(want))
+    return float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30))
+
+
+CASES = {
+    "retention_d128_s384": ("retention-recurrent", dict(batch=1, heads=2, seq=384, d_qk=128, d_v=128)),
+    "retention_d256_ragged": ("retention-recurrent", dict(batch=2, heads=1, seq=300, d_qk=256, d_v=256)),
+    "mamba2_d128_s300": ("mamba2-ssm", dict(batch=1, heads=2, seq=300, d_qk=128, d_v=128)),
+    "mamba2_dk128_dv256": ("mamba2-ssm", dict(batch=1, heads=1, seq=520, d_qk=128, d_v=256)),
+    "gated_retention_d256": ("gated-retention", dict(batch=1, heads=2, seq=256, d_qk=256, d_v=256)),
+    "retention_single_chunk_tail": ("retention-recurrent", dict(batch=1, heads=1, seq=77, d_qk=128, d_v=128)),
+}
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_linear_forward_matches_oracle(case):
+    name, kw = CASES[case]
+    spec = S.builtin(name, **kw)
+    arrays = oracle.generate(spec, seed=7)
+    o = af.linear_forward(spec, to_dev(arrays))
+    ref = rounded(arrays)
+    assert nw(o.double().cpu().numpy(), OR.chunk_forward(spec, ref, 64)) <= 2e-2
+    # chunked == stepwise (the reference's own invariant, test_engine.py:208-221)
+    assert nw(o.double().cpu().numpy(), OR.step_forward(spec, ref)) <= 2e-2
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_linear_backward_matches_oracle(case):
+    name, kw = CASES[case]
+    spec = S.builtin(name, **kw)
+    arrays = oracle.generate(spec, seed=8)
+    dev = to_dev(arrays)
+    rng = np.random.default_rng(3)
+    dout = torch.tensor(rng.uniform(-1, 1, (kw["batch"], kw["heads"], kw["seq"], kw["d_v"])),
+                        device="cuda").to(torch.bfloat16)
+    grads = af.linear_backward(spec, dev, dout)
+    want = OR.chunk_vjp(spec, rounded(arrays), dout.double().cpu().numpy(), chunk=64)
+    for k, w in want.items():
+        assert nw(grads[k].double().cpu().numpy(), w) <= 2e-2, k
+
+
+def test_run_chunk_recurrent_signature_and_autograd():
+    spec = S.builtin("mamba2-ssm", batch=1, heads=2, seq=256, d_qk=128, d_v=128)
+    arrays = to_dev(oracle.generate(spec, 1))
+    o1 = af.run_chunk_recurrent(spec, arrays, 64)
+    o2 = af.run_step_recurrent(spec, arrays)
+    assert torch.equal(o1, o2)
+    g = af.autodiff_grads(spec, arrays)
+    assert set(g) == {"q", "k", "v", "gate", "decay"}
+    assert g["gate"].shape == arrays["gate"].shape
+
+
+def test_nonfactorable_h_mod_raises():
+    base = S.builtin("retention-recurrent", heads=1, seq=128, d_qk=128, d_v=128)
+    spec = S.AttentionSpec(base.name, base.pattern, base.dims, q_mod=base.q_mod,
+                           h_mod=S.mod("h * h", "h"), extra_inputs=base.extra_inputs)
+    with pytest.raises(af.UnsupportedError):
+        af.run_chunk_recurrent(spec, to_dev(oracle.generate(base, 0)))
