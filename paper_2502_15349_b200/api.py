@@ -107,13 +107,53 @@ def _desc(plan: ParallelPlan, q, k, v, o, slope, dtype_code: int) -> rt.Parallel
     return c
 
 
+MLA_DQK, MLA_DV = 576, 512
+
+
+def mla_decode(q: torch.Tensor, kv: torch.Tensor, scale: float):
+    """K3 decode: softmax attention of every head of one query token over a shared latent cache.
+
+    q [B, H, 576] bf16, kv [B, Sk, 576] bf16 (V = kv[..., :512]) → (O [B, H, 512] bf16,
+    LSE [B, H] fp32).  Split-KV across ~2 waves of CTAs, merged by an LSE-weighted combine."""
+    if q.dim() != 3 or kv.dim() != 3 or q.shape[-1] != MLA_DQK or kv.shape[-1] != MLA_DQK \
+            or q.shape[0] != kv.shape[0]:
+        raise ShapeError("mla_decode wants q [B,H,576], kv [B,Sk,576]", q=tuple(q.shape),
+                         kv=tuple(kv.shape))
+    q = q.to(_BF16).contiguous()
+    kv = kv.to(_BF16).contiguous()
+    B, H, _ = q.shape
+    c = rt.MlaDesc()
+    c.batch, c.heads, c.seq_k, c.d_qk, c.d_v, c.scale = B, H, kv.shape[1], MLA_DQK, MLA_DV, scale
+    o = torch.empty(B, H, MLA_DV, device=q.device, dtype=_BF16)
+    lse = torch.empty(B, H, device=q.device, dtype=torch.float32)
+    L = rt.lib()
+    ws_n = L.af_mla_decode_workspace(c)
+    ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
+    rt.check(L.af_mla_decode(c, q.data_ptr(), kv.data_ptr(), o.data_ptr(), lse.data_ptr(),
+                             ws.data_ptr(), ws_n, _stream()), "af_mla_decode")
+    return o, lse
+
+
 def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: bool = False):
     """Forward of the parallel template → ``(O [B,H,Sq,Dv], LSE [B,H,Sq] fp32 or None)``.
 
     ``precision="bf16"`` runs the tcgen05 kernel (K1) on bf16 inputs (fp32 inputs are rounded);
-    ``"fp32"`` runs the exact-FFMA fp32 kernel (cfg1 parity path)."""
+    ``"fp32"`` runs the exact-FFMA fp32 kernel (cfg1 parity path).  MLA variants (``kv_shared``,
+    (Dqk, Dv) = (576, 512), one latent head) run K3: prefill, or the split-KV decode kernel when
+    seq_q == 1 and no mask applies."""
     spec = _spec(spec)
     plan = plan_parallel(spec)
+    d0 = spec.dims
+    if (spec.kv_shared and precision == "bf16" and (d0.d_qk, d0.d_v) == (MLA_DQK, MLA_DV)
+            and d0.seq_q == 1 and not plan.band.causal and plan.band.window is None):
+        q = _need(arrays, "q")
+        k = _need(arrays, "k")
+        _check_shape(q, (d0.batch, d0.heads, 1, MLA_DQK), "q")
+        _check_shape(k, (d0.batch, 1, d0.seq_k, MLA_DQK), "k")
+        o, lse = mla_decode(q[:, :, 0], k[:, 0], float(plan.scale))
+        if check_nan:
+            _check_nan(o, "kernel")
+        return o.unsqueeze(2), lse.unsqueeze(2)
     dtype = _BF16 if precision == "bf16" else torch.float32
     q, k, v, slope = _parallel_inputs(plan, arrays, dtype)
     d = spec.dims

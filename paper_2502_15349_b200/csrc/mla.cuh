@@ -1,0 +1,333 @@
+// K3 — MLA attention (DeepSeek-V2: Dqk = 576, Dv = 512, one latent KV head, V = K[:, :512]).
+//
+// Softmax attention over a shared latent cache, i.e. attnforge `engine.run_tiled_parallel`
+// (engine.py:423-505) with the builtin softmax rownorm (attention.py:556-572) on a variant whose
+// K/V are one latent head (V aliases the first d_v columns of K).  Two modes:
+//   prefill : rows = 128 query positions of one head, causal (top-left), grid over
+//             (query tile, head, value half)
+//   decode  : rows = the 128 heads of one query token (seq_q = 1, unmasked — SURVEY §0), grid
+//             over (batch, key split, value half); splits are merged by mla_combine_kernel.
+// Budget: the fp32 O accumulator of 128 rows x 512 would fill all of TMEM, so each CTA owns one
+// 256-wide value half (the two halves recompute S; 1.53x the QK^T work).  Q (128 x 576 bf16,
+// 144 KB) stays in shared memory; the latent KV streams through a 2-stage ring of 32-token tiles
+// (36 KB each).  TMEM: S double buffer [0,64) (P packed in place) | O [256,512).
+// Warps: 0-3 softmax rows (one row per thread, FA4-style lazy rescale), 4 TMA, 5 MMA.
+#pragma once
+#include <cuda.h>
+#include "params.h"
+#include "sm100.cuh"
+#include "parallel_fwd.cuh"
+
+namespace af {
+
+constexpr int kMlaDqk = 576;
+constexpr int kMlaDv = 512;
+constexpr int kMlaHalf = 256;
+constexpr int kMlaN = 32;  // keys per tile
+
+struct MlaParams {
+  int batch, heads, seq_q, seq_k;
+  float scale_log2;
+  int causal;
+  int splits;            // decode: key splits per batch
+  int split_len;         // decode: keys per split (multiple of kMlaN)
+  // prefill output (bf16 [B, H, Sq, 512], element strides) + LSE [B, H, Sq]
+  void* o;
+  int64_t o_sb, o_sh, o_ss;
+  float* lse;
+  // decode partials: fp32 [B, splits, H, 512] and lse [B, splits, H]
+  float* part_o;
+  float* part_lse;
+};
+
+struct MlaSmem {
+  static constexpr int kQBytes = 128 * kMlaDqk * 2;   // 9 boxes of [128 rows][128 B]
+  static constexpr int kKBytes = kMlaN * kMlaDqk * 2; // 9 boxes of [32 rows][128 B]
+  static constexpr int kQOff = 0;
+  static constexpr int kKOff = kQBytes;
+  static constexpr int kBarOff = kKOff + 2 * kKBytes;
+  // q_full, k_full[2], k_empty[2], s_full[2], p_ready, o_done
+  static constexpr int kNumBars = 9;
+  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
+  static constexpr int kTotal = kTmemSlotOff + 16;
+};
+
+template <bool kDecode>
+__global__ void __launch_bounds__(192, 1)
+    mla_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
+                   const __grid_constant__ CUtensorMap tm_kv, const MlaParams p) {
+  using L = MlaSmem;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* sQ = smem + L::kQOff;
+  uint8_t* sK = smem + L::kKOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = bars + 3;
+  uint64_t* s_full = bars + 5;
+  uint64_t* p_ready = bars + 7;
+  uint64_t* o_done = bars + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
+
+  const int warp = static_cast<int>(warp_id());
+  const int half = blockIdx.x & 1;  // value half: columns [256*half, 256*half + 256)
+  int b, h = 0, q0 = 0, split = 0, kv_lo, kv_hi;
+  if constexpr (kDecode) {
+    const int rest = blockIdx.x >> 1;
+    split = rest % p.splits;
+    b = rest / p.splits;
+    kv_lo = split * p.split_len;
+    kv_hi = min(p.seq_k, kv_lo + p.split_len);
+  } else {
+    const int q_tiles = (p.seq_q + 127) / 128;
+    const int rest = blockIdx.x >> 1;
+    const int qt_raw = rest % q_tiles;
+    const int bh = rest / q_tiles;
+    b = bh / p.heads;
+    h = bh % p.heads;
+    const int qt = p.causal ? q_tiles - 1 - qt_raw : qt_raw;
+    q0 = qt * 128;
+    kv_lo = 0;
+    kv_hi = p.seq_k;
+    if (p.causal) kv_hi = min(kv_hi, q0 + 128);
+  }
+  const int nk = kv_hi > kv_lo ? (kv_hi - kv_lo + kMlaN - 1) / kMlaN : 0;
+
+  if (warp == 4 && lane_id() == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+    }
+    mbar_init(p_ready, 4);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t kColO = 256;
+
+  if (warp == 4) {
+    if (elect_one() && nk > 0) {
+      mbar_expect_tx(q_full, L::kQBytes);
+      for (int c = 0; c < kMlaDqk / 64; ++c) {
+        if constexpr (kDecode)
+          tma_load_4d(sQ + c * (128 * 128), &tm_q, q_full, c * 64, 0, b, 0);
+        else
+          tma_load_4d(sQ + c * (128 * 128), &tm_q, q_full, c * 64, q0, h, b);
+      }
+      for (int n = 0; n < nk; ++n) {
+        const int s = n & 1;
+        mbar_wait(&k_empty[s], ((n >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[s], L::kKBytes);
+        const int j0 = kv_lo + n * kMlaN;
+        for (int c = 0; c < kMlaDqk / 64; ++c)
+          tma_load_4d_hint(sK + s * L::kKBytes + c * (kMlaN * 128), &tm_kv, &k_full[s], c * 64,
+                           j0, b, 0, kEvictLast);
+      }
+    }
+  } else if (warp == 5) {
+    if (elect_one() && nk > 0) {
+      constexpr uint32_t id_s = make_idesc_bf16(128, kMlaN, false, false);     // S = Q K^T
+      constexpr uint32_t id_o = make_idesc_bf16(128, kMlaHalf, false, true);   // O += P V
+      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK);
+      auto issue_s = [&](int n) {
+        const int s = n & 1;
+        mbar_wait(&k_full[s], (n >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kMlaDqk / 16; ++kk)
+          mma_ss(tmem + s * kMlaN,
+                 make_sdesc(aQ + (kk / 4) * (128 * 128) + (kk % 4) * 32, 0, 1024),
+                 make_sdesc(aK + s * L::kKBytes + (kk / 4) * (kMlaN * 128) + (kk % 4) * 32, 0,
+                            1024),
+                 id_s, kk > 0);
+        mma_commit(&s_full[s]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int n = 0; n < nk; ++n) {
+        const int s = n & 1;
+        if (n + 1 < nk) issue_s(n + 1);
+        mbar_wait(p_ready, n & 1);
+        tc_fence_after();
+        // V = latent K columns [256*half, 256*half+256): 4 boxes of [32 keys][64 dv], MN-major
+        const uint32_t vbase = aK + s * L::kKBytes + half * 4 * (kMlaN * 128);
+#pragma unroll
+        for (int kk = 0; kk < kMlaN / 16; ++kk)
+          mma_ts(tmem + kColO, tmem + s * kMlaN + kk * 8,
+                 make_sdesc(vbase + kk * 2048, kMlaN * 128, 1024), id_o, (n > 0 || kk > 0));
+        mma_commit(o_done);
+        mma_commit(&k_empty[s]);
+      }
+    }
+  } else {
+    // ───────────── softmax rows ─────────────
+    const int row = warp * 32 + static_cast<int>(lane_id());
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const int i = kDecode ? 0 : q0 + row;  // query position (prefill)
+    float m_run = -INFINITY, l_run = 0.0f;
+    for (int n = 0; n < nk; ++n) {
+      const int s = n & 1;
+      const int j0 = kv_lo + n * kMlaN;
+      mbar_wait(&s_full[s], (n >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[32];
+      tmem_ld32(tmem + lane_base + s * kMlaN, sr);
+      tmem_ld_wait();
+      float x[32];
+      float bmax = -INFINITY;
+      const bool full = (j0 + kMlaN <= kv_hi) && (kDecode || !p.causal || j0 + kMlaN - 1 <= q0);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        bool keep = true;
+        if (!full) keep = (j0 + e < kv_hi) && (kDecode || !p.causal || j0 + e <= i);
+        x[e] = keep ? __uint_as_float(sr[e]) * p.scale_log2 : -INFINITY;
+        bmax = fmaxf(bmax, x[e]);
+      }
+      const float m_new = fmaxf(m_run, bmax);
+      const bool need = (m_new - m_run) > 8.0f;
+      float factor = 1.0f;
+      if (need) {
+        factor = (m_run == -INFINITY) ? 0.0f : ex2(m_run - m_new);
+        m_run = m_new;
+      }
+      const float m_use = (m_run == -INFINITY) ? 0.0f : m_run;
+      uint32_t pk[16];
+      float lsum = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float e0 = ex2(x[e] - m_use), e1 = ex2(x[e + 1] - m_use);
+        lsum += e0 + e1;
+        pk[e / 2] = pack_bf16(e0, e1);
+      }
+      l_run = l_run * factor + lsum;
+      tmem_st16(tmem + lane_base + s * kMlaN, pk);
+      tmem_st_wait();
+      if (n > 0 && __any_sync(0xffffffffu, need)) {
+        mbar_wait(o_done, (n - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < kMlaHalf / 32; ++c) {
+          uint32_t orr[32];
+          tmem_ld32(tmem + lane_base + kColO + c * 32, orr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) orr[e] = __float_as_uint(__uint_as_float(orr[e]) * factor);
+          tmem_st32(tmem + lane_base + kColO + c * 32, orr);
+        }
+        tmem_st_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(p_ready);
+    }
+    // ───────────── epilogue ─────────────
+    if (nk > 0) {
+      mbar_wait(o_done, (nk - 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = (l_run == 0.0f) ? 0.0f : 1.0f / l_run;
+    const float lse = (l_run == 0.0f) ? -INFINITY : (m_run * kLn2 + logf(l_run));
+    if constexpr (kDecode) {
+      // rows are heads; partial (normalised) output of this split
+      const int hh = row;
+      float* dst = p.part_o + ((static_cast<int64_t>(b) * p.splits + split) * p.heads + hh) * kMlaDv +
+                   half * kMlaHalf;
+#pragma unroll 1
+      for (int c = 0; c < kMlaHalf / 32; ++c) {
+        uint32_t orr[32];
+        if (nk > 0) {
+          tmem_ld32(tmem + lane_base + kColO + c * 32, orr);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) orr[e] = 0u;
+        }
+        if (hh < p.heads) {
+          float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            d4[v] = make_float4(__uint_as_float(orr[v * 4]) * inv, __uint_as_float(orr[v * 4 + 1]) * inv,
+                                __uint_as_float(orr[v * 4 + 2]) * inv, __uint_as_float(orr[v * 4 + 3]) * inv);
+        }
+      }
+      if (half == 0 && hh < p.heads)
+        p.part_lse[(static_cast<int64_t>(b) * p.splits + split) * p.heads + hh] = lse;
+    } else {
+      const bool live = i < p.seq_q;
+      __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_sb + h * p.o_sh +
+                            static_cast<int64_t>(live ? i : 0) * p.o_ss + half * kMlaHalf;
+#pragma unroll 1
+      for (int c = 0; c < kMlaHalf / 32; ++c) {
+        uint32_t orr[32];
+        if (nk > 0) {
+          tmem_ld32(tmem + lane_base + kColO + c * 32, orr);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) orr[e] = 0u;
+        }
+        if (live) {
+          uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            d4[v] = make_uint4(
+                pack_bf16(__uint_as_float(orr[v * 8 + 0]) * inv, __uint_as_float(orr[v * 8 + 1]) * inv),
+                pack_bf16(__uint_as_float(orr[v * 8 + 2]) * inv, __uint_as_float(orr[v * 8 + 3]) * inv),
+                pack_bf16(__uint_as_float(orr[v * 8 + 4]) * inv, __uint_as_float(orr[v * 8 + 5]) * inv),
+                pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv));
+        }
+      }
+      if (half == 0 && live && p.lse != nullptr)
+        p.lse[(static_cast<int64_t>(b) * p.heads + h) * p.seq_q + i] = lse;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// Merge decode splits: O = sum_s e^{lse_s - lse} O_s, lse = log sum_s e^{lse_s}.
+__global__ void mla_combine_kernel(const float* __restrict__ part_o,
+                                   const float* __restrict__ part_lse, int batch, int heads,
+                                   int splits, __nv_bfloat16* __restrict__ o,
+                                   float* __restrict__ lse) {
+  const int bh = blockIdx.x;  // one block per (b, head), 128 threads x 4 columns
+  const int b = bh / heads, hh = bh % heads;
+  float mx = -INFINITY;
+  for (int s = 0; s < splits; ++s)
+    mx = fmaxf(mx, part_lse[(static_cast<int64_t>(b) * splits + s) * heads + hh]);
+  float den = 0.0f;
+  for (int s = 0; s < splits; ++s) {
+    const float l = part_lse[(static_cast<int64_t>(b) * splits + s) * heads + hh];
+    den += (l == -INFINITY) ? 0.0f : __expf(l - mx);
+  }
+  const int c = threadIdx.x * 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < splits; ++s) {
+    const float l = part_lse[(static_cast<int64_t>(b) * splits + s) * heads + hh];
+    if (l == -INFINITY) continue;
+    const float w = __expf(l - mx) / den;
+    const float4 v = *reinterpret_cast<const float4*>(
+        part_o + ((static_cast<int64_t>(b) * splits + s) * heads + hh) * kMlaDv + c);
+    acc.x += w * v.x;
+    acc.y += w * v.y;
+    acc.z += w * v.z;
+    acc.w += w * v.w;
+  }
+  uint2 out = make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+  *reinterpret_cast<uint2*>(o + (static_cast<int64_t>(b) * heads + hh) * kMlaDv + c) = out;
+  if (threadIdx.x == 0 && lse != nullptr)
+    lse[static_cast<int64_t>(b) * heads + hh] = (den == 0.0f) ? -INFINITY : mx + logf(den);
+}
+
+}  // namespace af

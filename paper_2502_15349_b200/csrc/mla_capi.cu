@@ -1,0 +1,101 @@
+// C-ABI for K3 (MLA): decode entry point + the prefill launcher used by af_parallel_fwd when the
+// variant is softmax over one shared latent head with (Dqk, Dv) = (576, 512) and V = K[:, :512].
+#include "host_common.h"
+#include "mla.cuh"
+
+namespace af {
+
+int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o, float* lse,
+                cudaStream_t s) {
+  AF_REQUIRE(d->heads_kv == 1, AF_ERR_UNSUPPORTED, "MLA prefill needs one latent KV head");
+  CUtensorMap tq, tkv;
+  const int64_t kv_st[4] = {0, d->k_stride[0], d->k_stride[2], 1};  // dims (576, Sk, B, 1)
+  if (!make_tmap_4d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDqk, d->seq_q, d->heads_q,
+                    d->batch, d->q_stride, 64, 128, true) ||
+      !make_tmap_4d(&tkv, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDqk, d->seq_k, d->batch, 1,
+                    kv_st, 64, kMlaN, true))
+    return AF_ERR_INPUT;
+  MlaParams p{};
+  p.batch = d->batch; p.heads = d->heads_q; p.seq_q = d->seq_q; p.seq_k = d->seq_k;
+  p.scale_log2 = d->scale * kLog2e;
+  AF_REQUIRE(!d->causal || d->diag_offset == 0, AF_ERR_UNSUPPORTED,
+             "MLA prefill supports the top-left causal mask (offset 0) only");
+  AF_REQUIRE(d->window <= 0, AF_ERR_UNSUPPORTED, "MLA prefill has no sliding window");
+  p.causal = d->causal;
+  p.o = o; p.o_sb = d->o_stride[0]; p.o_sh = d->o_stride[1]; p.o_ss = d->o_stride[2];
+  p.lse = lse;
+  auto kern = mla_fwd_kernel<false>;
+  static bool attr = false;
+  if (!attr) {
+    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MlaSmem::kTotal));
+    attr = true;
+  }
+  const int q_tiles = (d->seq_q + 127) / 128;
+  kern<<<q_tiles * d->batch * d->heads_q * 2, 192, MlaSmem::kTotal, s>>>(tq, tkv, p);
+  AF_CUDA_CHECK(cudaGetLastError());
+  return AF_OK;
+}
+
+namespace {
+int decode_splits(const af_mla_desc* d) {
+  const int ctas_per_split = d->batch * 2;
+  int splits = (2 * sm_count() + ctas_per_split - 1) / ctas_per_split;  // ~2 waves of CTAs
+  splits = std::max(1, std::min(splits, (d->seq_k + kMlaN - 1) / kMlaN));
+  return splits;
+}
+}  // namespace
+
+}  // namespace af
+
+extern "C" size_t af_mla_decode_workspace(const af_mla_desc* d) {
+  if (d == nullptr) return 0;
+  const size_t rows = static_cast<size_t>(d->batch) * af::decode_splits(d) * d->heads;
+  return rows * (af::kMlaDv + 1) * sizeof(float);
+}
+
+extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv, void* o,
+                             float* lse, void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace af;
+  AF_REQUIRE(d != nullptr, AF_ERR_INPUT, "null descriptor");
+  AF_REQUIRE(d->d_qk == kMlaDqk && d->d_v == kMlaDv, AF_ERR_UNSUPPORTED,
+             "MLA decode is built for (Dqk, Dv) = (576, 512), got (%d, %d)", d->d_qk, d->d_v);
+  AF_REQUIRE(d->heads >= 1 && d->heads <= 128, AF_ERR_UNSUPPORTED,
+             "MLA decode packs the heads of one token into a 128-row tile (heads=%d)", d->heads);
+  AF_REQUIRE(d->batch >= 1 && d->seq_k >= 1, AF_ERR_INPUT, "dims must be >= 1");
+  AF_REQUIRE(workspace_bytes >= af_mla_decode_workspace(d), AF_ERR_INPUT, "workspace too small");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int splits = decode_splits(d);
+  int split_len = (d->seq_k + splits - 1) / splits;
+  split_len = ((split_len + kMlaN - 1) / kMlaN) * kMlaN;
+  // q [B, H, 576] and kv [B, Sk, 576], contiguous
+  CUtensorMap tq, tkv;
+  const int64_t q_st[4] = {0, static_cast<int64_t>(d->heads) * kMlaDqk, kMlaDqk, 1};  // (576, H, B, 1)
+  const int64_t kv_st[4] = {0, static_cast<int64_t>(d->seq_k) * kMlaDqk, kMlaDqk, 1};
+  if (!make_tmap_4d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDqk, d->heads, d->batch, 1,
+                    q_st, 64, 128, true) ||
+      !make_tmap_4d(&tkv, kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDqk, d->seq_k, d->batch, 1,
+                    kv_st, 64, kMlaN, true))
+    return AF_ERR_INPUT;
+  MlaParams p{};
+  p.batch = d->batch; p.heads = d->heads; p.seq_q = 1; p.seq_k = d->seq_k;
+  p.scale_log2 = d->scale * kLog2e;
+  p.causal = 0;
+  p.splits = splits;
+  p.split_len = split_len;
+  float* part_o = static_cast<float*>(workspace);
+  float* part_lse = part_o + static_cast<size_t>(d->batch) * splits * d->heads * kMlaDv;
+  p.part_o = part_o;
+  p.part_lse = part_lse;
+  auto kern = mla_fwd_kernel<true>;
+  static bool attr = false;
+  if (!attr) {
+    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MlaSmem::kTotal));
+    attr = true;
+  }
+  kern<<<d->batch * splits * 2, 192, MlaSmem::kTotal, s>>>(tq, tkv, p);
+  AF_CUDA_CHECK(cudaGetLastError());
+  mla_combine_kernel<<<d->batch * d->heads, kMlaDv / 4, 0, s>>>(
+      part_o, part_lse, d->batch, d->heads, splits, static_cast<__nv_bfloat16*>(o), lse);
+  AF_CUDA_CHECK(cudaGetLastError());
+  return AF_OK;
+}

@@ -81,6 +81,11 @@ ParallelFwdParams make_fwd_params(const af_parallel_desc* d, void* o, float* lse
 
 }  // namespace af
 
+namespace af {
+int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o, float* lse,
+                cudaStream_t s);
+}
+
 extern "C" int af_parallel_fwd_f32(const af_parallel_desc* d, const void* q, const void* k,
                                    const void* v, void* o, float* lse, void* stream);
 
@@ -92,6 +97,13 @@ extern "C" int af_parallel_fwd(const af_parallel_desc* d, const void* q, const v
   if (d->dtype == AF_DTYPE_F32) return af_parallel_fwd_f32(d, q, k, v, o, lse, stream);
   AF_REQUIRE(d->dtype == AF_DTYPE_BF16, AF_ERR_INPUT, "unknown dtype %d", d->dtype);
   AF_REQUIRE(d->o_stride[3] == 1, AF_ERR_INPUT, "output feature stride must be 1");
+  if (d->d_qk == 576 && d->d_v == 512) {
+    // MLA: one latent head, V = K[:, :512] (same base pointer and strides)
+    AF_REQUIRE(d->family == AF_FAMILY_SOFTMAX && v == k && d->v_stride[0] == d->k_stride[0] &&
+                   d->v_stride[2] == d->k_stride[2],
+               AF_ERR_UNSUPPORTED, "(576, 512) heads are lowered only as MLA (softmax, V = K[:, :512])");
+    return mla_prefill(d, q, k, o, lse, reinterpret_cast<cudaStream_t>(stream));
+  }
   CUtensorMap tq, tk, tv;
   if (!make_tmap_4d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d->d_qk, d->seq_q, d->heads_q,
                     d->batch, d->q_stride, 64, kBlockM, true) ||

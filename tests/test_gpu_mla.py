@@ -1,0 +1,66 @@
+"""Parity of K3 (MLA: Dqk=576, Dv=512, one latent head, V = K[:, :512]) against the f64 oracle
+(the oracle expands the latent head and aliases V to the first 512 columns)."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from oracle import parallel as OP
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2502_15349_b200 as af  # noqa: E402
+from paper_2502_15349_b200 import spec as S  # noqa: E402
+
+
+def mla_spec(b, h, sq, sk, causal):
+    sp = replace(S.builtin("softmax", batch=b, heads=h, heads_kv=1, seq_q=sq, seq_k=sk, d_qk=576,
+                           d_v=512), kv_shared=True)
+    return S.with_causal_mask(sp) if causal else sp
+
+
+def inputs(b, h, sq, sk, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q = (torch.rand(b, h, sq, 576, device="cuda", generator=g) * 2 - 1).bfloat16()
+    k = (torch.rand(b, 1, sk, 576, device="cuda", generator=g) * 2 - 1).bfloat16()
+    return q, k
+
+
+@pytest.mark.parametrize("b,h,sq,sk,causal", [(1, 4, 300, 300, True), (1, 2, 256, 200, False),
+                                               (2, 3, 130, 130, True)])
+def test_mla_prefill_matches_oracle(b, h, sq, sk, causal):
+    q, k = inputs(b, h, sq, sk, 0)
+    o, lse = af.parallel_forward(mla_spec(b, h, sq, sk, causal), {"q": q, "k": k})
+    rows = np.arange(sq)
+    for bb in range(b):
+        for hh in range(h):
+            a = {"q": q[bb:bb + 1, hh:hh + 1].double().cpu().numpy(),
+                 "k": k[bb:bb + 1].double().cpu().numpy()}
+            wo, wl = OP.sampled_forward(mla_spec(1, 1, sq, sk, causal), a, rows)
+            got = o[bb, hh].double().cpu().numpy()
+            assert np.linalg.norm(got - wo[0, 0]) / np.linalg.norm(wo) <= 1e-2
+            assert np.max(np.abs(got - wo[0, 0])) <= 2e-2
+            assert np.max(np.abs(lse[bb, hh].double().cpu().numpy() - wl[0, 0])) <= 1e-3
+
+
+@pytest.mark.parametrize("b,h,sk", [(2, 128, 5000), (1, 128, 64), (3, 16, 1000)])
+def test_mla_decode_matches_oracle(b, h, sk):
+    q, k = inputs(b, h, 1, sk, 1)
+    o, lse = af.parallel_forward(mla_spec(b, h, 1, sk, False), {"q": q, "k": k})
+    assert o.shape == (b, h, 1, 512)
+    for bb in range(b):
+        for hh in (0, h // 2, h - 1):
+            a = {"q": q[bb:bb + 1, hh:hh + 1].double().cpu().numpy(),
+                 "k": k[bb:bb + 1].double().cpu().numpy()}
+            wo, wl = OP.sampled_forward(mla_spec(1, 1, 1, sk, False), a, np.array([0]))
+            assert np.max(np.abs(o[bb, hh, 0].double().cpu().numpy() - wo[0, 0, 0])) <= 2e-2
+            assert abs(float(lse[bb, hh, 0]) - float(wl[0, 0, 0])) <= 1e-3
+
+
+def test_mla_decode_entry_point_shapes():
+    q, k = inputs(2, 128, 1, 333, 2)
+    o, lse = af.api.mla_decode(q[:, :, 0], k[:, 0], 576 ** -0.5)
+    assert o.shape == (2, 128, 512) and lse.shape == (2, 128)
+    with pytest.raises(af.ShapeError):
+        af.api.mla_decode(q[:, :, 0, :64], k[:, 0], 1.0)
