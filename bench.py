@@ -1,19 +1,24 @@
 """Benchmark: attention fwd+bwd TFLOPS & % of bf16 tensor peak on B200 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], fits one GPU): Llama-3 8B GQA causal softmax attention, bf16,
-B=8 Hq=32 Hkv=8 S=8192 D=128 — one "step" = K1 forward (O, LSE) + K2 backward (dQ, dK, dV) for a
-synthetic batch.  Algorithmic flops: fwd 2·B·Hq·P·(Dqk+Dv), bwd 2·B·Hq·P·(3Dqk+2Dv)
-with P = S(S+1)/2 unmasked pairs per head → 1.540e13 flops per step.
+Default workload (BASELINE.json configs[1], fits one GPU): cfg2, Llama-3 8B GQA causal softmax
+attention, bf16, B=8 Hq=32 Hkv=8 S=8192 D=128 — one "step" = K1 forward (O, LSE) + K2 backward
+(dQ, dK, dV) of one synthetic batch.  ``--config`` selects any other BASELINE config (cfg1, cfg3,
+cfg4a, cfg4b, cfg5a, cfg5b; ``all`` prints one line per config).  Algorithmic work:
 
-  value   device-resident throughput (inputs in HBM before the timed region), TFLOPS
-  e2e     same metric through the public API with pinned HOST buffers: H2D of q,k,v,dO and D2H of
-          O,dQ,dK,dV inside the timed region
-  roofline  dominant kernel (K2 backward) achieved TFLOPS ÷ measured sustained bf16 peak
-  cpu_baseline  the float64 oracle port of the reference executors on the host cores
-                (bounded sample; rank 0 only)
+  parallel  fwd 2·B·H·P·(Dqk+Dv), bwd 2·B·H·P·(3Dqk+2Dv), P = unmasked (i, j) pairs per (b, h)
+  linear    fwd B·H·S·(2c(Dk+Dv)+4·Dk·Dv) with c = 64 (lowering.py:396-399), bwd 2× fwd
 
-Multi-GPU (torchrun): every rank runs its own cfg2 batch (weak scaling: batch×head units are
-independent, no data-path collective); time = max over ranks.  ``--impl reference`` times the
+  value     device-resident throughput (inputs in HBM before the timed region), TFLOPS
+  e2e       the same metric through the public host-buffer API (pipeline.HostPipeline): pinned
+            host inputs → H2D, kernels, D2H of every output, all inside the timed region
+  roofline  dominant kernel (K2 backward, or the forward of forward-only configs): achieved
+            TFLOPS ÷ measured sustained bf16 peak, or algorithmic GB/s ÷ measured HBM copy
+            bandwidth for the HBM-bound configs (MLA decode, linear template)
+  cpu_baseline  the float64 oracle port of the reference executors on the host cores (bounded
+                sample; rank 0, N=1 only)
+
+Multi-GPU (torchrun): every rank runs its own copy of the workload (weak scaling: batch×head units
+are independent, no data-path collective); time = max over ranks.  ``--impl reference`` times the
 reference's CPU algorithm (oracle port, all host cores) on rank 0 only.
 """
 
@@ -21,30 +26,55 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
 import sys
 import threading
 import time
+from dataclasses import dataclass
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-B, HQ, HKV, S, D = 8, 32, 8, 8192, 128
-PAIRS = S * (S + 1) // 2
-FWD_FLOPS = 2 * B * HQ * PAIRS * (D + D)
-BWD_FLOPS = 2 * B * HQ * PAIRS * (3 * D + 2 * D)
-STEP_FLOPS = FWD_FLOPS + BWD_FLOPS
 METRIC = "attention fwd+bwd TFLOPS & % bf16 tensor peak at 1/2/4/8 B200 vs CPU ref"
-WORKLOAD = "cfg2: Llama-3 8B GQA causal softmax attention fwd+bwd, bf16, B8 Hq32 Hkv8 S8192 D128"
+L2_BYTES = 126 * 2 ** 20
 
 _REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                 0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                 0x100: "display_clock_setting"}
+
+
+@dataclass(frozen=True)
+class Workload:
+    key: str
+    title: str
+    backward: bool
+    bound: str                 # "tensor" | "hbm" | "fp32-fma"
+    precision: str = "bf16"
+    cpu_seq: int = 1024        # sequence length of one CPU-baseline slice
+
+
+WORKLOADS = {
+    "cfg1": Workload("cfg1", "cfg1: causal softmax attention fwd, fp32, B1 H4 S512 D64 (the "
+                     "reference's own CPU-runnable case; exact-FFMA fp32 path)", False,
+                     "fp32-fma", "fp32", 512),
+    "cfg2": Workload("cfg2", "cfg2: Llama-3 8B GQA causal softmax attention fwd+bwd, bf16, B8 "
+                     "Hq32 Hkv8 S8192 D128", True, "tensor"),
+    "cfg3": Workload("cfg3", "cfg3: sigmoid attention + relative-position score_mod + causal "
+                     "sliding-window (W1024) mask_mod fwd+bwd, bf16, B8 H16 S4096 D128", True,
+                     "tensor", cpu_seq=2048),
+    "cfg4a": Workload("cfg4a", "cfg4a: DeepSeek-V2 MLA prefill fwd+bwd (latent KV, Dqk576 "
+                      "Dv512), bf16, B1 H128 S4096 causal", True, "tensor", cpu_seq=512),
+    "cfg4b": Workload("cfg4b", "cfg4b: DeepSeek-V2 MLA decode (Dqk576 Dv512), bf16, B16 H128 "
+                      "Sq1 over a 32k latent KV cache", False, "hbm", cpu_seq=4096),
+    "cfg5a": Workload("cfg5a", "cfg5a: RetNet retention (linear template, chunked) fwd+bwd, "
+                      "bf16, B4 H16 S8192 Dk=Dv=256", True, "hbm"),
+    "cfg5b": Workload("cfg5b", "cfg5b: Mamba2 SSD (linear template, chunked, differentiable "
+                      "gate/decay) fwd+bwd, bf16, B4 H32 S8192 Dk=Dv=128", True, "hbm"),
+}
 
 
 def dist_env():
@@ -62,6 +92,40 @@ def peaks() -> dict:
             "source": "fallback"}
 
 
+# ───────────────────────────── work model ─────────────────────────────
+
+def work(spec) -> dict:
+    """Algorithmic flops and HBM bytes of one forward / backward of ``spec``."""
+    from paper_2502_15349_b200 import configs
+    from paper_2502_15349_b200.spec import Pattern
+    d = spec.dims
+    b, h, hkv = d.batch, d.heads, d.kv_heads
+    if spec.pattern is Pattern.PARALLEL:
+        pairs = configs.unmasked_pairs(spec)
+        fwd = 2 * b * h * pairs * (d.d_qk + d.d_v)
+        bwd = 2 * b * h * pairs * (3 * d.d_qk + 2 * d.d_v)
+        kv = b * hkv * d.seq_k * (d.d_qk + (0 if spec.kv_shared else d.d_v)) * 2
+        qo = b * h * d.seq_q * (d.d_qk + d.d_v) * 2
+        fwd_bytes = kv + qo + b * h * d.seq_q * 4
+        bwd_bytes = 2 * (kv + qo) + b * h * d.seq_q * (d.d_v * 2 + 4)
+    else:
+        c = 64
+        fwd = b * h * d.seq_q * (2 * c * (d.d_qk + d.d_v) + 4 * d.d_qk * d.d_v)
+        bwd = 2 * fwd
+        tok = b * h * d.seq_q
+        ext = sum(4 * tok for _ in spec.extra_inputs)
+        fwd_bytes = tok * (2 * d.d_qk + 2 * d.d_v) * 2 + ext
+        bwd_bytes = tok * (2 * d.d_qk + d.d_v) * 2 * 2 + tok * d.d_v * 2 + 2 * ext
+    return {"fwd_flops": fwd, "bwd_flops": bwd, "fwd_bytes": fwd_bytes, "bwd_bytes": bwd_bytes}
+
+
+def build_spec(key: str, **kw):
+    from paper_2502_15349_b200 import configs
+    return configs.CONFIGS[key](**kw)
+
+
+# ───────────────────────────── clocks ─────────────────────────────
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -75,10 +139,11 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.15)
         except OSError:
             self.proc = None
         return self
@@ -116,37 +181,66 @@ class ClockSampler:
 
 # ───────────────────────────── CPU baseline (oracle port) ─────────────────────────────
 
+def _cpu_sample_spec(key: str, s_len: int):
+    """One (b, h) slice of the workload at a bounded sequence length."""
+    w = WORKLOADS[key]
+    if key == "cfg1":
+        return build_spec(key)          # runs in full
+    if key == "cfg2":
+        return build_spec(key, batch=1, heads=1, heads_kv=1, seq=s_len)
+    if key == "cfg3":
+        return build_spec(key, batch=1, heads=1, seq=s_len)
+    if key == "cfg4a":
+        return build_spec(key, batch=1, heads=1, seq=s_len)
+    if key == "cfg4b":
+        return build_spec(key, batch=1, heads=8, seq_k=s_len)
+    assert w.bound == "hbm"
+    return build_spec(key, batch=1, heads=1, seq=s_len)
+
+
 def _cpu_slice(args):
-    s_len, seed = args
+    key, s_len, seed = args
     import numpy as np
     from threadpoolctl import threadpool_limits
     import oracle
-    from oracle import parallel as OP
-    from paper_2502_15349_b200 import spec as SP
+    from oracle import parallel as OP, recurrent as OR
+    from paper_2502_15349_b200.spec import Pattern
+    spec = _cpu_sample_spec(key, s_len)
+    w = WORKLOADS[key]
     with threadpool_limits(1):
-        spec = SP.with_causal_mask(SP.builtin("softmax", batch=1, heads=1, seq=s_len, d_qk=D,
-                                              d_v=D))
         arrays = oracle.generate(spec, seed)
-        t0 = time.perf_counter()
-        o = OP.tiled_forward(spec, arrays, 64, 64)
         rng = np.random.default_rng(seed)
-        OP.parallel_vjp(spec, arrays, rng.uniform(-1, 1, o.shape))
+        t0 = time.perf_counter()
+        if spec.pattern is Pattern.PARALLEL:
+            o = OP.tiled_forward(spec, arrays, 64, 64)
+            if w.backward:
+                OP.parallel_vjp(spec, arrays, rng.uniform(-1, 1, o.shape))
+        else:
+            o = OR.chunk_forward(spec, arrays, 64)
+            if w.backward:
+                OR.chunk_vjp(spec, arrays, rng.uniform(-1, 1, o.shape), chunk=64)
         return time.perf_counter() - t0
 
 
-def cpu_baseline(s_len: int = 1024, slices: int | None = None) -> dict:
-    """Oracle tiled forward + closed-form VJP (f64) on one (b,h) slice per host core."""
+def cpu_baseline(key: str, s_len: int | None = None, slices: int | None = None) -> dict:
+    """The f64 oracle port of the reference executors, one workload slice per host core."""
     import multiprocessing as mp
+    w = WORKLOADS[key]
+    s_len = s_len or w.cpu_seq
     cores = slices or (os.cpu_count() or 1)
+    if key == "cfg1":
+        cores = 1                       # the whole config is one sample
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(cores) as pool:
-        pool.map(_cpu_slice, [(s_len, i) for i in range(cores)])
+        pool.map(_cpu_slice, [(key, s_len, i) for i in range(cores)])
     wall = time.perf_counter() - t0
-    pairs = s_len * (s_len + 1) // 2
-    flops = cores * (2 * pairs * 2 * D + 2 * pairs * 5 * D)
+    wk = work(_cpu_sample_spec(key, s_len))
+    flops = cores * (wk["fwd_flops"] + (wk["bwd_flops"] if w.backward else 0))
+    what = "fwd + VJP" if w.backward else "fwd"
     return {"value": flops / wall / 1e12, "unit": "TFLOPS", "cores": cores, "kind": "port",
-            "sample": f"{cores} (b,h) slices of cfg2 at S={s_len} (causal softmax fwd 64x64 "
-                      f"tiles + VJP, float64 oracle, one process per core): {wall:.2f} s wall",
+            "sample": f"{cores} slice(s) of {key} ({_cpu_sample_spec(key, s_len).dims}), {what} "
+                      f"with the float64 oracle (tiled 64x64 / chunk 64), one process per core: "
+                      f"{wall:.2f} s wall",
             "wall_s": wall}
 
 
@@ -154,12 +248,12 @@ def run_reference(args) -> None:
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    w = WORKLOADS[args.config]
     for _ in range(args.warmup):
-        cpu_baseline(args.cpu_seq)
-    vals = []
-    t_total = 0.0
+        cpu_baseline(args.config, args.cpu_seq)
+    vals, t_total = [], 0.0
     for _ in range(args.steps):
-        r = cpu_baseline(args.cpu_seq)
+        r = cpu_baseline(args.config, args.cpu_seq)
         vals.append(r["value"])
         t_total += r["wall_s"]
     v = statistics.median(vals)
@@ -168,7 +262,7 @@ def run_reference(args) -> None:
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD + f" (CPU sample at S={args.cpu_seq})"},
+            "config": {"workload": w.title + " (CPU sample, see cpu_baseline.sample)"},
             "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -177,32 +271,65 @@ def run_reference(args) -> None:
 
 # ───────────────────────────── GPU arm ─────────────────────────────
 
-def run_gpu(args) -> None:
+def device_inputs(spec, dev, seed: int):
+    """Synthetic inputs of the workload's shapes: q/k/v uniform[-1,1] bf16 (fp32 for the fp32
+    path), extras by their declared fill (unit gates 0.5+0.45·U, per-head constants)."""
+    import torch
+    g = torch.Generator(device=dev).manual_seed(seed)
+    d = spec.dims
+
+    def rnd(*shape, dtype=torch.bfloat16):
+        return (torch.rand(*shape, device=dev, generator=g) * 2 - 1).to(dtype)
+
+    arrays = {"q": rnd(d.batch, d.heads, d.seq_q, d.d_qk),
+              "k": rnd(d.batch, d.kv_heads, d.seq_k, d.d_qk)}
+    if not spec.kv_shared:
+        arrays["v"] = rnd(d.batch, d.kv_heads, d.seq_k, d.d_v)
+    for e in spec.extra_inputs:
+        shape = e.resolve_shape(d)
+        if e.fill == "unit":
+            arrays[e.name] = 0.5 + 0.45 * rnd(*shape, dtype=torch.float32)
+        elif e.fill == "constant_decay":
+            gm = torch.tensor(e.fill_params["gamma"], device=dev, dtype=torch.float32)
+            view = [1, -1, 1, 1] if shape[1] > 1 else [1, 1, 1, 1]
+            arrays[e.name] = gm.reshape(view).expand(*shape).contiguous()
+        else:
+            arrays[e.name] = rnd(*shape, dtype=torch.float32)
+    dout = rnd(d.batch, d.heads, d.seq_q, d.d_v)
+    return arrays, dout
+
+
+def run_gpu(args, key: str) -> dict | None:
     import torch
     import torch.distributed as dist
     import paper_2502_15349_b200 as af
-    from paper_2502_15349_b200 import spec as SP
+    from paper_2502_15349_b200 import runtime as rt
+    from paper_2502_15349_b200.pipeline import HostPipeline
+    from paper_2502_15349_b200.spec import Pattern
 
+    w = WORKLOADS[key]
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    spec = SP.with_causal_mask(SP.builtin("softmax", batch=B, heads=HQ, heads_kv=HKV, seq=S,
-                                          d_qk=D, d_v=D))
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-
-    def rnd(*shape):
-        return (torch.rand(*shape, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
-
-    q, k, v, do = rnd(B, HQ, S, D), rnd(B, HKV, S, D), rnd(B, HKV, S, D), rnd(B, HQ, S, D)
-    arrays = {"q": q, "k": k, "v": v}
+    spec = build_spec(key)
+    wk = work(spec)
+    arrays, dout = device_inputs(spec, dev, 1234 + rank)
+    if w.precision == "fp32":
+        arrays = {k: v.float() for k, v in arrays.items()}
+    in_bytes = sum(t.numel() * t.element_size() for t in arrays.values())
+    flush = torch.empty(2 * L2_BYTES // 4, device=dev, dtype=torch.float32) \
+        if in_bytes < 2 * L2_BYTES else None
     stream = torch.cuda.current_stream()
+    parallel = spec.pattern is Pattern.PARALLEL
 
-    def step():
-        o, lse = af.parallel_forward(spec, arrays)
-        grads = af.parallel_backward(spec, arrays, o, lse, do)
-        return o, grads
+    def fwd():
+        if parallel:
+            return af.parallel_forward(spec, arrays, precision=w.precision)
+        return af.linear_forward(spec, arrays), None
+
+    def bwd(o, lse):
+        if parallel:
+            return af.parallel_backward(spec, arrays, o, lse, dout)
+        return af.linear_backward(spec, arrays, dout)
 
     def barrier():
         if world > 1:
@@ -210,23 +337,26 @@ def run_gpu(args) -> None:
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        step()
+        o, lse = fwd()
+        if w.backward:
+            bwd(o, lse)
     barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    launches0 = rt.launch_count()
     with ClockSampler(local) as clk:
         barrier()
-        start.record(stream)
         for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()
             ev[i][0].record(stream)
-            o, lse = af.parallel_forward(spec, arrays)
+            o, lse = fwd()
             ev[i][1].record(stream)
-            af.parallel_backward(spec, arrays, o, lse, do)
+            if w.backward:
+                bwd(o, lse)
             ev[i][2].record(stream)
-        stop.record(stream)
         barrier()
-    ms = start.elapsed_time(stop) / args.steps
+    launches = rt.launch_count() - launches0
+    ms = sum(a.elapsed_time(c) for a, _, c in ev) / args.steps
     fwd_ms = sum(a.elapsed_time(b) for a, b, _ in ev) / args.steps
     bwd_ms = sum(b.elapsed_time(c) for _, b, c in ev) / args.steps
     t = torch.tensor([ms, fwd_ms, bwd_ms], device=dev)
@@ -234,80 +364,92 @@ def run_gpu(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, fwd_ms, bwd_ms = (float(x) for x in t.tolist())
 
-    # e2e through the public API with pinned host buffers
-    hq, hk, hv, hdo = (x.cpu().pin_memory() for x in (q, k, v, do))
-    ho = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
-    hdq = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
-    hdk = torch.empty(k.shape, dtype=torch.bfloat16).pin_memory()
-    hdv = torch.empty(v.shape, dtype=torch.bfloat16).pin_memory()
-    h2d = sum(x.numel() * 2 for x in (hq, hk, hv, hdo))
-    d2h = sum(x.numel() * 2 for x in (ho, hdq, hdk, hdv))
-
-    def e2e_step():
-        dq_, dk_, dv_, ddo = (x.to(dev, non_blocking=True) for x in (hq, hk, hv, hdo))
-        arr = {"q": dq_, "k": dk_, "v": dv_}
-        o_, lse_ = af.parallel_forward(spec, arr)
-        gr = af.parallel_backward(spec, arr, o_, lse_, ddo)
-        ho.copy_(o_, non_blocking=True)
-        hdq.copy_(gr["q"], non_blocking=True)
-        hdk.copy_(gr["k"], non_blocking=True)
-        hdv.copy_(gr["v"], non_blocking=True)
-
-    e2e_steps = max(1, min(args.steps, 5))
-    e2e_step()
+    # e2e through the public host-buffer API: pinned host inputs, H2D + kernels + D2H per step
+    pipe = HostPipeline(spec, device=dev, precision=w.precision)
+    host = {k: v.cpu().pin_memory() for k, v in arrays.items()}
+    hdo = dout.cpu().pin_memory() if w.backward else None
+    out = pipe(host, hdo)
     barrier()
+    h2d = sum(t.numel() * t.element_size() for t in host.values()) + \
+        (hdo.numel() * hdo.element_size() if hdo is not None else 0)
+    d2h = sum(t.numel() * t.element_size() for t in out.values())
+    e2e_steps = max(1, min(args.steps, 5))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
-        e2e_step()
+        pipe(host, hdo, out=out)
     e1.record(stream)
     barrier()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
+    del out, host, hdo, pipe
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.cpu_seq)
+        cpu = cpu_baseline(key, args.cpu_seq)
         cpu.pop("wall_s", None)
+    if rank != 0:
+        return None
 
-    if rank == 0:
-        pk = peaks()
-        value = world * STEP_FLOPS / (ms * 1e-3) / 1e12
-        bwd_tf = BWD_FLOPS / (bwd_ms * 1e-3) / 1e12
-        traffic = None
-        prof = ROOT / "profiles" / "roofline_traffic.json"
-        if prof.exists():
-            traffic = json.loads(prof.read_text()).get("bwd_dram_bytes_per_launch")
-        line = {
-            "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (uniform[-1,1] bf16, random per rank)",
-            "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": S,
-                       "heads_q": HQ, "heads_kv": HKV, "head_dim": D, "causal": True,
-                       "parallelism": f"batchxhead shards, {world} rank(s), no collective",
-                       "l2": "inputs larger than L2 (q 537 MB, k/v 134 MB each)"},
-            "frac_of_peak": value / world / pk["tflops_sustained"],
-            "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
-            "fwd_tflops": FWD_FLOPS / (fwd_ms * 1e-3) / 1e12, "bwd_tflops": bwd_tf,
-            "e2e": {"value": world * STEP_FLOPS / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
-            "roofline": {"kernel": "K2 parallel backward (af_parallel_bwd: K2a dK/dV + K2b dQ + "
-                                   "row-stat preprocess)",
-                         "bound": "tensor", "achieved": bwd_tf, "peak": pk["tflops_sustained"],
-                         "unit": "TFLOP/s", "frac": bwd_tf / pk["tflops_sustained"],
-                         "traffic": traffic,
-                         "peak_source": f"{pk['source']} bf16_tflops_sustained"},
-            "gpu_launches": args.steps * 4,  # K1 + preprocess + K2a + K2b per step
-            "clocks": clk.summary(),
-        }
-        if cpu is not None:
-            line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    pk = peaks()
+    step_flops = wk["fwd_flops"] + (wk["bwd_flops"] if w.backward else 0)
+    value = world * step_flops / (ms * 1e-3) / 1e12
+    dom = "bwd" if w.backward else "fwd"
+    dom_ms = bwd_ms if w.backward else fwd_ms
+    traffic = None
+    prof = ROOT / "profiles" / "roofline_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(key, {}).get(f"{dom}_dram_bytes_per_launch")
+    if w.bound == "hbm":
+        achieved = wk[f"{dom}_bytes"] / (dom_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
+                "algorithmic_bytes": wk[f"{dom}_bytes"],
+                "peak_source": f"{pk['source']} hbm_gbs"}
+    elif w.bound == "tensor":
+        achieved = wk[f"{dom}_flops"] / (dom_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tflops_sustained"],
+                "unit": "TFLOP/s", "frac": achieved / pk["tflops_sustained"], "traffic": traffic,
+                "peak_source": f"{pk['source']} bf16_tflops_sustained"}
+    else:  # exact fp32 FFMA path: nominal CUDA-core peak, 148 SMs x 128 FMA/clk x 1.965 GHz
+        achieved = wk["fwd_flops"] / (fwd_ms * 1e-3) / 1e12
+        peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        roof = {"bound": "fp32-fma", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "peak_source": "nominal fp32 FFMA (no measured figure)"}
+    roof["kernel"] = {"fwd": "forward kernel(s) of the config", "bwd": "backward kernels of "
+                      "the config"}[dom]
+    d = spec.dims
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if w.precision == "fp32" else "bf16",
+        "data": "synthetic (uniform[-1,1] inputs, per-rank seed)",
+        "config": {"workload": w.title, "global_batch": d.batch * world, "seq_len": d.seq_q,
+                   "seq_k": d.seq_k, "heads_q": d.heads, "heads_kv": d.kv_heads,
+                   "d_qk": d.d_qk, "d_v": d.d_v,
+                   "parallelism": f"batchxhead shards, {world} rank(s), no collective",
+                   "l2": ("L2 flushed (2x126 MB write) before every step" if flush is not None
+                          else f"inputs larger than L2 ({in_bytes / 1e6:.0f} MB per rank)")},
+        "frac_of_peak": (value / world / pk["tflops_sustained"]) if w.bound == "tensor" else None,
+        "fwd_ms": fwd_ms, "bwd_ms": bwd_ms if w.backward else None,
+        "fwd_tflops": wk["fwd_flops"] / (fwd_ms * 1e-3) / 1e12,
+        "bwd_tflops": wk["bwd_flops"] / (bwd_ms * 1e-3) / 1e12 if w.backward else None,
+        "tokens_per_s": world * d.batch * d.seq_q / (ms * 1e-3),
+        "e2e": {"value": world * step_flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "api": "paper_2502_15349_b200.pipeline.HostPipeline (pinned host tensors; H2D, "
+                       "kernels and D2H overlapped over batch/KV-head chunks)"},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    return line
 
 
 def main() -> None:
@@ -316,14 +458,30 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-seq", type=int, default=1024)
+    ap.add_argument("--config", choices=sorted(WORKLOADS) + ["all"], default="cfg2")
+    ap.add_argument("--cpu-seq", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps
+    keys = sorted(WORKLOADS) if args.config == "all" else [args.config]
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_gpu(args)
+        for k in keys:
+            args.config = k
+            run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    for k in keys:
+        line = run_gpu(args, k)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        torch.cuda.empty_cache()
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

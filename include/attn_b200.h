@@ -60,7 +60,8 @@ int af_parallel_fwd(const af_parallel_desc* desc, const void* q, const void* k, 
 size_t af_parallel_bwd_workspace(const af_parallel_desc* desc);
 
 /* VJP of af_parallel_fwd for cotangent dO (bf16).  dq/dk/dv use the q/k/v strides of desc; dk/dv
- * are summed over the query heads of each GQA group.  Replaces engine.autodiff_grads
+ * are summed over the query heads of each GQA group.  MLA lowering ((d_qk, d_v) = (576, 512),
+ * heads_kv = 1, v == k): dk receives the latent-cache gradient dK + [dV, 0] and dv is unused.  Replaces engine.autodiff_grads
  * (engine.py:630) over attention.build_parallel (attention.py:389) with seed dO. */
 int af_parallel_bwd(const af_parallel_desc* desc, const void* q, const void* k, const void* v,
                     const void* o, const float* lse, const void* dout, void* dq, void* dk,
@@ -117,6 +118,7 @@ int af_mla_decode(const af_mla_desc* desc, const void* q, const void* kv, void* 
 const char* af_status_string(int status);
 const char* af_last_error(void);      /* thread-local message of the last failing call */
 int af_device_sm_count(void);
+uint64_t af_launch_count(void);   /* kernels this library has launched (process-wide) */
 
 #ifdef __cplusplus
 }

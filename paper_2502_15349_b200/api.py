@@ -196,12 +196,18 @@ def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tens
     _check_shape(dout, (d.batch, d.heads, d.seq_q, d.d_v), "dout")
     dq = torch.empty_like(q, memory_format=torch.contiguous_format)
     dk = torch.empty(k.shape, device=k.device, dtype=_BF16)
-    dv = torch.empty(d.batch, d.kv_heads, d.seq_k, d.d_v, device=k.device, dtype=_BF16)
+    if spec.kv_shared:
+        # MLA lowering: V aliases K[..., :d_v]; the kernel writes dK + [dV, 0] into dk
+        if q.stride() != dq.stride() or k.stride() != dk.stride():
+            q, k = q.contiguous(), k.contiguous()
+        v = k[..., : d.d_v]
+        dv = dk[..., : d.d_v]
+    else:
+        dv = torch.empty(d.batch, d.kv_heads, d.seq_k, d.d_v, device=k.device, dtype=_BF16)
+        # dq/dk/dv are written with the q/k/v strides of the descriptor: use contiguous copies
+        if q.stride() != dq.stride() or k.stride() != dk.stride() or v.stride() != dv.stride():
+            q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16)
-    # dq/dk/dv are written with the q/k/v strides of the descriptor: use contiguous copies
-    if q.stride() != dq.stride() or k.stride() != dk.stride() or v.stride() != dv.stride():
-        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-        desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16)
     L = rt.lib()
     ws_n = L.af_parallel_bwd_workspace(desc)
     ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
@@ -211,8 +217,6 @@ def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tens
                                rt.ptr(lse), dout.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                dv.data_ptr(), ws.data_ptr(), ws_n, _stream()), "af_parallel_bwd")
     if spec.kv_shared:
-        dk = dk.clone()
-        dk[..., : d.d_v] += dv
         return {"q": dq, "k": dk}
     return {"q": dq, "k": dk, "v": dv}
 

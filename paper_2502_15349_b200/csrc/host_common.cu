@@ -2,6 +2,7 @@
 // library has no link-time dependency on libcuda) and device queries.
 #include "host_common.h"
 
+#include <atomic>
 #include <mutex>
 
 namespace af {
@@ -39,6 +40,9 @@ void set_error(const char* fmt, ...) {
 }
 
 const char* last_error() { return g_last_error.c_str(); }
+
+std::atomic<uint64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void ensure_context() {
   // The library links the CUDA runtime statically; a thread that has not touched CUDA through
@@ -128,5 +132,7 @@ const char* af_status_string(int status) {
 const char* af_last_error(void) { return af::last_error(); }
 
 int af_device_sm_count(void) { return af::sm_count(); }
+
+uint64_t af_launch_count(void) { return af::g_launches.load(std::memory_order_relaxed); }
 
 }  // extern "C"

@@ -38,6 +38,9 @@ bool make_tmap_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype,
                   bool swizzle128);
 
 int sm_count();
+
+// Process-wide count of kernels this library launched (af_launch_count()).
+void note_launch();
 void ensure_context();
 
 }  // namespace af

@@ -83,6 +83,7 @@ int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
     attr = true;
   }
   dim3 grid(d->batch * d->heads * (a.dvv / kLinVB));
+  ::af::note_launch();
   kern<<<grid, 320, L::kTotal, s>>>(tq, tk, tv, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
@@ -128,7 +129,8 @@ extern "C" int af_linear_fwd(const af_linear_desc* d, const void* q, const void*
 extern "C" size_t af_linear_bwd_workspace(const af_linear_desc* d) {
   if (d == nullptr) return 0;
   const size_t rows = static_cast<size_t>(d->batch) * d->heads * d->seq;
-  size_t bytes = rows * 2 * sizeof(float);
+  const size_t slots = static_cast<size_t>(d->d_k) / 32;  // dot partials per 32-column slot
+  size_t bytes = rows * 2 * slots * sizeof(float);
   if (d->key_gate != nullptr) bytes += rows * static_cast<size_t>(d->d_k) * 2;  // bf16 Km
   return bytes;
 }
@@ -143,17 +145,19 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
   AF_REQUIRE(workspace_bytes >= af_linear_bwd_workspace(d), AF_ERR_INPUT, "workspace too small");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int64_t n = static_cast<int64_t>(d->batch) * d->heads * d->seq;
+  const int slots = d->d_k / 32;
   float* dq_dot = static_cast<float*>(workspace);
-  float* dk_dot = dq_dot + n;
-  AF_CUDA_CHECK(cudaMemsetAsync(workspace, 0, static_cast<size_t>(2 * n) * sizeof(float), s));
+  float* dk_dot = dq_dot + n * slots;
+  AF_CUDA_CHECK(cudaMemsetAsync(workspace, 0, static_cast<size_t>(2 * n * slots) * sizeof(float), s));
   // Gated keys, materialised once (see gate_keys_kernel)
   const void* km = k;
   const int64_t* km_st = d->k_stride;
   int64_t km_contig[4] = {static_cast<int64_t>(d->heads) * d->seq * d->d_k,
                           static_cast<int64_t>(d->seq) * d->d_k, d->d_k, 1};
   if (d->key_gate != nullptr) {
-    __nv_bfloat16* kmb = reinterpret_cast<__nv_bfloat16*>(dk_dot + n);
+    __nv_bfloat16* kmb = reinterpret_cast<__nv_bfloat16*>(dk_dot + n * slots);
     const int64_t thr = n * (d->d_k / 8);
+    ::af::note_launch();
     gate_keys_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, s>>>(
         static_cast<const __nv_bfloat16*>(k), d->k_stride[0], d->k_stride[1], d->k_stride[2],
         step_tensor(d->key_gate, d->key_gate_stride), d->heads, d->seq, d->d_k, kmb, n);
@@ -188,7 +192,9 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
       AF_REQUIRE(d->key_gate != nullptr, AF_ERR_INPUT, "d_key_gate without a key gate");
       g = step_tensor(d_key_gate, d->key_gate_stride);
     }
-    linear_step_grads_kernel<<<d->batch * d->heads, 256, 0, s>>>(dq_dot, dk_dot, p, f0, f1, g);
+    ::af::note_launch();
+    linear_step_grads_kernel<<<d->batch * d->heads, 256, 0, s>>>(dq_dot, dk_dot, slots, p, f0,
+                                                                  f1, g);
     AF_CUDA_CHECK(cudaGetLastError());
   }
   return AF_OK;

@@ -64,7 +64,8 @@ struct LinearParams {
   int64_t o_sb, o_sh, o_ss;
   const void* dot_x;    // optional bf16 X with element strides: dot[t] += X_t . o_t
   int64_t x_sb, x_sh, x_ss;
-  float* dot;           // [B, H, S] fp32 (accumulated across value blocks)
+  float* dot;           // [dv/32 slots][B, H, S] fp32: one partial per 32-column slot, summed
+                        // in slot order by linear_step_grads_kernel (deterministic)
 };
 
 template <int DK>
@@ -416,7 +417,9 @@ __global__ void __launch_bounds__(320, 1)
                 dotacc += bf16_lo_(xe[q2]) * ov[v * 8 + 2 * q2] +
                           bf16_hi_(xe[q2]) * ov[v * 8 + 2 * q2 + 1];
             }
-            atomicAdd(p.dot + (static_cast<int64_t>(b) * p.heads + h) * p.seq + t, dotacc);
+            const int64_t rows = static_cast<int64_t>(p.batch) * p.heads * p.seq;
+            p.dot[(vb * 2 + half) * rows + (static_cast<int64_t>(b) * p.heads + h) * p.seq + t] =
+                dotacc;
           }
         }
       }
@@ -437,14 +440,22 @@ __global__ void __launch_bounds__(320, 1)
 // d gate += dk_dot / gate (k_mod = k * gate: dL/dgate = k . dKm).  One block per (b, h) sequence; outputs accumulate with
 // the strides of the corresponding input (broadcast axes sum via atomics).
 __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
-                                         const float* __restrict__ dk_dot, LinearParams p,
-                                         StepTensor dfac0, StepTensor dfac1, StepTensor dgate) {
+                                         const float* __restrict__ dk_dot, int slots,
+                                         LinearParams p, StepTensor dfac0, StepTensor dfac1,
+                                         StepTensor dgate) {
   __shared__ float part[32];
   const int bh = blockIdx.x;
   const int b = bh / p.heads, h = bh % p.heads;
   const int64_t base = static_cast<int64_t>(bh) * p.seq;
   const int seq = p.seq;
-  auto val = [&](int t) { return dq_dot[base + t] - dk_dot[base + t]; };
+  const int64_t rows = static_cast<int64_t>(p.batch) * p.heads * p.seq;
+  // per-slot partial dots, summed in a fixed slot order
+  auto dot = [&](const float* x, int t) {
+    float a = 0.0f;
+    for (int sl = 0; sl < slots; ++sl) a += x[sl * rows + base + t];
+    return a;
+  };
+  auto val = [&](int t) { return dot(dq_dot, t) - dot(dk_dot, t); };
   const int per = (seq + blockDim.x - 1) / blockDim.x;
   const int t0 = threadIdx.x * per;
   const int t1 = min(seq, t0 + per);
@@ -471,7 +482,7 @@ __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
                   dloga / p.fac[f].at(b, h, t));
     if (dgate.ptr != nullptr)
       atomicAdd(const_cast<float*>(dgate.ptr) + b * dgate.sb + h * dgate.sh + t * dgate.ss,
-                dk_dot[base + t] / p.u_scale.at(b, h, t));
+                dot(dk_dot, t) / p.u_scale.at(b, h, t));
   }
 }
 

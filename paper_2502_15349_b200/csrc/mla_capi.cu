@@ -31,6 +31,7 @@ int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o
     attr = true;
   }
   const int q_tiles = (d->seq_q + 127) / 128;
+  ::af::note_launch();
   kern<<<q_tiles * d->batch * d->heads_q * 2, 192, MlaSmem::kTotal, s>>>(tq, tkv, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
@@ -92,8 +93,10 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
     AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MlaSmem::kTotal));
     attr = true;
   }
+  ::af::note_launch();
   kern<<<d->batch * splits * 2, 192, MlaSmem::kTotal, s>>>(tq, tkv, p);
   AF_CUDA_CHECK(cudaGetLastError());
+  ::af::note_launch();
   mla_combine_kernel<<<d->batch * d->heads, kMlaDv / 4, 0, s>>>(
       part_o, part_lse, d->batch, d->heads, splits, static_cast<__nv_bfloat16*>(o), lse);
   AF_CUDA_CHECK(cudaGetLastError());

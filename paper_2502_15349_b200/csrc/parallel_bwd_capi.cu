@@ -5,6 +5,11 @@
 
 namespace af {
 int validate_parallel(const af_parallel_desc* d);
+size_t mla_bwd_workspace(const af_parallel_desc* d);
+int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void* o,
+            const float* lse, const void* dout, void* dq, void* dkv, void* workspace,
+            cudaStream_t s);
+inline bool is_mla(const af_parallel_desc* d) { return d->d_qk == 576 && d->d_v == 512; }
 namespace {
 
 inline int64_t pad_q(int seq_q) { return ((seq_q + kBlockM - 1) / kBlockM) * kBlockM; }
@@ -33,6 +38,7 @@ int launch_bwd(const BwdLaunch& a) {
       attr = true;
     }
     dim3 grid((a.d->seq_k + kBlockN - 1) / kBlockN, a.d->batch * a.d->heads_kv);
+    ::af::note_launch();
     kern<<<grid, 320, L::kTotal, a.s>>>(a.tq, a.tk, a.tv, a.tdo, a.p, a.lse2, a.delta, a.pad);
     AF_CUDA_CHECK(cudaGetLastError());
   }
@@ -45,6 +51,7 @@ int launch_bwd(const BwdLaunch& a) {
       attr = true;
     }
     dim3 grid((a.d->seq_q + kBlockM - 1) / kBlockM, a.d->batch * a.d->heads_q);
+    ::af::note_launch();
     kern<<<grid, 320, L::kTotal, a.s>>>(
         a.tk, a.tv, a.p, static_cast<const __nv_bfloat16*>(a.q),
         static_cast<const __nv_bfloat16*>(a.dout), a.d->q_stride[0], a.d->q_stride[1],
@@ -73,6 +80,7 @@ int dispatch_bwd(const BwdLaunch& a) {
 
 extern "C" size_t af_parallel_bwd_workspace(const af_parallel_desc* d) {
   if (d == nullptr) return 0;
+  if (af::is_mla(d)) return af::mla_bwd_workspace(d);
   const int64_t rows = static_cast<int64_t>(d->batch) * d->heads_q * af::pad_q(d->seq_q);
   return static_cast<size_t>(rows) * 2 * sizeof(float);
 }
@@ -90,6 +98,12 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
   AF_REQUIRE(d->family != AF_FAMILY_SOFTMAX || lse != nullptr, AF_ERR_INPUT,
              "softmax backward needs the forward LSE");
   AF_REQUIRE(d->q_stride[3] == 1 && d->o_stride[3] == 1, AF_ERR_INPUT, "feature stride must be 1");
+  if (is_mla(d)) {
+    // MLA lowering: V = K[:, :512] of one latent head; dk receives dK + [dV, 0], dv is unused
+    AF_REQUIRE(v == k && d->v_stride[0] == d->k_stride[0] && d->v_stride[2] == d->k_stride[2],
+               AF_ERR_UNSUPPORTED, "(576, 512) heads are lowered only as MLA (V = K[:, :512])");
+    return mla_bwd(d, q, k, o, lse, dout, dq, dk, workspace, reinterpret_cast<cudaStream_t>(stream));
+  }
   if (!((d->d_qk == 128 && d->d_v == 128) || (d->d_qk == 64 && d->d_v == 64))) {
     set_error("bf16 parallel backward: head dims (%d, %d) not instantiated", d->d_qk, d->d_v);
     return AF_ERR_UNSUPPORTED;
@@ -122,6 +136,7 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
     const int threads = 256;
     const unsigned blocks = static_cast<unsigned>((rows * 32 + threads - 1) / threads);
     auto pre = (d->d_v == 128) ? bwd_preprocess_kernel<128> : bwd_preprocess_kernel<64>;
+    ::af::note_launch();
     pre<<<blocks, threads, 0, a.s>>>(static_cast<const __nv_bfloat16*>(o),
                                      static_cast<const __nv_bfloat16*>(dout), lse, d->o_stride[0],
                                      d->o_stride[1], d->o_stride[2], d->o_stride[0],

@@ -21,6 +21,7 @@ int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorM
     attr_done = true;
   }
   dim3 grid((d->seq_q + 2 * kBlockM - 1) / (2 * kBlockM), d->batch * d->heads_q);
+  ::af::note_launch();
   kern<<<grid, kFwdThreads, L::kTotal, stream>>>(tq, tk, tv, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;

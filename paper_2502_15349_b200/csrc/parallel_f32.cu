@@ -124,6 +124,7 @@ extern "C" int af_parallel_fwd_f32(const af_parallel_desc* d, const void* q, con
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   dim3 grid((d->seq_q + kRows - 1) / kRows, d->batch * d->heads_q);
   auto args = [&](auto kern) {
+    ::af::note_launch();
     kern<<<grid, kRows, 0, s>>>(static_cast<const float*>(q), static_cast<const float*>(k),
                                 static_cast<const float*>(v), *d, static_cast<float*>(o), lse);
   };

@@ -79,7 +79,9 @@ AF_DEVICE bool kept(const MaskParams& m, int i, int j, int seq_k) {
 template <int kAct>
 AF_DEVICE float apply_act(float z) {
   if constexpr (kAct == kActSigmoid) {
-    return __frcp_rn(1.0f + ex2(-z * kLog2e));
+    // 1 / (1 + 2^(-z log2 e)): two MUFU ops (ex2, rcp.approx); __frcp_rn's IEEE fix-up path
+    // costs ~10x more and made the sigmoid variants SFU-latency bound.
+    return rcp_approx(1.0f + ex2(-z * kLog2e));
   } else if constexpr (kAct == kActRelu) {
     return fmaxf(z, 0.0f);
   } else {

@@ -1,0 +1,188 @@
+"""Host-buffer executor: H2D copy, kernels and D2H copy overlapped over independent units.
+
+The reference's callers hand the executors host arrays and read host arrays back
+(``engine.run_tiled_parallel`` / ``autodiff_grads``, engine.py:423, 630).  On a B200 the naive
+translation — copy everything in, compute, copy everything out — serialises two PCIe transfers
+with the kernels.  Batch × KV-head units are independent, so this executor splits the
+work into unit chunks and runs three CUDA streams:
+
+    h2d  : copy chunk c+1's inputs (pinned host → a device slot)
+    comp : K1 forward + K2 backward (or K4/K5) on chunk c
+    d2h  : copy chunk c-1's outputs back into the caller's pinned host tensors
+
+Host→device and device→host use separate copy engines, so in steady state the step costs
+max(H2D, kernels, D2H) per chunk instead of their sum.  Device input slots are double-buffered;
+output tensors come from the caching allocator and are ``record_stream``-ed onto the d2h stream.
+The call is stream-ordered with the caller's current stream on both ends (its events bracket the
+whole pipeline).
+"""
+
+from __future__ import annotations
+
+from dataclasses import replace
+
+import torch
+
+from . import api
+from .errors import InputError
+from .plan import plan_linear, plan_parallel
+from .spec import AttentionSpec, Pattern
+
+
+def _chunks(spec: AttentionSpec, max_chunks: int) -> list[tuple[int, int, int]]:
+    """(batch index | -1 for a batch range, lo, hi): batch ranges when B > 1, else KV-head
+    group ranges of the single batch element."""
+    d = spec.dims
+    if d.batch > 1:
+        n = min(max_chunks, d.batch)
+        bounds = [round(i * d.batch / n) for i in range(n + 1)]
+        return [(-1, bounds[i], bounds[i + 1]) for i in range(n)]
+    g = d.kv_heads
+    n = min(max_chunks, g)
+    bounds = [round(i * g / n) for i in range(n + 1)]
+    return [(0, bounds[i], bounds[i + 1]) for i in range(n)]
+
+
+def _sub_spec(spec: AttentionSpec, unit) -> AttentionSpec:
+    b, lo, hi = unit
+    d = spec.dims
+    if b < 0:
+        return replace(spec, dims=replace(d, batch=hi - lo))
+    r = d.heads // d.kv_heads
+    heads_kv = None if d.heads_kv is None else hi - lo
+    return replace(spec, dims=replace(d, batch=1, heads=(hi - lo) * r, heads_kv=heads_kv))
+
+
+def _slice(t: torch.Tensor, spec: AttentionSpec, unit, kv: bool) -> torch.Tensor:
+    """Slice a [B|1, H|1, ...] host tensor to one unit chunk."""
+    b, lo, hi = unit
+    d = spec.dims
+    if b < 0:
+        return t[lo:hi] if t.shape[0] > 1 else t
+    r = 1 if kv else d.heads // d.kv_heads
+    t = t[0:1]
+    return t[:, lo * r: hi * r] if t.shape[1] > 1 else t
+
+
+def _same_lowering(spec: AttentionSpec, sub: AttentionSpec) -> bool:
+    """A hook that reads the ``batch``/``heads`` constants would change meaning in a chunk."""
+    if spec.pattern is Pattern.PARALLEL:
+        a, b = plan_parallel(spec), plan_parallel(sub)
+        return (a.family, a.act, a.scale, a.bias, a.slope_const, a.band) == \
+               (b.family, b.act, b.scale, b.bias, b.slope_const, b.band)
+    a, b = plan_linear(spec), plan_linear(sub)
+    return (a.q_scale, a.decay_const) == (b.q_scale, b.decay_const)
+
+
+class HostPipeline:
+    """``HostPipeline(spec)(host_arrays, host_dout=None)`` → dict of pinned host tensors.
+
+    Forward only (``host_dout is None``): ``{"o", "lse"?}``.  Forward + backward: also the
+    gradients ``{"q", "k", "v"?, ...}`` exactly as ``parallel_backward`` / ``linear_backward``
+    return them.  ``out`` may pass preallocated pinned host tensors (same keys) to avoid
+    allocating pinned memory per call."""
+
+    def __init__(self, spec, device=None, max_chunks: int = 8, precision: str = "bf16"):
+        self.spec = api._spec(spec)
+        self.precision = precision
+        self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
+                       else torch.device(device))
+        units = _chunks(self.spec, max_chunks)
+        if len(units) > 1 and not _same_lowering(self.spec, _sub_spec(self.spec, units[0])):
+            units = [(-1, 0, self.spec.dims.batch)]  # one chunk: the spec itself
+        self.units = units
+        self.h2d = torch.cuda.Stream(self.device)
+        self.comp = torch.cuda.Stream(self.device)
+        self.d2h = torch.cuda.Stream(self.device)
+        self._slots: list[dict] = [{}, {}]
+
+    # device slot tensor for one host slice (reused across calls of the same shape)
+    def _slot(self, s: int, name: str, like: torch.Tensor) -> torch.Tensor:
+        t = self._slots[s].get(name)
+        if t is None or t.shape != like.shape or t.dtype != like.dtype:
+            with torch.cuda.stream(self.h2d):
+                t = torch.empty(like.shape, dtype=like.dtype, device=self.device)
+            self._slots[s][name] = t
+        return t
+
+    def _outputs_like(self, dev_out: dict) -> dict:
+        d = self.spec.dims
+        out = {}
+        for name, t in dev_out.items():
+            if t is None:
+                continue
+            shape = list(t.shape)
+            if self.units[0][0] < 0:
+                shape[0] = d.batch
+            else:
+                kv = name in ("k", "v") and d.heads_kv is not None
+                shape[1] = d.kv_heads if kv else d.heads
+            out[name] = torch.empty(shape, dtype=t.dtype).pin_memory()
+        return out
+
+    def _run_unit(self, arrays: dict, dout):
+        spec = self._unit_spec
+        if spec.pattern is Pattern.PARALLEL:
+            o, lse = api.parallel_forward(spec, arrays, precision=self.precision)
+            res = {"o": o, "lse": lse}
+            if dout is not None:
+                res.update(api.parallel_backward(spec, arrays, o, lse, dout))
+        else:
+            o = api.linear_forward(spec, arrays)
+            res = {"o": o}
+            if dout is not None:
+                res.update(api.linear_backward(spec, arrays, dout))
+        return res
+
+    def __call__(self, host_arrays: dict, host_dout=None, out: dict | None = None) -> dict:
+        for name, t in list(host_arrays.items()) + ([("dout", host_dout)] if host_dout is not
+                                                    None else []):
+            if not isinstance(t, torch.Tensor) or t.is_cuda:
+                raise InputError("HostPipeline takes host tensors", name=name)
+        caller = torch.cuda.current_stream(self.device)
+        start = torch.cuda.Event()
+        start.record(caller)
+        for s in (self.h2d, self.comp, self.d2h):
+            s.wait_event(start)
+        kv_names = {"k", "v"}
+        in_ready = [torch.cuda.Event() for _ in self.units]
+        comp_done = [torch.cuda.Event() for _ in self.units]
+        host_out = out
+        for c, unit in enumerate(self.units):
+            s = c % 2
+            self._unit_spec = _sub_spec(self.spec, unit)
+            if c >= 2:
+                self.h2d.wait_event(comp_done[c - 2])  # slot s inputs no longer read
+            dev = {}
+            with torch.cuda.stream(self.h2d):
+                for name, t in host_arrays.items():
+                    if name in ("qidx", "kidx"):
+                        continue
+                    hs = _slice(t, self.spec, unit, name in kv_names)
+                    dt = self._slot(s, name, hs)
+                    dt.copy_(hs, non_blocking=True)
+                    dev[name] = dt
+                ddo = None
+                if host_dout is not None:
+                    hs = _slice(host_dout, self.spec, unit, False)
+                    ddo = self._slot(s, "dout", hs)
+                    ddo.copy_(hs, non_blocking=True)
+                in_ready[c].record(self.h2d)
+            self.comp.wait_event(in_ready[c])
+            with torch.cuda.stream(self.comp):
+                res = self._run_unit(dev, ddo)
+                comp_done[c].record(self.comp)
+            if host_out is None:
+                host_out = self._outputs_like(res)
+            self.d2h.wait_event(comp_done[c])
+            with torch.cuda.stream(self.d2h):
+                for name, t in res.items():
+                    if t is None:
+                        continue
+                    t.record_stream(self.d2h)
+                    _slice(host_out[name], self.spec, unit, name in kv_names and
+                           self.spec.dims.heads_kv is not None).copy_(t, non_blocking=True)
+        end = torch.cuda.Event()
+        end.record(self.d2h)
+        caller.wait_event(end)
+        return host_out

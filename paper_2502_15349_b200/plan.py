@@ -373,7 +373,7 @@ def _affine_score(e, consts: dict, extras: dict):
     return tau, -dcoef, slope_extra, -slope_coef, bias
 
 
-def plan_parallel(spec: AttentionSpec) -> ParallelPlan:
+def _plan_parallel(spec: AttentionSpec) -> ParallelPlan:
     if spec.pattern is not Pattern.PARALLEL:
         raise InputError("variant is not a parallel-pattern variant", variant=spec.name)
     spec.validate()
@@ -469,7 +469,7 @@ def _substitute(e, name: str, by):
     return H.Fn(e.func, tuple(_substitute(a, name, by) for a in e.args))
 
 
-def plan_linear(spec: AttentionSpec, chunk: int = 64) -> LinearPlan:
+def _plan_linear(spec: AttentionSpec, chunk: int = 64) -> LinearPlan:
     if spec.pattern is not Pattern.RECURRENT:
         raise InputError("variant is not a recurrent-pattern variant", variant=spec.name)
     spec.validate()
@@ -520,3 +520,31 @@ def plan_linear(spec: AttentionSpec, chunk: int = 64) -> LinearPlan:
     q_scale = _scalar_mod(spec.q_mod, "q", consts)
     return LinearPlan(spec, q_scale=q_scale, decay_factors=tuple(names), decay_const=const,
                       k_gate=k_gate, chunk=chunk)
+
+
+# ───────────────────────────── plan cache ─────────────────────────────
+# Lowering classifies hooks numerically (milliseconds of host work); a spec's plan is a pure
+# function of the spec, so plans are memoised by the spec's repr (specs may hold unhashable
+# fill-parameter dicts).  Bounded, insertion-ordered eviction.
+_CACHE: dict = {}
+_CACHE_MAX = 256
+
+
+def _cached(key, make):
+    hit = _CACHE.get(key)
+    if hit is None:
+        hit = make()
+        if len(_CACHE) >= _CACHE_MAX:
+            _CACHE.pop(next(iter(_CACHE)))
+        _CACHE[key] = hit
+    return hit
+
+
+def plan_parallel(spec: AttentionSpec) -> ParallelPlan:
+    """Lower a parallel-pattern spec to its kernel plan (memoised; see ``_plan_parallel``)."""
+    return _cached(("parallel", repr(spec)), lambda: _plan_parallel(spec))
+
+
+def plan_linear(spec: AttentionSpec, chunk: int = 64) -> LinearPlan:
+    """Lower a recurrent-pattern spec to its kernel plan (memoised; see ``_plan_linear``)."""
+    return _cached(("linear", chunk, repr(spec)), lambda: _plan_linear(spec, chunk))

@@ -73,6 +73,7 @@ SIGNATURES: dict[str, tuple] = {
     "af_status_string": (C.c_char_p, [C.c_int]),
     "af_last_error": (C.c_char_p, []),
     "af_device_sm_count": (C.c_int, []),
+    "af_launch_count": (C.c_uint64, []),
 }
 
 _lock = threading.Lock()
@@ -127,3 +128,8 @@ def strides4(t) -> I64x4:
 def step_strides(t) -> I64x3:
     """[b, h, s] element strides of a rank-4 per-step tensor [B|1, H|1, S, 1] (0 = broadcast)."""
     return I64x3(*[0 if t.shape[i] == 1 else int(t.stride(i)) for i in range(3)])
+
+
+def launch_count() -> int:
+    """Kernels the native library has launched in this process (its own counter)."""
+    return int(lib().af_launch_count())
