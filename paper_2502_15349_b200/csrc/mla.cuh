@@ -9,8 +9,11 @@
 //             over (batch, key split, value half); splits are merged by mla_combine_kernel.
 // Budget: the fp32 O accumulator of 128 rows x 512 would fill all of TMEM, so each CTA owns one
 // 256-wide value half (the two halves recompute S; 1.53x the QK^T work).  Q (128 x 576 bf16,
-// 144 KB) stays in shared memory; the latent KV streams through a 2-stage ring of 32-token tiles
-// (36 KB each).  TMEM: S double buffer [0,64) (P packed in place) | O [256,512).
+// 144 KB) is split: columns [0, 256) sit in TMEM as the A operand of TS MMAs (no shared-memory
+// A reads — the S GEMM at N = 64 is otherwise bound by re-reading Q from smem every tile),
+// columns [256, 576) stay in smem (80 KB), which leaves room for a 2-stage ring of 64-key latent
+// tiles (72 KB each).  TMEM: S double buffer [0,128) (P packed in place) | O half [128,384) |
+// Q[:, 0:256] packed bf16 [384,512).
 // Warps: 0-3 softmax rows (one row per thread, FA4-style lazy rescale), 4 TMA, 5 MMA.
 #pragma once
 #include <cuda.h>
@@ -23,7 +26,8 @@ namespace af {
 constexpr int kMlaDqk = 576;
 constexpr int kMlaDv = 512;
 constexpr int kMlaHalf = 256;
-constexpr int kMlaN = 32;  // keys per tile
+constexpr int kMlaN = 64;     // keys per tile
+constexpr int kMlaQT = 256;   // Q columns [0, 256) live in TMEM (TS MMA), [256, 576) in smem
 
 struct MlaParams {
   int batch, heads, seq_q, seq_k;
@@ -31,6 +35,9 @@ struct MlaParams {
   int causal;
   int splits;            // decode: key splits per batch
   int split_len;         // decode: keys per split (multiple of kMlaN)
+  // Q rows for the TMEM part (bf16, element strides [b, h, s]; decode: s = head, h unused)
+  const __nv_bfloat16* q;
+  int64_t q_sb, q_sh, q_ss;
   // prefill output (bf16 [B, H, Sq, 512], element strides) + LSE [B, H, Sq]
   void* o;
   int64_t o_sb, o_sh, o_ss;
@@ -40,14 +47,19 @@ struct MlaParams {
   float* part_lse;
 };
 
+// Shared memory: Q columns [256, 576) as 5 boxes [128 rows][64] (80 KB) + a 2-stage ring of
+// 64-key latent tiles (9 boxes [64 keys][64] = 72 KB each).  TMEM (512 columns): S double buffer
+// [0, 128) (P packed in place) | O half [128, 384) | Q columns [0, 256) packed bf16 [384, 512).
 struct MlaSmem {
-  static constexpr int kQBytes = 128 * kMlaDqk * 2;   // 9 boxes of [128 rows][128 B]
-  static constexpr int kKBytes = kMlaN * kMlaDqk * 2; // 9 boxes of [32 rows][128 B]
+  static constexpr int kQBox = 128 * 128;
+  static constexpr int kKBox = kMlaN * 128;
+  static constexpr int kQBytes = 5 * kQBox;
+  static constexpr int kKBytes = 9 * kKBox;
   static constexpr int kQOff = 0;
   static constexpr int kKOff = kQBytes;
   static constexpr int kBarOff = kKOff + 2 * kKBytes;
-  // q_full, k_full[2], k_empty[2], s_full[2], p_ready, o_done
-  static constexpr int kNumBars = 9;
+  // q_full, q_ready, k_full[2], k_empty[2], s_full[2], p_ready, o_done
+  static constexpr int kNumBars = 10;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -62,11 +74,12 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sK = smem + L::kKOff;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = bars + 3;
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_ready = bars + 7;
-  uint64_t* o_done = bars + 8;
+  uint64_t* q_ready = bars + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = bars + 4;
+  uint64_t* s_full = bars + 6;
+  uint64_t* p_ready = bars + 8;
+  uint64_t* o_done = bars + 9;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -95,6 +108,7 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 4 && lane_id() == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_ready, 4);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -109,25 +123,26 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr uint32_t kColO = 256;
+  constexpr uint32_t kColO = 128, kColQ = 384;
 
   if (warp == 4) {
     if (elect_one() && nk > 0) {
       mbar_expect_tx(q_full, L::kQBytes);
-      for (int c = 0; c < kMlaDqk / 64; ++c) {
+      for (int c = 0; c < 5; ++c) {
+        const int col = kMlaQT + c * 64;
         if constexpr (kDecode)
-          tma_load_4d(sQ + c * (128 * 128), &tm_q, q_full, c * 64, 0, b, 0);
+          tma_load_4d(sQ + c * L::kQBox, &tm_q, q_full, col, 0, b, 0);
         else
-          tma_load_4d(sQ + c * (128 * 128), &tm_q, q_full, c * 64, q0, h, b);
+          tma_load_4d(sQ + c * L::kQBox, &tm_q, q_full, col, q0, h, b);
       }
       for (int n = 0; n < nk; ++n) {
         const int s = n & 1;
         mbar_wait(&k_empty[s], ((n >> 1) & 1) ^ 1);
         mbar_expect_tx(&k_full[s], L::kKBytes);
         const int j0 = kv_lo + n * kMlaN;
-        for (int c = 0; c < kMlaDqk / 64; ++c)
-          tma_load_4d_hint(sK + s * L::kKBytes + c * (kMlaN * 128), &tm_kv, &k_full[s], c * 64,
-                           j0, b, 0, kEvictLast);
+        for (int c = 0; c < 9; ++c)
+          tma_load_4d_hint(sK + s * L::kKBytes + c * L::kKBox, &tm_kv, &k_full[s], c * 64, j0, b,
+                           0, kEvictLast);
       }
     }
   } else if (warp == 5) {
@@ -139,28 +154,33 @@ __global__ void __launch_bounds__(192, 1)
         const int s = n & 1;
         mbar_wait(&k_full[s], (n >> 1) & 1);
         tc_fence_after();
+        const uint32_t kb = aK + s * L::kKBytes;
 #pragma unroll
-        for (int kk = 0; kk < kMlaDqk / 16; ++kk)
+        for (int kk = 0; kk < kMlaQT / 16; ++kk)  // Q columns [0, 256) from TMEM
+          mma_ts(tmem + s * kMlaN, tmem + kColQ + kk * 8,
+                 make_sdesc(kb + (kk / 4) * L::kKBox + (kk % 4) * 32, 0, 1024), id_s, kk > 0);
+#pragma unroll
+        for (int kk = kMlaQT / 16; kk < kMlaDqk / 16; ++kk)  // columns [256, 576) from smem
           mma_ss(tmem + s * kMlaN,
-                 make_sdesc(aQ + (kk / 4) * (128 * 128) + (kk % 4) * 32, 0, 1024),
-                 make_sdesc(aK + s * L::kKBytes + (kk / 4) * (kMlaN * 128) + (kk % 4) * 32, 0,
-                            1024),
-                 id_s, kk > 0);
+                 make_sdesc(aQ + (kk / 4 - 4) * L::kQBox + (kk % 4) * 32, 0, 1024),
+                 make_sdesc(kb + (kk / 4) * L::kKBox + (kk % 4) * 32, 0, 1024), id_s, 1u);
         mma_commit(&s_full[s]);
       };
       mbar_wait(q_full, 0);
+      mbar_wait(q_ready, 0);
+      tc_fence_after();
       issue_s(0);
       for (int n = 0; n < nk; ++n) {
         const int s = n & 1;
         if (n + 1 < nk) issue_s(n + 1);
         mbar_wait(p_ready, n & 1);
         tc_fence_after();
-        // V = latent K columns [256*half, 256*half+256): 4 boxes of [32 keys][64 dv], MN-major
-        const uint32_t vbase = aK + s * L::kKBytes + half * 4 * (kMlaN * 128);
+        // V = latent columns [256*half, +256): boxes 4*half .. 4*half+3 of the tile, MN-major
+        const uint32_t vbase = aK + s * L::kKBytes + half * 4 * L::kKBox;
 #pragma unroll
         for (int kk = 0; kk < kMlaN / 16; ++kk)
           mma_ts(tmem + kColO, tmem + s * kMlaN + kk * 8,
-                 make_sdesc(vbase + kk * 2048, kMlaN * 128, 1024), id_o, (n > 0 || kk > 0));
+                 make_sdesc(vbase + kk * 2048, L::kKBox, 1024), id_o, (n > 0 || kk > 0));
         mma_commit(o_done);
         mma_commit(&k_empty[s]);
       }
@@ -170,20 +190,45 @@ __global__ void __launch_bounds__(192, 1)
     const int row = warp * 32 + static_cast<int>(lane_id());
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
     const int i = kDecode ? 0 : q0 + row;  // query position (prefill)
+    {  // Q columns [0, 256) of this row -> TMEM (packed bf16 pairs, A-operand layout)
+      const bool live = kDecode ? row < p.heads : i < p.seq_q;
+      const __nv_bfloat16* qrow =
+          kDecode ? p.q + b * p.q_sb + static_cast<int64_t>(live ? row : 0) * p.q_ss
+                  : p.q + b * p.q_sb + h * p.q_sh + static_cast<int64_t>(live ? i : 0) * p.q_ss;
+#pragma unroll
+      for (int c = 0; c < kMlaQT / 64; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint4 x = live ? *reinterpret_cast<const uint4*>(qrow + c * 64 + v * 8)
+                               : make_uint4(0u, 0u, 0u, 0u);
+          w[v * 4 + 0] = x.x;
+          w[v * 4 + 1] = x.y;
+          w[v * 4 + 2] = x.z;
+          w[v * 4 + 3] = x.w;
+        }
+        tmem_st32(tmem + lane_base + kColQ + c * 32, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(q_ready);
+    }
     float m_run = -INFINITY, l_run = 0.0f;
     for (int n = 0; n < nk; ++n) {
       const int s = n & 1;
       const int j0 = kv_lo + n * kMlaN;
       mbar_wait(&s_full[s], (n >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[32];
-      tmem_ld32(tmem + lane_base + s * kMlaN, sr);
+      uint32_t sr[64];
+      tmem_ld32(tmem + lane_base + s * kMlaN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(tmem + lane_base + s * kMlaN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
       tmem_ld_wait();
-      float x[32];
+      float x[64];
       float bmax = -INFINITY;
       const bool full = (j0 + kMlaN <= kv_hi) && (kDecode || !p.causal || j0 + kMlaN - 1 <= q0);
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
+      for (int e = 0; e < 64; ++e) {
         bool keep = true;
         if (!full) keep = (j0 + e < kv_hi) && (kDecode || !p.causal || j0 + e <= i);
         x[e] = keep ? __uint_as_float(sr[e]) * p.scale_log2 : -INFINITY;
@@ -197,16 +242,16 @@ __global__ void __launch_bounds__(192, 1)
         m_run = m_new;
       }
       const float m_use = (m_run == -INFINITY) ? 0.0f : m_run;
-      uint32_t pk[16];
+      uint32_t pk[32];
       float lsum = 0.0f;
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
+      for (int e = 0; e < 64; e += 2) {
         const float e0 = ex2(x[e] - m_use), e1 = ex2(x[e + 1] - m_use);
         lsum += e0 + e1;
         pk[e / 2] = pack_bf16(e0, e1);
       }
       l_run = l_run * factor + lsum;
-      tmem_st16(tmem + lane_base + s * kMlaN, pk);
+      tmem_st32(tmem + lane_base + s * kMlaN, pk);
       tmem_st_wait();
       if (n > 0 && __any_sync(0xffffffffu, need)) {
         mbar_wait(o_done, (n - 1) & 1);

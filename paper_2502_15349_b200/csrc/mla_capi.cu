@@ -22,6 +22,8 @@ int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o
              "MLA prefill supports the top-left causal mask (offset 0) only");
   AF_REQUIRE(d->window <= 0, AF_ERR_UNSUPPORTED, "MLA prefill has no sliding window");
   p.causal = d->causal;
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.q_sb = d->q_stride[0]; p.q_sh = d->q_stride[1]; p.q_ss = d->q_stride[2];
   p.o = o; p.o_sb = d->o_stride[0]; p.o_sh = d->o_stride[1]; p.o_ss = d->o_stride[2];
   p.lse = lse;
   auto kern = mla_fwd_kernel<false>;
@@ -81,6 +83,8 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
   p.batch = d->batch; p.heads = d->heads; p.seq_q = 1; p.seq_k = d->seq_k;
   p.scale_log2 = d->scale * kLog2e;
   p.causal = 0;
+  p.q = static_cast<const __nv_bfloat16*>(q);
+  p.q_sb = static_cast<int64_t>(d->heads) * kMlaDqk; p.q_sh = 0; p.q_ss = kMlaDqk;
   p.splits = splits;
   p.split_len = split_len;
   float* part_o = static_cast<float*>(workspace);
