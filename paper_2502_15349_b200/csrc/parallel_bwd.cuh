@@ -426,8 +426,8 @@ struct BwdQSmem {
   static constexpr int kKOff = 0;
   static constexpr int kVOff = kKOff + kStages * kKBytes;
   static constexpr int kBarOff = kVOff + kStages * kVBytes;
-  // full[S], empty[S], qa_ready, s_full, dp_full, ds_ready, acc_full
-  static constexpr int kNumBars = 2 * kStages + 5;
+  // full[S], empty[S], qa_ready, s_full[2], dp_full[2], ds_ready[2], acc_full
+  static constexpr int kNumBars = 2 * kStages + 8;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -464,10 +464,10 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* full = bars;
   uint64_t* empty = full + kStages;
   uint64_t* qa_ready = empty + kStages;
-  uint64_t* s_full = qa_ready + 1;
-  uint64_t* dp_full = s_full + 1;
-  uint64_t* ds_ready = dp_full + 1;
-  uint64_t* acc_full = ds_ready + 1;
+  uint64_t* s_full = qa_ready + 1;   // [2]: one per 64-key column half
+  uint64_t* dp_full = s_full + 2;    // [2]
+  uint64_t* ds_ready = dp_full + 2;  // [2]
+  uint64_t* acc_full = ds_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -488,9 +488,11 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(qa_ready, 8);
-    mbar_init(s_full, 1);
-    mbar_init(dp_full, 1);
-    mbar_init(ds_ready, 8);
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&s_full[x], 1);
+      mbar_init(&dp_full[x], 1);
+      mbar_init(&ds_ready[x], 4);
+    }
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
@@ -522,43 +524,57 @@ __global__ void __launch_bounds__(320, 1)
   } else if (warp == 9) {
     // ───────────── MMA issuer ─────────────
     if (elect_one() && nk > 0) {
-      constexpr uint32_t id_s = make_idesc_bf16(kBlockM, kBlockN, false, false);  // S = Q K^T
-      constexpr uint32_t id_dp = make_idesc_bf16(kBlockM, kBlockN, false, false); // dP = dO V^T
-      constexpr uint32_t id_dq = make_idesc_bf16(kBlockM, D, false, true);        // dQ += dS K
+      // The 128 key columns are processed as two 64-wide halves x = 0, 1 with their own
+      // barriers: while the row warps of one half compute P / dS, the tensor pipe runs the other
+      // half's dQ and the next tile's S / dP for the half already released (no TMEM to spare for
+      // a second S/dP buffer, so the halves double-buffer each other).
+      constexpr uint32_t id_s = make_idesc_bf16(kBlockM, kBlockN / 2, false, false);  // S = Q K^T
+      constexpr uint32_t id_dq = make_idesc_bf16(kBlockM, D, false, true);            // dQ += dS K
       const uint32_t aK = smem_u32(sK), aV = smem_u32(sV);
-      auto kmajor = [](uint32_t base, int kk, int rows) {
-        return make_sdesc(base + (kk / 4) * (rows * 128) + (kk % 4) * 32, 0, 1024);
-      };
-      auto issue_sdp = [&](int n) {
+      auto issue_sdp = [&](int n, int x) {
         const int s = n % kStages;
-        mbar_wait(&full[s], (n / kStages) & 1);
-        tc_fence_after();
+        const uint32_t kx = aK + s * L::kKBytes + x * 64 * 128;
+        const uint32_t vx = aV + s * L::kVBytes + x * 64 * 128;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_ts(tmem + kColS, tmem + kColQA + kk * 8, kmajor(aK + s * L::kKBytes, kk, kBlockN),
-                 id_s, kk > 0);
-        mma_commit(s_full);
+          mma_ts(tmem + kColS + x * 64, tmem + kColQA + kk * 8,
+                 make_sdesc(kx + (kk / 4) * (kBlockN * 128) + (kk % 4) * 32, 0, 1024), id_s,
+                 kk > 0);
+        mma_commit(&s_full[x]);
 #pragma unroll
         for (int kk = 0; kk < DV / 16; ++kk)
-          mma_ts(tmem + kColDP, tmem + kColOA + kk * 8, kmajor(aV + s * L::kVBytes, kk, kBlockN),
-                 id_dp, kk > 0);
-        mma_commit(dp_full);
+          mma_ts(tmem + kColDP + x * 64, tmem + kColOA + kk * 8,
+                 make_sdesc(vx + (kk / 4) * (kBlockN * 128) + (kk % 4) * 32, 0, 1024), id_s,
+                 kk > 0);
+        mma_commit(&dp_full[x]);
       };
-      // S0 dP0 | dQ0 S1 dP1 | dQ1 S2 dP2 | ...  (S_{n+1} follows dQ_n, which reads dS_n)
       mbar_wait(qa_ready, 0);
+      mbar_wait(&full[0], 0);
       tc_fence_after();
-      issue_sdp(0);
+      issue_sdp(0, 0);
+      issue_sdp(0, 1);
       for (int n = 0; n < nk; ++n) {
         const int s = n % kStages;
-        mbar_wait(ds_ready, n & 1);
-        tc_fence_after();
+        const bool more = n + 1 < nk;
+        for (int x = 0; x < 2; ++x) {
+          mbar_wait(&ds_ready[x], n & 1);
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < kBlockN / 16; ++kk)
-          mma_ts(tmem + kColDQ, tmem + kColS + split_col(kk),
-                 make_sdesc(aK + s * L::kKBytes + kk * 16 * 128, kBlockN * 128, 1024), id_dq,
-                 (n > 0 || kk > 0));
-        mma_commit(&empty[s]);
-        if (n + 1 < nk) issue_sdp(n + 1);
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = x * 4 + k4;
+            mma_ts(tmem + kColDQ, tmem + kColS + split_col(kk),
+                   make_sdesc(aK + s * L::kKBytes + kk * 16 * 128, kBlockN * 128, 1024), id_dq,
+                   (n > 0 || kk > 0));
+          }
+          if (x == 1) mma_commit(&empty[s]);
+          if (more) {
+            if (x == 0) {
+              mbar_wait(&full[(n + 1) % kStages], ((n + 1) / kStages) & 1);
+              tc_fence_after();
+            }
+            issue_sdp(n + 1, x);
+          }
+        }
       }
       mma_commit(acc_full);
     }
@@ -613,7 +629,7 @@ __global__ void __launch_bounds__(320, 1)
     for (int n = 0; n < nk; ++n) {
       const int c0 = (band.jb_lo + n) * kBlockN;
       const bool fullblk = tile_fully_kept(p.mask, q0, c0, p.seq_q, p.seq_k);
-      mbar_wait(s_full, n & 1);
+      mbar_wait(&s_full[half], n & 1);
       tc_fence_after();
       uint32_t pk[32];
       uint32_t gmask[2];
@@ -660,7 +676,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         gmask[c2] = bits;
       }
-      mbar_wait(dp_full, n & 1);
+      mbar_wait(&dp_full[half], n & 1);
       tc_fence_after();
       uint32_t dsk[32];
 #pragma unroll
@@ -675,7 +691,7 @@ __global__ void __launch_bounds__(320, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive(ds_ready);
+      if (lane_id() == 0) mbar_arrive(&ds_ready[half]);
     }
     // ───────────── epilogue: dQ = tau * acc (bf16); each warp stores D/2 columns ─────────────
     if (nk > 0) {
