@@ -83,10 +83,12 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
-  const int bhs = p.batch * p.heads;
-  // heaviest key tiles (lowest index under a causal mask) first
-  const int kt = static_cast<int>(blockIdx.x) / bhs;
-  const int bh = static_cast<int>(blockIdx.x) % bhs;
+  // CTA order (b, h)-major with the key tiles of one head adjacent, and every CTA walks its query
+  // tiles from the last one down: the CTAs of one head stream the same Q / dO tiles at the same
+  // time, so each is read from HBM once and served to the other key tiles from L2.
+  const int k_tiles = p.k_pad / 128;
+  const int kt = static_cast<int>(blockIdx.x) % k_tiles;
+  const int bh = static_cast<int>(blockIdx.x) / k_tiles;
   const int b = bh / p.heads, h = bh % p.heads;
   const int k0 = kt * 128;
   const int q_tiles = p.q_pad / 128;
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(320, 1)
       int slot = 0;
       uint32_t ph = 0;
       for (int n = 0; n < nq; ++n) {
-        const int q0 = (qt_lo + n) * 128;
+        const int q0 = (q_tiles - 1 - n) * 128;
         const int t = n & 1;
         mbar_wait(&stat_empty[t], ((n >> 1) & 1) ^ 1);
         mbar_expect_tx(&stat_full[t], 2 * 128 * 4);
@@ -140,11 +142,9 @@ __global__ void __launch_bounds__(320, 1)
           mbar_wait(&empty[slot], ph ^ 1);
           mbar_expect_tx(&full[slot], L::kBox);
           if (c < 9)
-            tma_load_4d_hint(sRing + slot * L::kBox, &tm_q, &full[slot], c * 64, q0, h, b,
-                             kEvictFirst);
+            tma_load_4d(sRing + slot * L::kBox, &tm_q, &full[slot], c * 64, q0, h, b);
           else
-            tma_load_4d_hint(sRing + slot * L::kBox, &tm_do, &full[slot], (c - 9) * 64, q0, h, b,
-                             kEvictFirst);
+            tma_load_4d(sRing + slot * L::kBox, &tm_do, &full[slot], (c - 9) * 64, q0, h, b);
           if (++slot == kStages) {
             slot = 0;
             ph ^= 1;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(320, 1)
     const int cb = half * 64;
     for (int n = 0; n < nq; ++n) {
       const int t = n & 1;
-      const int q0 = (qt_lo + n) * 128;
+      const int q0 = (q_tiles - 1 - n) * 128;
       const int i = q0 + row;
       mbar_wait(&stat_full[t], (n >> 1) & 1);
       const float l2 = sStat[t * 256 + row];
@@ -347,8 +347,10 @@ __global__ void __launch_bounds__(192, 1)
             tma_load_4d_hint(sb + nb * 8192, &tm_b1, &full[slot], n0 + nb * 64,
                              kt * 128 + c * 64, b, 0, kEvictLast);
         } else {
+          // query tiles from the last one down: CTAs of different key tiles then stream the same
+          // Q / dO tiles concurrently (L2 reuse)
           const int hh = h_lo + item / (it_hi - it_lo);
-          const int qt = it_lo + item % (it_hi - it_lo);
+          const int qt = it_hi - 1 - item % (it_hi - it_lo);
           // chunk, product (0: dS'/Q, 1: P/dO); the rope columns (n0 >= 512) have no dO term
           const int c = per_item == 4 ? sub / 2 : sub;
           const int prod = per_item == 4 ? sub % 2 : 0;
@@ -359,8 +361,7 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_4d(sa, ta, &full[slot], tile * 128, r0, bhh, 0);
           tma_load_4d(sa + 8192, ta, &full[slot], tile * 128 + 64, r0, bhh, 0);
           for (int nb = 0; nb < N / 64; ++nb)
-            tma_load_4d_hint(sb + nb * 8192, tb, &full[slot], n0 + nb * 64, r0, hh, b,
-                             kEvictFirst);
+            tma_load_4d(sb + nb * 8192, tb, &full[slot], n0 + nb * 64, r0, hh, b);
         }
         if (++slot == kStages) {
           slot = 0;

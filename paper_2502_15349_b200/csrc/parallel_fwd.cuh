@@ -272,13 +272,15 @@ __global__ void __launch_bounds__(320, 1)
       const bool full = block_fully_kept(p.mask, r0, c0, p.seq_k);
 
       if constexpr (kFamily == kFamilySoftmax) {
+        // Fully-kept blocks (the bulk of a causal sweep): the row max is taken on the raw scores
+        // and the scale folds into one FFMA per element; a quarter of the exponentials run as a
+        // polynomial on the FMA pipe so the MUFU stream stays below the MMA time.
+        const bool fast = full && p.scale_log2 > 0.0f;
         float bmax = -INFINITY;
-        if (full) {
+        if (fast) {
 #pragma unroll
-          for (int c = 0; c < kBlockN; ++c) {
-            s[c] *= p.scale_log2;
-            bmax = fmaxf(bmax, s[c]);
-          }
+          for (int c = 0; c < kBlockN; ++c) bmax = fmaxf(bmax, s[c]);
+          bmax *= p.scale_log2;
         } else {
 #pragma unroll
           for (int c = 0; c < kBlockN; ++c) {
@@ -297,12 +299,25 @@ __global__ void __launch_bounds__(320, 1)
         const float m_use = (m_run == -INFINITY) ? 0.0f : m_run;
         float lsum = 0.0f;
         uint32_t pk[kBlockN / 2];
+        if (fast) {
 #pragma unroll
-        for (int c = 0; c < kBlockN; c += 2) {
-          const float e0 = ex2(s[c] - m_use);
-          const float e1 = ex2(s[c + 1] - m_use);
-          lsum += e0 + e1;
-          pk[c / 2] = pack_bf16(e0, e1);
+          for (int c = 0; c < kBlockN; c += 2) {
+            const float x0 = fmaf(s[c], p.scale_log2, -m_use);
+            const float x1 = fmaf(s[c + 1], p.scale_log2, -m_use);
+            const bool poly = (c & 6) == 0;  // columns c % 8 in {0, 1}: 25 %
+            const float e0 = poly ? exp2_poly(x0) : ex2(x0);
+            const float e1 = poly ? exp2_poly(x1) : ex2(x1);
+            lsum += e0 + e1;
+            pk[c / 2] = pack_bf16(e0, e1);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < kBlockN; c += 2) {
+            const float e0 = ex2(s[c] - m_use);
+            const float e1 = ex2(s[c + 1] - m_use);
+            lsum += e0 + e1;
+            pk[c / 2] = pack_bf16(e0, e1);
+          }
         }
         l_run = l_run * factor + lsum;
 #pragma unroll
