@@ -21,6 +21,9 @@
 
 namespace af {
 
+#ifndef AF_EXP2_POLY_MASK
+#define AF_EXP2_POLY_MASK 14  // column pairs with (c & mask) == 0 use exp2_poly: 14 -> 12.5 %
+#endif
 constexpr int kBlockM = 128;  // query rows per tile (TMEM lanes)
 constexpr int kBlockN = 128;  // keys per block
 constexpr float kLog2e = 1.4426950408889634f;
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(320, 1)
 
       if constexpr (kFamily == kFamilySoftmax) {
         // Fully-kept blocks (the bulk of a causal sweep): the row max is taken on the raw scores
-        // and the scale folds into one FFMA per element; a quarter of the exponentials run as a
+        // and the scale folds into one FFMA per element; an eighth of the exponentials run as a
         // polynomial on the FMA pipe so the MUFU stream stays below the MMA time.
         const bool fast = full && p.scale_log2 > 0.0f;
         float bmax = -INFINITY;
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(320, 1)
           for (int c = 0; c < kBlockN; c += 2) {
             const float x0 = fmaf(s[c], p.scale_log2, -m_use);
             const float x1 = fmaf(s[c + 1], p.scale_log2, -m_use);
-            const bool poly = (c & 6) == 0;  // columns c % 8 in {0, 1}: 25 %
+            const bool poly = (c & AF_EXP2_POLY_MASK) == 0;  // default: c % 16 in {0, 1}, 12.5 % (swept: 25 % and 6 % are slower)
             const float e0 = poly ? exp2_poly(x0) : ex2(x0);
             const float e1 = poly ? exp2_poly(x1) : ex2(x1);
             lsum += e0 + e1;
