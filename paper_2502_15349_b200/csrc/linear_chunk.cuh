@@ -17,7 +17,8 @@
 // One CTA owns one (b, h, value block) and walks the chunks in order (reverse: last to first),
 // carrying the [DK x 64] fp32 state in TMEM.  Warps 0-7: two per chunk row (= TMEM lane), each
 // owning one half of the columns (scan of log a, decay weights, P = S o D, state rescale, bf16
-// state copy, output epilogue); warp 8: TMA producer; warp 9: TMEM allocator + MMA issuer.
+// state copy); warps 8-11: output epilogue of the previous chunk (OI / QH double-buffered);
+// warp 12: TMA producer; warp 13: TMEM allocator + MMA issuer.
 // TMEM: S [0,128) (packed P) | OI [128,192) | QH x2 [192,320) | H [320, 320+64*DK/128)
 // MMAs (all M=128): S = Q K^T (SS), QH = Q Hb (SS, Hb = bf16 state copy in smem), OI = P V (TS),
 // H += K^T Vw (SS, K^T read MN-major straight from the K tile, Vw = diag(w) V).
@@ -78,12 +79,14 @@ struct LinSmem {
   static constexpr int kVOff = kKOff + kStages * kQBytes;
   static constexpr int kVwOff = kVOff + kStages * kVBytes;
   static constexpr int kHbOff = kVwOff + kVBytes;
-  static constexpr int kLOff = kHbOff + DK * kLinVB * 2;
-  static constexpr int kUOff = kLOff + kLinChunk * 4;
-  static constexpr int kScanOff = kUOff + kLinChunk * 4;
-  // ring: full[S], empty[S]; then s_full qh_full oi_full h_full | p_ready vw_ready h_scaled hb_ready
-  static constexpr int kBarOff = kScanOff + 64;
-  static constexpr int kNumBars = 2 * kStages + 8;
+  static constexpr int kLOff = kHbOff + DK * kLinVB * 2;  // [2][128] cumsum log2 a, per parity
+  static constexpr int kUOff = kLOff + 2 * kLinChunk * 4;  // [2][128] key/value-side scale
+  static constexpr int kRawOff = kUOff + 2 * kLinChunk * 4;  // [3][128] raw factors (cp.async)
+  static constexpr int kCpOff = kRawOff + 3 * kLinChunk * 4;  // [2][128] per-row output decay
+  // ring: full[S], empty[S]; s_full qh_full oi_full[2] h_full scan_ready[2] (1 arrival) |
+  // p_ready vw_ready h_scaled hb_ready scan_free[2] (8 row warps) | oi_empty[2] cp_ready[2] (4)
+  static constexpr int kBarOff = kCpOff + 2 * kLinChunk * 4;
+  static constexpr int kNumBars = 2 * kStages + 17;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -100,8 +103,13 @@ AF_DEVICE uint4* swz_row(uint8_t* base, int r, int g) {
   return reinterpret_cast<uint4*>(base + r * 128 + ((g ^ (r & 7)) << 4));
 }
 
+// Warp roles: 0-7 chunk-row warps (two per TMEM lane quarter), 8-11 output warps (one per lane
+// quarter: O = s_out (OI + cp Q H) of chunk n runs while the row warps already work on chunk n+1;
+// OI and QH are double-buffered in TMEM), 12 TMA producer, 13 TMEM allocator + MMA issuer.
+constexpr int kLinThreads = 448;
+
 template <int DK, bool kReverse>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kLinThreads, 1)
     linear_chunk_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const LinearParams p) {
@@ -115,20 +123,25 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sV = smem + L::kVOff;
   uint8_t* sVw = smem + L::kVwOff;
   uint8_t* sHb = smem + L::kHbOff;
-  float* sL = reinterpret_cast<float*>(smem + L::kLOff);   // in-chunk cumsum of log2 a
-  float* sU = reinterpret_cast<float*>(smem + L::kUOff);   // key/value-side scale
-  float* sScan = reinterpret_cast<float*>(smem + L::kScanOff);
+  float* sLb = reinterpret_cast<float*>(smem + L::kLOff);  // in-chunk cumsum of log2 a [2][128]
+  float* sUb = reinterpret_cast<float*>(smem + L::kUOff);  // key/value-side scale [2][128]
+  float* sRaw = reinterpret_cast<float*>(smem + L::kRawOff);
+  float* sCp = reinterpret_cast<float*>(smem + L::kCpOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* full = bars;                 // Q, K, V of one chunk landed (one tx barrier)
   uint64_t* empty = bars + kStages;      // the chunk's Q, K, V may be overwritten
   uint64_t* s_full = bars + 2 * kStages;
   uint64_t* qh_full = s_full + 1;
-  uint64_t* oi_full = s_full + 2;
-  uint64_t* h_full = s_full + 3;
-  uint64_t* p_ready = s_full + 4;
-  uint64_t* vw_ready = s_full + 5;
-  uint64_t* h_scaled = s_full + 6;
-  uint64_t* hb_ready = s_full + 7;
+  uint64_t* oi_full = s_full + 2;        // [2]
+  uint64_t* h_full = s_full + 4;
+  uint64_t* p_ready = s_full + 5;
+  uint64_t* vw_ready = s_full + 6;
+  uint64_t* h_scaled = s_full + 7;
+  uint64_t* hb_ready = s_full + 8;
+  uint64_t* oi_empty = s_full + 9;       // [2]
+  uint64_t* cp_ready = s_full + 11;      // [2]
+  uint64_t* scan_ready = s_full + 13;    // [2]
+  uint64_t* scan_free = s_full + 15;     // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -139,12 +152,17 @@ __global__ void __launch_bounds__(320, 1)
   const int h = bh % p.heads;
   const int nchunks = (p.seq + kLinChunk - 1) / kLinChunk;
 
-  if (warp == 8 && lane_id() == 0) {
-    for (int i = 0; i < 2 * kStages + 4; ++i) mbar_init(&bars[i], 1);
-    for (int i = 2 * kStages + 4; i < L::kNumBars; ++i) mbar_init(&bars[i], 8);
+  if (warp == 12 && lane_id() == 0) {
+    for (int i = 0; i < 2 * kStages + 5; ++i) mbar_init(&bars[i], 1);
+    for (int i = 2 * kStages + 5; i < 2 * kStages + 9; ++i) mbar_init(&bars[i], 8);
+    for (int i = 2 * kStages + 9; i < 2 * kStages + 13; ++i) mbar_init(&bars[i], 4);
+    mbar_init(&scan_ready[0], 1);
+    mbar_init(&scan_ready[1], 1);
+    mbar_init(&scan_free[0], 8);
+    mbar_init(&scan_free[1], 8);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == 13) tmem_alloc<512>(tmem_slot);
   if (warp < 8) {  // zero the bf16 state copy: chunk 0 multiplies Q by H_in = 0
     for (int i = threadIdx.x; i < DK * kLinVB * 2 / 16; i += 256)
       reinterpret_cast<uint4*>(sHb)[i] = make_uint4(0, 0, 0, 0);
@@ -154,16 +172,78 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // S [0,128) | OI [128,192) | QH x2 [192,320) | H [320, 320 + 64*DK/128)
-  constexpr uint32_t kColS = 0, kColOI = 128, kColQH = 192, kColH = 320;
+  // S [0,128) | OI x2 [128,256) | QH x2 [256,384) | H [384, 384 + 64*DK/128)
+  constexpr uint32_t kColS = 0, kColOI = 128, kColQH = 256, kColH = 384;
 
-  if (warp == 8) {
-    // ───────────── TMA producer ─────────────
-    if (elect_one()) {
-      for (int n = 0; n < nchunks; ++n) {
-        const int c = kReverse ? nchunks - 1 - n : n;
-        const int t0 = c * kLinChunk;
-        const int st = n % kStages;
+  if (warp == 12) {
+    // ───────────── producer warp: TMA ring + the per-step decay scan ─────────────
+    // The raw per-step factors of chunk n+1 are fetched with cp.async while chunk n is handed out
+    // (plain loads would be waited on by every later barrier of the issuing warp), then
+    // log2 a, its in-chunk inclusive cumsum and the key-side scale go to sL/sU[n % 2].
+    const int lane = static_cast<int>(lane_id());
+    const int nraw = p.nfac + (p.u_scale.ptr != nullptr ? 1 : 0);
+    auto fetch_raw = [&](int n) {
+      const int c = kReverse ? nchunks - 1 - n : n;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rr = lane * 4 + j;
+        const int t = c * kLinChunk + rr;
+        if (n < nchunks && t < p.seq) {
+          for (int f = 0; f < nraw; ++f) {
+            const StepTensor& ts = f < p.nfac ? p.fac[f] : p.u_scale;
+            const float* src = ts.ptr + b * ts.sb + h * ts.sh + t * ts.ss;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             smem_u32(sRaw + f * kLinChunk + rr)),
+                         "l"(src)
+                         : "memory");
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch_raw(0);
+    for (int n = 0; n < nchunks; ++n) {
+      const int c = kReverse ? nchunks - 1 - n : n;
+      const int t0 = c * kLinChunk;
+      const int st = n % kStages;
+      const int pb = n & 1;
+      __syncwarp();
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      float x[4], us[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int rr = lane * 4 + j;
+        const bool live = t0 + rr < p.seq;
+        x[j] = 0.0f;
+        us[j] = 1.0f;
+        if (live) {
+          x[j] = p.log_const * kLog2e_;
+          for (int f = 0; f < p.nfac; ++f) x[j] += __log2f(sRaw[f * kLinChunk + rr]);
+          if (p.u_scale.ptr != nullptr) us[j] = sRaw[p.nfac * kLinChunk + rr];
+        }
+      }
+      __syncwarp();
+      fetch_raw(n + 1);  // sRaw consumed: prefetch the next chunk
+      x[1] += x[0];
+      x[2] += x[1];
+      x[3] += x[2];
+      float tot = x[3];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, tot, off);
+        if (lane >= off) tot += y;
+      }
+      const float excl = tot - x[3];
+      if (n >= 2) mbar_wait(&scan_free[pb], ((n >> 1) - 1) & 1);  // chunk n-2 done with sL[pb]
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        sLb[pb * kLinChunk + lane * 4 + j] = excl + x[j];
+        sUb[pb * kLinChunk + lane * 4 + j] = us[j];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&scan_ready[pb]);
+      // Q, K, V of chunk n (after the scan: the scan never waits on the ring)
+      if (elect_one()) {
         mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
         mbar_expect_tx(&full[st], 2 * L::kQBytes + L::kVBytes);
         for (int x = 0; x < DK / 64; ++x) {
@@ -174,8 +254,10 @@ __global__ void __launch_bounds__(320, 1)
         }
         tma_load_4d(sV + st * L::kVBytes, &tm_v, &full[st], vb * kLinVB, t0, h, b);
       }
+      __syncwarp();
     }
-  } else if (warp == 9) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else if (warp == 13) {
     // ───────────── MMA issuer:  S | QH | H update | OI ─────────────
     if (elect_one()) {
       constexpr uint32_t id_s = make_idesc_bf16(128, 128, false, false);     // S = Q K^T
@@ -200,6 +282,7 @@ __global__ void __launch_bounds__(320, 1)
           mma_ss(tmem + kColS, kmaj(qa, kk), kmaj(ka, kk), id_s, kk > 0);
         mma_commit(s_full);
         if (n > 0) mbar_wait(hb_ready, (n - 1) & 1);
+        if (n >= 2) mbar_wait(&oi_empty[ph], ((n >> 1) - 1) & 1);  // chunk n-2's output read
         AF_LT(1, n);
         tc_fence_after();
 #pragma unroll
@@ -224,11 +307,75 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kLinChunk / 16; ++kk)
-          mma_ts(tmem + kColOI, tmem + kColS + split_col_lin(kk),
+          mma_ts(tmem + kColOI + ph * kLinVB, tmem + kColS + split_col_lin(kk),
                  make_sdesc(va + kk * 2048, 16384, 1024), id_oi, kk > 0);
-        mma_commit(oi_full);
+        mma_commit(&oi_full[ph]);
         mma_commit(&empty[st]);
       }
+    }
+  } else if (warp >= 8) {
+    // ───────────── output warps: O = s_out (OI + cp QH) of chunk n, 64 columns per row ─────────
+    const int wq = warp - 8;
+    const int r = wq * 32 + static_cast<int>(lane_id());
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    for (int n = 0; n < nchunks; ++n) {
+      const int c = kReverse ? nchunks - 1 - n : n;
+      const int t = c * kLinChunk + r;
+      const uint32_t ph = n & 1;
+      const bool live = t < p.seq;
+      mbar_wait(&cp_ready[ph], (n >> 1) & 1);
+      const float cp = sCp[ph * kLinChunk + r];
+      const float rs = (p.o_rowscale.ptr != nullptr && live) ? p.o_rowscale.at(b, h, t) : 1.0f;
+      mbar_wait(&oi_full[ph], (n >> 1) & 1);
+      if (warp == 8 && lane_id() == 0) AF_LT(9, n);
+      tc_fence_after();
+#pragma unroll 1
+      for (int half = 0; half < 2; ++half) {
+        const int col0 = vb * kLinVB + half * 32;
+        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_sb + h * p.o_sh +
+                              static_cast<int64_t>(live ? t : 0) * p.o_ss + col0;
+        uint32_t oi[32], qh[32];
+        tmem_ld32(tmem + lane_base + kColOI + ph * kLinVB + half * 32, oi);
+        tmem_ld32(tmem + lane_base + kColQH + ph * kLinVB + half * 32, qh);
+        tmem_ld_wait();
+        if (half == 1) {  // both halves read: release the OI / QH buffers and sCp[ph]
+          tc_fence_before();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&oi_empty[ph]);
+        }
+        float ov[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          ov[e] = p.out_scale * fmaf(cp, __uint_as_float(qh[e]), __uint_as_float(oi[e]));
+        if (live) {
+          uint4* d4 = reinterpret_cast<uint4*>(orow);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            d4[v] = make_uint4(pack_bf16(rs * ov[v * 8 + 0], rs * ov[v * 8 + 1]),
+                               pack_bf16(rs * ov[v * 8 + 2], rs * ov[v * 8 + 3]),
+                               pack_bf16(rs * ov[v * 8 + 4], rs * ov[v * 8 + 5]),
+                               pack_bf16(rs * ov[v * 8 + 6], rs * ov[v * 8 + 7]));
+          if (p.dot_x != nullptr) {
+            const uint4* x4 = reinterpret_cast<const uint4*>(
+                reinterpret_cast<const __nv_bfloat16*>(p.dot_x) + b * p.x_sb + h * p.x_sh +
+                static_cast<int64_t>(t) * p.x_ss + col0);
+            float dotacc = 0.0f;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              const uint4 xv = x4[v];
+              const uint32_t* xe = reinterpret_cast<const uint32_t*>(&xv);
+#pragma unroll
+              for (int q2 = 0; q2 < 4; ++q2)
+                dotacc += bf16_lo_(xe[q2]) * ov[v * 8 + 2 * q2] +
+                          bf16_hi_(xe[q2]) * ov[v * 8 + 2 * q2 + 1];
+            }
+            const int64_t rows = static_cast<int64_t>(p.batch) * p.heads * p.seq;
+            p.dot[(vb * 2 + half) * rows + (static_cast<int64_t>(b) * p.heads + h) * p.seq + t] =
+                dotacc;
+          }
+        }
+      }
+      if (warp == 8 && lane_id() == 0) AF_LT(10, n);
     }
   } else {
     // ───────────── chunk-row warps: two per TMEM lane quarter, column halves ─────────────
@@ -236,53 +383,33 @@ __global__ void __launch_bounds__(320, 1)
     const int half = warp / 4;
     const int r = wq * 32 + static_cast<int>(lane_id());
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    // log2 a of this row for chunk n (prefetched one chunk ahead; rows past seq: a = 1)
-    auto load_x = [&](int n) -> float2 {
-      const int c = kReverse ? nchunks - 1 - n : n;
-      const int t = c * kLinChunk + r;
-      float x = 0.0f, us = 1.0f;
-      if (n < nchunks && t < p.seq) {
-        x = p.log_const * kLog2e_;
-        for (int f = 0; f < p.nfac; ++f) x += __log2f(p.fac[f].at(b, h, t));
-        if (p.u_scale.ptr != nullptr) us = p.u_scale.at(b, h, t);
-      }
-      return make_float2(x, us);
-    };
-    float2 nxt = half == 0 ? load_x(0) : make_float2(0.0f, 1.0f);
     for (int n = 0; n < nchunks; ++n) {
       const int c = kReverse ? nchunks - 1 - n : n;
       const int t = c * kLinChunk + r;
       const uint32_t ph = n & 1;
       const int st = n % kStages;
       const bool live = t < p.seq;
-      // every row warp is done reading sL / sU of the previous chunk
-      if (n > 0) named_bar_sync(3, 256);
-      // (a) in-chunk inclusive cumsum of log2 a (warps of half 0; shared through smem)
-      if (half == 0) {
-        float x = nxt.x;
-        const float us = nxt.y;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const float y = __shfl_up_sync(0xffffffffu, x, off);
-          if (static_cast<int>(lane_id()) >= off) x += y;
-        }
-        if (lane_id() == 31) sScan[wq] = x;
-        named_bar_sync(1, 128);
-        float pre = 0.0f;
-        for (int w = 0; w < wq; ++w) pre += sScan[w];
-        sL[r] = x + pre;
-        sU[r] = us;
-        nxt = load_x(n + 1);  // prefetch the next chunk's decay factors
-      }
-      named_bar_sync(2, 256);
+      (void)live;
+      // (a) the producer warp's scan of log2 a for this chunk
+      const float* sL = sLb + ph * kLinChunk;
+      const float* sU = sUb + ph * kLinChunk;
+      mbar_wait(&scan_ready[ph], (n >> 1) & 1);
+      if (threadIdx.x == 0) AF_LT(14, n);
       const float l_r = sL[r];
       const float l_last = sL[kLinChunk - 1];
       const float g = exp2f(l_last);
       const float cp = kReverse ? exp2f(l_last - l_r) : exp2f(l_r);
       const float wgt = sU[r] * (kReverse ? exp2f(l_r) : exp2f(l_last - l_r));
+      if (half == 0) {  // hand cp to the output warps (sCp[ph] is free once chunk n-2 is out)
+        if (n >= 2) mbar_wait(&oi_empty[ph], ((n >> 1) - 1) & 1);
+        sCp[ph * kLinChunk + r] = cp;
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&cp_ready[ph]);
+      }
       if (threadIdx.x == 0) AF_LT(4, n);
       // (b) Vw = diag(w * u_scale) V (this half's 4 granules; the previous state update is done)
       mbar_wait(&full[st], (n / kStages) & 1);
+      if (threadIdx.x == 0) AF_LT(13, n);
 #pragma unroll
       for (int gq = 0; gq < 4; ++gq) {
         const int gidx = half * 4 + gq;
@@ -324,12 +451,22 @@ __global__ void __launch_bounds__(320, 1)
         uint32_t pk[32];
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
+          // warp-uniform 32x32 sub-block class: rows [wq*32, +32) x key columns [u0, u0+32)
+          const int u0 = half * 64 + cc * 32;
+          const int r0w = wq * 32;
+          const bool none = kReverse ? (u0 + 31 < r0w) : (u0 > r0w + 31);   // all masked
+          const bool all = kReverse ? (u0 >= r0w + 31) : (u0 + 31 <= r0w);  // none masked
+          if (none) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) pk[cc * 16 + e] = 0u;
+            continue;
+          }
           uint32_t sr[32];
-          tmem_ld32(tmem + lane_base + kColS + half * 64 + cc * 32, sr);
+          tmem_ld32(tmem + lane_base + kColS + u0, sr);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
-            const int u = half * 64 + cc * 32 + e;
+            const int u = u0 + e;
             const float4 l4 = *reinterpret_cast<const float4*>(sL + u);
             const float4 u4 = *reinterpret_cast<const float4*>(sU + u);
             const float lu[4] = {l4.x, l4.y, l4.z, l4.w};
@@ -337,7 +474,7 @@ __global__ void __launch_bounds__(320, 1)
             float pv[4];
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
-              const bool keep = kReverse ? (u + x >= r) : (u + x <= r);
+              const bool keep = all || (kReverse ? (u + x >= r) : (u + x <= r));
               const float d = ex2(kReverse ? lu[x] - l_r : l_r - lu[x]) * uu[x];
               pv[x] = keep ? __uint_as_float(sr[e + x]) * d : 0.0f;
             }
@@ -348,6 +485,8 @@ __global__ void __launch_bounds__(320, 1)
         tmem_st32(tmem + lane_base + kColS + half * 64, pk);  // packed: see split_col_lin
         tmem_st_wait();
       }
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&scan_free[ph]);  // last read of sL / sU of this chunk
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(p_ready);
@@ -377,59 +516,12 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(hb_ready);
       if (threadIdx.x == 0) AF_LT(12, n);
-      // (e) O = s_out (OI + cp QH) for this half's 32 output columns (QH is double-buffered,
-      //     so the next chunk's Q H can already run)
-      mbar_wait(oi_full, ph);
-      if (threadIdx.x == 0) AF_LT(9, n);
-      tc_fence_after();
-      {
-        const float rs = (p.o_rowscale.ptr != nullptr && live) ? p.o_rowscale.at(b, h, t) : 1.0f;
-        const int col0 = vb * kLinVB + half * 32;
-        __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_sb + h * p.o_sh +
-                              static_cast<int64_t>(live ? t : 0) * p.o_ss + col0;
-        uint32_t oi[32], qh[32];
-        tmem_ld32(tmem + lane_base + kColOI + half * 32, oi);
-        tmem_ld32(tmem + lane_base + kColQH + ph * kLinVB + half * 32, qh);
-        tmem_ld_wait();
-        float ov[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e)
-          ov[e] = p.out_scale * fmaf(cp, __uint_as_float(qh[e]), __uint_as_float(oi[e]));
-        if (live) {
-          uint4* d4 = reinterpret_cast<uint4*>(orow);
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            d4[v] = make_uint4(pack_bf16(rs * ov[v * 8 + 0], rs * ov[v * 8 + 1]),
-                               pack_bf16(rs * ov[v * 8 + 2], rs * ov[v * 8 + 3]),
-                               pack_bf16(rs * ov[v * 8 + 4], rs * ov[v * 8 + 5]),
-                               pack_bf16(rs * ov[v * 8 + 6], rs * ov[v * 8 + 7]));
-          if (p.dot_x != nullptr) {
-            const uint4* x4 = reinterpret_cast<const uint4*>(
-                reinterpret_cast<const __nv_bfloat16*>(p.dot_x) + b * p.x_sb + h * p.x_sh +
-                static_cast<int64_t>(t) * p.x_ss + col0);
-            float dotacc = 0.0f;
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const uint4 xv = x4[v];
-              const uint32_t* xe = reinterpret_cast<const uint32_t*>(&xv);
-#pragma unroll
-              for (int q2 = 0; q2 < 4; ++q2)
-                dotacc += bf16_lo_(xe[q2]) * ov[v * 8 + 2 * q2] +
-                          bf16_hi_(xe[q2]) * ov[v * 8 + 2 * q2 + 1];
-            }
-            const int64_t rows = static_cast<int64_t>(p.batch) * p.heads * p.seq;
-            p.dot[(vb * 2 + half) * rows + (static_cast<int64_t>(b) * p.heads + h) * p.seq + t] =
-                dotacc;
-          }
-        }
-      }
-      if (threadIdx.x == 0) AF_LT(10, n);
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 13) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }

@@ -17,7 +17,7 @@ buf = np.zeros((16, 128), dtype=np.int64)
 fn = rt.lib().af_debug_lin_trace_read; fn.restype = ctypes.c_int; fn.argtypes = [ctypes.c_void_p]
 assert fn(buf.ctypes.data) == 0
 names = ["mma:full", "mma:hb_ready(n-1)", "mma:p_ready", "mma:vw&h_scaled", "wg:(a) done", "wg:(b) vw done",
-         "wg:(d) scaled", "wg:s_full", "wg:(c) P done", "wg:oi&qh", "wg:(e) done", "wg:h_full", "wg:(f) hb done"]
+         "wg:(d) scaled", "wg:s_full", "wg:(c) P done", "wg:oi&qh", "wg:(e) done", "wg:h_full", "wg:(f) hb done", "wg:full passed", "wg:scan ready"]
 for it in (10, 11, 40):
     base = buf[0, it]
     print(f"chunk {it}: period {buf[0, it+1] - base}")
