@@ -33,7 +33,7 @@ enum {
 
 /* ---- parallel template (attention.py:389-449, engine.py:423-505) ---- */
 enum { AF_FAMILY_SOFTMAX = 0, AF_FAMILY_ELEMENTWISE = 1 };
-enum { AF_ACT_IDENTITY = 0, AF_ACT_SIGMOID = 1, AF_ACT_RELU = 2 };
+enum { AF_ACT_IDENTITY = 0, AF_ACT_SIGMOID = 1, AF_ACT_RELU = 2, AF_ACT_RELU2 = 3 };
 enum { AF_DTYPE_BF16 = 0, AF_DTYPE_F32 = 1 };
 
 typedef struct af_parallel_desc {

@@ -95,7 +95,8 @@ def _desc(plan: ParallelPlan, q, k, v, o, slope, dtype_code: int) -> rt.Parallel
     d = plan.spec.dims
     c = rt.ParallelDesc()
     c.batch, c.heads_q, c.heads_kv = d.batch, d.heads, d.kv_heads
-    c.seq_q, c.seq_k, c.d_qk, c.d_v = d.seq_q, d.seq_k, d.d_qk, d.d_v
+    c.seq_q, c.seq_k = d.seq_q, d.seq_k
+    c.d_qk, c.d_v = int(q.shape[-1]), int(v.shape[-1])  # kernel (possibly padded) head dims
     c.dtype = dtype_code
     c.q_stride, c.k_stride, c.v_stride = rt.strides4(q), rt.strides4(k), rt.strides4(v)
     c.o_stride = rt.strides4(o)
@@ -108,6 +109,23 @@ def _desc(plan: ParallelPlan, q, k, v, o, slope, dtype_code: int) -> rt.Parallel
 
 
 MLA_DQK, MLA_DV = 576, 512
+_KERNEL_DIMS = ((64, 64), (128, 128))
+
+
+def _padded_dim(spec, precision: str) -> int | None:
+    """Head dims the bf16 tcgen05 kernels are not instantiated for (e.g. the reference's
+    16/32-wide variant files) run zero-padded to 64 or 128: zero q/k columns add nothing to
+    Q K^T, zero v columns only produce output columns that are sliced off, and the q_mod scale
+    was already fixed from the spec's own dims.  None = run as is."""
+    d = spec.dims
+    if precision != "bf16" or spec.kv_shared or (d.d_qk, d.d_v) in _KERNEL_DIMS:
+        return None
+    m = max(d.d_qk, d.d_v)
+    return None if m > 128 else (64 if m <= 64 else 128)
+
+
+def _pad_last(t: torch.Tensor, n: int) -> torch.Tensor:
+    return t if t.shape[-1] == n else torch.nn.functional.pad(t, (0, n - t.shape[-1]))
 
 
 def mla_decode(q: torch.Tensor, kv: torch.Tensor, scale: float):
@@ -157,12 +175,17 @@ def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: 
     dtype = _BF16 if precision == "bf16" else torch.float32
     q, k, v, slope = _parallel_inputs(plan, arrays, dtype)
     d = spec.dims
-    o = torch.empty(d.batch, d.heads, d.seq_q, d.d_v, device=q.device, dtype=dtype)
+    pad = _padded_dim(spec, precision)
+    if pad is not None:
+        q, k, v = _pad_last(q, pad), _pad_last(k, pad), _pad_last(v, pad)
+    o = torch.empty(d.batch, d.heads, d.seq_q, v.shape[-1], device=q.device, dtype=dtype)
     lse = (torch.empty(d.batch, d.heads, d.seq_q, device=q.device, dtype=torch.float32)
            if plan.has_lse else None)
     desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16 if dtype == _BF16 else rt.AF_DTYPE_F32)
     rt.check(rt.lib().af_parallel_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                       o.data_ptr(), rt.ptr(lse), _stream()), "af_parallel_fwd")
+    if pad is not None:
+        o = o[..., : d.d_v].contiguous()
     if check_nan:
         _check_nan(o, "kernel")
     return o, lse
@@ -188,6 +211,10 @@ def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tens
     plan = plan_parallel(spec)
     q, k, v, slope = _parallel_inputs(plan, arrays, _BF16)
     d = spec.dims
+    pad = _padded_dim(spec, "bf16")
+    if pad is not None:
+        g = parallel_backward_padded(spec, plan, (q, k, v, slope), o, lse, dout, pad)
+        return g
     o = _as(o, _BF16)
     dout = _as(dout, _BF16).contiguous() if dout.stride() != o.stride() else _as(dout, _BF16)
     if dout.stride() != o.stride():
@@ -221,6 +248,28 @@ def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tens
     return {"q": dq, "k": dk, "v": dv}
 
 
+def parallel_backward_padded(spec, plan, qkvs, o, lse, dout, pad: int) -> dict:
+    """Backward on zero-padded head dims (see ``_padded_dim``); gradients sliced back."""
+    q, k, v, slope = qkvs
+    d = spec.dims
+    q, k, v = (_pad_last(t, pad).contiguous() for t in (q, k, v))
+    o = _pad_last(_as(o, _BF16), pad).contiguous()
+    dout = _pad_last(_as(dout, _BF16), pad).contiguous()
+    _check_shape(dout, (d.batch, d.heads, d.seq_q, pad), "dout")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16)
+    L = rt.lib()
+    ws_n = L.af_parallel_bwd_workspace(desc)
+    ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
+    if plan.family == FAMILY_SOFTMAX and lse is None:
+        raise InputError("softmax backward needs the forward LSE")
+    rt.check(L.af_parallel_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                               rt.ptr(lse), dout.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                               dv.data_ptr(), ws.data_ptr(), ws_n, _stream()), "af_parallel_bwd")
+    return {"q": dq[..., : d.d_qk].contiguous(), "k": dk[..., : d.d_qk].contiguous(),
+            "v": dv[..., : d.d_v].contiguous()}
+
+
 # ───────────────────────────── recurrent template ─────────────────────────────
 
 def _step_tensor(arrays: dict, name: str, d) -> torch.Tensor:
@@ -235,7 +284,8 @@ def _linear_desc(plan: LinearPlan, arrays: dict, q, k, v, o):
     """Descriptor + the fp32 per-step tensors it points to (kept alive by the caller)."""
     d = plan.spec.dims
     c = rt.LinearDesc()
-    c.batch, c.heads, c.seq, c.d_k, c.d_v = d.batch, d.heads, d.seq_q, d.d_qk, d.d_v
+    c.batch, c.heads, c.seq = d.batch, d.heads, d.seq_q
+    c.d_k, c.d_v = int(q.shape[-1]), int(v.shape[-1])  # kernel (possibly padded) dims
     c.chunk = 128
     c.q_scale = float(plan.q_scale)
     c.q_stride, c.k_stride, c.v_stride, c.o_stride = (rt.strides4(q), rt.strides4(k),
@@ -258,13 +308,25 @@ def _linear_desc(plan: LinearPlan, arrays: dict, q, k, v, o):
     return c, keep
 
 
+def _linear_pad(d) -> tuple[int, int]:
+    """Kernel dims of the linear template: 128 or 256 for both the key and the value dim (the
+    backward runs the chunked kernel with the value dim in the key role).  Smaller dims run
+    zero-padded (zero q/k columns add nothing to q.k or to the state, zero v columns only produce
+    sliced-off output columns); the q_mod scale comes from the spec."""
+    def up(n):
+        return 128 if n <= 128 else (256 if n <= 256 else n)
+    return up(d.d_qk), up(d.d_v)
+
+
 def _linear_qkv(plan: LinearPlan, arrays: dict):
     d = plan.spec.dims
     q, k, v = _need(arrays, "q"), _need(arrays, "k"), _need(arrays, "v")
     _check_shape(q, (d.batch, d.heads, d.seq_q, d.d_qk), "q")
     _check_shape(k, (d.batch, d.heads, d.seq_k, d.d_qk), "k")
     _check_shape(v, (d.batch, d.heads, d.seq_k, d.d_v), "v")
-    return _as(q, _BF16), _as(k, _BF16), _as(v, _BF16)
+    pk, pv = _linear_pad(d)
+    return (_pad_last(_as(q, _BF16), pk), _pad_last(_as(k, _BF16), pk),
+            _pad_last(_as(v, _BF16), pv))
 
 
 def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = False):
@@ -274,10 +336,12 @@ def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = Fa
     plan = plan_linear(spec, chunk)
     q, k, v = _linear_qkv(plan, arrays)
     d = spec.dims
-    o = torch.empty(d.batch, d.heads, d.seq_q, d.d_v, device=q.device, dtype=_BF16)
+    o = torch.empty(d.batch, d.heads, d.seq_q, v.shape[-1], device=q.device, dtype=_BF16)
     desc, _keep = _linear_desc(plan, arrays, q, k, v, o)
     rt.check(rt.lib().af_linear_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                     o.data_ptr(), None, _stream()), "af_linear_fwd")
+    if o.shape[-1] != d.d_v:
+        o = o[..., : d.d_v].contiguous()
     if check_nan:
         _check_nan(o, "chunk")
     return o
@@ -305,6 +369,7 @@ def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 128) ->
     d = spec.dims
     dout = _as(dout, _BF16).contiguous()
     _check_shape(dout, (d.batch, d.heads, d.seq_q, d.d_v), "dout")
+    dout = _pad_last(dout, v.shape[-1]).contiguous()
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     # dout / dq use the o / q stride slots of the descriptor (all contiguous here)
     desc, keep = _linear_desc(plan, arrays, q, k, v, dout)
@@ -323,7 +388,8 @@ def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 128) ->
                              dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
                              rt.C.cast(dfac, rt.C.c_void_p), rt.ptr(dgate), ws.data_ptr(), ws_n,
                              _stream()), "af_linear_bwd")
-    grads = {"q": dq, "k": dk, "v": dv}
+    grads = {"q": dq[..., : d.d_qk], "k": dk[..., : d.d_qk], "v": dv[..., : d.d_v]}
+    grads = {n: (t if t.is_contiguous() else t.contiguous()) for n, t in grads.items()}
     for name, g in grads_x.items():
         grads[name] = g.reshape(_need(arrays, name).shape)
     return grads

@@ -79,6 +79,9 @@ AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float
     } else if constexpr (kAct == kActSigmoid) {
       ds0 = dp0 * p0 * (1.0f - p0);
       ds1 = dp1 * p1 * (1.0f - p1);
+    } else if constexpr (kAct == kActRelu2) {  // d relu(z)^2 / dz = 2 relu(z) = 2 sqrt(p)
+      ds0 = dp0 * 2.0f * sqrt_approx(p0);
+      ds1 = dp1 * 2.0f * sqrt_approx(p1);
     } else {
       ds0 = ((gmask >> e) & 1u) ? dp0 : 0.0f;
       ds1 = ((gmask >> (e + 1)) & 1u) ? dp1 : 0.0f;

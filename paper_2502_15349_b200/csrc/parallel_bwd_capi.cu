@@ -68,6 +68,7 @@ int dispatch_bwd(const BwdLaunch& a) {
   switch (a.d->act) {
     case AF_ACT_SIGMOID: return launch_bwd<D, DV, kFamilyElementwise, kActSigmoid>(a);
     case AF_ACT_RELU: return launch_bwd<D, DV, kFamilyElementwise, kActRelu>(a);
+    case AF_ACT_RELU2: return launch_bwd<D, DV, kFamilyElementwise, kActRelu2>(a);
     case AF_ACT_IDENTITY: return launch_bwd<D, DV, kFamilyElementwise, kActIdentity>(a);
     default: break;
   }

@@ -34,6 +34,7 @@ int dispatch_family(const af_parallel_desc* d, const CUtensorMap& tq, const CUte
   switch (d->act) {
     case AF_ACT_SIGMOID: return launch_fwd<D, DV, kFamilyElementwise, kActSigmoid>(d, tq, tk, tv, p, s);
     case AF_ACT_RELU: return launch_fwd<D, DV, kFamilyElementwise, kActRelu>(d, tq, tk, tv, p, s);
+    case AF_ACT_RELU2: return launch_fwd<D, DV, kFamilyElementwise, kActRelu2>(d, tq, tk, tv, p, s);
     case AF_ACT_IDENTITY: return launch_fwd<D, DV, kFamilyElementwise, kActIdentity>(d, tq, tk, tv, p, s);
     default: break;
   }

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(kRows) parallel_fwd_f32_kernel(
         float z = s[r] - slope * static_cast<float>(i - j) + d.bias;
         if (d.act == AF_ACT_SIGMOID) z = 1.f / (1.f + expf(-z));
         else if (d.act == AF_ACT_RELU) z = fmaxf(z, 0.f);
+        else if (d.act == AF_ACT_RELU2) z = fmaxf(z, 0.f) * fmaxf(z, 0.f);
         s[r] = kept32(m, i, j, d.seq_k) ? z : 0.f;
       }
     }

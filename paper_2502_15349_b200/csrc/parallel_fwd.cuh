@@ -87,6 +87,9 @@ AF_DEVICE float apply_act(float z) {
     return rcp_approx(1.0f + ex2(-z * kLog2e));
   } else if constexpr (kAct == kActRelu) {
     return fmaxf(z, 0.0f);
+  } else if constexpr (kAct == kActRelu2) {
+    const float r = fmaxf(z, 0.0f);
+    return r * r;
   } else {
     return z;
   }

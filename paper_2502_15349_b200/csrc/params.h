@@ -15,6 +15,7 @@ enum Act : int {
   kActIdentity = 0,
   kActSigmoid = 1,
   kActRelu = 2,
+  kActRelu2 = 3,  // relu(z)^2 (squared-relu variant; post-scales folded into z by the planner)
 };
 
 // Band mask derived from the variant's mask_mod expressions:

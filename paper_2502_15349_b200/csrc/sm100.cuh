@@ -258,6 +258,11 @@ AF_DEVICE float exp2_poly(float x) {
                             0.6935868263244629f), f, 0.9999627470970154f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+AF_DEVICE float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 AF_DEVICE float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));

@@ -34,7 +34,7 @@ from .errors import UnsupportedError, InputError
 from .spec import (AttentionSpec, DirectRowNorm, OnlineRowNorm, Pattern, diagonal_scale)
 
 FAMILY_SOFTMAX, FAMILY_ELEMENTWISE = 0, 1
-ACT_IDENTITY, ACT_SIGMOID, ACT_RELU = 0, 1, 2
+ACT_IDENTITY, ACT_SIGMOID, ACT_RELU, ACT_RELU2 = 0, 1, 2, 3
 
 
 @dataclass
@@ -282,10 +282,34 @@ def is_online_softmax(rn, consts: dict) -> bool:
     return True
 
 
-def _strip_act(e):
+def _strip_act(e, consts: dict):
+    """Split ``c * act(inner)`` into (act, inner, fold) where the constant post-scale c is folded
+    into the affine inner argument by ``fold`` (relu(x)*c = relu(c x), relu(x)^2*c =
+    relu(sqrt(c) x)^2 for c > 0; identity is linear).  Sigmoid admits no post-scale."""
+    post = 1.0
+    while isinstance(e, H.BinOp) and e.op in "*/":
+        cl, cr = H.const_value(e.lhs, consts), H.const_value(e.rhs, consts)
+        if cr is not None and cr != 0 and math.isfinite(cr):
+            post *= cr if e.op == "*" else 1.0 / cr
+            e = e.lhs
+        elif cl is not None and e.op == "*" and math.isfinite(cl):
+            post *= cl
+            e = e.rhs
+        else:
+            break
+    act, inner = ACT_IDENTITY, e
     if isinstance(e, H.Fn) and e.func in ("sigmoid", "relu"):
-        return (ACT_SIGMOID if e.func == "sigmoid" else ACT_RELU), e.args[0]
-    return ACT_IDENTITY, e
+        act, inner = (ACT_SIGMOID if e.func == "sigmoid" else ACT_RELU), e.args[0]
+    elif (isinstance(e, H.BinOp) and e.op == "*" and isinstance(e.lhs, H.Fn)
+          and e.lhs.func == "relu" and isinstance(e.rhs, H.Fn) and e.rhs.func == "relu"
+          and H.to_source(e.lhs.args[0]) == H.to_source(e.rhs.args[0])):
+        act, inner = ACT_RELU2, e.lhs.args[0]
+    if post == 1.0:
+        return act, inner, 1.0
+    if act == ACT_SIGMOID or post <= 0:
+        raise UnsupportedError("a constant factor outside sigmoid / a non-positive post-scale is "
+                               "not lowered", post=post)
+    return act, inner, (math.sqrt(post) if act == ACT_RELU2 else post)
 
 
 def _affine_score(e, consts: dict, extras: dict):
@@ -418,13 +442,18 @@ def _plan_parallel(spec: AttentionSpec) -> ParallelPlan:
     expr = H.Name("s")
     for m in plain:
         expr = _substitute(m.expr, "s", expr)
-    act, inner = _strip_act(expr)
+    act, inner, fold = _strip_act(expr, consts)
     extras = {e.name: e for e in spec.extra_inputs}
     aff = _affine_score(inner, consts, extras)
     if aff is None:
-        raise UnsupportedError("score_mod is not act(a*s + slope*(qidx-kidx) + c)",
+        raise UnsupportedError("score_mod is not c*act(a*s + slope*(qidx-kidx) + b)",
                                expr=H.to_source(expr))
     tau, slope_c, slope_x, slope_xc, bias = aff
+    if fold != 1.0:
+        if slope_x is not None:
+            raise UnsupportedError("post-scaled activations with a per-head slope extra are "
+                                   "not lowered")
+        tau, slope_c, bias = tau * fold, slope_c * fold, bias * fold
     if any(v != 0.0 for v in mask_vals):
         raise UnsupportedError("masks ahead of a norm-free score must zero the score (s*0/1)")
     if slope_x is not None:

@@ -219,7 +219,7 @@ def test_unlowered_variant_raises_not_falls_back():
     arrays = to_dev(oracle.generate(spec, 0))
     with pytest.raises(af.UnsupportedError):
         af.run_tiled_parallel(spec, arrays)
-    spec = S.builtin("softmax", heads=2, seq=128, d_qk=32, d_v=32)
+    spec = S.builtin("softmax-diff", heads=2, seq=128, d_qk=128, d_v=256)  # Dv > 128
     with pytest.raises(af.UnsupportedError):
         af.parallel_forward(spec, to_dev(oracle.generate(spec, 0)))
 
