@@ -49,6 +49,8 @@ typedef struct af_parallel_desc {
   int32_t window;            /* >0: also keep only i + diag_offset - j < window            */
   const float* slope;        /* elementwise family: z -= slope[h] * (i - j); may be NULL     */
   float bias;                /* elementwise family: z += bias                               */
+  float cap_a, cap_b;        /* softmax family soft-cap z -> cap_a * tanh(cap_b * z); cap_b = 0
+                                disables it (capped-softmax variant: 30 * tanh(z / 30))      */
 } af_parallel_desc;
 
 /* O = template_forward(q, k, v); lse[b,h,i] = log-sum-exp of row i (softmax family, may be NULL).
@@ -113,6 +115,16 @@ size_t af_mla_decode_workspace(const af_mla_desc* desc);
  * Replaces engine.run_tiled_parallel with seq_q = 1 (test_engine.py:224-230). */
 int af_mla_decode(const af_mla_desc* desc, const void* q, const void* kv, void* o, float* lse,
                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- feature maps (q_mod / k_mod / v_mod that are a function of the tensor alone) ---- */
+enum { AF_FM_NONE = 0, AF_FM_SILU = 1, AF_FM_SIGMOID = 2, AF_FM_RELU = 3, AF_FM_TANH = 4,
+       AF_FM_EXP = 5 };
+
+/* y = f(x) (backward = 0) or y = dy * f'(x) (backward = 1) over n contiguous bf16 elements
+ * (n a multiple of 8).  Applied ahead of the template kernels; replaces the per-tile evaluation
+ * of the mod hooks in engine._premod_qkv (engine.py:511-522) / build_parallel. */
+int af_feature_map(int kind, int backward, const void* x, const void* dy, void* y, int64_t n,
+                   void* stream);
 
 /* ---- diagnostics ---- */
 const char* af_status_string(int status);

@@ -68,6 +68,35 @@ def _check_nan(out: torch.Tensor, what: str) -> torch.Tensor:
     return out
 
 
+# ───────────────────────────── feature maps ─────────────────────────────
+
+def _fmap(kind: int, x: torch.Tensor, dy: torch.Tensor | None = None) -> torch.Tensor:
+    """f(x) (or dy * f'(x)) for an elementwise q/k/v feature map, on the GPU
+    (``af_feature_map``); bf16 in and out."""
+    if kind == 0:
+        return x if dy is None else dy
+    shape = x.shape
+    xf = _as(x, _BF16).contiguous().reshape(-1)
+    n = xf.numel()
+    pad = (-n) % 8
+    if pad:
+        xf = torch.nn.functional.pad(xf, (0, pad))
+    gf = None
+    if dy is not None:
+        gf = _as(dy, _BF16).contiguous().reshape(-1)
+        if pad:
+            gf = torch.nn.functional.pad(gf, (0, pad))
+    y = torch.empty_like(xf)
+    rt.check(rt.lib().af_feature_map(int(kind), int(dy is not None), xf.data_ptr(),
+                                     rt.ptr(gf), y.data_ptr(), xf.numel(), _stream()),
+             "af_feature_map")
+    return y[:n].reshape(shape)
+
+
+def _maps(plan) -> tuple[int, int, int]:
+    return getattr(plan, "q_map", 0), getattr(plan, "k_map", 0), getattr(plan, "v_map", 0)
+
+
 # ───────────────────────────── parallel template ─────────────────────────────
 
 def _parallel_inputs(plan: ParallelPlan, arrays: dict, dtype):
@@ -88,6 +117,11 @@ def _parallel_inputs(plan: ParallelPlan, arrays: dict, dtype):
         slope = slope.expand(d.heads).contiguous() if slope.numel() == 1 else slope.contiguous()
     elif plan.slope_const != 0.0:
         slope = torch.full((d.heads,), plan.slope_const, device=q.device, dtype=torch.float32)
+    qm, km, vm = _maps(plan)
+    if qm or km or vm:
+        if dtype != _BF16 or plan.spec.kv_shared:
+            raise UnsupportedError("feature maps run on the bf16 path of non-MLA variants only")
+        q, k, v = _fmap(qm, q), _fmap(km, k), _fmap(vm, v)
     return _as(q, dtype), _as(k, dtype), _as(v, dtype), slope
 
 
@@ -105,6 +139,7 @@ def _desc(plan: ParallelPlan, q, k, v, o, slope, dtype_code: int) -> rt.Parallel
         plan.band.kernel_window
     c.slope = rt.ptr(slope)
     c.bias = float(plan.bias)
+    c.cap_a, c.cap_b = float(plan.cap_a), float(plan.cap_b)
     return c
 
 
@@ -209,6 +244,16 @@ def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tens
     dk/dv summed over each GQA group; for ``kv_shared`` the V gradient is folded into dk)."""
     spec = _spec(spec)
     plan = plan_parallel(spec)
+    maps = _maps(plan)
+    g = _parallel_backward_mapped(spec, plan, arrays, o, lse, dout)
+    if any(maps):  # chain the feature maps: dL/dx = dL/df(x) * f'(x)
+        for name, kind in zip("qkv", maps):
+            if kind and name in g:
+                g[name] = _fmap(kind, _need(arrays, name), g[name])
+    return g
+
+
+def _parallel_backward_mapped(spec, plan, arrays: dict, o, lse, dout) -> dict:
     q, k, v, slope = _parallel_inputs(plan, arrays, _BF16)
     d = spec.dims
     pad = _padded_dim(spec, "bf16")
@@ -324,6 +369,8 @@ def _linear_qkv(plan: LinearPlan, arrays: dict):
     _check_shape(q, (d.batch, d.heads, d.seq_q, d.d_qk), "q")
     _check_shape(k, (d.batch, d.heads, d.seq_k, d.d_qk), "k")
     _check_shape(v, (d.batch, d.heads, d.seq_k, d.d_v), "v")
+    qm, km, vm = _maps(plan)
+    q, k, v = _fmap(qm, q), _fmap(km, k), _fmap(vm, v)
     pk, pv = _linear_pad(d)
     return (_pad_last(_as(q, _BF16), pk), _pad_last(_as(k, _BF16), pk),
             _pad_last(_as(v, _BF16), pv))
@@ -390,6 +437,9 @@ def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 128) ->
                              _stream()), "af_linear_bwd")
     grads = {"q": dq[..., : d.d_qk], "k": dk[..., : d.d_qk], "v": dv[..., : d.d_v]}
     grads = {n: (t if t.is_contiguous() else t.contiguous()) for n, t in grads.items()}
+    for name, kind in zip("qkv", _maps(plan)):  # chain the feature maps
+        if kind:
+            grads[name] = _fmap(kind, _need(arrays, name), grads[name])
     for name, g in grads_x.items():
         grads[name] = g.reshape(_need(arrays, name).shape)
     return grads

@@ -64,9 +64,10 @@ AF_DEVICE void store_row_bf16(__nv_bfloat16* dst, const uint32_t (&r)[N], float 
 }
 
 // dS from packed P and fp32 dP for 32 columns (both families)
+// (soft-capped softmax: gk holds the packed factor cap_a cap_b (1 - t^2) of d s'/d s)
 template <int kFamily, int kAct, bool kRowDelta>
 AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float* del_col,
-                       float del_row, uint32_t gmask, uint32_t* dsk) {
+                       float del_row, uint32_t gmask, uint32_t* dsk, const uint32_t* gk) {
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
     const uint32_t w = pk[e / 2];
@@ -76,6 +77,10 @@ AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float
     if constexpr (kFamily == kFamilySoftmax) {
       ds0 = p0 * (dp0 - (kRowDelta ? del_row : del_col[e]));
       ds1 = p1 * (dp1 - (kRowDelta ? del_row : del_col[e + 1]));
+      if constexpr (kAct == kActSoftcap) {
+        ds0 *= bf16_lo(gk[e / 2]);
+        ds1 *= bf16_hi(gk[e / 2]);
+      }
     } else if constexpr (kAct == kActSigmoid) {
       ds0 = dp0 * p0 * (1.0f - p0);
       ds1 = dp1 * p1 * (1.0f - p1);
@@ -306,6 +311,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(s_full, n & 1);
       tc_fence_after();
       uint32_t pk[32];
+      uint32_t gk[32];  // soft-cap derivative factors (kActSoftcap only)
       uint32_t gmask[2];
 #pragma unroll
       for (int c2 = 0; c2 < 2; ++c2) {
@@ -313,7 +319,24 @@ __global__ void __launch_bounds__(320, 1)
         tmem_ld32(tmem + lane_base + kColS + cb + c2 * 32, sr);
         tmem_ld_wait();
         uint32_t bits = 0u;
-        if constexpr (kFamily == kFamilySoftmax) {
+        if constexpr (kFamily == kFamilySoftmax && kAct == kActSoftcap) {
+          const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
+          const float cap_g = p.cap_a * p.cap_b;
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float pv[2], gv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              const int i = q0 + cb + c2 * 32 + e + x;
+              const bool keep = fullblk || (kept(p.mask, i, j, p.seq_k) && i < p.seq_q);
+              const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
+              pv[x] = keep ? ex2(fmaf(cap_out, t, -lse_s[c2 * 32 + e + x])) : 0.0f;
+              gv[x] = cap_g * fmaf(-t, t, 1.0f);
+            }
+            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+            gk[c2 * 16 + e / 2] = pack_bf16(gv[0], gv[1]);
+          }
+        } else if constexpr (kFamily == kFamilySoftmax) {
           if (fullblk) {
 #pragma unroll
             for (int e = 0; e < 32; e += 4) {
@@ -375,7 +398,7 @@ __global__ void __launch_bounds__(320, 1)
         tmem_ld32(tmem + lane_base + kColDP + cb + c2 * 32, dr);
         tmem_ld_wait();
         make_ds<kFamily, kAct, false>(pk + c2 * 16, dr, del_s + c2 * 32, 0.0f, gmask[c2],
-                                      dsk + c2 * 16);
+                                      dsk + c2 * 16, gk + c2 * 16);
       }
       tmem_st32(tmem + lane_base + kColDP + pcol, dsk);
       tmem_st_wait();
@@ -635,6 +658,7 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&s_full[half], n & 1);
       tc_fence_after();
       uint32_t pk[32];
+      uint32_t gk[32];  // soft-cap derivative factors (kActSoftcap only)
       uint32_t gmask[2];
 #pragma unroll
       for (int c2 = 0; c2 < 2; ++c2) {
@@ -643,7 +667,23 @@ __global__ void __launch_bounds__(320, 1)
         tmem_ld_wait();
         uint32_t bits = 0u;
         const int jb = c0 + cb + c2 * 32;
-        if constexpr (kFamily == kFamilySoftmax) {
+        if constexpr (kFamily == kFamilySoftmax && kAct == kActSoftcap) {
+          const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
+          const float cap_g = p.cap_a * p.cap_b;
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float pv[2], gv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              const bool keep = fullblk || kept(p.mask, i, jb + e + x, p.seq_k);
+              const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
+              pv[x] = keep ? ex2(fmaf(cap_out, t, -l2)) : 0.0f;
+              gv[x] = cap_g * fmaf(-t, t, 1.0f);
+            }
+            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+            gk[c2 * 16 + e / 2] = pack_bf16(gv[0], gv[1]);
+          }
+        } else if constexpr (kFamily == kFamilySoftmax) {
           if (fullblk) {
 #pragma unroll
             for (int e = 0; e < 32; e += 2)
@@ -687,7 +727,8 @@ __global__ void __launch_bounds__(320, 1)
         uint32_t dr[32];
         tmem_ld32(tmem + lane_base + kColDP + cb + c2 * 32, dr);
         tmem_ld_wait();
-        make_ds<kFamily, kAct, true>(pk + c2 * 16, dr, nullptr, dl, gmask[c2], dsk + c2 * 16);
+        make_ds<kFamily, kAct, true>(pk + c2 * 16, dr, nullptr, dl, gmask[c2], dsk + c2 * 16,
+                                     gk + c2 * 16);
       }
       // dS (packed) over this warp's own S columns: A operand of dQ += dS K
       tmem_st32(tmem + lane_base + kColS + pcol, dsk);

@@ -64,7 +64,10 @@ int launch_bwd(const BwdLaunch& a) {
 
 template <int D, int DV>
 int dispatch_bwd(const BwdLaunch& a) {
-  if (a.d->family == AF_FAMILY_SOFTMAX) return launch_bwd<D, DV, kFamilySoftmax, kActIdentity>(a);
+  if (a.d->family == AF_FAMILY_SOFTMAX) {
+    if (a.d->cap_b != 0.0f) return launch_bwd<D, DV, kFamilySoftmax, kActSoftcap>(a);
+    return launch_bwd<D, DV, kFamilySoftmax, kActIdentity>(a);
+  }
   switch (a.d->act) {
     case AF_ACT_SIGMOID: return launch_bwd<D, DV, kFamilyElementwise, kActSigmoid>(a);
     case AF_ACT_RELU: return launch_bwd<D, DV, kFamilyElementwise, kActRelu>(a);
@@ -101,7 +104,8 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
   AF_REQUIRE(d->q_stride[3] == 1 && d->o_stride[3] == 1, AF_ERR_INPUT, "feature stride must be 1");
   if (is_mla(d)) {
     // MLA lowering: V = K[:, :512] of one latent head; dk receives dK + [dV, 0], dv is unused
-    AF_REQUIRE(v == k && d->v_stride[0] == d->k_stride[0] && d->v_stride[2] == d->k_stride[2],
+    AF_REQUIRE(v == k && d->cap_b == 0.0f && d->v_stride[0] == d->k_stride[0] &&
+                   d->v_stride[2] == d->k_stride[2],
                AF_ERR_UNSUPPORTED, "(576, 512) heads are lowered only as MLA (V = K[:, :512])");
     return mla_bwd(d, q, k, o, lse, dout, dq, dk, workspace, reinterpret_cast<cudaStream_t>(stream));
   }
@@ -151,6 +155,7 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
   p.scale = d->scale; p.scale_log2 = d->scale * kLog2e;
   p.mask.causal = d->causal; p.mask.diag_offset = d->diag_offset; p.mask.window = d->window;
   p.act = d->act; p.slope = d->slope; p.bias = d->bias;
+  p.cap_a = d->cap_a; p.cap_b = d->cap_b;
   p.lse = lse2; p.delta = delta; p.dq_accum = nullptr;
   p.dk = dk; p.dv = dv;
   p.dk_stride_b = d->k_stride[0]; p.dk_stride_h = d->k_stride[1]; p.dk_stride_s = d->k_stride[2];

@@ -30,7 +30,10 @@ int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorM
 template <int D, int DV>
 int dispatch_family(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
                     const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t s) {
-  if (d->family == AF_FAMILY_SOFTMAX) return launch_fwd<D, DV, kFamilySoftmax, kActIdentity>(d, tq, tk, tv, p, s);
+  if (d->family == AF_FAMILY_SOFTMAX) {
+    if (d->cap_b != 0.0f) return launch_fwd<D, DV, kFamilySoftmax, kActSoftcap>(d, tq, tk, tv, p, s);
+    return launch_fwd<D, DV, kFamilySoftmax, kActIdentity>(d, tq, tk, tv, p, s);
+  }
   switch (d->act) {
     case AF_ACT_SIGMOID: return launch_fwd<D, DV, kFamilyElementwise, kActSigmoid>(d, tq, tk, tv, p, s);
     case AF_ACT_RELU: return launch_fwd<D, DV, kFamilyElementwise, kActRelu>(d, tq, tk, tv, p, s);
@@ -73,6 +76,8 @@ ParallelFwdParams make_fwd_params(const af_parallel_desc* d, void* o, float* lse
   p.act = d->act;
   p.slope = d->slope;
   p.bias = d->bias;
+  p.cap_a = d->cap_a;
+  p.cap_b = d->cap_b;
   p.o = o;
   p.o_stride_b = d->o_stride[0];
   p.o_stride_h = d->o_stride[1];
@@ -101,7 +106,8 @@ extern "C" int af_parallel_fwd(const af_parallel_desc* d, const void* q, const v
   AF_REQUIRE(d->o_stride[3] == 1, AF_ERR_INPUT, "output feature stride must be 1");
   if (d->d_qk == 576 && d->d_v == 512) {
     // MLA: one latent head, V = K[:, :512] (same base pointer and strides)
-    AF_REQUIRE(d->family == AF_FAMILY_SOFTMAX && v == k && d->v_stride[0] == d->k_stride[0] &&
+    AF_REQUIRE(d->family == AF_FAMILY_SOFTMAX && d->cap_b == 0.0f && v == k &&
+                   d->v_stride[0] == d->k_stride[0] &&
                    d->v_stride[2] == d->k_stride[2],
                AF_ERR_UNSUPPORTED, "(576, 512) heads are lowered only as MLA (softmax, V = K[:, :512])");
     return mla_prefill(d, q, k, o, lse, reinterpret_cast<cudaStream_t>(stream));

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kRows) parallel_fwd_f32_kernel(
     if (d.family == AF_FAMILY_SOFTMAX) {
       float bmax = -INFINITY;
       for (int r = 0; r < kKeys; ++r) {
+        if (d.cap_b != 0.f) s[r] = d.cap_a * tanhf(d.cap_b * s[r]);  // soft-cap (scaled logits)
         if (!kept32(m, i, j0 + r, d.seq_k)) s[r] = -INFINITY;
         bmax = fmaxf(bmax, s[r]);
       }

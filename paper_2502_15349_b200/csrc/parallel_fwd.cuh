@@ -281,7 +281,9 @@ __global__ void __launch_bounds__(320, 1)
         // Fully-kept blocks (the bulk of a causal sweep): the row max is taken on the raw scores
         // and the scale folds into one FFMA per element; an eighth of the exponentials run as a
         // polynomial on the FMA pipe so the MUFU stream stays below the MMA time.
-        const bool fast = full && p.scale_log2 > 0.0f;
+        constexpr bool kCap = kAct == kActSoftcap;
+        const bool fast = !kCap && full && p.scale_log2 > 0.0f;
+        const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
         float bmax = -INFINITY;
         if (fast) {
 #pragma unroll
@@ -290,7 +292,8 @@ __global__ void __launch_bounds__(320, 1)
         } else {
 #pragma unroll
           for (int c = 0; c < kBlockN; ++c) {
-            s[c] = kept(p.mask, i, c0 + c, p.seq_k) ? s[c] * p.scale_log2 : -INFINITY;
+            const float x = kCap ? cap_out * tanh_precise(cap_in * s[c]) : s[c] * p.scale_log2;
+            s[c] = (full || kept(p.mask, i, c0 + c, p.seq_k)) ? x : -INFINITY;
             bmax = fmaxf(bmax, s[c]);
           }
         }

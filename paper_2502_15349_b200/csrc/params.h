@@ -16,6 +16,7 @@ enum Act : int {
   kActSigmoid = 1,
   kActRelu = 2,
   kActRelu2 = 3,  // relu(z)^2 (squared-relu variant; post-scales folded into z by the planner)
+  kActSoftcap = 4,  // softmax family: z -> cap_a tanh(cap_b z) ahead of the softmax
 };
 
 // Band mask derived from the variant's mask_mod expressions:
@@ -37,6 +38,7 @@ struct ParallelFwdParams {
   int act;
   const float* slope;  // per q-head slope (may be null)
   float bias;
+  float cap_a, cap_b;  // softmax soft-cap (kActSoftcap): z -> cap_a tanh(cap_b z)
   // output O (bf16) with element strides, LSE fp32 [B, Hq, Sq] (may be null)
   void* o;
   int64_t o_stride_b, o_stride_h, o_stride_s;
@@ -50,6 +52,7 @@ struct ParallelBwdParams {
   int act;
   const float* slope;
   float bias;
+  float cap_a, cap_b;  // softmax soft-cap (kActSoftcap)
   const float* lse;    // [B, Hq, Sq] natural-log LSE (softmax family)
   const float* delta;  // [B, Hq, Sq] rowsum(dO*O) (softmax family)
   float* dq_accum;     // [B, Hq, Sq, Dqk] fp32 accumulator (zeroed)

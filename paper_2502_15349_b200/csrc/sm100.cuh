@@ -258,6 +258,15 @@ AF_DEVICE float exp2_poly(float x) {
                             0.6935868263244629f), f, 0.9999627470970154f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// tanh(y) = 1 - 2 / (1 + 2^(2 y log2 e)): absolute error ~1e-7 over the whole range (the
+// soft-cap multiplies it by the cap, so absolute — not relative — accuracy is what matters);
+// saturates to +-1 without NaN.
+AF_DEVICE float tanh_precise(float y) {
+  float r;
+  const float e = ex2(2.0f * 1.4426950408889634f * y);
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return 1.0f - 2.0f * r;
+}
 AF_DEVICE float sqrt_approx(float x) {
   float r;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));

@@ -68,6 +68,10 @@ class Band:
         return 0 if self.window is None else self.window + self.diag_offset
 
 
+FM_NONE, FM_SILU, FM_SIGMOID, FM_RELU, FM_TANH, FM_EXP = range(6)
+_FM_BY_FUNC = {"sigmoid": FM_SIGMOID, "relu": FM_RELU, "tanh": FM_TANH, "exp": FM_EXP}
+
+
 @dataclass
 class ParallelPlan:
     spec: AttentionSpec
@@ -78,6 +82,11 @@ class ParallelPlan:
     slope_extra: str | None = None  # per-head extra multiplying -(qidx - kidx)
     slope_const: float = 0.0        # constant multiplier of -(qidx - kidx)
     bias: float = 0.0
+    q_map: int = FM_NONE            # elementwise feature maps applied ahead of the kernels
+    k_map: int = FM_NONE
+    v_map: int = FM_NONE
+    cap_a: float = 0.0              # softmax family soft-cap s -> cap_a * tanh(cap_b * s)
+    cap_b: float = 0.0              # (0 = none; e.g. capped-softmax: 30 * tanh(s / 30))
 
     @property
     def has_lse(self) -> bool:
@@ -92,6 +101,9 @@ class LinearPlan:
     decay_const: float = 1.0
     k_gate: str | None = None             # extra multiplying k (k_mod = k * gate)
     chunk: int = 64
+    q_map: int = FM_NONE                  # elementwise feature maps applied ahead of the kernels
+    k_map: int = FM_NONE
+    v_map: int = FM_NONE
 
 
 # ───────────────────────────── helpers ─────────────────────────────
@@ -112,6 +124,31 @@ def _scalar_mod(fn, var: str, consts: dict) -> float:
     raise UnsupportedError(f"{var}_mod is not a compile-time scalar on this template "
                            "(elementwise feature maps with extras are not lowered yet)",
                            source=fn.source)
+
+
+def _feature_map(fn, var: str, consts: dict) -> tuple[int, float]:
+    """(map kind, scalar) for a q/k/v mod: a compile-time scalar multiple (kind FM_NONE) or one
+    of the elementwise maps the feature-map kernel implements, f(var) with f in {var *
+    sigmoid(var), sigmoid, relu, tanh, exp}."""
+    if fn is None:
+        return FM_NONE, 1.0
+    try:
+        return FM_NONE, _scalar_mod(fn, var, consts)
+    except UnsupportedError:
+        pass
+    e = fn.expr
+
+    def is_var(z):
+        return isinstance(z, H.Name) and z.name == var
+
+    if isinstance(e, H.Fn) and e.func in _FM_BY_FUNC and len(e.args) == 1 and is_var(e.args[0]):
+        return _FM_BY_FUNC[e.func], 1.0
+    if isinstance(e, H.BinOp) and e.op == "*":
+        for x, y in ((e.lhs, e.rhs), (e.rhs, e.lhs)):
+            if is_var(x) and isinstance(y, H.Fn) and y.func == "sigmoid" and is_var(y.args[0]):
+                return FM_SILU, 1.0
+    raise UnsupportedError(f"{var}_mod is neither a compile-time scalar nor a supported "
+                           "elementwise feature map", source=fn.source)
 
 
 def _linear_in_index(e, consts: dict):
@@ -402,9 +439,13 @@ def _plan_parallel(spec: AttentionSpec) -> ParallelPlan:
         raise InputError("variant is not a parallel-pattern variant", variant=spec.name)
     spec.validate()
     consts = spec.dims.const_env()
-    scale = _scalar_mod(spec.q_mod, "q", consts) * _scalar_mod(spec.k_mod, "k", consts)
-    if spec.v_mod is not None and _scalar_mod(spec.v_mod, "v", consts) != 1.0:
+    q_map, q_sc = _feature_map(spec.q_mod, "q", consts)
+    k_map, k_sc = _feature_map(spec.k_mod, "k", consts)
+    v_map, v_sc = _feature_map(spec.v_mod, "v", consts)
+    scale = q_sc * k_sc
+    if v_sc != 1.0:
         raise UnsupportedError("v_mod scaling is not lowered", source=spec.v_mod.source)
+    maps = dict(q_map=q_map, k_map=k_map, v_map=v_map)
     if spec.output_mod is not None:
         raise UnsupportedError("output_mod is not lowered on the parallel template yet",
                                source=spec.output_mod.source)
@@ -424,16 +465,20 @@ def _plan_parallel(spec: AttentionSpec) -> ParallelPlan:
             plain.append(m)
     rn = spec.rownorm
     if rn is not None and is_online_softmax(rn if isinstance(rn, OnlineRowNorm) else None, consts):
+        cap = (0.0, 0.0)
         if plain:
-            raise UnsupportedError("score_mod ahead of the online softmax is not lowered yet",
-                                   source=plain[0].source)
+            cap = _softcap(plain, consts)
+            if cap is None:
+                raise UnsupportedError("score_mod ahead of the online softmax must be a soft-cap "
+                                       "A * tanh(s * B)", source=plain[0].source)
         if any(v != -math.inf for v in mask_vals):
             raise UnsupportedError("softmax masks must use the additive -inf form")
-        return ParallelPlan(spec, FAMILY_SOFTMAX, scale=scale, band=band)
+        return ParallelPlan(spec, FAMILY_SOFTMAX, scale=scale, band=band, cap_a=cap[0],
+                            cap_b=cap[1], **maps)
     if isinstance(rn, DirectRowNorm) and _direct_is_softmax(rn, consts):
         if plain or any(v != -math.inf for v in mask_vals):
             raise UnsupportedError("direct softmax with score mods is not lowered")
-        return ParallelPlan(spec, FAMILY_SOFTMAX, scale=scale, band=band)
+        return ParallelPlan(spec, FAMILY_SOFTMAX, scale=scale, band=band, **maps)
     if rn is not None:
         raise UnsupportedError("row normalisation is neither online softmax nor absent; the "
                                "abssum-clamp / generic online forms are not lowered yet",
@@ -466,7 +511,33 @@ def _plan_parallel(spec: AttentionSpec) -> ParallelPlan:
     if slope_x is not None and slope_xc != 1.0:
         raise UnsupportedError("slope extra must enter with coefficient 1", coef=slope_xc)
     return ParallelPlan(spec, FAMILY_ELEMENTWISE, act=act, scale=scale * tau, band=band,
-                        slope_extra=slope_x, slope_const=slope_c, bias=bias)
+                        slope_extra=slope_x, slope_const=slope_c, bias=bias, **maps)
+
+
+def _softcap(mods, consts: dict) -> tuple[float, float] | None:
+    """A single score mod of the form ``A * tanh(s * B)`` (or ``tanh(s / C) * A``, constants) —
+    the logit soft-cap ahead of the softmax."""
+    if len(mods) != 1:
+        return None
+    e = mods[0].expr
+    a = 1.0
+    if isinstance(e, H.BinOp) and e.op == "*":
+        for x, y in ((e.lhs, e.rhs), (e.rhs, e.lhs)):
+            c = H.const_value(x, consts)
+            if c is not None and isinstance(y, H.Fn) and y.func == "tanh":
+                a, e = c, y
+                break
+    if not (isinstance(e, H.Fn) and e.func == "tanh"):
+        return None
+    inner = e.args[0]
+    try:
+        b = _scalar_mod(type("M", (), {"expr": inner, "source": H.to_source(inner)})(), "s",
+                        consts)
+    except UnsupportedError:
+        return None
+    if not (math.isfinite(a) and math.isfinite(b)) or a == 0.0:
+        return None
+    return a, b
 
 
 def _direct_is_softmax(rn: DirectRowNorm, consts) -> bool:
@@ -538,17 +609,25 @@ def _plan_linear(spec: AttentionSpec, chunk: int = 64) -> LinearPlan:
                         and y.name in extras:
                     k_gate, ok = y.name, True
         if not ok:
-            raise UnsupportedError("k_mod must be k * <per-step extra> on the linear template",
-                                   source=spec.k_mod.source)
-    if spec.v_mod is not None:
-        raise UnsupportedError("v_mod is not lowered on the linear template yet",
-                               source=spec.v_mod.source)
+            k_map_, k_sc = _feature_map(spec.k_mod, "k", consts)
+            if k_map_ == FM_NONE:
+                raise UnsupportedError("k_mod must be k * <per-step extra> or an elementwise "
+                                       "feature map on the linear template",
+                                       source=spec.k_mod.source)
+            if k_sc != 1.0:
+                raise UnsupportedError("scaled k feature maps are not lowered",
+                                       source=spec.k_mod.source)
+    k_map = FM_NONE if k_gate is not None or spec.k_mod is None else \
+        _feature_map(spec.k_mod, "k", consts)[0]
+    v_map, v_scale = _feature_map(spec.v_mod, "v", consts)
     if spec.output_mod is not None:
         raise UnsupportedError("output_mod is not lowered on the linear template yet",
                                source=spec.output_mod.source)
-    q_scale = _scalar_mod(spec.q_mod, "q", consts)
-    return LinearPlan(spec, q_scale=q_scale, decay_factors=tuple(names), decay_const=const,
-                      k_gate=k_gate, chunk=chunk)
+    q_map, q_scale = _feature_map(spec.q_mod, "q", consts)
+    # o is linear in v: a scalar v_mod folds into the output scale
+    return LinearPlan(spec, q_scale=q_scale * v_scale, decay_factors=tuple(names),
+                      decay_const=const, k_gate=k_gate, chunk=chunk, q_map=q_map, k_map=k_map,
+                      v_map=v_map)
 
 
 # ───────────────────────────── plan cache ─────────────────────────────

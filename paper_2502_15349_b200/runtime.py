@@ -20,6 +20,7 @@ AF_OK, AF_ERR_INPUT, AF_ERR_SHAPE, AF_ERR_UNSUPPORTED, AF_ERR_NAN, AF_ERR_CUDA =
 AF_FAMILY_SOFTMAX, AF_FAMILY_ELEMENTWISE = 0, 1
 AF_ACT_IDENTITY, AF_ACT_SIGMOID, AF_ACT_RELU, AF_ACT_RELU2 = 0, 1, 2, 3
 AF_DTYPE_BF16, AF_DTYPE_F32 = 0, 1
+AF_FM_NONE, AF_FM_SILU, AF_FM_SIGMOID, AF_FM_RELU, AF_FM_TANH, AF_FM_EXP = range(6)
 
 I64x4 = C.c_int64 * 4
 
@@ -32,7 +33,7 @@ class ParallelDesc(C.Structure):
         ("q_stride", I64x4), ("k_stride", I64x4), ("v_stride", I64x4), ("o_stride", I64x4),
         ("family", C.c_int32), ("act", C.c_int32), ("scale", C.c_float),
         ("causal", C.c_int32), ("diag_offset", C.c_int32), ("window", C.c_int32),
-        ("slope", C.c_void_p), ("bias", C.c_float),
+        ("slope", C.c_void_p), ("bias", C.c_float), ("cap_a", C.c_float), ("cap_b", C.c_float),
     ]
 
 
@@ -70,6 +71,7 @@ SIGNATURES: dict[str, tuple] = {
                                 P]),  # (desc, q, k, v, dout, dq, dk, dv, d_factor**, d_gate, ws..)
     "af_mla_decode_workspace": (C.c_size_t, [C.POINTER(MlaDesc)]),
     "af_mla_decode": (C.c_int, [C.POINTER(MlaDesc), P, P, P, P, P, C.c_size_t, P]),
+    "af_feature_map": (C.c_int, [C.c_int, C.c_int, P, P, P, C.c_int64, P]),
     "af_status_string": (C.c_char_p, [C.c_int]),
     "af_last_error": (C.c_char_p, []),
     "af_device_sm_count": (C.c_int, []),
