@@ -32,7 +32,7 @@ enum {
 };
 
 /* ---- parallel template (attention.py:389-449, engine.py:423-505) ---- */
-enum { AF_FAMILY_SOFTMAX = 0, AF_FAMILY_ELEMENTWISE = 1 };
+enum { AF_FAMILY_SOFTMAX = 0, AF_FAMILY_ELEMENTWISE = 1, AF_FAMILY_ABSSUM = 2 };
 enum { AF_ACT_IDENTITY = 0, AF_ACT_SIGMOID = 1, AF_ACT_RELU = 2, AF_ACT_RELU2 = 3 };
 enum { AF_DTYPE_BF16 = 0, AF_DTYPE_F32 = 1 };
 
@@ -47,10 +47,15 @@ typedef struct af_parallel_desc {
   int32_t causal;            /* band mask from mask_mod: keep j <= i + diag_offset         */
   int32_t diag_offset;
   int32_t window;            /* >0: also keep only i + diag_offset - j < window            */
-  const float* slope;        /* elementwise family: z -= slope[h] * (i - j); may be NULL     */
+  const float* slope;        /* elementwise family: z -= slope[h] * (i - j); may be NULL.
+                                abssum family: log2 gamma_h of the causal decay mask
+                                z = tau q.k gamma_h^(i-j) [j <= i]                          */
   float bias;                /* elementwise family: z += bias                               */
   float cap_a, cap_b;        /* softmax family soft-cap z -> cap_a * tanh(cap_b * z); cap_b = 0
-                                disables it (capped-softmax variant: 30 * tanh(z / 30))      */
+                                disables it (capped-softmax variant: 30 * tanh(z / 30)).
+                                abssum family: cap_a = 1 divides rows by clamp(sum|z|, 1, inf)
+                                (retention-parallel), 0 leaves them unnormalised; lse then
+                                receives the row abs-sum                                     */
 } af_parallel_desc;
 
 /* O = template_forward(q, k, v); lse[b,h,i] = log-sum-exp of row i (softmax family, may be NULL).

@@ -29,7 +29,8 @@ import torch
 
 from . import runtime as rt
 from .errors import InputError, NanError, ShapeError, UnsupportedError
-from .plan import FAMILY_SOFTMAX, LinearPlan, ParallelPlan, plan_linear, plan_parallel
+from .plan import (FAMILY_ABSSUM, FAMILY_SOFTMAX, LinearPlan, ParallelPlan, plan_linear,
+                   plan_parallel)
 from .spec import AttentionSpec, Pattern, from_reference
 
 _BF16 = torch.bfloat16
@@ -112,7 +113,11 @@ def _parallel_inputs(plan: ParallelPlan, arrays: dict, dtype):
         v = _need(arrays, "v")
         _check_shape(v, (d.batch, hkv, d.seq_k, d.d_v), "v")
     slope = None
-    if plan.slope_extra is not None:
+    if plan.family == FAMILY_ABSSUM:
+        _check_decay_mask(plan, _need(arrays, plan.decay_extra), q.device)
+        slope = torch.tensor([math.log2(g) for g in plan.decay_gammas], device=q.device,
+                             dtype=torch.float32)
+    elif plan.slope_extra is not None:
         slope = _need(arrays, plan.slope_extra).to(torch.float32).reshape(-1)
         slope = slope.expand(d.heads).contiguous() if slope.numel() == 1 else slope.contiguous()
     elif plan.slope_const != 0.0:
@@ -140,7 +145,36 @@ def _desc(plan: ParallelPlan, q, k, v, o, slope, dtype_code: int) -> rt.Parallel
     c.slope = rt.ptr(slope)
     c.bias = float(plan.bias)
     c.cap_a, c.cap_b = float(plan.cap_a), float(plan.cap_b)
+    if plan.family == FAMILY_ABSSUM:  # cap_a = 1: rows divided by clamp(sum |s|, 1, inf)
+        c.cap_a, c.cap_b = (1.0 if plan.normalize else 0.0), 0.0
     return c
+
+
+_MASK_CHECKED: dict = {}
+
+
+def _check_decay_mask(plan: ParallelPlan, mask: torch.Tensor, device) -> None:
+    """The abssum kernels synthesise the causal decay mask gamma_h^(i-j) in-register from the
+    extra's declared fill; a mask tensor holding anything else is not lowered.  Checked once per
+    tensor version (a GPU pass over the mask)."""
+    d = plan.spec.dims
+    key = (mask.data_ptr(), mask._version, tuple(mask.shape), plan.decay_gammas)
+    if _MASK_CHECKED.get(key):
+        return
+    _check_shape(mask, (1, d.heads, d.seq_q, d.seq_k), plan.decay_extra)
+    i = torch.arange(d.seq_q, device=device, dtype=torch.float64).view(1, 1, -1, 1)
+    j = torch.arange(d.seq_k, device=device, dtype=torch.float64).view(1, 1, 1, -1)
+    g = torch.tensor(plan.decay_gammas, device=device, dtype=torch.float64).view(1, -1, 1, 1)
+    want = torch.where(i >= j, g ** (i - j).clamp(min=0), torch.zeros((), device=device,
+                                                                        dtype=torch.float64))
+    err = (mask.to(device=device, dtype=torch.float64) - want).abs().max().item()
+    if not err <= 1e-6:
+        raise UnsupportedError("decay-mask extra differs from its declared causal_decay_mask "
+                               "fill; arbitrary materialised score masks are not lowered",
+                               extra=plan.decay_extra, max_abs_diff=err)
+    if len(_MASK_CHECKED) > 64:
+        _MASK_CHECKED.clear()
+    _MASK_CHECKED[key] = True
 
 
 MLA_DQK, MLA_DV = 576, 512
@@ -283,8 +317,8 @@ def _parallel_backward_mapped(spec, plan, arrays: dict, o, lse, dout) -> dict:
     L = rt.lib()
     ws_n = L.af_parallel_bwd_workspace(desc)
     ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
-    if plan.family == FAMILY_SOFTMAX and lse is None:
-        raise InputError("softmax backward needs the forward LSE")
+    if plan.family in (FAMILY_SOFTMAX, FAMILY_ABSSUM) and lse is None:
+        raise InputError("softmax / abssum backward needs the forward row statistic")
     rt.check(L.af_parallel_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                rt.ptr(lse), dout.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                dv.data_ptr(), ws.data_ptr(), ws_n, _stream()), "af_parallel_bwd")
@@ -306,8 +340,8 @@ def parallel_backward_padded(spec, plan, qkvs, o, lse, dout, pad: int) -> dict:
     L = rt.lib()
     ws_n = L.af_parallel_bwd_workspace(desc)
     ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
-    if plan.family == FAMILY_SOFTMAX and lse is None:
-        raise InputError("softmax backward needs the forward LSE")
+    if plan.family in (FAMILY_SOFTMAX, FAMILY_ABSSUM) and lse is None:
+        raise InputError("softmax / abssum backward needs the forward row statistic")
     rt.check(L.af_parallel_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                rt.ptr(lse), dout.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                dv.data_ptr(), ws.data_ptr(), ws_n, _stream()), "af_parallel_bwd")

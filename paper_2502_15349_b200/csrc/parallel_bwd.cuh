@@ -81,6 +81,12 @@ AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float
         ds0 *= bf16_lo(gk[e / 2]);
         ds1 *= bf16_hi(gk[e / 2]);
       }
+    } else if constexpr (kFamily == kFamilyAbssum) {
+      // ds = (dP - [a >= 1] sign(s) D) / c, times the decay mask (gk = M / c); sign(0) = +1
+      const float d0 = kRowDelta ? del_row : del_col[e];
+      const float d1 = kRowDelta ? del_row : del_col[e + 1];
+      ds0 = (dp0 - (((gmask >> e) & 1u) ? d0 : -d0)) * bf16_lo(gk[e / 2]);
+      ds1 = (dp1 - (((gmask >> (e + 1)) & 1u) ? d1 : -d1)) * bf16_hi(gk[e / 2]);
     } else if constexpr (kAct == kActSigmoid) {
       ds0 = dp0 * p0 * (1.0f - p0);
       ds1 = dp1 * p1 * (1.0f - p1);
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       const bool fullblk = tile_fully_kept(p.mask, q0, k0, p.seq_q, p.seq_k);
       float slope = 0.0f;
-      if constexpr (kFamily == kFamilyElementwise) {
+      if constexpr (kFamily != kFamilySoftmax) {
         if (p.slope != nullptr) slope = p.slope[h];
       }
       const float* lse_s = sLse + s * kBlockM + cb;
@@ -332,6 +338,25 @@ __global__ void __launch_bounds__(320, 1)
               const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
               pv[x] = keep ? ex2(fmaf(cap_out, t, -lse_s[c2 * 32 + e + x])) : 0.0f;
               gv[x] = cap_g * fmaf(-t, t, 1.0f);
+            }
+            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+            gk[c2 * 16 + e / 2] = pack_bf16(gv[0], gv[1]);
+          }
+        } else if constexpr (kFamily == kFamilyAbssum) {
+          const bool norm = p.cap_a != 0.0f;
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float pv[2], gv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              const int i = q0 + cb + c2 * 32 + e + x;
+              const bool keep = fullblk || (kept(p.mask, i, j, p.seq_k) && i < p.seq_q);
+              const float rc = norm ? rcp_approx(fmaxf(lse_s[c2 * 32 + e + x], 1.0f)) : 1.0f;
+              const float m = ex2(static_cast<float>(i - j) * slope);
+              const float z = __uint_as_float(sr[e + x]) * p.scale * m;
+              pv[x] = keep ? z * rc : 0.0f;
+              gv[x] = keep ? m * rc : 0.0f;
+              bits |= (z >= 0.0f) ? (1u << (e + x)) : 0u;
             }
             pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
             gk[c2 * 16 + e / 2] = pack_bf16(gv[0], gv[1]);
@@ -648,7 +673,7 @@ __global__ void __launch_bounds__(320, 1)
     const float l2 = live ? lse2[srow] : INFINITY;  // +inf -> P = 0
     const float dl = live ? delta[srow] : 0.0f;
     float slope = 0.0f;
-    if constexpr (kFamily == kFamilyElementwise) {
+    if constexpr (kFamily != kFamilySoftmax) {
       if (p.slope != nullptr) slope = p.slope[h];
     }
     const float fi = static_cast<float>(i);
@@ -679,6 +704,24 @@ __global__ void __launch_bounds__(320, 1)
               const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
               pv[x] = keep ? ex2(fmaf(cap_out, t, -l2)) : 0.0f;
               gv[x] = cap_g * fmaf(-t, t, 1.0f);
+            }
+            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+            gk[c2 * 16 + e / 2] = pack_bf16(gv[0], gv[1]);
+          }
+        } else if constexpr (kFamily == kFamilyAbssum) {
+          const float rc = (p.cap_a != 0.0f) ? rcp_approx(fmaxf(l2, 1.0f)) : 1.0f;
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float pv[2], gv[2];
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+              const int jj = jb + e + x;
+              const bool keep = live && (fullblk || kept(p.mask, i, jj, p.seq_k));
+              const float m = ex2(static_cast<float>(i - jj) * slope);
+              const float z = __uint_as_float(sr[e + x]) * p.scale * m;
+              pv[x] = keep ? z * rc : 0.0f;
+              gv[x] = keep ? m * rc : 0.0f;
+              bits |= (z >= 0.0f) ? (1u << (e + x)) : 0u;
             }
             pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
             gk[c2 * 16 + e / 2] = pack_bf16(gv[0], gv[1]);
@@ -783,7 +826,9 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
   const int i = static_cast<int>(gw % seq_q_pad);
   const int b = static_cast<int>(bh / heads), h = static_cast<int>(bh % heads);
   float acc = 0.0f;
-  if (i < seq_q && family == kFamilySoftmax) {
+  // family 2 = abssum (normalised rows), 3 = abssum without the row norm (internal codes)
+  const bool need_d = family == kFamilySoftmax || family == 2;
+  if (i < seq_q && need_d) {
     const __nv_bfloat16* orow = o + b * o_sb + h * o_sh + static_cast<int64_t>(i) * o_ss;
     const __nv_bfloat16* drow = dout + b * do_sb + h * do_sh + static_cast<int64_t>(i) * do_ss;
     for (int c = lane * 2; c < DV; c += 64) {
@@ -796,12 +841,18 @@ __global__ void bwd_preprocess_kernel(const __nv_bfloat16* __restrict__ o,
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) {
-    delta[gw] = acc;
     float l = INFINITY;
-    if (i < seq_q && family == kFamilySoftmax) {
-      const float v = lse[(static_cast<int64_t>(b) * heads + h) * seq_q + i];
-      l = (v == -INFINITY) ? INFINITY : v * kLog2e;  // fully-masked row: P = 0
+    if (family == kFamilySoftmax) {
+      if (i < seq_q) {
+        const float v = lse[(static_cast<int64_t>(b) * heads + h) * seq_q + i];
+        l = (v == -INFINITY) ? INFINITY : v * kLog2e;  // fully-masked row: P = 0
+      }
+    } else if (family == 2 || family == 3) {  // row abs-sum a_i; D only where the clamp is off
+      const float a = (i < seq_q) ? lse[(static_cast<int64_t>(b) * heads + h) * seq_q + i] : 0.0f;
+      l = (i < seq_q) ? a : INFINITY;
+      if (family == 3 || a < 1.0f) acc = 0.0f;
     }
+    delta[gw] = acc;
     lse2[gw] = l;
   }
 }

@@ -68,6 +68,7 @@ int dispatch_bwd(const BwdLaunch& a) {
     if (a.d->cap_b != 0.0f) return launch_bwd<D, DV, kFamilySoftmax, kActSoftcap>(a);
     return launch_bwd<D, DV, kFamilySoftmax, kActIdentity>(a);
   }
+  if (a.d->family == AF_FAMILY_ABSSUM) return launch_bwd<D, DV, kFamilyAbssum, kActIdentity>(a);
   switch (a.d->act) {
     case AF_ACT_SIGMOID: return launch_bwd<D, DV, kFamilyElementwise, kActSigmoid>(a);
     case AF_ACT_RELU: return launch_bwd<D, DV, kFamilyElementwise, kActRelu>(a);
@@ -99,8 +100,8 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
   AF_REQUIRE(d->dtype == AF_DTYPE_BF16, AF_ERR_UNSUPPORTED, "backward runs on bf16 inputs only");
   AF_REQUIRE(workspace_bytes >= af_parallel_bwd_workspace(d), AF_ERR_INPUT,
              "workspace too small (%zu < %zu)", workspace_bytes, af_parallel_bwd_workspace(d));
-  AF_REQUIRE(d->family != AF_FAMILY_SOFTMAX || lse != nullptr, AF_ERR_INPUT,
-             "softmax backward needs the forward LSE");
+  AF_REQUIRE((d->family != AF_FAMILY_SOFTMAX && d->family != AF_FAMILY_ABSSUM) || lse != nullptr,
+             AF_ERR_INPUT, "softmax / abssum backward needs the forward row statistic (lse)");
   AF_REQUIRE(d->q_stride[3] == 1 && d->o_stride[3] == 1, AF_ERR_INPUT, "feature stride must be 1");
   if (is_mla(d)) {
     // MLA lowering: V = K[:, :512] of one latent head; dk receives dK + [dV, 0], dv is unused
@@ -146,7 +147,9 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
                                      static_cast<const __nv_bfloat16*>(dout), lse, d->o_stride[0],
                                      d->o_stride[1], d->o_stride[2], d->o_stride[0],
                                      d->o_stride[1], d->o_stride[2], d->heads_q, d->seq_q, a.pad,
-                                     d->family, lse2, delta, rows);
+                                     (d->family == AF_FAMILY_ABSSUM && d->cap_a == 0.0f)
+                                         ? 3 : d->family,
+                                     lse2, delta, rows);
     AF_CUDA_CHECK(cudaGetLastError());
   }
   ParallelBwdParams& p = a.p;

@@ -34,6 +34,7 @@ int dispatch_family(const af_parallel_desc* d, const CUtensorMap& tq, const CUte
     if (d->cap_b != 0.0f) return launch_fwd<D, DV, kFamilySoftmax, kActSoftcap>(d, tq, tk, tv, p, s);
     return launch_fwd<D, DV, kFamilySoftmax, kActIdentity>(d, tq, tk, tv, p, s);
   }
+  if (d->family == AF_FAMILY_ABSSUM) return launch_fwd<D, DV, kFamilyAbssum, kActIdentity>(d, tq, tk, tv, p, s);
   switch (d->act) {
     case AF_ACT_SIGMOID: return launch_fwd<D, DV, kFamilyElementwise, kActSigmoid>(d, tq, tk, tv, p, s);
     case AF_ACT_RELU: return launch_fwd<D, DV, kFamilyElementwise, kActRelu>(d, tq, tk, tv, p, s);
@@ -54,8 +55,11 @@ int validate_parallel(const af_parallel_desc* d) {
              AF_ERR_INPUT, "dims must be >= 1");
   AF_REQUIRE(d->heads_q % d->heads_kv == 0, AF_ERR_SHAPE,
              "heads_q (%d) must be a multiple of heads_kv (%d)", d->heads_q, d->heads_kv);
-  AF_REQUIRE(d->family == AF_FAMILY_SOFTMAX || d->family == AF_FAMILY_ELEMENTWISE, AF_ERR_INPUT,
-             "unknown hook family %d", d->family);
+  AF_REQUIRE(d->family == AF_FAMILY_SOFTMAX || d->family == AF_FAMILY_ELEMENTWISE ||
+                 d->family == AF_FAMILY_ABSSUM,
+             AF_ERR_INPUT, "unknown hook family %d", d->family);
+  AF_REQUIRE(d->family != AF_FAMILY_ABSSUM || d->slope != nullptr, AF_ERR_INPUT,
+             "abssum family needs the per-head log2 decay (slope)");
   return AF_OK;
 }
 

@@ -87,6 +87,15 @@ __global__ void __launch_bounds__(kRows) parallel_fwd_f32_kernel(
       m_run = m_new;
 #pragma unroll
       for (int c = 0; c < DV; ++c) acc[c] *= rsc;
+    } else if (d.family == AF_FAMILY_ABSSUM) {
+      // retention-parallel: s * gamma^(i-j) on the band, row abs-sum in l_run (slope = log2 g)
+      for (int r = 0; r < kKeys; ++r) {
+        const int j = j0 + r;
+        const float z = kept32(m, i, j, d.seq_k) ? s[r] * exp2f(static_cast<float>(i - j) * slope)
+                                                 : 0.f;
+        l_run += fabsf(z);
+        s[r] = z;
+      }
     } else {
       for (int r = 0; r < kKeys; ++r) {
         const int j = j0 + r;
@@ -111,6 +120,11 @@ __global__ void __launch_bounds__(kRows) parallel_fwd_f32_kernel(
     if (lse != nullptr)
       lse[(static_cast<int64_t>(b) * d.heads_q + h) * d.seq_q + i] =
           (l_run == 0.f) ? -INFINITY : m_run + logf(l_run);
+  } else if (d.family == AF_FAMILY_ABSSUM) {
+    const float inv = (d.cap_a != 0.f) ? 1.f / fmaxf(l_run, 1.f) : 1.f;
+#pragma unroll
+    for (int c = 0; c < DV; ++c) op[c] = acc[c] * inv;
+    if (lse != nullptr) lse[(static_cast<int64_t>(b) * d.heads_q + h) * d.seq_q + i] = l_run;
   } else {
 #pragma unroll
     for (int c = 0; c < DV; ++c) op[c] = acc[c];

@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(320, 1)
     float m_run = -INFINITY;  // running max, log2-scaled units
     float l_run = 0.0f;
     float slope = 0.0f;
-    if constexpr (kFamily == kFamilyElementwise) {
+    if constexpr (kFamily != kFamilySoftmax) {
       if (p.slope != nullptr) slope = p.slope[h];
     }
     const float fi = static_cast<float>(i);
@@ -349,6 +349,27 @@ __global__ void __launch_bounds__(320, 1)
           }
           tmem_st_wait();
         }
+      } else if constexpr (kFamily == kFamilyAbssum) {
+        // s = tau q.k gamma^(i-j) on the kept band (slope = log2 gamma); l_run = sum |s|
+        uint32_t pk[kBlockN / 2];
+        const float base = (fi - static_cast<float>(c0)) * slope;
+        float asum = 0.0f;
+#pragma unroll
+        for (int c = 0; c < kBlockN; c += 2) {
+          float e0 = s[c] * p.scale * ex2(base - slope * static_cast<float>(c));
+          float e1 = s[c + 1] * p.scale * ex2(base - slope * static_cast<float>(c + 1));
+          if (!full) {
+            if (!kept(p.mask, i, c0 + c, p.seq_k)) e0 = 0.0f;
+            if (!kept(p.mask, i, c0 + c + 1, p.seq_k)) e1 = 0.0f;
+          }
+          asum += fabsf(e0) + fabsf(e1);
+          pk[c / 2] = pack_bf16(e0, e1);
+        }
+        l_run += asum;
+#pragma unroll
+        for (int c = 0; c < kBlockN / 64; ++c)
+          tmem_st32(s_tmem + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
+        tmem_st_wait();
       } else {
         uint32_t pk[kBlockN / 2];
         const float bias = p.bias + slope * static_cast<float>(c0) - slope * fi;
@@ -377,6 +398,9 @@ __global__ void __launch_bounds__(320, 1)
     // ───────────── epilogue: O / l, LSE ─────────────
     float inv = 1.0f;
     if constexpr (kFamily == kFamilySoftmax) inv = (l_run == 0.0f) ? 0.0f : 1.0f / l_run;
+    if constexpr (kFamily == kFamilyAbssum) {
+      if (p.cap_a != 0.0f) inv = 1.0f / fmaxf(l_run, 1.0f);
+    }
     if (nk > 0) {
       mbar_wait(&o_done[t], (nk - 1) & 1);
       tc_fence_after();
@@ -411,6 +435,10 @@ __global__ void __launch_bounds__(320, 1)
         const float lse = (l_run == 0.0f) ? -INFINITY : (m_run * kLn2 + logf(l_run));
         p.lse[(static_cast<int64_t>(b) * p.heads_q + h) * p.seq_q + i] = lse;
       }
+    }
+    if constexpr (kFamily == kFamilyAbssum) {  // row statistic for the backward: sum_j |s_ij|
+      if (p.lse != nullptr && i < p.seq_q)
+        p.lse[(static_cast<int64_t>(b) * p.heads_q + h) * p.seq_q + i] = l_run;
     }
   }
 

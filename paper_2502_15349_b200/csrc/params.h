@@ -9,6 +9,9 @@ namespace af {
 enum Family : int {
   kFamilySoftmax = 0,      // online softmax rownorm (attention.py:556-572)
   kFamilyElementwise = 1,  // score mods only, no rownorm (sigmoid / relu / identity)
+  kFamilyAbssum = 2,       // retention-parallel: causal decay mask gamma_h^(i-j) (slope[h] holds
+                           // log2 gamma_h) and rows / clamp(sum |s|, 1, inf) when cap_a != 0
+                           // (attention.py:575-586, 600-671)
 };
 
 enum Act : int {

@@ -33,7 +33,7 @@ from . import hooklang as H
 from .errors import UnsupportedError, InputError
 from .spec import (AttentionSpec, DirectRowNorm, OnlineRowNorm, Pattern, diagonal_scale)
 
-FAMILY_SOFTMAX, FAMILY_ELEMENTWISE = 0, 1
+FAMILY_SOFTMAX, FAMILY_ELEMENTWISE, FAMILY_ABSSUM = 0, 1, 2
 ACT_IDENTITY, ACT_SIGMOID, ACT_RELU, ACT_RELU2 = 0, 1, 2, 3
 
 
@@ -87,10 +87,17 @@ class ParallelPlan:
     v_map: int = FM_NONE
     cap_a: float = 0.0              # softmax family soft-cap s -> cap_a * tanh(cap_b * s)
     cap_b: float = 0.0              # (0 = none; e.g. capped-softmax: 30 * tanh(s / 30))
+    # abssum family (retention-parallel): s = tau q.k * gamma_h^(i-j) [j <= i], rows divided by
+    # clamp(sum_j |s|, 1, inf) when `normalize`; the decay mask extra is synthesised in-kernel
+    decay_extra: str | None = None
+    decay_gammas: tuple = ()
+    normalize: bool = False
 
     @property
     def has_lse(self) -> bool:
-        return self.family == FAMILY_SOFTMAX
+        """Whether the forward emits a per-row statistic: the LSE (softmax family) or the
+        row abs-sum a_i (abssum family; the backward's clamp(a_i, 1) and [a_i >= 1])."""
+        return self.family in (FAMILY_SOFTMAX, FAMILY_ABSSUM)
 
 
 @dataclass
@@ -452,6 +459,23 @@ def _plan_parallel(spec: AttentionSpec) -> ParallelPlan:
     band = Band()
     plain, mask_vals = [], []
     seen_mask = False
+    rn = spec.rownorm
+    masks = [m for m in spec.score_mods if m.ismask]
+    decay_mods = [m for m in masks if _decay_mask(spec, [m]) is not None]
+    if (len(decay_mods) == 1 and len(masks) == len(spec.score_mods)
+            and (rn is None or is_online_abssum(rn, consts))):
+        # retention-parallel: a causal decay-mask extra (synthesised in-kernel; its zeros above the
+        # diagonal make the band causal), further 0/1 band masks, abssum-clamp rows
+        dname, gammas = _decay_mask(spec, decay_mods)
+        dband = Band(upper=0)
+        for m in masks:
+            if m is decay_mods[0]:
+                continue
+            if _mask_kind(m, consts, dband) != 0.0:
+                raise UnsupportedError("masks next to a decay mask must zero the score (s*0/1)",
+                                       source=m.source)
+        return ParallelPlan(spec, FAMILY_ABSSUM, scale=scale, band=dband, decay_extra=dname,
+                            decay_gammas=gammas, normalize=rn is not None, **maps)
     for m in spec.score_mods:
         if m.ismask:
             seen_mask = True
@@ -463,7 +487,6 @@ def _plan_parallel(spec: AttentionSpec) -> ParallelPlan:
             if seen_mask:
                 raise UnsupportedError("score_mod after a mask_mod is not lowered", source=m.source)
             plain.append(m)
-    rn = spec.rownorm
     if rn is not None and is_online_softmax(rn if isinstance(rn, OnlineRowNorm) else None, consts):
         cap = (0.0, 0.0)
         if plain:
@@ -538,6 +561,46 @@ def _softcap(mods, consts: dict) -> tuple[float, float] | None:
     if not (math.isfinite(a) and math.isfinite(b)) or a == 0.0:
         return None
     return a, b
+
+
+def is_online_abssum(rn, consts: dict) -> bool:
+    """Numerical fingerprint of the abssum-clamp rownorm (attention.py:575-586): rows divided by
+    clamp(sum |s|, 1, inf), for arbitrary blockings."""
+    if not isinstance(rn, OnlineRowNorm):
+        return False
+    rng = np.random.default_rng(99)
+    s = rng.uniform(-0.2, 0.2, size=(5, 24))
+    s[1] *= 0.01   # |row| sum < 1: the clamp floor
+    s[2, 10:] = 0.0
+    s[3] *= 10.0
+    a = np.sum(np.abs(s), -1, keepdims=True)
+    want = s / np.clip(a, 1.0, None)
+    try:
+        for splits in ([], [1, 2, 9, 17], [12]):
+            if not np.allclose(_run_online(rn, consts, s, splits), want, atol=1e-12, rtol=1e-10):
+                return False
+    except Exception:  # noqa: BLE001 - any evaluation failure means "not abssum"
+        return False
+    return True
+
+
+def _decay_mask(spec: AttentionSpec, mods) -> tuple[str, tuple] | None:
+    """A single multiplicative mask ``s * X`` where X is a [1, heads, seq_q, seq_k] extra with the
+    reference's causal_decay_mask fill (gamma_h^(i-j) on j <= i, 0 above the diagonal)."""
+    if len(mods) != 1:
+        return None
+    e = mods[0].expr
+    extras = {x.name: x for x in spec.extra_inputs}
+    if not (isinstance(e, H.BinOp) and e.op == "*"):
+        return None
+    for x, y in ((e.lhs, e.rhs), (e.rhs, e.lhs)):
+        if isinstance(x, H.Name) and x.name == "s" and isinstance(y, H.Name) and y.name in extras:
+            ex = extras[y.name]
+            if ex.fill == "causal_decay_mask" and tuple(ex.shape) == (1, "heads", "seq_q", "seq_k"):
+                g = tuple(float(v) for v in ex.fill_params["gamma"])
+                if len(g) == spec.dims.heads and all(0.0 < v <= 1.0 for v in g):
+                    return ex.name, g
+    return None
 
 
 def _direct_is_softmax(rn: DirectRowNorm, consts) -> bool:

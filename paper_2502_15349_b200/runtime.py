@@ -17,7 +17,7 @@ from . import errors
 _LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libattn_b200.so"
 
 AF_OK, AF_ERR_INPUT, AF_ERR_SHAPE, AF_ERR_UNSUPPORTED, AF_ERR_NAN, AF_ERR_CUDA = range(6)
-AF_FAMILY_SOFTMAX, AF_FAMILY_ELEMENTWISE = 0, 1
+AF_FAMILY_SOFTMAX, AF_FAMILY_ELEMENTWISE, AF_FAMILY_ABSSUM = 0, 1, 2
 AF_ACT_IDENTITY, AF_ACT_SIGMOID, AF_ACT_RELU, AF_ACT_RELU2 = 0, 1, 2, 3
 AF_DTYPE_BF16, AF_DTYPE_F32 = 0, 1
 AF_FM_NONE, AF_FM_SILU, AF_FM_SIGMOID, AF_FM_RELU, AF_FM_TANH, AF_FM_EXP = range(6)

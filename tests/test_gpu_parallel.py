@@ -97,6 +97,14 @@ BF16_CASES = {
     "sigmoid_relpos_swa_s1024": lambda: sigmoid_swa_spec(1, 4, 1024, 128, 256),
     "relu_causal_d64": lambda: spec_gqa("relu", 1, 2, None, 384, 384, 64),
     "sigmoid_noncausal_gqa": lambda: spec_gqa("sigmoid", 1, 4, 2, 256, 256, 128, causal=False),
+    # retention-parallel: causal decay mask synthesised in-kernel + abssum-clamp rows
+    "retention_parallel_s512_d128": lambda: S.builtin("retention-parallel", batch=1, heads=4,
+                                                      seq=512, d_qk=128, d_v=128),
+    "squared_relu_causal_d64": lambda: S.spec_from_dict({
+        "name": "squared-relu", "pattern": "parallel",
+        "dims": {"batch": 1, "heads": 2, "seq_q": 300, "seq_k": 300, "dqk": 64, "dv": 64},
+        "q_mod": "q / sqrt(dimqk)", "score_mod": "relu(s) * relu(s) / seqk",
+        "masks": [{"expr": "where(kidx <= qidx, s, 0)", "ismask": True}]}),
 }
 
 
@@ -108,7 +116,7 @@ def test_bf16_forward_matches_oracle(case):
     ref = rounded(arrays)
     want = OP.tiled_forward(spec, ref, 128, 128)
     assert_bf16_out(o, want)
-    if lse is not None:
+    if lse is not None and af.plan_parallel(spec).family == 0:  # softmax rows: LSE
         assert_lse(lse, OP.lse_rows(spec, ref))
 
 
@@ -217,6 +225,8 @@ def test_autograd_module_matches_backward():
 def test_unlowered_variant_raises_not_falls_back():
     spec = S.with_causal_mask(S.builtin("retention-parallel", heads=2, seq=128, d_qk=64, d_v=64))
     arrays = to_dev(oracle.generate(spec, 0))
+    af.run_tiled_parallel(spec, arrays)  # the declared causal decay mask lowers ...
+    arrays["mask"] = torch.rand_like(arrays["mask"])  # ... an arbitrary materialised one does not
     with pytest.raises(af.UnsupportedError):
         af.run_tiled_parallel(spec, arrays)
     spec = S.builtin("softmax-diff", heads=2, seq=128, d_qk=128, d_v=256)  # Dv > 128

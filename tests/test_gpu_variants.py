@@ -66,10 +66,14 @@ def test_fixture_through_bf16_kernels(name):
         got = o.double().cpu().numpy()
         assert _nw(got, want) <= 1e-2
         assert np.max(np.abs(got - want)) <= 2e-2 * max(1.0, float(np.max(np.abs(want))))
-        if lse is not None:
+        if lse is not None and af.plan_parallel(spec).family == 0:  # softmax: the LSE
             wl = OP.lse_rows(spec, ra)
             fin = np.isfinite(wl)
             assert np.max(np.abs(lse.double().cpu().numpy()[fin] - wl[fin]), initial=0.0) <= 1e-3
+        elif lse is not None:  # abssum family: the row statistic is sum_j |s_ij|
+            z = OP.final_scores(spec, ra)[4]
+            wa = np.sum(np.abs(np.where(np.isfinite(z), z, 0.0)), axis=-1)
+            assert _nw(lse.double().cpu().numpy(), wa) <= 1e-2
         grads = af.parallel_backward(spec, dev, o, lse, dout_t)
         wg = OP.parallel_vjp(spec, ra, dout_r)
     else:
