@@ -26,7 +26,15 @@ namespace af {
 constexpr int kMlaDqk = 576;
 constexpr int kMlaDv = 512;
 constexpr int kMlaHalf = 256;
-constexpr int kMlaN = 64;     // keys per tile
+// keys per latent tile and ring depth: prefill (KV reused from L2 across heads, compute bound)
+// 64-key tiles x 2 stages; decode (KV streamed once from HBM) 32-key tiles x 4 stages, i.e. three
+// tiles of prefetch distance, to hide the HBM latency behind the S / softmax / PV chain.
+template <bool kDecode>
+struct MlaTile {
+  static constexpr int kN = kDecode ? 32 : 64;
+  static constexpr int kStages = kDecode ? 4 : 2;
+};
+constexpr int kMlaN = 64;     // prefill tile (split lengths of decode are multiples of both)
 constexpr int kMlaQT = 256;   // Q columns [0, 256) live in TMEM (TS MMA), [256, 576) in smem
 
 struct MlaParams {
@@ -50,16 +58,17 @@ struct MlaParams {
 // Shared memory: Q columns [256, 576) as 5 boxes [128 rows][64] (80 KB) + a 2-stage ring of
 // 64-key latent tiles (9 boxes [64 keys][64] = 72 KB each).  TMEM (512 columns): S double buffer
 // [0, 128) (P packed in place) | O half [128, 384) | Q columns [0, 256) packed bf16 [384, 512).
+template <int kN, int kSt>
 struct MlaSmem {
   static constexpr int kQBox = 128 * 128;
-  static constexpr int kKBox = kMlaN * 128;
+  static constexpr int kKBox = kN * 128;
   static constexpr int kQBytes = 5 * kQBox;
   static constexpr int kKBytes = 9 * kKBox;
   static constexpr int kQOff = 0;
   static constexpr int kKOff = kQBytes;
-  static constexpr int kBarOff = kKOff + 2 * kKBytes;
-  // q_full, q_ready, k_full[2], k_empty[2], s_full[2], p_ready, o_done
-  static constexpr int kNumBars = 10;
+  static constexpr int kBarOff = kKOff + kSt * kKBytes;
+  // q_full, q_ready, k_full[kSt], k_empty[kSt], s_full[2], p_ready, o_done
+  static constexpr int kNumBars = 6 + 2 * kSt;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -68,7 +77,9 @@ template <bool kDecode>
 __global__ void __launch_bounds__(192, 1)
     mla_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                    const __grid_constant__ CUtensorMap tm_kv, const MlaParams p) {
-  using L = MlaSmem;
+  constexpr int kN = MlaTile<kDecode>::kN;
+  constexpr int kSt = MlaTile<kDecode>::kStages;
+  using L = MlaSmem<kN, kSt>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + L::kQOff;
   uint8_t* sK = smem + L::kKOff;
@@ -76,10 +87,10 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* q_full = bars;
   uint64_t* q_ready = bars + 1;
   uint64_t* k_full = bars + 2;
-  uint64_t* k_empty = bars + 4;
-  uint64_t* s_full = bars + 6;
-  uint64_t* p_ready = bars + 8;
-  uint64_t* o_done = bars + 9;
+  uint64_t* k_empty = bars + 2 + kSt;
+  uint64_t* s_full = bars + 2 + 2 * kSt;
+  uint64_t* p_ready = s_full + 2;
+  uint64_t* o_done = p_ready + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -104,16 +115,17 @@ __global__ void __launch_bounds__(192, 1)
     kv_hi = p.seq_k;
     if (p.causal) kv_hi = min(kv_hi, q0 + 128);
   }
-  const int nk = kv_hi > kv_lo ? (kv_hi - kv_lo + kMlaN - 1) / kMlaN : 0;
+  const int nk = kv_hi > kv_lo ? (kv_hi - kv_lo + kN - 1) / kN : 0;
 
   if (warp == 4 && lane_id() == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_ready, 4);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
-      mbar_init(&s_full[s], 1);
     }
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
     mbar_init(p_ready, 4);
     mbar_init(o_done, 1);
     fence_barrier_init();
@@ -136,10 +148,10 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_4d(sQ + c * L::kQBox, &tm_q, q_full, col, q0, h, b);
       }
       for (int n = 0; n < nk; ++n) {
-        const int s = n & 1;
-        mbar_wait(&k_empty[s], ((n >> 1) & 1) ^ 1);
+        const int s = n % kSt;
+        mbar_wait(&k_empty[s], ((n / kSt) & 1) ^ 1);
         mbar_expect_tx(&k_full[s], L::kKBytes);
-        const int j0 = kv_lo + n * kMlaN;
+        const int j0 = kv_lo + n * kN;
         for (int c = 0; c < 9; ++c)
           tma_load_4d_hint(sK + s * L::kKBytes + c * L::kKBox, &tm_kv, &k_full[s], c * 64, j0, b,
                            0, kEvictLast);
@@ -147,21 +159,22 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 5) {
     if (elect_one() && nk > 0) {
-      constexpr uint32_t id_s = make_idesc_bf16(128, kMlaN, false, false);     // S = Q K^T
+      constexpr uint32_t id_s = make_idesc_bf16(128, kN, false, false);        // S = Q K^T
       constexpr uint32_t id_o = make_idesc_bf16(128, kMlaHalf, false, true);   // O += P V
       const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK);
       auto issue_s = [&](int n) {
-        const int s = n & 1;
-        mbar_wait(&k_full[s], (n >> 1) & 1);
+        const int s = n & 1;  // TMEM S buffer
+        const int st = n % kSt;
+        mbar_wait(&k_full[st], (n / kSt) & 1);
         tc_fence_after();
-        const uint32_t kb = aK + s * L::kKBytes;
+        const uint32_t kb = aK + st * L::kKBytes;
 #pragma unroll
         for (int kk = 0; kk < kMlaQT / 16; ++kk)  // Q columns [0, 256) from TMEM
-          mma_ts(tmem + s * kMlaN, tmem + kColQ + kk * 8,
+          mma_ts(tmem + s * kN, tmem + kColQ + kk * 8,
                  make_sdesc(kb + (kk / 4) * L::kKBox + (kk % 4) * 32, 0, 1024), id_s, kk > 0);
 #pragma unroll
         for (int kk = kMlaQT / 16; kk < kMlaDqk / 16; ++kk)  // columns [256, 576) from smem
-          mma_ss(tmem + s * kMlaN,
+          mma_ss(tmem + s * kN,
                  make_sdesc(aQ + (kk / 4 - 4) * L::kQBox + (kk % 4) * 32, 0, 1024),
                  make_sdesc(kb + (kk / 4) * L::kKBox + (kk % 4) * 32, 0, 1024), id_s, 1u);
         mma_commit(&s_full[s]);
@@ -172,17 +185,18 @@ __global__ void __launch_bounds__(192, 1)
       issue_s(0);
       for (int n = 0; n < nk; ++n) {
         const int s = n & 1;
+        const int st = n % kSt;
         if (n + 1 < nk) issue_s(n + 1);
         mbar_wait(p_ready, n & 1);
         tc_fence_after();
         // V = latent columns [256*half, +256): boxes 4*half .. 4*half+3 of the tile, MN-major
-        const uint32_t vbase = aK + s * L::kKBytes + half * 4 * L::kKBox;
+        const uint32_t vbase = aK + st * L::kKBytes + half * 4 * L::kKBox;
 #pragma unroll
-        for (int kk = 0; kk < kMlaN / 16; ++kk)
-          mma_ts(tmem + kColO, tmem + s * kMlaN + kk * 8,
+        for (int kk = 0; kk < kN / 16; ++kk)
+          mma_ts(tmem + kColO, tmem + s * kN + kk * 8,
                  make_sdesc(vbase + kk * 2048, L::kKBox, 1024), id_o, (n > 0 || kk > 0));
         mma_commit(o_done);
-        mma_commit(&k_empty[s]);
+        mma_commit(&k_empty[st]);
       }
     }
   } else {
@@ -217,18 +231,20 @@ __global__ void __launch_bounds__(192, 1)
     float m_run = -INFINITY, l_run = 0.0f;
     for (int n = 0; n < nk; ++n) {
       const int s = n & 1;
-      const int j0 = kv_lo + n * kMlaN;
+      const int j0 = kv_lo + n * kN;
       mbar_wait(&s_full[s], (n >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[64];
-      tmem_ld32(tmem + lane_base + s * kMlaN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(tmem + lane_base + s * kMlaN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_ld_wait();
-      float x[64];
-      float bmax = -INFINITY;
-      const bool full = (j0 + kMlaN <= kv_hi) && (kDecode || !p.causal || j0 + kMlaN - 1 <= q0);
+      uint32_t sr[kN];
 #pragma unroll
-      for (int e = 0; e < 64; ++e) {
+      for (int c = 0; c < kN / 32; ++c)
+        tmem_ld32(tmem + lane_base + s * kN + c * 32,
+                  *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
+      tmem_ld_wait();
+      float x[kN];
+      float bmax = -INFINITY;
+      const bool full = (j0 + kN <= kv_hi) && (kDecode || !p.causal || j0 + kN - 1 <= q0);
+#pragma unroll
+      for (int e = 0; e < kN; ++e) {
         bool keep = true;
         if (!full) keep = (j0 + e < kv_hi) && (kDecode || !p.causal || j0 + e <= i);
         x[e] = keep ? __uint_as_float(sr[e]) * p.scale_log2 : -INFINITY;
@@ -242,16 +258,19 @@ __global__ void __launch_bounds__(192, 1)
         m_run = m_new;
       }
       const float m_use = (m_run == -INFINITY) ? 0.0f : m_run;
-      uint32_t pk[32];
+      uint32_t pk[kN / 2];
       float lsum = 0.0f;
 #pragma unroll
-      for (int e = 0; e < 64; e += 2) {
+      for (int e = 0; e < kN; e += 2) {
         const float e0 = ex2(x[e] - m_use), e1 = ex2(x[e + 1] - m_use);
         lsum += e0 + e1;
         pk[e / 2] = pack_bf16(e0, e1);
       }
       l_run = l_run * factor + lsum;
-      tmem_st32(tmem + lane_base + s * kMlaN, pk);
+      if constexpr (kN == 64)
+        tmem_st32(tmem + lane_base + s * kN, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      else
+        tmem_st16(tmem + lane_base + s * kN, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       tmem_st_wait();
       if (n > 0 && __any_sync(0xffffffffu, need)) {
         mbar_wait(o_done, (n - 1) & 1);

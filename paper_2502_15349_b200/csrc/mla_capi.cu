@@ -5,6 +5,9 @@
 
 namespace af {
 
+using PrefillSmem = MlaSmem<MlaTile<false>::kN, MlaTile<false>::kStages>;
+using DecodeSmem = MlaSmem<MlaTile<true>::kN, MlaTile<true>::kStages>;
+
 int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o, float* lse,
                 cudaStream_t s) {
   AF_REQUIRE(d->heads_kv == 1, AF_ERR_UNSUPPORTED, "MLA prefill needs one latent KV head");
@@ -13,7 +16,7 @@ int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o
   if (!make_tmap_4d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDqk, d->seq_q, d->heads_q,
                     d->batch, d->q_stride, 64, 128, true) ||
       !make_tmap_4d(&tkv, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDqk, d->seq_k, d->batch, 1,
-                    kv_st, 64, kMlaN, true))
+                    kv_st, 64, MlaTile<false>::kN, true))
     return AF_ERR_INPUT;
   MlaParams p{};
   p.batch = d->batch; p.heads = d->heads_q; p.seq_q = d->seq_q; p.seq_k = d->seq_k;
@@ -29,12 +32,12 @@ int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o
   auto kern = mla_fwd_kernel<false>;
   static bool attr = false;
   if (!attr) {
-    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MlaSmem::kTotal));
+    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PrefillSmem::kTotal));
     attr = true;
   }
   const int q_tiles = (d->seq_q + 127) / 128;
   ::af::note_launch();
-  kern<<<q_tiles * d->batch * d->heads_q * 2, 192, MlaSmem::kTotal, s>>>(tq, tkv, p);
+  kern<<<q_tiles * d->batch * d->heads_q * 2, 192, PrefillSmem::kTotal, s>>>(tq, tkv, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
 }
@@ -43,7 +46,7 @@ namespace {
 int decode_splits(const af_mla_desc* d) {
   const int ctas_per_split = d->batch * 2;
   int splits = (2 * sm_count() + ctas_per_split - 1) / ctas_per_split;  // ~2 waves of CTAs
-  splits = std::max(1, std::min(splits, (d->seq_k + kMlaN - 1) / kMlaN));
+  splits = std::max(1, std::min(splits, (d->seq_k + MlaTile<true>::kN - 1) / MlaTile<true>::kN));
   return splits;
 }
 }  // namespace
@@ -69,7 +72,7 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int splits = decode_splits(d);
   int split_len = (d->seq_k + splits - 1) / splits;
-  split_len = ((split_len + kMlaN - 1) / kMlaN) * kMlaN;
+  split_len = ((split_len + MlaTile<true>::kN - 1) / MlaTile<true>::kN) * MlaTile<true>::kN;
   // q [B, H, 576] and kv [B, Sk, 576], contiguous
   CUtensorMap tq, tkv;
   const int64_t q_st[4] = {0, static_cast<int64_t>(d->heads) * kMlaDqk, kMlaDqk, 1};  // (576, H, B, 1)
@@ -77,7 +80,7 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
   if (!make_tmap_4d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDqk, d->heads, d->batch, 1,
                     q_st, 64, 128, true) ||
       !make_tmap_4d(&tkv, kv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDqk, d->seq_k, d->batch, 1,
-                    kv_st, 64, kMlaN, true))
+                    kv_st, 64, MlaTile<true>::kN, true))
     return AF_ERR_INPUT;
   MlaParams p{};
   p.batch = d->batch; p.heads = d->heads; p.seq_q = 1; p.seq_k = d->seq_k;
@@ -94,11 +97,11 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
   auto kern = mla_fwd_kernel<true>;
   static bool attr = false;
   if (!attr) {
-    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, MlaSmem::kTotal));
+    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DecodeSmem::kTotal));
     attr = true;
   }
   ::af::note_launch();
-  kern<<<d->batch * splits * 2, 192, MlaSmem::kTotal, s>>>(tq, tkv, p);
+  kern<<<d->batch * splits * 2, 192, DecodeSmem::kTotal, s>>>(tq, tkv, p);
   AF_CUDA_CHECK(cudaGetLastError());
   ::af::note_launch();
   mla_combine_kernel<<<d->batch * d->heads, kMlaDv / 4, 0, s>>>(
