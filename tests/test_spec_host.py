@@ -125,3 +125,65 @@ def test_band_mask_offsets():
         band = P.Band()
         P._mask_kind(S.mod(src, "s", ismask=True), {}, band)
         assert (band.upper, band.window) == (upper, window), src
+
+
+# ───────────── lowering of the §8(f) hook families (CPU: planner only) ─────────────
+
+def _load(name):
+    from conftest import load_golden
+    return load_golden(name)[0]
+
+
+def test_squared_relu_post_scale_folds_into_the_argument():
+    spec = _load("variant_squared-relu")
+    plan = P.plan_parallel(spec)
+    d = spec.dims
+    assert plan.family == P.FAMILY_ELEMENTWISE and plan.act == P.ACT_RELU2
+    # relu(tau s)^2 / seqk == relu(tau s / sqrt(seqk))^2
+    assert math.isclose(plan.scale, d.d_qk ** -0.5 / math.sqrt(d.seq_k), rel_tol=1e-12)
+    assert plan.band.upper == 0
+
+
+def test_capped_softmax_is_softmax_with_a_softcap():
+    plan = P.plan_parallel(_load("variant_capped-softmax"))
+    assert plan.family == P.FAMILY_SOFTMAX
+    assert (plan.cap_a, plan.cap_b) == (30.0, 1.0 / 30.0)
+
+
+def test_retention_parallel_is_the_abssum_family():
+    for name in ("tiny_retention-parallel", "tiny_causal_retention-parallel"):
+        spec = _load(name)
+        plan = P.plan_parallel(spec)
+        assert plan.family == P.FAMILY_ABSSUM and plan.normalize and plan.band.upper == 0
+        assert plan.decay_extra == "mask"
+        assert plan.decay_gammas == tuple(spec.extra_inputs[0].fill_params["gamma"])
+    # unnormalised retention: same family, no row norm
+    sp = S.builtin("retention-parallel", heads=2, seq=16, d_qk=8, d_v=8, normalized=False)
+    assert not P.plan_parallel(sp).normalize
+
+
+def test_abssum_fingerprint_rejects_softmax_and_vice_versa():
+    c = S.builtin("softmax", heads=1, seq=8, d_qk=4, d_v=4)
+    r = S.builtin("retention-parallel", heads=1, seq=8, d_qk=4, d_v=4)
+    env = c.dims.const_env()
+    assert P.is_online_softmax(c.rownorm, env) and not P.is_online_abssum(c.rownorm, env)
+    assert P.is_online_abssum(r.rownorm, env) and not P.is_online_softmax(r.rownorm, env)
+
+
+def test_feature_maps_recognised():
+    spec = _load("variant_silu-retention")
+    plan = P.plan_linear(spec)
+    assert plan.v_map == P.FM_SILU and plan.q_map == P.FM_NONE
+    consts = spec.dims.const_env()
+    for src, kind in (("relu(q)", P.FM_RELU), ("sigmoid(q) * q", P.FM_SILU), ("exp(q)", P.FM_EXP),
+                      ("tanh(q)", P.FM_TANH), ("q * 0.5", P.FM_NONE)):
+        assert P._feature_map(S.mod(src, "q"), "q", consts)[0] == kind
+    with pytest.raises(E.UnsupportedError):
+        P._feature_map(S.mod("q * q", "q"), "q", consts)
+
+
+def test_every_reference_fixture_lowers():
+    from conftest import golden_cases
+    for name in golden_cases():
+        spec = _load(name)
+        (P.plan_parallel if spec.pattern.value == "parallel" else P.plan_linear)(spec)
