@@ -6,7 +6,6 @@
 namespace af {
 namespace {
 
-constexpr int kFwdThreads = 320;
 
 template <int D, int DV, int kFamily, int kAct>
 int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
@@ -22,7 +21,7 @@ int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorM
   }
   dim3 grid((d->seq_q + 2 * kBlockM - 1) / (2 * kBlockM), d->batch * d->heads_q);
   ::af::note_launch();
-  kern<<<grid, kFwdThreads, L::kTotal, stream>>>(tq, tk, tv, p);
+  kern<<<grid, fwd_threads(kFamily), L::kTotal, stream>>>(tq, tk, tv, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
 }

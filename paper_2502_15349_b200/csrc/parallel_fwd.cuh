@@ -41,8 +41,21 @@ struct FwdSmem {
   // barriers: q_full, k_full[S], k_empty[S], v_full[S], v_empty[S], s_full[2], p_full[2], o_done[2]
   static constexpr int kNumBars = 1 + 4 * kStages + 6;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
-  static constexpr int kTotal = kTmemSlotOff + 16 + 1024;  // + alignment slack
+  static constexpr int kRowSumOff = kTmemSlotOff + 16;  // [2 tiles][2 halves][128] fp32
+  static constexpr int kTotal = kRowSumOff + 2 * 2 * 128 * 4 + 1024;  // + alignment slack
 };
+
+// Non-softmax families have no running row max, so each score row is split over two warps
+// (64 key columns each; 16 row warps): twice the warps to hide the SFU / issue latency of the
+// activation, with only the abssum row sum combined once at the end.  Softmax keeps one warp per
+// row (its max / rescale protocol is per row).
+__host__ __device__ constexpr int fwd_row_split(int family) {
+  return family == kFamilySoftmax ? 1 : 2;
+}
+__host__ __device__ constexpr int fwd_threads(int family) {
+  return 32 * (8 * fwd_row_split(family) + 2);
+}
+AF_DEVICE uint32_t fwd_split_col(int kk) { return kk < 4 ? kk * 8 : 64 + (kk - 4) * 8; }
 
 struct TileBand {
   int jb_lo, jb_hi;  // key-block range [jb_lo, jb_hi)
@@ -96,7 +109,7 @@ AF_DEVICE float apply_act(float z) {
 }
 
 template <int D, int DV, int kFamily, int kAct, int kStages>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(fwd_threads(kFamily), 1)
     parallel_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const ParallelFwdParams p) {
@@ -118,6 +131,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* p_full = s_full + 2;
   uint64_t* o_done = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
+  float* sRowSum = reinterpret_cast<float*>(smem + L::kRowSumOff);
+  constexpr int kSplit = fwd_row_split(kFamily);
+  constexpr int kTmaWarp = 8 * kSplit, kMmaWarp = 8 * kSplit + 1;
 
   const int warp = static_cast<int>(warp_id());
   const int q_blocks = (p.seq_q + 2 * kBlockM - 1) / (2 * kBlockM);
@@ -133,7 +149,7 @@ __global__ void __launch_bounds__(320, 1)
   const TileBand band = key_band(p.mask, q0, q_end, p.seq_k);
   const int nk = band.jb_hi - band.jb_lo;
 
-  if (warp == 8 && lane_id() == 0) {
+  if (warp == kTmaWarp && lane_id() == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&k_full[s], 1);
@@ -143,7 +159,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 4);  // one arrival per row warp
+      mbar_init(&p_full[t], 4 * kSplit);  // one arrival per row warp
       mbar_init(&o_done[t], 1);
     }
     fence_barrier_init();
@@ -151,13 +167,13 @@ __global__ void __launch_bounds__(320, 1)
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == kTmaWarp) {
     // ───────────── TMA producer ─────────────
     if (elect_one() && nk > 0) {
       mbar_expect_tx(q_full, 2 * L::kQBytes);
@@ -181,7 +197,7 @@ __global__ void __launch_bounds__(320, 1)
                            kv0, hk, b, kEvictLast);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     // ───────────── MMA issuer ─────────────
     if (elect_one() && nk > 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(kBlockM, kBlockN, false, false);
@@ -211,7 +227,8 @@ __global__ void __launch_bounds__(320, 1)
         for (int kk = 0; kk < kBlockN / 16; ++kk) {
           const uint64_t bdesc =
               make_sdesc(sv_addr + s * L::kVBytes + kk * 16 * 128, kBlockN * 128, 1024);
-          mma_ts(d_tmem, p_tmem + kk * 8, bdesc, idesc_o, (n > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(d_tmem, p_tmem + (kSplit == 2 ? fwd_split_col(kk) : kk * 8), bdesc, idesc_o,
+                 (n > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(&o_done[t]);
       };
@@ -244,6 +261,105 @@ __global__ void __launch_bounds__(320, 1)
           issue_s(1, n + 1);
           mma_commit(&k_empty[s1]);
         }
+      }
+    }
+  } else if constexpr (kSplit == 2) {
+    // ───────────── row warps, two per score row (non-softmax families) ─────────────
+    const int t = warp / 8;          // query tile
+    const int wq = warp % 4;         // TMEM lane quarter
+    const int ch = (warp / 4) % 2;   // key-column half of the 128-wide block
+    const int row = wq * 32 + static_cast<int>(lane_id());
+    const int i = q0 + t * kBlockM + row;
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t s_tmem = tmem + lane_base + t * kBlockN + ch * 64;
+    const uint32_t o_tmem = tmem + lane_base + 2 * kBlockN + t * DV + ch * (DV / 2);
+    const int r0 = q0 + t * kBlockM;
+    const float slope = (p.slope != nullptr) ? p.slope[h] : 0.0f;
+    const float fi = static_cast<float>(i);
+    float l_run = 0.0f;
+    for (int n = 0; n < nk; ++n) {
+      const int c0 = (band.jb_lo + n) * kBlockN;
+      const int cb = c0 + ch * 64;
+      mbar_wait(&s_full[t], n & 1);
+      tc_fence_after();
+      uint32_t sr[64];
+      tmem_ld32(s_tmem, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(s_tmem + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld_wait();
+      const float* s = reinterpret_cast<const float*>(sr);
+      const bool full = block_fully_kept(p.mask, r0, c0, p.seq_k);
+      uint32_t pk[32];
+      if constexpr (kFamily == kFamilyAbssum) {
+        const float base = (fi - static_cast<float>(cb)) * slope;
+        float asum = 0.0f;
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          float e0 = s[c] * p.scale * ex2(base - slope * static_cast<float>(c));
+          float e1 = s[c + 1] * p.scale * ex2(base - slope * static_cast<float>(c + 1));
+          if (!full) {
+            if (!kept(p.mask, i, cb + c, p.seq_k)) e0 = 0.0f;
+            if (!kept(p.mask, i, cb + c + 1, p.seq_k)) e1 = 0.0f;
+          }
+          asum += fabsf(e0) + fabsf(e1);
+          pk[c / 2] = pack_bf16(e0, e1);
+        }
+        l_run += asum;
+      } else {
+        const float bias = p.bias + slope * static_cast<float>(cb) - slope * fi;
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          float e0 = apply_act<kAct>(s[c] * p.scale + bias + slope * static_cast<float>(c));
+          float e1 = apply_act<kAct>(s[c + 1] * p.scale + bias + slope * static_cast<float>(c + 1));
+          if (!full) {
+            if (!kept(p.mask, i, cb + c, p.seq_k)) e0 = 0.0f;
+            if (!kept(p.mask, i, cb + c + 1, p.seq_k)) e1 = 0.0f;
+          }
+          pk[c / 2] = pack_bf16(e0, e1);
+        }
+      }
+      // packed P of this key half over its own S columns (the PV MMA reads fwd_split_col)
+      tmem_st32(s_tmem, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&p_full[t]);
+    }
+    // ───────────── epilogue: O (this warp's DV/2 columns), abssum row statistic ─────────────
+    float inv = 1.0f;
+    if constexpr (kFamily == kFamilyAbssum) {
+      sRowSum[(t * 2 + ch) * 128 + row] = l_run;
+      named_bar_sync(1 + t, 256);
+      const float total = sRowSum[t * 2 * 128 + row] + sRowSum[(t * 2 + 1) * 128 + row];
+      if (p.cap_a != 0.0f) inv = 1.0f / fmaxf(total, 1.0f);
+      if (ch == 0 && p.lse != nullptr && i < p.seq_q)
+        p.lse[(static_cast<int64_t>(b) * p.heads_q + h) * p.seq_q + i] = total;
+    }
+    if (nk > 0) {
+      mbar_wait(&o_done[t], (nk - 1) & 1);
+      tc_fence_after();
+    }
+    __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_stride_b +
+                          h * p.o_stride_h + static_cast<int64_t>(i) * p.o_stride_s +
+                          ch * (DV / 2);
+#pragma unroll
+    for (int c = 0; c < DV / 64; ++c) {
+      uint32_t orr[32];
+      if (nk > 0) {
+        tmem_ld32(o_tmem + c * 32, orr);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) orr[e] = 0u;
+      }
+      if (i < p.seq_q) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          dst[v] = make_uint4(
+              pack_bf16(__uint_as_float(orr[v * 8 + 0]) * inv, __uint_as_float(orr[v * 8 + 1]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 2]) * inv, __uint_as_float(orr[v * 8 + 3]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 4]) * inv, __uint_as_float(orr[v * 8 + 5]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv));
       }
     }
   } else {
@@ -444,7 +560,7 @@ __global__ void __launch_bounds__(320, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
