@@ -29,6 +29,17 @@
 
 namespace af {
 
+#ifndef AF_BWD_POLY_MASK
+#define AF_BWD_POLY_MASK 6  // fully-kept tiles: pairs with (e & mask) == 0 use exp2_poly (25 %; swept: 12.5 % 13.4 ms, 25 % 13.3 ms, 100 % 14.9 ms, none 14.0 ms)
+#endif
+// P recompute exponential: MUFU ex2, or the FMA-pipe polynomial for the selected pairs
+AF_DEVICE float bwd_exp2(float x, int e) {
+  if constexpr (AF_BWD_POLY_MASK >= 0) {
+    if ((e & AF_BWD_POLY_MASK) == 0) return exp2_poly(x);
+  }
+  return ex2(x);
+}
+
 // packed (bf16x2) TMEM column of the k-th 16-wide K slice of a P / dS A operand
 AF_DEVICE uint32_t split_col(int kk) { return kk < 4 ? kk * 8 : 64 + (kk - 4) * 8; }
 
@@ -367,11 +378,11 @@ __global__ void __launch_bounds__(320, 1)
             for (int e = 0; e < 32; e += 4) {
               const float4 l4 = *reinterpret_cast<const float4*>(lse_s + c2 * 32 + e);
               pk[c2 * 16 + e / 2] =
-                  pack_bf16(ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x)),
-                            ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y)));
+                  pack_bf16(bwd_exp2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x), e),
+                            bwd_exp2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y), e));
               pk[c2 * 16 + e / 2 + 1] =
-                  pack_bf16(ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z)),
-                            ex2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w)));
+                  pack_bf16(bwd_exp2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z), e + 2),
+                            bwd_exp2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w), e + 2));
             }
           } else {
 #pragma unroll
@@ -731,8 +742,8 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
             for (int e = 0; e < 32; e += 2)
               pk[c2 * 16 + e / 2] =
-                  pack_bf16(ex2(fmaf(__uint_as_float(sr[e]), p.scale_log2, -l2)),
-                            ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l2)));
+                  pack_bf16(bwd_exp2(fmaf(__uint_as_float(sr[e]), p.scale_log2, -l2), e),
+                            bwd_exp2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l2), e));
           } else {
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
