@@ -29,10 +29,13 @@ constexpr int kMlaHalf = 256;
 // keys per latent tile and ring depth: prefill (KV reused from L2 across heads, compute bound)
 // 64-key tiles x 2 stages; decode (KV streamed once from HBM) 32-key tiles x 4 stages, i.e. three
 // tiles of prefetch distance, to hide the HBM latency behind the S / softmax / PV chain.
+#ifndef AF_MLA_PREFILL_N
+#define AF_MLA_PREFILL_N 64
+#endif
 template <bool kDecode>
 struct MlaTile {
-  static constexpr int kN = kDecode ? 32 : 64;
-  static constexpr int kStages = kDecode ? 4 : 2;
+  static constexpr int kN = kDecode ? 32 : AF_MLA_PREFILL_N;
+  static constexpr int kStages = kDecode ? 4 : (AF_MLA_PREFILL_N == 32 ? 4 : 2);
 };
 constexpr int kMlaN = 64;     // prefill tile (split lengths of decode are multiples of both)
 constexpr int kMlaQT = 256;   // Q columns [0, 256) live in TMEM (TS MMA), [256, 576) in smem
