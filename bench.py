@@ -464,6 +464,18 @@ def main() -> None:
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 untimed warm-up steps
     keys = sorted(WORKLOADS) if args.config == "all" else [args.config]
+    if len(keys) > 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        # one fresh process per config, so no config inherits another's allocator / host state
+        for k in keys:
+            cmd = [sys.executable, str(Path(__file__).resolve()), "--config", k, "--impl",
+                   args.impl, "--steps", str(args.steps), "--warmup", str(args.warmup),
+                   "--gpus", str(args.gpus)]
+            if args.cpu_seq is not None:
+                cmd += ["--cpu-seq", str(args.cpu_seq)]
+            if args.no_cpu:
+                cmd.append("--no-cpu")
+            subprocess.run(cmd, check=False)
+        return
     if args.impl == "reference":
         for k in keys:
             args.config = k

@@ -91,6 +91,9 @@ typedef struct af_linear_desc {
   int64_t decay_factor_stride[2][3];
   const float* key_gate;
   int64_t key_gate_stride[3];
+  int32_t decay_hint;        /* 1: the per-step decay is expected to stay mild (constant fills such
+                                as RetNet's gamma_h >= 0.5), enabling the factorised-decay kernel
+                                variant (still checked per chunk at run time); 0: generic */
 } af_linear_desc;
 
 /* o_t = q_scale * q_t h_t,  h_t = a_t h_{t-1} + (k_t * gate_t)^T v_t,  h_0 = 0.

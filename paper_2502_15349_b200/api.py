@@ -366,6 +366,7 @@ def _linear_desc(plan: LinearPlan, arrays: dict, q, k, v, o):
     c.batch, c.heads, c.seq = d.batch, d.heads, d.seq_q
     c.d_k, c.d_v = int(q.shape[-1]), int(v.shape[-1])  # kernel (possibly padded) dims
     c.chunk = 128
+    c.decay_hint = int(plan.decay_hint)
     c.q_scale = float(plan.q_scale)
     c.q_stride, c.k_stride, c.v_stride, c.o_stride = (rt.strides4(q), rt.strides4(k),
                                                       rt.strides4(v), rt.strides4(o))

@@ -48,7 +48,7 @@ LinearParams base_params(const af_linear_desc* d) {
   return p;
 }
 
-template <int DK, bool kRev>
+template <int DK, bool kRev, bool kFac>
 int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
   using L = LinSmem<DK>;
   CUtensorMap tq, tk, tv;
@@ -76,7 +76,7 @@ int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
     p.x_ss = a.x_st[2];
   }
   p.dot = a.dot;
-  auto kern = linear_chunk_kernel<DK, kRev>;
+  auto kern = linear_chunk_kernel<DK, kRev, kFac>;
   static bool attr = false;
   if (!attr) {
     AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
@@ -94,8 +94,15 @@ int run_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
     set_error("linear template: value dim %d is not a multiple of %d", a.dvv, kLinVB);
     return AF_ERR_UNSUPPORTED;
   }
-  if (a.dqk == 128) return a.reverse ? launch_la<128, true>(d, a, s) : launch_la<128, false>(d, a, s);
-  if (a.dqk == 256) return a.reverse ? launch_la<256, true>(d, a, s) : launch_la<256, false>(d, a, s);
+  const bool fac = d->decay_hint != 0;
+  if (a.dqk == 128) {
+    if (fac) return a.reverse ? launch_la<128, true, true>(d, a, s) : launch_la<128, false, true>(d, a, s);
+    return a.reverse ? launch_la<128, true, false>(d, a, s) : launch_la<128, false, false>(d, a, s);
+  }
+  if (a.dqk == 256) {
+    if (fac) return a.reverse ? launch_la<256, true, true>(d, a, s) : launch_la<256, false, true>(d, a, s);
+    return a.reverse ? launch_la<256, true, false>(d, a, s) : launch_la<256, false, false>(d, a, s);
+  }
   set_error("linear template: key dim %d not instantiated (128, 256)", a.dqk);
   return AF_ERR_UNSUPPORTED;
 }

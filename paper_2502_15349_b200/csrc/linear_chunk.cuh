@@ -83,9 +83,12 @@ struct LinSmem {
   static constexpr int kUOff = kLOff + 2 * kLinChunk * 4;  // [2][128] key/value-side scale
   static constexpr int kRawOff = kUOff + 2 * kLinChunk * 4;  // [3][128] raw factors (cp.async)
   static constexpr int kCpOff = kRawOff + 3 * kLinChunk * 4;  // [2][128] per-row output decay
+  // [2][128] column factor e^{-+L_u} u_u of the factorised decay and [2] per-chunk flags
+  static constexpr int kEcOff = kCpOff + 2 * kLinChunk * 4;
+  static constexpr int kFlagOff = kEcOff + 2 * kLinChunk * 4;
   // ring: full[S], empty[S]; s_full qh_full oi_full[2] h_full scan_ready[2] (1 arrival) |
   // p_ready vw_ready h_scaled hb_ready scan_free[2] (8 row warps) | oi_empty[2] cp_ready[2] (4)
-  static constexpr int kBarOff = kCpOff + 2 * kLinChunk * 4;
+  static constexpr int kBarOff = kFlagOff + 16;
   static constexpr int kNumBars = 2 * kStages + 17;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
@@ -108,7 +111,7 @@ AF_DEVICE uint4* swz_row(uint8_t* base, int r, int g) {
 // OI and QH are double-buffered in TMEM), 12 TMA producer, 13 TMEM allocator + MMA issuer.
 constexpr int kLinThreads = 448;
 
-template <int DK, bool kReverse>
+template <int DK, bool kReverse, bool kFac>
 __global__ void __launch_bounds__(kLinThreads, 1)
     linear_chunk_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
@@ -127,6 +130,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   float* sUb = reinterpret_cast<float*>(smem + L::kUOff);  // key/value-side scale [2][128]
   float* sRaw = reinterpret_cast<float*>(smem + L::kRawOff);
   float* sCp = reinterpret_cast<float*>(smem + L::kCpOff);
+  float* sEcb = reinterpret_cast<float*>(smem + L::kEcOff);
+  int* sFlag = reinterpret_cast<int*>(smem + L::kFlagOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* full = bars;                 // Q, K, V of one chunk landed (one tx barrier)
   uint64_t* empty = bars + kStages;      // the chunk's Q, K, V may be overwritten
@@ -234,12 +239,22 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         if (lane >= off) tot += y;
       }
       const float excl = tot - x[3];
+      // Factorised decay D[i,u] = e^{L_i} e^{-L_u} (reverse: e^{-L_i} e^{L_u}) when every |L| of
+      // the chunk stays below 2^100: one multiply per element instead of an ex2.
+      float amax = fmaxf(fabsf(excl + x[0]), fabsf(excl + x[3]));
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+      const bool fac = kFac && amax <= 100.0f;
       if (n >= 2) mbar_wait(&scan_free[pb], ((n >> 1) - 1) & 1);  // chunk n-2 done with sL[pb]
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        sLb[pb * kLinChunk + lane * 4 + j] = excl + x[j];
+        const float lj = excl + x[j];
+        sLb[pb * kLinChunk + lane * 4 + j] = lj;
         sUb[pb * kLinChunk + lane * 4 + j] = us[j];
+        sEcb[pb * kLinChunk + lane * 4 + j] = fac ? exp2f(kReverse ? lj : -lj) * us[j] : 0.0f;
       }
+      if (lane == 0) sFlag[pb] = fac ? 1 : 0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&scan_ready[pb]);
       // Q, K, V of chunk n (after the scan: the scan never waits on the ring)
@@ -393,10 +408,13 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       // (a) the producer warp's scan of log2 a for this chunk
       const float* sL = sLb + ph * kLinChunk;
       const float* sU = sUb + ph * kLinChunk;
+      const float* sEc = sEcb + ph * kLinChunk;
       mbar_wait(&scan_ready[ph], (n >> 1) & 1);
       if (threadIdx.x == 0) AF_LT(14, n);
       const float l_r = sL[r];
       const float l_last = sL[kLinChunk - 1];
+      const bool fac = kFac && sFlag[ph] != 0;
+      const float er = fac ? exp2f(kReverse ? -l_r : l_r) : 0.0f;
       const float g = exp2f(l_last);
       const float cp = kReverse ? exp2f(l_last - l_r) : exp2f(l_r);
       const float wgt = sU[r] * (kReverse ? exp2f(l_r) : exp2f(l_last - l_r));
@@ -464,6 +482,23 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           uint32_t sr[32];
           tmem_ld32(tmem + lane_base + kColS + u0, sr);
           tmem_ld_wait();
+          if (fac) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              const int u = u0 + e;
+              const float4 c4 = *reinterpret_cast<const float4*>(sEc + u);
+              const float cu[4] = {c4.x, c4.y, c4.z, c4.w};
+              float pv[4];
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {
+                const bool keep = all || (kReverse ? (u + x >= r) : (u + x <= r));
+                pv[x] = keep ? __uint_as_float(sr[e + x]) * (er * cu[x]) : 0.0f;
+              }
+              pk[cc * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+              pk[cc * 16 + e / 2 + 1] = pack_bf16(pv[2], pv[3]);
+            }
+            continue;
+          }
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
             const int u = u0 + e;

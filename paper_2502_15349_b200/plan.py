@@ -111,6 +111,7 @@ class LinearPlan:
     q_map: int = FM_NONE                  # elementwise feature maps applied ahead of the kernels
     k_map: int = FM_NONE
     v_map: int = FM_NONE
+    decay_hint: bool = False              # mild constant decay fills: factorised-decay kernel
 
 
 # ───────────────────────────── helpers ─────────────────────────────
@@ -688,9 +689,13 @@ def _plan_linear(spec: AttentionSpec, chunk: int = 64) -> LinearPlan:
                                source=spec.output_mod.source)
     q_map, q_scale = _feature_map(spec.q_mod, "q", consts)
     # o is linear in v: a scalar v_mod folds into the output scale
+    hint = 0.5 <= const and all(
+        extras[nm].fill == "constant_decay"
+        and all(0.5 <= float(g) <= 1.0 for g in extras[nm].fill_params.get("gamma", [0.0]))
+        for nm in names)
     return LinearPlan(spec, q_scale=q_scale * v_scale, decay_factors=tuple(names),
                       decay_const=const, k_gate=k_gate, chunk=chunk, q_map=q_map, k_map=k_map,
-                      v_map=v_map)
+                      v_map=v_map, decay_hint=hint)
 
 
 # ───────────────────────────── plan cache ─────────────────────────────

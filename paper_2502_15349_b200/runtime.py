@@ -47,7 +47,7 @@ class LinearDesc(C.Structure):
         ("q_stride", I64x4), ("k_stride", I64x4), ("v_stride", I64x4), ("o_stride", I64x4),
         ("log_decay_const", C.c_float), ("n_decay_factors", C.c_int32),
         ("decay_factor", C.c_void_p * 2), ("decay_factor_stride", I64x3 * 2),
-        ("key_gate", C.c_void_p), ("key_gate_stride", I64x3),
+        ("key_gate", C.c_void_p), ("key_gate_stride", I64x3), ("decay_hint", C.c_int32),
     ]
 
 
