@@ -241,3 +241,30 @@ def test_run_tiled_parallel_accepts_reference_signature():
     o2 = af.run_tiled_parallel(spec, arrays, 16, 128)
     assert torch.equal(o1, o2)
     assert af.bind(spec).run(arrays).shape == o1.shape
+
+
+def test_bshd_strided_inputs_match_contiguous():
+    """[B, S, H, D] activations passed as permuted views (element strides, unit feature stride)
+    give the same results as contiguous [B, H, S, D] copies — forward and backward."""
+    spec = spec_gqa("softmax", 2, 8, 2, 384, 384, 128)
+    arrays = oracle.generate(spec, seed=4)
+    dev = to_dev(arrays)
+    bshd = {n: dev[n].permute(0, 2, 1, 3).contiguous().permute(0, 2, 1, 3) for n in "qkv"}
+    assert not bshd["q"].is_contiguous()
+    o1, l1 = af.parallel_forward(spec, dev)
+    o2, l2 = af.parallel_forward(spec, bshd)
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    dout = torch.rand_like(o1)
+    g1 = af.parallel_backward(spec, dev, o1, l1, dout)
+    g2 = af.parallel_backward(spec, bshd, o2, l2, dout)
+    for n in "qkv":
+        assert torch.equal(g1[n], g2[n]), n
+
+
+def test_nan_inputs_raise_nan_error():
+    """The reference raises on NaN in the final output (engine.py:391-395)."""
+    spec = spec_gqa("softmax", 1, 2, None, 128, 128, 64)
+    dev = to_dev(oracle.generate(spec, seed=1))
+    dev["q"][0, 0, 5, 3] = float("nan")
+    with pytest.raises(af.NanError):
+        af.run_tiled_parallel(spec, dev)
