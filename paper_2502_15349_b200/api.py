@@ -178,7 +178,7 @@ def _check_decay_mask(plan: ParallelPlan, mask: torch.Tensor, device) -> None:
 
 
 MLA_DQK, MLA_DV = 576, 512
-_KERNEL_DIMS = ((64, 64), (128, 128))
+_KERNEL_DIMS = ((64, 64), (128, 128), (192, 128))
 
 
 def _padded_dim(spec, precision: str) -> int | None:
@@ -190,7 +190,9 @@ def _padded_dim(spec, precision: str) -> int | None:
     if precision != "bf16" or spec.kv_shared or (d.d_qk, d.d_v) in _KERNEL_DIMS:
         return None
     m = max(d.d_qk, d.d_v)
-    return None if m > 128 else (64 if m <= 64 else 128)
+    if m > 128:
+        return None
+    return 64 if m <= 64 else 128
 
 
 def _pad_last(t: torch.Tensor, n: int) -> torch.Tensor:
@@ -250,9 +252,17 @@ def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: 
     o = torch.empty(d.batch, d.heads, d.seq_q, v.shape[-1], device=q.device, dtype=dtype)
     lse = (torch.empty(d.batch, d.heads, d.seq_q, device=q.device, dtype=torch.float32)
            if plan.has_lse else None)
-    desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16 if dtype == _BF16 else rt.AF_DTYPE_F32)
-    rt.check(rt.lib().af_parallel_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                      o.data_ptr(), rt.ptr(lse), _stream()), "af_parallel_fwd")
+    # Value dims above the kernel's 128 (softmax-diff's 256) run as 128-wide value slices: the
+    # normalised scores P do not depend on V, so each slice is exact (S is recomputed per slice)
+    vw = 128 if (precision == "bf16" and v.shape[-1] > 128 and v.shape[-1] % 128 == 0
+                 and q.shape[-1] <= 128) else v.shape[-1]
+    for c0 in range(0, v.shape[-1], vw):
+        vs, os_ = v[..., c0:c0 + vw], o[..., c0:c0 + vw]
+        desc = _desc(plan, q, k, vs, os_, slope,
+                     rt.AF_DTYPE_BF16 if dtype == _BF16 else rt.AF_DTYPE_F32)
+        rt.check(rt.lib().af_parallel_fwd(desc, q.data_ptr(), k.data_ptr(), vs.data_ptr(),
+                                          os_.data_ptr(), rt.ptr(lse), _stream()),
+                 "af_parallel_fwd")
     if pad is not None:
         o = o[..., : d.d_v].contiguous()
     if check_nan:

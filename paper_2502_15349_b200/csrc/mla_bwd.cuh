@@ -16,6 +16,10 @@
 //               sum_{h in group, q tiles} dS'^T Q[:, n0:] + P^T dO[:, n0:] (dO only below 512);
 //               fp32 partials per head group, summed in group order by a reduce kernel.
 // No atomics: results are bitwise deterministic.
+//
+// The same phases serve every head-dim pair K2 cannot hold in TMEM (K2a needs S^T | dP^T | dV | dK
+// = 256 + Dv + Dqk columns): softmax-deepseek (192, 128) and softmax-diff (128, 256) run them with
+// separate K and V tiles, GQA head groups, and dK / dV accumulated by their own GEMMs.
 #pragma once
 #include <cuda.h>
 #include "params.h"
@@ -28,7 +32,7 @@ constexpr int kMbDqk = 576;
 constexpr int kMbDv = 512;
 
 struct MlaBwdParams {
-  int batch, heads, seq_q, seq_k, q_pad, k_pad;
+  int batch, heads, heads_kv, seq_q, seq_k, q_pad, k_pad;
   float scale, scale_log2;
   MaskParams mask;
   const float* lse2;   // [B*H, q_pad] LSE * log2(e) (+inf for padded / fully-masked rows)
@@ -38,17 +42,21 @@ struct MlaBwdParams {
   // dQ output (bf16, q strides) and dKV partials fp32 [G, B, k_pad, 576]
   void* dq;
   int64_t dq_sb, dq_sh, dq_ss;
-  float* dkv_part;
-  int groups;
+  float* dkv_part;   // fp32 partials [G, B*Hkv, k_pad, width] of the key-side GEMM
+  int groups;        // head chunks per KV head (partials summed in chunk order)
+  int part_width;    // columns of one partial row (576 for MLA, Dqk for dK, Dv for dV)
 };
 
 // ═══════════════════════════════ 1. scores ═══════════════════════════════
 
+template <int D, int DV, bool kShared>
 struct MlaScoresSmem {
   static constexpr int kStages = 4;
   static constexpr int kBox = 128 * 128;              // [128 rows][64 bf16]
-  static constexpr int kKOff = 0;                     // 9 boxes: the resident K tile
-  static constexpr int kRingOff = kKOff + 9 * kBox;   // streamed Q / dO boxes
+  static constexpr int kKB = D / 64, kVB = DV / 64;   // boxes per K / V row tile
+  static constexpr int kKOff = 0;                     // the resident K (and V) tile
+  static constexpr int kVOff = kKOff + kKB * kBox;
+  static constexpr int kRingOff = kVOff + (kShared ? 0 : kVB) * kBox;  // streamed Q / dO boxes
   static constexpr int kStatOff = kRingOff + kStages * kBox;  // [2][2][128] fp32
   static constexpr int kBarOff = kStatOff + 2 * 2 * 128 * 4;
   // k_full, full[S], empty[S], stat_full[2], stat_empty[2], s_full[2], acc_empty[2]
@@ -62,14 +70,18 @@ __host__ __device__ inline int mla_q_tile_lo(const MaskParams& m, int k0) {
   return m.causal ? max(0, k0 - m.diag_offset) / 128 : 0;
 }
 
+template <int D, int DV, bool kShared>
 __global__ void __launch_bounds__(320, 1)
     mla_bwd_scores_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_k, const MlaBwdParams p) {
-  using L = MlaScoresSmem;
+                          const __grid_constant__ CUtensorMap tm_k,
+                          const __grid_constant__ CUtensorMap tm_v, const MlaBwdParams p) {
+  using L = MlaScoresSmem<D, DV, kShared>;
   constexpr int kStages = L::kStages;
+  constexpr int kKB = L::kKB, kVB = L::kVB, kPerTile = kKB + kVB;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sK = smem + L::kKOff;
+  uint8_t* sV = kShared ? sK : smem + L::kVOff;
   uint8_t* sRing = smem + L::kRingOff;
   float* sStat = reinterpret_cast<float*>(smem + L::kStatOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -90,6 +102,7 @@ __global__ void __launch_bounds__(320, 1)
   const int kt = static_cast<int>(blockIdx.x) % k_tiles;
   const int bh = static_cast<int>(blockIdx.x) / k_tiles;
   const int b = bh / p.heads, h = bh % p.heads;
+  const int hk = h / (p.heads / p.heads_kv);
   const int k0 = kt * 128;
   const int q_tiles = p.q_pad / 128;
   const int qt_lo = mla_q_tile_lo(p.mask, k0);
@@ -118,8 +131,11 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 8) {
     // ───────────── TMA producer ─────────────
     if (elect_one() && nq > 0) {
-      mbar_expect_tx(k_full, 9 * L::kBox);
-      for (int c = 0; c < 9; ++c) tma_load_4d(sK + c * L::kBox, &tm_k, k_full, c * 64, k0, b, 0);
+      mbar_expect_tx(k_full, (kKB + (kShared ? 0 : kVB)) * L::kBox);
+      for (int c = 0; c < kKB; ++c) tma_load_4d(sK + c * L::kBox, &tm_k, k_full, c * 64, k0, hk, b);
+      if constexpr (!kShared)
+        for (int c = 0; c < kVB; ++c)
+          tma_load_4d(sV + c * L::kBox, &tm_v, k_full, c * 64, k0, hk, b);
       int slot = 0;
       uint32_t ph = 0;
       for (int n = 0; n < nq; ++n) {
@@ -138,13 +154,13 @@ __global__ void __launch_bounds__(320, 1)
             "[%3];" ::"r"(smem_u32(sStat + t * 256 + 128)),
             "l"(p.delta + row), "r"(128 * 4), "r"(smem_u32(&stat_full[t]))
             : "memory");
-        for (int c = 0; c < 17; ++c) {
+        for (int c = 0; c < kPerTile; ++c) {
           mbar_wait(&empty[slot], ph ^ 1);
           mbar_expect_tx(&full[slot], L::kBox);
-          if (c < 9)
+          if (c < kKB)
             tma_load_4d(sRing + slot * L::kBox, &tm_q, &full[slot], c * 64, q0, h, b);
           else
-            tma_load_4d(sRing + slot * L::kBox, &tm_do, &full[slot], (c - 9) * 64, q0, h, b);
+            tma_load_4d(sRing + slot * L::kBox, &tm_do, &full[slot], (c - kKB) * 64, q0, h, b);
           if (++slot == kStages) {
             slot = 0;
             ph ^= 1;
@@ -156,7 +172,7 @@ __global__ void __launch_bounds__(320, 1)
     // ───────────── MMA issuer ─────────────
     if (elect_one() && nq > 0) {
       constexpr uint32_t id = make_idesc_bf16(128, 128, false, false);
-      const uint32_t aR = smem_u32(sRing), aK = smem_u32(sK);
+      const uint32_t aR = smem_u32(sRing), aK = smem_u32(sK), aV = smem_u32(sV);
       mbar_wait(k_full, 0);
       int slot = 0;
       uint32_t ph = 0;
@@ -165,15 +181,17 @@ __global__ void __launch_bounds__(320, 1)
         mbar_wait(&acc_empty[t], ((n >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_s = tmem + t * 256, d_dp = tmem + t * 256 + 128;
-        for (int c = 0; c < 17; ++c) {
+        for (int c = 0; c < kPerTile; ++c) {
           mbar_wait(&full[slot], ph);
           tc_fence_after();
-          const int kc = c < 9 ? c : c - 9;  // K box (V = K boxes 0..7)
+          const bool is_s = c < kKB;
+          // S += Q_c K_c^T ; dP += dO_c V_c^T (MLA: V = K boxes 0 .. Dv/64 - 1)
+          const uint32_t bb = is_s ? aK + c * L::kBox : aV + (c - kKB) * L::kBox;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_ss(c < 9 ? d_s : d_dp, make_sdesc(aR + slot * L::kBox + kk * 32, 0, 1024),
-                   make_sdesc(aK + kc * L::kBox + kk * 32, 0, 1024), id,
-                   (c == 0 || c == 9) && kk == 0 ? 0u : 1u);
+            mma_ss(is_s ? d_s : d_dp, make_sdesc(aR + slot * L::kBox + kk * 32, 0, 1024),
+                   make_sdesc(bb + kk * 32, 0, 1024), id,
+                   (c == 0 || c == kKB) && kk == 0 ? 0u : 1u);
           mma_commit(&empty[slot]);
           if (++slot == kStages) {
             slot = 0;
@@ -245,14 +263,16 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
-// ═══════════════════════════════ 2/3. dQ and dKV GEMMs ═══════════════════════════════
+// ═══════════════════════════════ 2/3. dQ and key-side GEMMs ═══════════════════════════════
 // One accumulator tile of 128 rows x N columns in TMEM, fed by a ring of stages:
 //   stage = A (16 KB: one [128][64] K-major box, or two [64][64] boxes MN-major)
 //         + B (N/64 boxes [64 K-rows][64 cols], MN-major)
-// kDQ : rows = queries of (b, h, q tile); items = visible key tiles; A = dS' (K-major),
-//       B = K[:, n0:n0+N].
-// kDKV: rows = keys of (b, key tile); items = (h in group, visible q tile); per 64-query chunk two
-//       products: A = dS'^T (MN-major), B = Q[:, n0:]; A = P^T, B = dO[:, n0:] (n0 < 512 only).
+// kGemmDQ : rows = queries of (b, h, q tile); items = visible key tiles; A = dS' (K-major),
+//           B = K[hk][:, n0:n0+N].
+// key side: rows = keys of (b, hk, key tile); items = (h in the head chunk, visible q tile); per
+//           64-query chunk one or two products: A = dS'^T (MN-major), B = Q[:, n0:] (dK, and MLA's
+//           latent dKV) and A = P^T, B = dO[:, n0:] (dV, and MLA's dKV for n0 < 512).
+enum GemmMode : int { kGemmDQ = 0, kGemmDKV = 1, kGemmDK = 2, kGemmDV = 3 };
 
 template <int N>
 struct MlaGemmSmem {
@@ -264,18 +284,19 @@ struct MlaGemmSmem {
   static constexpr int kNumBars = 2 * kStages + 1;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
-  static constexpr int kTmemCols = N >= 512 ? 512 : (N >= 256 ? 256 : (N >= 128 ? 128 : 64));
+  static constexpr int kTmemCols = N > 256 ? 512 : (N > 128 ? 256 : (N > 64 ? 128 : 64));
 };
 
-template <bool kDKV, int N>
+template <int kMode, int N>
 __global__ void __launch_bounds__(192, 1)
     mla_bwd_gemm_kernel(const __grid_constant__ CUtensorMap tm_a1,   // dS'
-                        const __grid_constant__ CUtensorMap tm_a2,   // P (kDKV)
-                        const __grid_constant__ CUtensorMap tm_b1,   // K (kDQ) / Q (kDKV)
-                        const __grid_constant__ CUtensorMap tm_b2,   // dO (kDKV)
+                        const __grid_constant__ CUtensorMap tm_a2,   // P (key side)
+                        const __grid_constant__ CUtensorMap tm_b1,   // K (dQ) / Q (key side)
+                        const __grid_constant__ CUtensorMap tm_b2,   // dO (key side)
                         const MlaBwdParams p, int n0) {
   using L = MlaGemmSmem<N>;
   constexpr int kStages = L::kStages;
+  constexpr bool kKey = kMode != kGemmDQ;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* full = bars;
@@ -283,35 +304,40 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* acc_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
   const int warp = static_cast<int>(warp_id());
+  const int group = p.heads / p.heads_kv;
 
   // ── work decomposition ──
-  int b, tile, h_lo = 0, h_hi = 0, bh = 0;
-  int it_lo = 0, it_hi = 0;  // contraction tile range (key tiles for kDQ, q tiles for kDKV)
-  const int q_tiles = p.q_pad / 128, k_tiles = p.k_pad / 128;
-  if constexpr (!kDKV) {
+  int b, hk, tile, h_lo = 0, h_hi = 0, bh = 0, g = 0, bk = 0;
+  int it_lo = 0, it_hi = 0;  // contraction tile range (key tiles for dQ, q tiles key-side)
+  const int q_tiles = p.q_pad / 128;
+  if constexpr (!kKey) {
     // blockIdx.x = (q tile, b*H + h), heaviest (last) query tiles first under a causal mask
     const int bhs = p.batch * p.heads;
     const int raw = static_cast<int>(blockIdx.x) / bhs;
     bh = static_cast<int>(blockIdx.x) % bhs;
     b = bh / p.heads;
+    hk = (bh % p.heads) / group;
     tile = p.mask.causal ? q_tiles - 1 - raw : raw;
     const TileBand band = key_band(p.mask, tile * 128, min(p.seq_q, tile * 128 + 128), p.seq_k);
     it_lo = band.jb_lo;
     it_hi = band.jb_hi;
   } else {
-    // blockIdx.x = (key tile, b, group), heaviest (first) key tiles first
-    const int per = p.batch * p.groups;
+    // blockIdx.x = (key tile, b*Hkv + hk, head chunk), heaviest (first) key tiles first
+    const int per = p.batch * p.heads_kv * p.groups;
     tile = static_cast<int>(blockIdx.x) / per;
     const int rest = static_cast<int>(blockIdx.x) % per;
-    b = rest / p.groups;
-    const int g = rest % p.groups;
-    h_lo = g * p.heads / p.groups;
-    h_hi = (g + 1) * p.heads / p.groups;
+    bk = rest / p.groups;
+    g = rest % p.groups;
+    b = bk / p.heads_kv;
+    hk = bk % p.heads_kv;
+    h_lo = hk * group + g * group / p.groups;
+    h_hi = hk * group + (g + 1) * group / p.groups;
     it_lo = mla_q_tile_lo(p.mask, tile * 128);
     it_hi = q_tiles;
   }
-  const int per_item = kDKV ? (n0 < kMbDv ? 4 : 2) : 2;  // stages per contraction tile
-  const int n_items = kDKV ? (h_hi - h_lo) * max(0, it_hi - it_lo) : max(0, it_hi - it_lo);
+  // stages per contraction tile: two 64-row chunks x products
+  const int per_item = (kMode == kGemmDKV && n0 < kMbDv) ? 4 : 2;
+  const int n_items = kKey ? (h_hi - h_lo) * max(0, it_hi - it_lo) : max(0, it_hi - it_lo);
   const int n_stages_total = n_items * per_item;
 
   if (warp == 4 && lane_id() == 0) {
@@ -339,21 +365,21 @@ __global__ void __launch_bounds__(192, 1)
         mbar_expect_tx(&full[slot], L::kStage);
         uint8_t* sa = smem + slot * L::kStage;
         uint8_t* sb = sa + L::kABytes;
-        if constexpr (!kDKV) {
+        if constexpr (!kKey) {
           const int kt = it_lo + item;
           const int c = sub;  // 64-key chunk
           tma_load_4d(sa, &tm_a1, &full[slot], kt * 128 + c * 64, tile * 128, bh, 0);
           for (int nb = 0; nb < N / 64; ++nb)
             tma_load_4d_hint(sb + nb * 8192, &tm_b1, &full[slot], n0 + nb * 64,
-                             kt * 128 + c * 64, b, 0, kEvictLast);
+                             kt * 128 + c * 64, hk, b, kEvictLast);
         } else {
           // query tiles from the last one down: CTAs of different key tiles then stream the same
           // Q / dO tiles concurrently (L2 reuse)
           const int hh = h_lo + item / (it_hi - it_lo);
           const int qt = it_hi - 1 - item % (it_hi - it_lo);
-          // chunk, product (0: dS'/Q, 1: P/dO); the rope columns (n0 >= 512) have no dO term
+          // chunk, product (0: dS'/Q, 1: P/dO)
           const int c = per_item == 4 ? sub / 2 : sub;
-          const int prod = per_item == 4 ? sub % 2 : 0;
+          const int prod = per_item == 4 ? sub % 2 : (kMode == kGemmDV ? 1 : 0);
           const int bhh = b * p.heads + hh;
           const int r0 = qt * 128 + c * 64;
           const CUtensorMap* ta = prod == 0 ? &tm_a1 : &tm_a2;
@@ -373,7 +399,7 @@ __global__ void __launch_bounds__(192, 1)
     // ───────────── MMA issuer ─────────────
     if (elect_one()) {
       constexpr int kN = N >= 256 ? 256 : N;  // per-instruction N
-      constexpr uint32_t id = make_idesc_bf16(128, kN, kDKV, true);
+      constexpr uint32_t id = make_idesc_bf16(128, kN, kKey, true);
       int slot = 0;
       uint32_t ph = 0;
       for (int st = 0; st < n_stages_total; ++st) {
@@ -383,7 +409,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t sb = sa + L::kABytes;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = kDKV ? make_sdesc(sa + kk * 2048, 8192, 1024)
+          const uint64_t ad = kKey ? make_sdesc(sa + kk * 2048, 8192, 1024)
                                    : make_sdesc(sa + kk * 32, 0, 1024);
 #pragma unroll
           for (int nh = 0; nh < N / kN; ++nh)
@@ -417,7 +443,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) r[e] = 0u;
       }
-      if constexpr (!kDKV) {
+      if constexpr (!kKey) {
         const int i = tile * 128 + row;
         if (i < p.seq_q) {
           const int h = bh % p.heads;
@@ -433,8 +459,9 @@ __global__ void __launch_bounds__(192, 1)
         }
       } else {
         const int j = tile * 128 + row;
-        const int g = static_cast<int>(blockIdx.x) % (p.batch * p.groups) % p.groups;
-        float* dst = p.dkv_part + ((static_cast<int64_t>(g) * p.batch + b) * p.k_pad + j) * kMbDqk +
+        float* dst = p.dkv_part +
+                     ((static_cast<int64_t>(g) * p.batch * p.heads_kv + bk) * p.k_pad + j) *
+                         p.part_width +
                      n0 + c * 32;
         float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
@@ -453,28 +480,30 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-// dKV[b, j, :] = bf16( sum_g part[g, b, j, :] )  (group order fixed: deterministic)
-__global__ void mla_bwd_reduce_kernel(const float* __restrict__ part, int groups, int batch,
-                                      int seq_k, int k_pad, __nv_bfloat16* __restrict__ dkv,
-                                      int64_t dkv_sb, int64_t dkv_ss) {
+// out[b, hk, j, :] = bf16( sum_g part[g, b*Hkv + hk, j, :] )  (group order fixed: deterministic)
+__global__ void mla_bwd_reduce_kernel(const float* __restrict__ part, int groups, int bhk,
+                                      int heads_kv, int seq_k, int k_pad, int width, int pitch,
+                                      __nv_bfloat16* __restrict__ out, int64_t o_sb,
+                                      int64_t o_sh, int64_t o_ss) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // 4 cols
-  const int64_t per_row = kMbDqk / 4;
-  const int64_t total = static_cast<int64_t>(batch) * seq_k * per_row;
+  const int64_t per_row = width / 4;
+  const int64_t total = static_cast<int64_t>(bhk) * seq_k * per_row;
   if (idx >= total) return;
   const int c4 = static_cast<int>(idx % per_row);
   const int64_t bj = idx / per_row;
-  const int b = static_cast<int>(bj / seq_k), j = static_cast<int>(bj % seq_k);
+  const int bk = static_cast<int>(bj / seq_k), j = static_cast<int>(bj % seq_k);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int g = 0; g < groups; ++g) {
     const float4 v = *reinterpret_cast<const float4*>(
-        part + ((static_cast<int64_t>(g) * batch + b) * k_pad + j) * kMbDqk + c4 * 4);
+        part + ((static_cast<int64_t>(g) * bhk + bk) * k_pad + j) * pitch + c4 * 4);
     acc.x += v.x;
     acc.y += v.y;
     acc.z += v.z;
     acc.w += v.w;
   }
-  *reinterpret_cast<uint2*>(dkv + b * dkv_sb + static_cast<int64_t>(j) * dkv_ss + c4 * 4) =
-      make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
+  const int b = bk / heads_kv, hk = bk % heads_kv;
+  *reinterpret_cast<uint2*>(out + b * o_sb + hk * o_sh + static_cast<int64_t>(j) * o_ss +
+                            c4 * 4) = make_uint2(pack_bf16(acc.x, acc.y), pack_bf16(acc.z, acc.w));
 }
 
 }  // namespace af

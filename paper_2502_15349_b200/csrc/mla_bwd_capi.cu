@@ -1,6 +1,9 @@
-// Host side of K3b (MLA backward): workspace layout, tensor maps and the five launches
-// (row statistics, scores, dQ GEMM x2, dKV GEMM x2, group reduce).  Called by af_parallel_bwd when
-// the descriptor is the MLA lowering ((Dqk, Dv) = (576, 512), one KV head, V = K[:, :512]).
+// Host side of K3b, the materialised softmax backward (mla_bwd.cuh): workspace layout, tensor maps
+// and the launches (row statistics, scores, dQ GEMM(s), key-side GEMM(s), group reduces).  Called
+// by af_parallel_bwd for the MLA lowering ((Dqk, Dv) = (576, 512), one KV head, V = K[:, :512])
+// and for the head-dim pairs K2 cannot hold in TMEM: (192, 128) and (128, 256).
+#include <algorithm>
+
 #include "host_common.h"
 #include "mla_bwd.cuh"
 #include "parallel_bwd.cuh"
@@ -10,23 +13,27 @@ namespace {
 
 constexpr int64_t pad128(int64_t x) { return ((x + 127) / 128) * 128; }
 
-struct MlaBwdLayout {
-  int64_t q_pad, k_pad, rows, groups;
+struct MatLayout {
+  int64_t q_pad, k_pad, rows, groups, part_width;
   size_t stats, scores, part, total;
 };
 
-MlaBwdLayout mla_layout(const af_parallel_desc* d) {
-  MlaBwdLayout l{};
+MatLayout mat_layout(const af_parallel_desc* d, bool shared) {
+  MatLayout l{};
   l.q_pad = pad128(d->seq_q);
   l.k_pad = pad128(d->seq_k);
   l.rows = static_cast<int64_t>(d->batch) * d->heads_q * l.q_pad;
-  // head groups of the dKV GEMM: enough CTAs for ~4 waves, at most one group per head
+  // head chunks of the key-side GEMMs: enough CTAs for ~4 waves, at most one chunk per head
   const int64_t k_tiles = l.k_pad / 128;
-  const int64_t want = (4 * sm_count() + k_tiles * d->batch - 1) / (k_tiles * d->batch);
-  l.groups = std::max<int64_t>(1, std::min<int64_t>(want, d->heads_q));
+  const int64_t units = k_tiles * d->batch * d->heads_kv;
+  const int64_t group = d->heads_q / d->heads_kv;
+  const int64_t want = (4 * sm_count() + units - 1) / units;
+  l.groups = std::max<int64_t>(1, std::min<int64_t>(want, group));
+  l.part_width = shared ? d->d_qk : std::max(d->d_qk, d->d_v);
   l.stats = static_cast<size_t>(l.rows) * 2 * sizeof(float);
   l.scores = static_cast<size_t>(l.rows) * l.k_pad * 2;  // one bf16 [B*H, q_pad, k_pad] buffer
-  l.part = static_cast<size_t>(l.groups) * d->batch * l.k_pad * kMbDqk * sizeof(float);
+  l.part = static_cast<size_t>(l.groups) * d->batch * d->heads_kv * l.k_pad * l.part_width *
+           sizeof(float);
   l.total = l.stats + 2 * l.scores + l.part;
   return l;
 }
@@ -46,21 +53,40 @@ bool tmap_3d(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64
                       true);
 }
 
-}  // namespace
+template <int kMode, int N>
+int launch_gemm(const CUtensorMap& a1, const CUtensorMap& a2, const CUtensorMap& b1,
+                const CUtensorMap& b2, const MlaBwdParams& p, int n0, unsigned grid,
+                cudaStream_t s) {
+  auto kern = mla_bwd_gemm_kernel<kMode, N>;
+  static bool attr = false;
+  if (!attr) {
+    if (set_smem(kern, MlaGemmSmem<N>::kTotal) != AF_OK) return AF_ERR_CUDA;
+    attr = true;
+  }
+  ::af::note_launch();
+  kern<<<grid, 192, MlaGemmSmem<N>::kTotal, s>>>(a1, a2, b1, b2, p, n0);
+  AF_CUDA_CHECK(cudaGetLastError());
+  return AF_OK;
+}
 
-size_t mla_bwd_workspace(const af_parallel_desc* d) { return mla_layout(d).total; }
+int launch_reduce(const MlaBwdParams& p, const MatLayout& l, const af_parallel_desc* d,
+                  int width, void* out, const int64_t* out_stride, cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(d->batch) * d->heads_kv * d->seq_k * (width / 4);
+  ::af::note_launch();
+  mla_bwd_reduce_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+      p.dkv_part, static_cast<int>(l.groups), d->batch * d->heads_kv, d->heads_kv, d->seq_k,
+      static_cast<int>(l.k_pad), width, static_cast<int>(l.part_width),
+      static_cast<__nv_bfloat16*>(out), out_stride[0],
+      out_stride[1], out_stride[2]);
+  AF_CUDA_CHECK(cudaGetLastError());
+  return AF_OK;
+}
 
-int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void* o,
-            const float* lse, const void* dout, void* dq, void* dkv, void* workspace,
-            cudaStream_t s) {
-  AF_REQUIRE(d->heads_kv == 1, AF_ERR_UNSUPPORTED, "MLA backward needs one latent KV head");
-  AF_REQUIRE(d->family == AF_FAMILY_SOFTMAX, AF_ERR_UNSUPPORTED, "MLA backward is softmax only");
-  AF_REQUIRE(!d->causal || d->diag_offset == 0, AF_ERR_UNSUPPORTED,
-             "MLA backward supports the top-left causal mask (offset 0) only");
-  AF_REQUIRE(d->window <= 0, AF_ERR_UNSUPPORTED, "MLA backward has no sliding window");
-  AF_REQUIRE(d->k_stride[3] == 1 && d->q_stride[3] == 1 && d->o_stride[3] == 1, AF_ERR_INPUT,
-             "feature stride must be 1");
-  const MlaBwdLayout l = mla_layout(d);
+template <int D, int DV, bool kShared>
+int run_materialized(const af_parallel_desc* d, const void* q, const void* k, const void* v,
+                     const void* o, const float* lse, const void* dout, void* dq, void* dk,
+                     void* dv, void* workspace, cudaStream_t s) {
+  const MatLayout l = mat_layout(d, kShared);
   float* lse2 = static_cast<float*>(workspace);
   float* delta = lse2 + l.rows;
   uint8_t* base = static_cast<uint8_t*>(workspace) + l.stats;
@@ -72,7 +98,7 @@ int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void*
     const int threads = 256;
     const unsigned blocks = static_cast<unsigned>((l.rows * 32 + threads - 1) / threads);
     ::af::note_launch();
-    bwd_preprocess_kernel<kMbDv><<<blocks, threads, 0, s>>>(
+    bwd_preprocess_kernel<DV><<<blocks, threads, 0, s>>>(
         static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse,
         d->o_stride[0], d->o_stride[1], d->o_stride[2], d->o_stride[0], d->o_stride[1],
         d->o_stride[2], d->heads_q, d->seq_q, static_cast<int>(l.q_pad), AF_FAMILY_SOFTMAX,
@@ -83,6 +109,7 @@ int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void*
   MlaBwdParams p{};
   p.batch = d->batch;
   p.heads = d->heads_q;
+  p.heads_kv = d->heads_kv;
   p.seq_q = d->seq_q;
   p.seq_k = d->seq_k;
   p.q_pad = static_cast<int>(l.q_pad);
@@ -102,88 +129,97 @@ int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void*
   p.dq_ss = d->q_stride[2];
   p.dkv_part = part;
   p.groups = static_cast<int>(l.groups);
+  p.part_width = static_cast<int>(l.part_width);
 
-  const int64_t kv_st[4] = {0, d->k_stride[0], d->k_stride[2], 1};  // (576, Sk, B, 1)
   const int64_t bhs = static_cast<int64_t>(d->batch) * d->heads_q;
   const int q_tiles = static_cast<int>(l.q_pad / 128), k_tiles = static_cast<int>(l.k_pad / 128);
 
-  {  // 1. scores
-    CUtensorMap tq, tdo, tk;
-    if (!make_tmap_4d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMbDqk, d->seq_q, d->heads_q,
+  {  // 1. scores: P and dS' = tau P (dP - D) for the visible blocks
+    using SL = MlaScoresSmem<D, DV, kShared>;
+    CUtensorMap tq, tdo, tk, tv;
+    if (!make_tmap_4d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_q, d->heads_q,
                       d->batch, d->q_stride, 64, 128, true) ||
-        !make_tmap_4d(&tdo, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMbDv, d->seq_q,
-                      d->heads_q, d->batch, d->o_stride, 64, 128, true) ||
-        !make_tmap_4d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMbDqk, d->seq_k, d->batch, 1,
-                      kv_st, 64, 128, true))
+        !make_tmap_4d(&tdo, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, DV, d->seq_q, d->heads_q,
+                      d->batch, d->o_stride, 64, 128, true) ||
+        !make_tmap_4d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_k, d->heads_kv,
+                      d->batch, d->k_stride, 64, 128, true) ||
+        !make_tmap_4d(&tv, kShared ? k : v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                      kShared ? D : DV, d->seq_k, d->heads_kv, d->batch,
+                      kShared ? d->k_stride : d->v_stride, 64, 128, true))
       return AF_ERR_INPUT;
+    auto kern = mla_bwd_scores_kernel<D, DV, kShared>;
     static bool attr = false;
     if (!attr) {
-      if (set_smem(mla_bwd_scores_kernel, MlaScoresSmem::kTotal) != AF_OK) return AF_ERR_CUDA;
+      if (set_smem(kern, SL::kTotal) != AF_OK) return AF_ERR_CUDA;
       attr = true;
     }
     ::af::note_launch();
-    mla_bwd_scores_kernel<<<static_cast<unsigned>(k_tiles * bhs), 320, MlaScoresSmem::kTotal, s>>>(
-        tq, tdo, tk, p);
+    kern<<<static_cast<unsigned>(k_tiles * bhs), 320, SL::kTotal, s>>>(tq, tdo, tk, tv, p);
     AF_CUDA_CHECK(cudaGetLastError());
   }
 
-  {  // 2. dQ = dS' K  (N = 512, then the 64 rope columns)
-    CUtensorMap tds, tkb;
-    if (!tmap_3d(&tds, dsbuf, l.k_pad, l.q_pad, bhs, 64, 128) ||
-        !make_tmap_4d(&tkb, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMbDqk, d->seq_k, d->batch, 1,
-                      kv_st, 64, 64, true))
-      return AF_ERR_INPUT;
-    static bool attr = false;
-    if (!attr) {
-      if (set_smem(mla_bwd_gemm_kernel<false, 512>, MlaGemmSmem<512>::kTotal) != AF_OK ||
-          set_smem(mla_bwd_gemm_kernel<false, 64>, MlaGemmSmem<64>::kTotal) != AF_OK)
-        return AF_ERR_CUDA;
-      attr = true;
-    }
-    const unsigned grid = static_cast<unsigned>(q_tiles * bhs);
-    ::af::note_launch();
-    mla_bwd_gemm_kernel<false, 512><<<grid, 192, MlaGemmSmem<512>::kTotal, s>>>(tds, tds, tkb, tkb,
-                                                                               p, 0);
-    AF_CUDA_CHECK(cudaGetLastError());
-    ::af::note_launch();
-    mla_bwd_gemm_kernel<false, 64><<<grid, 192, MlaGemmSmem<64>::kTotal, s>>>(tds, tds, tkb, tkb,
-                                                                             p, 512);
-    AF_CUDA_CHECK(cudaGetLastError());
+  // maps shared by the GEMMs
+  CUtensorMap tds_q, tds_k, tp_k, tkb, tqb, tdob;
+  if (!tmap_3d(&tds_q, dsbuf, l.k_pad, l.q_pad, bhs, 64, 128) ||
+      !tmap_3d(&tds_k, dsbuf, l.k_pad, l.q_pad, bhs, 64, 64) ||
+      !tmap_3d(&tp_k, pbuf, l.k_pad, l.q_pad, bhs, 64, 64) ||
+      !make_tmap_4d(&tkb, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_k, d->heads_kv,
+                    d->batch, d->k_stride, 64, 64, true) ||
+      !make_tmap_4d(&tqb, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_q, d->heads_q,
+                    d->batch, d->q_stride, 64, 64, true) ||
+      !make_tmap_4d(&tdob, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, DV, d->seq_q, d->heads_q,
+                    d->batch, d->o_stride, 64, 64, true))
+    return AF_ERR_INPUT;
+  const unsigned gq = static_cast<unsigned>(q_tiles * bhs);
+  const unsigned gk = static_cast<unsigned>(k_tiles * d->batch * d->heads_kv * l.groups);
+  int st;
+  if constexpr (kShared) {  // MLA: dQ in 512 + 64 columns, one latent dKV accumulator
+    if ((st = launch_gemm<kGemmDQ, 512>(tds_q, tds_q, tkb, tkb, p, 0, gq, s)) != AF_OK) return st;
+    if ((st = launch_gemm<kGemmDQ, 64>(tds_q, tds_q, tkb, tkb, p, 512, gq, s)) != AF_OK) return st;
+    if ((st = launch_gemm<kGemmDKV, 512>(tds_k, tp_k, tqb, tdob, p, 0, gk, s)) != AF_OK) return st;
+    if ((st = launch_gemm<kGemmDKV, 64>(tds_k, tp_k, tqb, tdob, p, 512, gk, s)) != AF_OK) return st;
+    return launch_reduce(p, l, d, D, dk, d->k_stride, s);
+  } else {
+    if ((st = launch_gemm<kGemmDQ, D>(tds_q, tds_q, tkb, tkb, p, 0, gq, s)) != AF_OK) return st;
+    if ((st = launch_gemm<kGemmDK, D>(tds_k, tp_k, tqb, tdob, p, 0, gk, s)) != AF_OK) return st;
+    if ((st = launch_reduce(p, l, d, D, dk, d->k_stride, s)) != AF_OK) return st;
+    if ((st = launch_gemm<kGemmDV, DV>(tds_k, tp_k, tqb, tdob, p, 0, gk, s)) != AF_OK) return st;
+    return launch_reduce(p, l, d, DV, dv, d->v_stride, s);
   }
+}
 
-  {  // 3. dKV partials = sum_{h in group} dS'^T Q + P^T dO, then the group reduce
-    CUtensorMap tds, tp, tqb, tdob;
-    if (!tmap_3d(&tds, dsbuf, l.k_pad, l.q_pad, bhs, 64, 64) ||
-        !tmap_3d(&tp, pbuf, l.k_pad, l.q_pad, bhs, 64, 64) ||
-        !make_tmap_4d(&tqb, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMbDqk, d->seq_q, d->heads_q,
-                      d->batch, d->q_stride, 64, 64, true) ||
-        !make_tmap_4d(&tdob, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMbDv, d->seq_q,
-                      d->heads_q, d->batch, d->o_stride, 64, 64, true))
-      return AF_ERR_INPUT;
-    static bool attr = false;
-    if (!attr) {
-      if (set_smem(mla_bwd_gemm_kernel<true, 512>, MlaGemmSmem<512>::kTotal) != AF_OK ||
-          set_smem(mla_bwd_gemm_kernel<true, 64>, MlaGemmSmem<64>::kTotal) != AF_OK)
-        return AF_ERR_CUDA;
-      attr = true;
-    }
-    const unsigned grid = static_cast<unsigned>(k_tiles * d->batch * l.groups);
-    ::af::note_launch();
-    mla_bwd_gemm_kernel<true, 512><<<grid, 192, MlaGemmSmem<512>::kTotal, s>>>(tds, tp, tqb, tdob,
-                                                                              p, 0);
-    AF_CUDA_CHECK(cudaGetLastError());
-    ::af::note_launch();
-    mla_bwd_gemm_kernel<true, 64><<<grid, 192, MlaGemmSmem<64>::kTotal, s>>>(tds, tp, tqb, tdob, p,
-                                                                            512);
-    AF_CUDA_CHECK(cudaGetLastError());
-    const int64_t total = static_cast<int64_t>(d->batch) * d->seq_k * (kMbDqk / 4);
-    ::af::note_launch();
-    mla_bwd_reduce_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-        part, static_cast<int>(l.groups), d->batch, d->seq_k, static_cast<int>(l.k_pad),
-        static_cast<__nv_bfloat16*>(dkv), d->k_stride[0], d->k_stride[2]);
-    AF_CUDA_CHECK(cudaGetLastError());
+}  // namespace
+
+bool materialized_bwd_dims(const af_parallel_desc* d) {
+  return (d->d_qk == 576 && d->d_v == 512) || (d->d_qk == 192 && d->d_v == 128) ||
+         (d->d_qk == 128 && d->d_v == 256);
+}
+
+size_t mla_bwd_workspace(const af_parallel_desc* d) {
+  return mat_layout(d, d->d_qk == 576 && d->d_v == 512).total;
+}
+
+int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void* v, const void* o,
+            const float* lse, const void* dout, void* dq, void* dk, void* dv, void* workspace,
+            cudaStream_t s) {
+  AF_REQUIRE(d->family == AF_FAMILY_SOFTMAX && d->cap_b == 0.0f, AF_ERR_UNSUPPORTED,
+             "the materialised backward (head dims %d/%d) is softmax only", d->d_qk, d->d_v);
+  AF_REQUIRE(!d->causal || d->diag_offset == 0, AF_ERR_UNSUPPORTED,
+             "the materialised backward supports the top-left causal mask (offset 0) only");
+  AF_REQUIRE(d->window <= 0, AF_ERR_UNSUPPORTED, "the materialised backward has no sliding window");
+  AF_REQUIRE(d->k_stride[3] == 1 && d->q_stride[3] == 1 && d->o_stride[3] == 1 &&
+                 d->v_stride[3] == 1,
+             AF_ERR_INPUT, "feature stride must be 1");
+  if (d->d_qk == 576 && d->d_v == 512) {
+    AF_REQUIRE(d->heads_kv == 1, AF_ERR_UNSUPPORTED, "MLA backward needs one latent KV head");
+    return run_materialized<576, 512, true>(d, q, k, v, o, lse, dout, dq, dk, dv, workspace, s);
   }
-  return AF_OK;
+  if (d->d_qk == 192 && d->d_v == 128)
+    return run_materialized<192, 128, false>(d, q, k, v, o, lse, dout, dq, dk, dv, workspace, s);
+  if (d->d_qk == 128 && d->d_v == 256)
+    return run_materialized<128, 256, false>(d, q, k, v, o, lse, dout, dq, dk, dv, workspace, s);
+  set_error("materialised backward: head dims (%d, %d) not instantiated", d->d_qk, d->d_v);
+  return AF_ERR_UNSUPPORTED;
 }
 
 }  // namespace af

@@ -6,8 +6,9 @@
 namespace af {
 int validate_parallel(const af_parallel_desc* d);
 size_t mla_bwd_workspace(const af_parallel_desc* d);
-int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void* o,
-            const float* lse, const void* dout, void* dq, void* dkv, void* workspace,
+bool materialized_bwd_dims(const af_parallel_desc* d);
+int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void* v, const void* o,
+            const float* lse, const void* dout, void* dq, void* dk, void* dv, void* workspace,
             cudaStream_t s);
 inline bool is_mla(const af_parallel_desc* d) { return d->d_qk == 576 && d->d_v == 512; }
 namespace {
@@ -85,7 +86,7 @@ int dispatch_bwd(const BwdLaunch& a) {
 
 extern "C" size_t af_parallel_bwd_workspace(const af_parallel_desc* d) {
   if (d == nullptr) return 0;
-  if (af::is_mla(d)) return af::mla_bwd_workspace(d);
+  if (af::materialized_bwd_dims(d)) return af::mla_bwd_workspace(d);
   const int64_t rows = static_cast<int64_t>(d->batch) * d->heads_q * af::pad_q(d->seq_q);
   return static_cast<size_t>(rows) * 2 * sizeof(float);
 }
@@ -108,8 +109,12 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
     AF_REQUIRE(v == k && d->cap_b == 0.0f && d->v_stride[0] == d->k_stride[0] &&
                    d->v_stride[2] == d->k_stride[2],
                AF_ERR_UNSUPPORTED, "(576, 512) heads are lowered only as MLA (V = K[:, :512])");
-    return mla_bwd(d, q, k, o, lse, dout, dq, dk, workspace, reinterpret_cast<cudaStream_t>(stream));
+    return mla_bwd(d, q, k, v, o, lse, dout, dq, dk, dv, workspace,
+                   reinterpret_cast<cudaStream_t>(stream));
   }
+  if (materialized_bwd_dims(d))  // head dims beyond K2's TMEM budget: (192, 128), (128, 256)
+    return mla_bwd(d, q, k, v, o, lse, dout, dq, dk, dv, workspace,
+                   reinterpret_cast<cudaStream_t>(stream));
   if (!((d->d_qk == 128 && d->d_v == 128) || (d->d_qk == 64 && d->d_v == 64))) {
     set_error("bf16 parallel backward: head dims (%d, %d) not instantiated", d->d_qk, d->d_v);
     return AF_ERR_UNSUPPORTED;

@@ -10,7 +10,7 @@ namespace {
 template <int D, int DV, int kFamily, int kAct>
 int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
                const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t stream) {
-  constexpr int kStages = 2;
+  constexpr int kStages = D > 128 ? 1 : 2;  // D = 192: two 48 KB Q tiles leave room for one stage
   using L = FwdSmem<D, DV, kStages>;
   auto kern = parallel_fwd_kernel<D, DV, kFamily, kAct, kStages>;
   static bool attr_done = false;
@@ -127,6 +127,7 @@ extern "C" int af_parallel_fwd(const af_parallel_desc* d, const void* q, const v
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (d->d_qk == 128 && d->d_v == 128) return dispatch_family<128, 128>(d, tq, tk, tv, p, s);
   if (d->d_qk == 64 && d->d_v == 64) return dispatch_family<64, 64>(d, tq, tk, tv, p, s);
+  if (d->d_qk == 192 && d->d_v == 128) return dispatch_family<192, 128>(d, tq, tk, tv, p, s);
   set_error("bf16 parallel forward: head dims (%d, %d) not instantiated", d->d_qk, d->d_v);
   return AF_ERR_UNSUPPORTED;
 }

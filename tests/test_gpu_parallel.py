@@ -97,6 +97,11 @@ BF16_CASES = {
     "sigmoid_relpos_swa_s1024": lambda: sigmoid_swa_spec(1, 4, 1024, 128, 256),
     "relu_causal_d64": lambda: spec_gqa("relu", 1, 2, None, 384, 384, 64),
     "sigmoid_noncausal_gqa": lambda: spec_gqa("sigmoid", 1, 4, 2, 256, 256, 128, causal=False),
+    # builtins at their own head dims beyond K2's TMEM budget (materialised backward)
+    "softmax_deepseek_192_128_gqa": lambda: S.with_causal_mask(S.builtin(
+        "softmax-deepseek", batch=1, heads=4, heads_kv=2, seq=384, d_qk=192, d_v=128)),
+    "softmax_diff_128_256_ragged": lambda: S.with_causal_mask(S.builtin(
+        "softmax-diff", batch=2, heads=2, seq=300, d_qk=128, d_v=256)),
     # retention-parallel: causal decay mask synthesised in-kernel + abssum-clamp rows
     "retention_parallel_s512_d128": lambda: S.builtin("retention-parallel", batch=1, heads=4,
                                                       seq=512, d_qk=128, d_v=128),
@@ -229,7 +234,7 @@ def test_unlowered_variant_raises_not_falls_back():
     arrays["mask"] = torch.rand_like(arrays["mask"])  # ... an arbitrary materialised one does not
     with pytest.raises(af.UnsupportedError):
         af.run_tiled_parallel(spec, arrays)
-    spec = S.builtin("softmax-diff", heads=2, seq=128, d_qk=128, d_v=256)  # Dv > 128
+    spec = S.builtin("softmax", heads=2, seq=128, d_qk=320, d_v=320)  # no kernel for 320
     with pytest.raises(af.UnsupportedError):
         af.parallel_forward(spec, to_dev(oracle.generate(spec, 0)))
 
