@@ -401,20 +401,35 @@ __global__ void __launch_bounds__(320, 1)
           }
         } else {
           const float zb = p.bias - slope * (static_cast<float>(q0 + cb + c2 * 32) - fj);
+          if (fullblk) {  // compact fast path: no per-element mask tests
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float pv[2];
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-              const int i = q0 + cb + c2 * 32 + e + x;
-              const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
-                                   zb - slope * static_cast<float>(e + x));
-              const bool keep = fullblk || (kept(p.mask, i, j, p.seq_k) && i < p.seq_q);
-              const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
-              bits |= (keep && g) ? (1u << (e + x)) : 0u;
-              pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
+            for (int e = 0; e < 32; e += 2) {
+              const float z0 = fmaf(__uint_as_float(sr[e]), p.scale, zb - slope * static_cast<float>(e));
+              const float z1 = fmaf(__uint_as_float(sr[e + 1]), p.scale,
+                                    zb - slope * static_cast<float>(e + 1));
+              if constexpr (kAct == kActRelu) {
+                bits |= (z0 >= 0.0f ? (1u << e) : 0u) | (z1 >= 0.0f ? (2u << e) : 0u);
+              } else {
+                bits |= 3u << e;
+              }
+              pk[c2 * 16 + e / 2] = pack_bf16(apply_act<kAct>(z0), apply_act<kAct>(z1));
             }
-            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+          } else {
+#pragma unroll 2
+            for (int e = 0; e < 32; e += 2) {
+              float pv[2];
+#pragma unroll
+              for (int x = 0; x < 2; ++x) {
+                const int i = q0 + cb + c2 * 32 + e + x;
+                const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
+                                     zb - slope * static_cast<float>(e + x));
+                const bool keep = kept(p.mask, i, j, p.seq_k) && i < p.seq_q;
+                const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
+                bits |= (keep && g) ? (1u << (e + x)) : 0u;
+                pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
+              }
+              pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+            }
           }
         }
         gmask[c2] = bits;
@@ -756,19 +771,34 @@ __global__ void __launch_bounds__(320, 1)
           }
         } else {
           const float zb = p.bias - slope * (fi - static_cast<float>(jb));
+          if (fullblk && live) {  // compact fast path: no per-element mask tests
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float pv[2];
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-              const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
-                                   zb + slope * static_cast<float>(e + x));
-              const bool keep = live && (fullblk || kept(p.mask, i, jb + e + x, p.seq_k));
-              const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
-              bits |= (keep && g) ? (1u << (e + x)) : 0u;
-              pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
+            for (int e = 0; e < 32; e += 2) {
+              const float z0 = fmaf(__uint_as_float(sr[e]), p.scale, zb + slope * static_cast<float>(e));
+              const float z1 = fmaf(__uint_as_float(sr[e + 1]), p.scale,
+                                    zb + slope * static_cast<float>(e + 1));
+              if constexpr (kAct == kActRelu) {
+                bits |= (z0 >= 0.0f ? (1u << e) : 0u) | (z1 >= 0.0f ? (2u << e) : 0u);
+              } else {
+                bits |= 3u << e;
+              }
+              pk[c2 * 16 + e / 2] = pack_bf16(apply_act<kAct>(z0), apply_act<kAct>(z1));
             }
-            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+          } else {
+#pragma unroll 2
+            for (int e = 0; e < 32; e += 2) {
+              float pv[2];
+#pragma unroll
+              for (int x = 0; x < 2; ++x) {
+                const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
+                                     zb + slope * static_cast<float>(e + x));
+                const bool keep = live && kept(p.mask, i, jb + e + x, p.seq_k);
+                const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
+                bits |= (keep && g) ? (1u << (e + x)) : 0u;
+                pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
+              }
+              pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+            }
           }
         }
         gmask[c2] = bits;
