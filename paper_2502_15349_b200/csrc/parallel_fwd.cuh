@@ -306,15 +306,23 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
         l_run += asum;
       } else {
         const float bias = p.bias + slope * static_cast<float>(cb) - slope * fi;
+        if (full) {  // compact fast path: no per-element mask tests
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          float e0 = apply_act<kAct>(s[c] * p.scale + bias + slope * static_cast<float>(c));
-          float e1 = apply_act<kAct>(s[c + 1] * p.scale + bias + slope * static_cast<float>(c + 1));
-          if (!full) {
+          for (int c = 0; c < 64; c += 2)
+            pk[c / 2] =
+                pack_bf16(apply_act<kAct>(s[c] * p.scale + bias + slope * static_cast<float>(c)),
+                          apply_act<kAct>(s[c + 1] * p.scale + bias +
+                                          slope * static_cast<float>(c + 1)));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; c += 2) {
+            float e0 = apply_act<kAct>(s[c] * p.scale + bias + slope * static_cast<float>(c));
+            float e1 =
+                apply_act<kAct>(s[c + 1] * p.scale + bias + slope * static_cast<float>(c + 1));
             if (!kept(p.mask, i, cb + c, p.seq_k)) e0 = 0.0f;
             if (!kept(p.mask, i, cb + c + 1, p.seq_k)) e1 = 0.0f;
+            pk[c / 2] = pack_bf16(e0, e1);
           }
-          pk[c / 2] = pack_bf16(e0, e1);
         }
       }
       // packed P of this key half over its own S columns (the PV MMA reads fwd_split_col)
