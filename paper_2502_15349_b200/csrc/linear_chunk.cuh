@@ -71,13 +71,14 @@ struct LinearParams {
 
 template <int DK>
 struct LinSmem {
-  static constexpr int kStages = DK == 128 ? 2 : 1;  // Q/K/V ring depth (smem bound at DK=256)
+  static constexpr int kStages = DK == 128 ? 2 : 1;   // Q/K ring depth (smem bound at DK=256)
+  static constexpr int kVStages = DK == 128 ? 3 : 2;  // V ring: released later (after O I), deeper
   static constexpr int kQBytes = kLinChunk * DK * 2;
   static constexpr int kVBytes = kLinChunk * kLinVB * 2;
   static constexpr int kQOff = 0;
   static constexpr int kKOff = kQOff + kStages * kQBytes;
   static constexpr int kVOff = kKOff + kStages * kQBytes;
-  static constexpr int kVwOff = kVOff + kStages * kVBytes;
+  static constexpr int kVwOff = kVOff + kVStages * kVBytes;
   static constexpr int kHbOff = kVwOff + kVBytes;
   static constexpr int kLOff = kHbOff + DK * kLinVB * 2;  // [2][128] cumsum log2 a, per parity
   static constexpr int kUOff = kLOff + 2 * kLinChunk * 4;  // [2][128] key/value-side scale
@@ -89,7 +90,7 @@ struct LinSmem {
   // ring: full[S], empty[S]; s_full qh_full oi_full[2] h_full scan_ready[2] (1 arrival) |
   // p_ready vw_ready h_scaled hb_ready scan_free[2] (8 row warps) | oi_empty[2] cp_ready[2] (4)
   static constexpr int kBarOff = kFlagOff + 16;
-  static constexpr int kNumBars = 2 * kStages + 17;
+  static constexpr int kNumBars = 2 * kStages + 17 + 2 * kVStages;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -147,6 +148,9 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   uint64_t* cp_ready = s_full + 11;      // [2]
   uint64_t* scan_ready = s_full + 13;    // [2]
   uint64_t* scan_free = s_full + 15;     // [2]
+  constexpr int kVSt = L::kVStages;
+  uint64_t* vfull = s_full + 17;         // [kVSt]: V of one chunk landed
+  uint64_t* vempty = vfull + kVSt;       // [kVSt]: that V may be overwritten
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -165,6 +169,10 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     mbar_init(&scan_ready[1], 1);
     mbar_init(&scan_free[0], 8);
     mbar_init(&scan_free[1], 8);
+    for (int i = 0; i < kVSt; ++i) {
+      mbar_init(&vfull[i], 1);
+      mbar_init(&vempty[i], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 13) tmem_alloc<512>(tmem_slot);
@@ -260,14 +268,17 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       // Q, K, V of chunk n (after the scan: the scan never waits on the ring)
       if (elect_one()) {
         mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
-        mbar_expect_tx(&full[st], 2 * L::kQBytes + L::kVBytes);
+        mbar_expect_tx(&full[st], 2 * L::kQBytes);
         for (int x = 0; x < DK / 64; ++x) {
           tma_load_4d(sQ + st * L::kQBytes + x * (kLinChunk * 128), &tm_q, &full[st], x * 64, t0,
                       h, b);
           tma_load_4d(sK + st * L::kQBytes + x * (kLinChunk * 128), &tm_k, &full[st], x * 64, t0,
                       h, b);
         }
-        tma_load_4d(sV + st * L::kVBytes, &tm_v, &full[st], vb * kLinVB, t0, h, b);
+        const int sv = n % kVSt;
+        mbar_wait(&vempty[sv], ((n / kVSt) & 1) ^ 1);
+        mbar_expect_tx(&vfull[sv], L::kVBytes);
+        tma_load_4d(sV + sv * L::kVBytes, &tm_v, &vfull[sv], vb * kLinVB, t0, h, b);
       }
       __syncwarp();
     }
@@ -288,7 +299,8 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         const uint32_t ph = n & 1;
         const int st = n % kStages;
         const uint32_t qa = aQ + st * L::kQBytes, ka = aK + st * L::kQBytes;
-        const uint32_t va = aV + st * L::kVBytes;
+        const int sv = n % kVSt;
+        const uint32_t va = aV + sv * L::kVBytes;
         mbar_wait(&full[st], (n / kStages) & 1);
         AF_LT(0, n);
         tc_fence_after();
@@ -317,7 +329,9 @@ __global__ void __launch_bounds__(kLinThreads, 1)
                    make_sdesc(ka + hh * 2 * (kLinChunk * 128) + kk * 2048, kLinChunk * 128, 1024),
                    make_sdesc(aVw + kk * 2048, 16384, 1024), id_h, (n > 0 || kk > 0));
         mma_commit(h_full);
+        mma_commit(&empty[st]);  // Q, K of this chunk: last read by the state update
         mbar_wait(p_ready, ph);
+        mbar_wait(&vfull[sv], (n / kVSt) & 1);
         AF_LT(2, n);
         tc_fence_after();
 #pragma unroll
@@ -325,7 +339,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           mma_ts(tmem + kColOI + ph * kLinVB, tmem + kColS + split_col_lin(kk),
                  make_sdesc(va + kk * 2048, 16384, 1024), id_oi, kk > 0);
         mma_commit(&oi_full[ph]);
-        mma_commit(&empty[st]);
+        mma_commit(&vempty[sv]);  // V: last read by O I (the row warps' Vw copy came earlier)
       }
     }
   } else if (warp >= 8) {
@@ -426,12 +440,13 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       }
       if (threadIdx.x == 0) AF_LT(4, n);
       // (b) Vw = diag(w * u_scale) V (this half's 4 granules; the previous state update is done)
-      mbar_wait(&full[st], (n / kStages) & 1);
+      const int sv = n % kVSt;
+      mbar_wait(&vfull[sv], (n / kVSt) & 1);
       if (threadIdx.x == 0) AF_LT(13, n);
 #pragma unroll
       for (int gq = 0; gq < 4; ++gq) {
         const int gidx = half * 4 + gq;
-        uint4 vv = *swz_row(sV + st * L::kVBytes, r, gidx);
+        uint4 vv = *swz_row(sV + sv * L::kVBytes, r, gidx);
         uint32_t* e = reinterpret_cast<uint32_t*>(&vv);
 #pragma unroll
         for (int q2 = 0; q2 < 4; ++q2)
