@@ -369,6 +369,7 @@ def run_gpu(args, key: str) -> dict | None:
     host = {k: v.cpu().pin_memory() for k, v in arrays.items()}
     hdo = dout.cpu().pin_memory() if w.backward else None
     out = pipe(host, hdo)
+    pipe(host, hdo, out=out)  # second warm-up: the chunk streams' allocator pools are populated
     barrier()
     h2d = sum(t.numel() * t.element_size() for t in host.values()) + \
         (hdo.numel() * hdo.element_size() if hdo is not None else 0)

@@ -97,9 +97,16 @@ typedef struct af_linear_desc {
 } af_linear_desc;
 
 /* o_t = q_scale * q_t h_t,  h_t = a_t h_{t-1} + (k_t * gate_t)^T v_t,  h_0 = 0.
- * final_state must be NULL (reserved).  Replaces engine.run_chunk_recurrent (engine.py:554). */
+ * final_state (may be NULL): fp32 [B, H, d_k, d_v] receives h_S, the state after the last token.
+ * Replaces engine.run_chunk_recurrent (engine.py:554). */
 int af_linear_fwd(const af_linear_desc* desc, const void* q, const void* k, const void* v,
                   void* o, float* final_state, void* stream);
+
+/* One generation step (desc->seq == 1): state <- a_t state + (k_t * gate_t)^T v_t (fp32
+ * [B, H, d_k, d_v], in place), o_t = q_scale * q_t state.  The body of engine.run_step_recurrent
+ * (engine.py:539-547) for a carried state, e.g. af_linear_fwd's final_state of the prompt. */
+int af_linear_step(const af_linear_desc* desc, const void* q, const void* k, const void* v,
+                   float* state, void* o, void* stream);
 
 size_t af_linear_bwd_workspace(const af_linear_desc* desc);
 

@@ -18,7 +18,7 @@ from .spec import (AttentionSpec, Dims, ExtraInput, ModificationFn, DirectRowNor
                    from_reference, BUILTIN_NAMES, BUILTIN_DIMS)
 from .plan import plan_parallel, plan_linear, ParallelPlan, LinearPlan
 from .api import (parallel_forward, parallel_backward, run_tiled_parallel, run_naive_parallel,
-                  linear_forward, linear_backward, run_chunk_recurrent, run_step_recurrent,
+                  linear_forward, linear_backward, linear_step, run_chunk_recurrent, run_step_recurrent,
                   autodiff_grads, bind, AttentionEngine, mla_decode)
 from . import api
 

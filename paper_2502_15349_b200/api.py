@@ -421,21 +421,54 @@ def _linear_qkv(plan: LinearPlan, arrays: dict):
             _pad_last(_as(v, _BF16), pv))
 
 
-def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = False):
+def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = False,
+                   return_state: bool = False):
     """Chunked linear template forward (K4) → O [B,H,S,Dv] bf16.  The decay factors of h_mod
-    and the k_mod gate are applied inside the kernel."""
+    and the k_mod gate are applied inside the kernel.  ``return_state=True`` also returns the
+    fp32 state after the last token, [B,H,Dk,Dv] (the recurrence's h_S, for ``linear_step``)."""
     spec = _spec(spec)
     plan = plan_linear(spec, chunk)
     q, k, v = _linear_qkv(plan, arrays)
     d = spec.dims
     o = torch.empty(d.batch, d.heads, d.seq_q, v.shape[-1], device=q.device, dtype=_BF16)
+    state = (torch.empty(d.batch, d.heads, q.shape[-1], v.shape[-1], device=q.device,
+                         dtype=torch.float32) if return_state else None)
     desc, _keep = _linear_desc(plan, arrays, q, k, v, o)
     rt.check(rt.lib().af_linear_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                    o.data_ptr(), None, _stream()), "af_linear_fwd")
+                                    o.data_ptr(), rt.ptr(state), _stream()), "af_linear_fwd")
     if o.shape[-1] != d.d_v:
         o = o[..., : d.d_v].contiguous()
     if check_nan:
         _check_nan(o, "chunk")
+    if return_state:
+        return o, state[..., : d.d_qk, : d.d_v].contiguous()
+    return o
+
+
+def linear_step(spec, arrays: dict, state: torch.Tensor) -> torch.Tensor:
+    """One generation step of the recurrent template (K4s): ``arrays`` hold ONE new token
+    (q/k/v [B,H,1,D], per-step extras [B|1,H|1,1,1]); ``state`` (fp32 [B,H,Dk,Dv], e.g. from
+    ``linear_forward(..., return_state=True)``) is advanced in place; returns o_t [B,H,1,Dv].
+    The body of engine.run_step_recurrent (engine.py:539-547) for a carried state."""
+    spec = _spec(spec)
+    d = spec.dims
+    if d.seq_q != 1 or d.seq_k != 1:
+        raise ShapeError("linear_step takes a one-token spec (seq = 1)", seq=d.seq_q)
+    plan = plan_linear(spec)
+    q, k, v = _need(arrays, "q"), _need(arrays, "k"), _need(arrays, "v")
+    _check_shape(q, (d.batch, d.heads, 1, d.d_qk), "q")
+    _check_shape(k, (d.batch, d.heads, 1, d.d_qk), "k")
+    _check_shape(v, (d.batch, d.heads, 1, d.d_v), "v")
+    qm, km, vm = _maps(plan)
+    q, k, v = (_as(_fmap(m, t), _BF16).contiguous() for m, t in ((qm, q), (km, k), (vm, v)))
+    if state.dtype != torch.float32 or tuple(state.shape) != (d.batch, d.heads, d.d_qk, d.d_v) \
+            or not state.is_contiguous() or not state.is_cuda:
+        raise ShapeError("state must be contiguous fp32 [B,H,Dk,Dv] on the GPU",
+                         got=tuple(state.shape))
+    o = torch.empty(d.batch, d.heads, 1, d.d_v, device=q.device, dtype=_BF16)
+    desc, _keep = _linear_desc(plan, arrays, q, k, v, o)
+    rt.check(rt.lib().af_linear_step(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                     state.data_ptr(), o.data_ptr(), _stream()), "af_linear_step")
     return o
 
 

@@ -23,6 +23,7 @@ struct LaArgs {
   const int64_t* x_st;
   float* dot;
   bool reverse;
+  float* final_state = nullptr;
 };
 
 StepTensor step_tensor(const float* ptr, const int64_t* st) {
@@ -76,6 +77,7 @@ int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
     p.x_ss = a.x_st[2];
   }
   p.dot = a.dot;
+  p.final_state = a.final_state;
   auto kern = linear_chunk_kernel<DK, kRev, kFac>;
   static bool attr = false;
   if (!attr) {
@@ -127,9 +129,8 @@ extern "C" int af_linear_fwd(const af_linear_desc* d, const void* q, const void*
   using namespace af;
   int st = validate_linear(d);
   if (st != AF_OK) return st;
-  AF_REQUIRE(final_state == nullptr, AF_ERR_UNSUPPORTED, "final_state output is not built yet");
   LaArgs a{q, k, v, d->q_stride, d->k_stride, d->v_stride, d->d_k, d->d_v, o, d->o_stride,
-           d->q_scale, true, false, nullptr, nullptr, nullptr, false};
+           d->q_scale, true, false, nullptr, nullptr, nullptr, false, final_state};
   return run_la(d, a, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -65,6 +65,7 @@ struct LinearParams {
   int64_t o_sb, o_sh, o_ss;
   const void* dot_x;    // optional bf16 X with element strides: dot[t] += X_t . o_t
   int64_t x_sb, x_sh, x_ss;
+  float* final_state;   // optional fp32 [B, H, dqk, dv]: the state after the last token (forward)
   float* dot;           // [dv/32 slots][B, H, S] fp32: one partial per 32-column slot, summed
                         // in slot order by linear_step_grads_kernel (deterministic)
 };
@@ -566,6 +567,24 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(hb_ready);
       if (threadIdx.x == 0) AF_LT(12, n);
+      if (!kReverse && p.final_state != nullptr && n == nchunks - 1) {
+        // the state after the last chunk (run_step_recurrent's h_S): fp32 [dk][dv] rows, this
+        // half's 32 columns of the CTA's 64-column value block
+#pragma unroll
+        for (int hh = 0; hh < kHalves; ++hh) {
+          const int dk = hh * 128 + r;
+          uint32_t hr[32];
+          tmem_ld32(tmem + lane_base + kColH + hh * kLinVB + half * 32, hr);
+          tmem_ld_wait();
+          float4* dst = reinterpret_cast<float4*>(
+              p.final_state + ((static_cast<int64_t>(b) * p.heads + h) * p.dqk + dk) * p.dv +
+              vb * kLinVB + half * 32);
+#pragma unroll
+          for (int v4 = 0; v4 < 8; ++v4)
+            dst[v4] = make_float4(__uint_as_float(hr[v4 * 4]), __uint_as_float(hr[v4 * 4 + 1]),
+                                  __uint_as_float(hr[v4 * 4 + 2]), __uint_as_float(hr[v4 * 4 + 3]));
+        }
+      }
     }
   }
 

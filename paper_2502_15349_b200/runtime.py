@@ -66,6 +66,7 @@ SIGNATURES: dict[str, tuple] = {
     "af_parallel_bwd": (C.c_int, [C.POINTER(ParallelDesc), P, P, P, P, P, P, P, P, P, P,
                                   C.c_size_t, P]),
     "af_linear_fwd": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P]),
+    "af_linear_step": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P]),
     "af_linear_bwd_workspace": (C.c_size_t, [C.POINTER(LinearDesc)]),
     "af_linear_bwd": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P, P, P, P, P, C.c_size_t,
                                 P]),  # (desc, q, k, v, dout, dq, dk, dv, d_factor**, d_gate, ws..)

@@ -86,3 +86,30 @@ def test_nonfactorable_h_mod_raises():
                            h_mod=S.mod("h * h", "h"), extra_inputs=base.extra_inputs)
     with pytest.raises(af.UnsupportedError):
         af.run_chunk_recurrent(spec, to_dev(oracle.generate(base, 0)))
+
+
+@pytest.mark.parametrize("name,dk,dv", [("retention-recurrent", 128, 128), ("mamba2-ssm", 64, 64),
+                                        ("gated-retention", 256, 256)])
+def test_prompt_state_then_decode_steps(name, dk, dv):
+    """linear_forward(return_state) over a prompt, then linear_step token by token, matches the
+    f64 stepwise recurrence (engine.run_step_recurrent) over the whole sequence, and the carried
+    state matches the chunked forward's final state over the longer sequence."""
+    from dataclasses import replace as dreplace
+    b, h, s, extra = 2, 3, 200, 3
+    full = S.builtin(name, batch=b, heads=h, seq=s + extra, d_qk=dk, d_v=dv)
+    a = oracle.generate(full, 8)
+    want = OR.step_forward(full, rounded(a))
+    prompt = S.builtin(name, batch=b, heads=h, seq=s, d_qk=dk, d_v=dv)
+
+    def cut(arr, lo, hi):
+        return {k: (v[:, :, lo:hi] if v.shape[2] > 1 else v) for k, v in arr.items()}
+
+    o, state = af.linear_forward(prompt, to_dev(cut(a, 0, s)), return_state=True)
+    assert state.shape == (b, h, dk, dv) and state.dtype == torch.float32
+    assert nw(o.double().cpu().numpy(), want[:, :, :s]) <= 2e-2
+    one = dreplace(prompt, dims=dreplace(prompt.dims, seq_q=1, seq_k=1))
+    for t in range(s, s + extra):
+        ot = af.linear_step(one, to_dev(cut(a, t, t + 1)), state)
+        assert nw(ot.double().cpu().numpy(), want[:, :, t:t + 1]) <= 2e-2, t
+    _, state_full = af.linear_forward(full, to_dev(a), return_state=True)
+    assert nw(state.double().cpu().numpy(), state_full.double().cpu().numpy()) <= 1e-2
