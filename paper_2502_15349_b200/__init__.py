@@ -21,5 +21,6 @@ from .api import (parallel_forward, parallel_backward, run_tiled_parallel, run_n
                   linear_forward, linear_backward, linear_step, run_chunk_recurrent, run_step_recurrent,
                   autodiff_grads, bind, AttentionEngine, mla_decode)
 from . import api
+from .emit import code_generation
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -187,3 +187,17 @@ def test_every_reference_fixture_lowers():
     for name in golden_cases():
         spec = _load(name)
         (P.plan_parallel if spec.pattern.value == "parallel" else P.plan_linear)(spec)
+
+
+def test_emit_is_deterministic_for_every_fixture():
+    """Kernel-dialect emission of the chosen B200 plan (lowering.code_generation's shape)."""
+    from conftest import golden_cases
+    import paper_2502_15349_b200 as af
+    for name in golden_cases():
+        spec = _load(name)
+        text = af.code_generation(spec)
+        assert text == af.code_generation(spec)
+        assert text.startswith(f'kernel "{spec.name}" template ') and text.rstrip().endswith("}")
+    from paper_2502_15349_b200 import configs
+    for key, make in configs.CONFIGS.items():
+        assert "tmem" in af.code_generation(make())
