@@ -51,9 +51,14 @@ struct MlaBwdParams {
 
 template <int D, int DV, bool kShared>
 struct MlaScoresSmem {
-  static constexpr int kStages = 4;
   static constexpr int kBox = 128 * 128;              // [128 rows][64 bf16]
   static constexpr int kKB = D / 64, kVB = DV / 64;   // boxes per K / V row tile
+  // ring depth: whatever shared memory the resident K (and V) tile leaves (the streamed Q / dO
+  // boxes are consumed in ~256 cycles each, so the ring depth sets the bytes in flight)
+  static constexpr int kStages =
+      (225 * 1024 - (kKB + (kShared ? 0 : kVB)) * kBox - 4096) / kBox > 12
+          ? 12
+          : (225 * 1024 - (kKB + (kShared ? 0 : kVB)) * kBox - 4096) / kBox;
   static constexpr int kKOff = 0;                     // the resident K (and V) tile
   static constexpr int kVOff = kKOff + kKB * kBox;
   static constexpr int kRingOff = kVOff + (kShared ? 0 : kVB) * kBox;  // streamed Q / dO boxes
