@@ -522,8 +522,13 @@ AF_DEVICE void load_row_words(const __nv_bfloat16* src, bool live, uint32_t (&w)
   }
 }
 
+// K2b runs 16 row warps (four per TMEM lane quarter, 32 score columns each): its row math (P
+// recompute + dS) is the critical path between the MMAs, and more warps hide the SFU latency.
+constexpr int kDqRowWarps = 16;
+constexpr int kDqThreads = 32 * (kDqRowWarps + 2);
+
 template <int D, int DV, int kFamily, int kAct>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kDqThreads, 1)
     parallel_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, const ParallelBwdParams p,
                            const __nv_bfloat16* __restrict__ q,
@@ -559,21 +564,23 @@ __global__ void __launch_bounds__(320, 1)
   const TileBand band = key_band(p.mask, q0, min(p.seq_q, q0 + kBlockM), p.seq_k);
   const int nk = band.jb_hi - band.jb_lo;
 
-  if (warp == 8 && lane_id() == 0) {
+  constexpr int kRW = kDqRowWarps, kTmaW = kRW, kMmaW = kRW + 1;
+  constexpr int kCpw = kBlockN / (kRW / 4);  // score columns per row warp (32)
+  if (warp == kTmaW && lane_id() == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(qa_ready, 8);
+    mbar_init(qa_ready, kRW);
     for (int x = 0; x < 2; ++x) {
       mbar_init(&s_full[x], 1);
       mbar_init(&dp_full[x], 1);
-      mbar_init(&ds_ready[x], 4);
+      mbar_init(&ds_ready[x], kRW / 2);
     }
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaW) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -581,7 +588,7 @@ __global__ void __launch_bounds__(320, 1)
   // S [0,128) | dP [128,256) | dQ [256,256+D) | Q^A [384,384+D/2) | dO^A [448,448+DV/2)
   constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColQA = 384, kColOA = 448;
 
-  if (warp == 8) {
+  if (warp == kTmaW) {
     // ───────────── TMA producer: K/V ring ─────────────
     if (elect_one() && nk > 0) {
       for (int n = 0; n < nk; ++n) {
@@ -598,7 +605,7 @@ __global__ void __launch_bounds__(320, 1)
                            kv0, hk, b, kEvictLast);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaW) {
     // ───────────── MMA issuer ─────────────
     if (elect_one() && nk > 0) {
       // The 128 key columns are processed as two 64-wide halves x = 0, 1 with their own
@@ -639,7 +646,9 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
             const int kk = x * 4 + k4;
-            mma_ts(tmem + kColDQ, tmem + kColS + split_col(kk),
+            // packed dS of keys [16kk, 16kk + 16): the row warp owning those columns stored it
+            // at the start of its own column range
+            mma_ts(tmem + kColDQ, tmem + kColS + kCpw * (kk / (kCpw / 16)) + 8 * (kk % (kCpw / 16)),
                    make_sdesc(aK + s * L::kKBytes + kk * 16 * 128, kBlockN * 128, 1024), id_dq,
                    (n > 0 || kk > 0));
           }
@@ -658,37 +667,40 @@ __global__ void __launch_bounds__(320, 1)
   } else {
     // ───────────── query-row warps ─────────────
     const int wq = warp % 4;
-    const int half = warp / 4;
+    const int sub = warp / 4;              // column slice of this warp
+    const int cb = sub * kCpw;
+    const int half = cb / 64;              // MMA column half it belongs to
     const int row = wq * 32 + static_cast<int>(lane_id());
     const int i = q0 + row;
     const bool live = i < p.seq_q;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const int cb = half * 64;
-    const uint32_t pcol = half * 64;
-    // Park this row's Q and dO (bf16) in TMEM as the K-major A operands: warp half h writes the
-    // packed words [h*D/4, (h+1)*D/4) of Q^A and [h*DV/4, ...) of dO^A.
+    const uint32_t pcol = cb;
+    constexpr int kNP = kCpw / 32;         // 32-column pieces per warp
+    // Park this row's Q and dO (bf16) in TMEM as the K-major A operands: the four warps of a
+    // lane quarter each write a quarter of the packed words (D/8 of Q^A, DV/8 of dO^A).
     {
+      static_assert(kRW == 16, "parking split assumes four warps per lane quarter");
       const __nv_bfloat16* qrow =
-          q + b * q_sb + h * q_sh + static_cast<int64_t>(live ? i : 0) * q_ss + half * (D / 2);
+          q + b * q_sb + h * q_sh + static_cast<int64_t>(live ? i : 0) * q_ss + sub * (D / 4);
       const __nv_bfloat16* orow = dout + b * do_sb + h * do_sh +
-                                  static_cast<int64_t>(live ? i : 0) * do_ss + half * (DV / 2);
+                                  static_cast<int64_t>(live ? i : 0) * do_ss + sub * (DV / 4);
       if constexpr (D == 128) {
-        uint32_t w[32];
-        load_row_words<32>(qrow, live, w);
-        tmem_st32(tmem + lane_base + kColQA + half * 32, w);
-      } else {
         uint32_t w[16];
         load_row_words<16>(qrow, live, w);
-        tmem_st16(tmem + lane_base + kColQA + half * 16, w);
+        tmem_st16(tmem + lane_base + kColQA + sub * 16, w);
+      } else {
+        uint32_t w[8];
+        load_row_words<8>(qrow, live, w);
+        tmem_st8(tmem + lane_base + kColQA + sub * 8, w);
       }
       if constexpr (DV == 128) {
-        uint32_t w[32];
-        load_row_words<32>(orow, live, w);
-        tmem_st32(tmem + lane_base + kColOA + half * 32, w);
-      } else {
         uint32_t w[16];
         load_row_words<16>(orow, live, w);
-        tmem_st16(tmem + lane_base + kColOA + half * 16, w);
+        tmem_st16(tmem + lane_base + kColOA + sub * 16, w);
+      } else {
+        uint32_t w[8];
+        load_row_words<8>(orow, live, w);
+        tmem_st8(tmem + lane_base + kColOA + sub * 8, w);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -708,11 +720,11 @@ __global__ void __launch_bounds__(320, 1)
       const bool fullblk = tile_fully_kept(p.mask, q0, c0, p.seq_q, p.seq_k);
       mbar_wait(&s_full[half], n & 1);
       tc_fence_after();
-      uint32_t pk[32];
-      uint32_t gk[32];  // soft-cap derivative factors (kActSoftcap only)
-      uint32_t gmask[2];
+      uint32_t pk[16 * kNP];
+      uint32_t gk[16 * kNP];  // soft-cap derivative factors (kActSoftcap only)
+      uint32_t gmask[kNP];
 #pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
+      for (int c2 = 0; c2 < kNP; ++c2) {
         uint32_t sr[32];
         tmem_ld32(tmem + lane_base + kColS + cb + c2 * 32, sr);
         tmem_ld_wait();
@@ -805,9 +817,9 @@ __global__ void __launch_bounds__(320, 1)
       }
       mbar_wait(&dp_full[half], n & 1);
       tc_fence_after();
-      uint32_t dsk[32];
+      uint32_t dsk[16 * kNP];
 #pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
+      for (int c2 = 0; c2 < kNP; ++c2) {
         uint32_t dr[32];
         tmem_ld32(tmem + lane_base + kColDP + cb + c2 * 32, dr);
         tmem_ld_wait();
@@ -815,36 +827,49 @@ __global__ void __launch_bounds__(320, 1)
                                      gk + c2 * 16);
       }
       // dS (packed) over this warp's own S columns: A operand of dQ += dS K
-      tmem_st32(tmem + lane_base + kColS + pcol, dsk);
+      if constexpr (kNP == 2)
+        tmem_st32(tmem + lane_base + kColS + pcol, *reinterpret_cast<uint32_t(*)[32]>(dsk));
+      else
+        tmem_st16(tmem + lane_base + kColS + pcol, *reinterpret_cast<uint32_t(*)[16]>(dsk));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&ds_ready[half]);
     }
-    // ───────────── epilogue: dQ = tau * acc (bf16); each warp stores D/2 columns ─────────────
+    // ───────────── epilogue: dQ = tau * acc (bf16); each warp stores D/4 columns ─────────────
     if (nk > 0) {
       mbar_wait(acc_full, 0);
       tc_fence_after();
     }
     __nv_bfloat16* dqrow = reinterpret_cast<__nv_bfloat16*>(dq) + b * q_sb + h * q_sh +
-                           static_cast<int64_t>(live ? i : 0) * q_ss + half * (D / 2);
-#pragma unroll 1
-    for (int c = 0; c < D / 64; ++c) {
+                           static_cast<int64_t>(live ? i : 0) * q_ss + sub * (D / 4);
+    if constexpr (D / 4 == 32) {
       uint32_t r[32];
       if (nk > 0) {
-        tmem_ld32(tmem + lane_base + kColDQ + half * (D / 2) + c * 32, r);
+        tmem_ld32(tmem + lane_base + kColDQ + sub * 32, r);
         tmem_ld_wait();
       } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e) r[e] = 0u;
       }
-      if (live) store_row_bf16<32>(dqrow + c * 32, r, p.scale);
+      if (live) store_row_bf16<32>(dqrow, r, p.scale);
+    } else {
+      static_assert(D / 4 == 16, "dQ epilogue slice");
+      uint32_t r[16];
+      if (nk > 0) {
+        tmem_ld16(tmem + lane_base + kColDQ + sub * 16, r);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[e] = 0u;
+      }
+      if (live) store_row_bf16<16>(dqrow, r, p.scale);
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kMmaW) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }

@@ -53,7 +53,7 @@ int launch_bwd(const BwdLaunch& a) {
     }
     dim3 grid((a.d->seq_q + kBlockM - 1) / kBlockM, a.d->batch * a.d->heads_q);
     ::af::note_launch();
-    kern<<<grid, 320, L::kTotal, a.s>>>(
+    kern<<<grid, kDqThreads, L::kTotal, a.s>>>(
         a.tk, a.tv, a.p, static_cast<const __nv_bfloat16*>(a.q),
         static_cast<const __nv_bfloat16*>(a.dout), a.d->q_stride[0], a.d->q_stride[1],
         a.d->q_stride[2], a.d->o_stride[0], a.d->o_stride[1], a.d->o_stride[2], a.dq, a.lse2,
