@@ -134,8 +134,12 @@ struct BwdKVSmem {
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
 
+// K2a also runs 16 row warps (four per TMEM lane quarter, 32 query columns each).
+constexpr int kKvRowWarps = 16;
+constexpr int kKvThreads = 32 * (kKvRowWarps + 2);
+
 template <int D, int DV, int kFamily, int kAct>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(kKvThreads, 1)
     parallel_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q,
                              const __grid_constant__ CUtensorMap tm_k,
                              const __grid_constant__ CUtensorMap tm_v,
@@ -177,7 +181,10 @@ __global__ void __launch_bounds__(320, 1)
   const int tiles_per_head = qt_hi - qt_lo;
   const int niter = tiles_per_head * group;
 
-  if (warp == 8 && lane_id() == 0) {
+  constexpr int kRW = kKvRowWarps, kTmaW = kRW, kMmaW = kRW + 1;
+  constexpr int kCpw = kBlockM / (kRW / 4);  // query columns per row warp (32)
+  constexpr int kNP = kCpw / 32;
+  if (warp == kTmaW && lane_id() == 0) {
     mbar_init(kv_full, 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -185,19 +192,19 @@ __global__ void __launch_bounds__(320, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(dp_full, 1);
-    mbar_init(p_ready, 8);
-    mbar_init(ds_ready, 8);
+    mbar_init(p_ready, kRW);
+    mbar_init(ds_ready, kRW);
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == kMmaW) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t kColS = 0, kColDP = 128, kColDV = 256, kColDK = 256 + DV;
 
-  if (warp == 8) {
+  if (warp == kTmaW) {
     // ───────────── TMA producer ─────────────
     if (elect_one() && niter > 0) {
       mbar_expect_tx(kv_full, L::kKBytes + L::kVBytes);
@@ -236,7 +243,7 @@ __global__ void __launch_bounds__(320, 1)
             : "memory");
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaW) {
     // ───────────── MMA issuer ─────────────
     if (elect_one() && niter > 0) {
       constexpr uint32_t id_s = make_idesc_bf16(kBlockN, kBlockM, false, false);   // S^T = K Q^T
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kBlockM / 16; ++kk)
-          mma_ts(tmem + kColDV, tmem + kColS + split_col(kk),
+          mma_ts(tmem + kColDV, tmem + kColS + (kCpw * (kk / (kCpw / 16)) + 8 * (kk % (kCpw / 16))),
                  make_sdesc(aO + s * L::kOBytes + kk * 16 * 128, kBlockM * 128, 1024), id_dv,
                  (n > 0 || kk > 0));
         if (n + 1 < niter) {
@@ -290,7 +297,7 @@ __global__ void __launch_bounds__(320, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kBlockM / 16; ++kk)
-          mma_ts(tmem + kColDK, tmem + kColDP + split_col(kk),
+          mma_ts(tmem + kColDK, tmem + kColDP + (kCpw * (kk / (kCpw / 16)) + 8 * (kk % (kCpw / 16))),
                  make_sdesc(aQ + s * L::kQBytes + kk * 16 * 128, kBlockM * 128, 1024), id_dk,
                  (n > 0 || kk > 0));
         mma_commit(&empty[s]);
@@ -301,12 +308,12 @@ __global__ void __launch_bounds__(320, 1)
   } else {
     // ───────────── key-row warps ─────────────
     const int wq = warp % 4;
-    const int half = warp / 4;
+    const int sub = warp / 4;        // query-column slice of this warp
     const int row = wq * 32 + static_cast<int>(lane_id());
     const int j = k0 + row;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const int cb = half * 64;
-    const uint32_t pcol = half * 64;
+    const int cb = sub * kCpw;
+    const uint32_t pcol = cb;
     const float fj = static_cast<float>(j);
     int hi_ = 0, qt_ = 0;
     for (int n = 0; n < niter; ++n) {
@@ -327,11 +334,11 @@ __global__ void __launch_bounds__(320, 1)
 
       mbar_wait(s_full, n & 1);
       tc_fence_after();
-      uint32_t pk[32];
-      uint32_t gk[32];  // soft-cap derivative factors (kActSoftcap only)
-      uint32_t gmask[2];
+      uint32_t pk[16 * kNP];
+      uint32_t gk[16 * kNP];  // soft-cap derivative factors (kActSoftcap only)
+      uint32_t gmask[kNP];
 #pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
+      for (int c2 = 0; c2 < kNP; ++c2) {
         uint32_t sr[32];
         tmem_ld32(tmem + lane_base + kColS + cb + c2 * 32, sr);
         tmem_ld_wait();
@@ -434,7 +441,10 @@ __global__ void __launch_bounds__(320, 1)
         }
         gmask[c2] = bits;
       }
-      tmem_st32(tmem + lane_base + kColS + pcol, pk);
+      if constexpr (kNP == 2)
+        tmem_st32(tmem + lane_base + kColS + pcol, *reinterpret_cast<uint32_t(*)[32]>(pk));
+      else
+        tmem_st16(tmem + lane_base + kColS + pcol, *reinterpret_cast<uint32_t(*)[16]>(pk));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -442,35 +452,41 @@ __global__ void __launch_bounds__(320, 1)
 
       mbar_wait(dp_full, n & 1);
       tc_fence_after();
-      uint32_t dsk[32];
+      uint32_t dsk[16 * kNP];
 #pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2) {
+      for (int c2 = 0; c2 < kNP; ++c2) {
         uint32_t dr[32];
         tmem_ld32(tmem + lane_base + kColDP + cb + c2 * 32, dr);
         tmem_ld_wait();
         make_ds<kFamily, kAct, false>(pk + c2 * 16, dr, del_s + c2 * 32, 0.0f, gmask[c2],
                                       dsk + c2 * 16, gk + c2 * 16);
       }
-      tmem_st32(tmem + lane_base + kColDP + pcol, dsk);
+      if constexpr (kNP == 2)
+        tmem_st32(tmem + lane_base + kColDP + pcol, *reinterpret_cast<uint32_t(*)[32]>(dsk));
+      else
+        tmem_st16(tmem + lane_base + kColDP + pcol, *reinterpret_cast<uint32_t(*)[16]>(dsk));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(ds_ready);
     }
-    // ───────────── epilogue: warps 0-3 store dV rows, warps 4-7 store dK rows ─────────────
+    // ───────────── epilogue: slices 0-1 store dV rows, slices 2-3 store dK rows ─────────────
     if (niter > 0) {
       mbar_wait(acc_full, 0);
       tc_fence_after();
     }
     const bool live = j < p.seq_k;
-    const int ncol = half == 0 ? DV : D;
-    const uint32_t col0 = half == 0 ? kColDV : kColDK;
-    const float mul = half == 0 ? 1.0f : p.scale;
+    const bool is_v = sub < (kRW / 8);
+    const int part = is_v ? sub : sub - kRW / 8;  // which half of the dV / dK columns
+    const int ncol = (is_v ? DV : D) / (kRW / 8);
+    const uint32_t col0 = (is_v ? kColDV : kColDK) + part * ncol;
+    const float mul = is_v ? 1.0f : p.scale;
     __nv_bfloat16* dst =
-        half == 0 ? reinterpret_cast<__nv_bfloat16*>(p.dv) + b * p.dv_stride_b +
-                        hk * p.dv_stride_h + static_cast<int64_t>(live ? j : 0) * p.dv_stride_s
-                  : reinterpret_cast<__nv_bfloat16*>(p.dk) + b * p.dk_stride_b +
-                        hk * p.dk_stride_h + static_cast<int64_t>(live ? j : 0) * p.dk_stride_s;
+        (is_v ? reinterpret_cast<__nv_bfloat16*>(p.dv) + b * p.dv_stride_b +
+                    hk * p.dv_stride_h + static_cast<int64_t>(live ? j : 0) * p.dv_stride_s
+              : reinterpret_cast<__nv_bfloat16*>(p.dk) + b * p.dk_stride_b +
+                    hk * p.dk_stride_h + static_cast<int64_t>(live ? j : 0) * p.dk_stride_s) +
+        part * ncol;
 #pragma unroll 1
     for (int c = 0; c < ncol / 32; ++c) {
       uint32_t r[32];
@@ -487,7 +503,7 @@ __global__ void __launch_bounds__(320, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kMmaW) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }

@@ -40,7 +40,8 @@ int launch_bwd(const BwdLaunch& a) {
     }
     dim3 grid((a.d->seq_k + kBlockN - 1) / kBlockN, a.d->batch * a.d->heads_kv);
     ::af::note_launch();
-    kern<<<grid, 320, L::kTotal, a.s>>>(a.tq, a.tk, a.tv, a.tdo, a.p, a.lse2, a.delta, a.pad);
+    kern<<<grid, kKvThreads, L::kTotal, a.s>>>(a.tq, a.tk, a.tv, a.tdo, a.p, a.lse2, a.delta,
+                                               a.pad);
     AF_CUDA_CHECK(cudaGetLastError());
   }
   {

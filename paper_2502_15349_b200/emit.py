@@ -92,9 +92,10 @@ def _parallel(spec: AttentionSpec) -> list[str]:
                   "  }"]
     else:
         lines += ["  backward atomic_free {",
-                  "    kernel K2a parallel_bwd_dkdv_kernel cta 320 grid key_tiles x b*heads_kv "
+                  "    kernel K2a parallel_bwd_dkdv_kernel cta 576 (16 row warps) grid key_tiles x "
+                  "b*heads_kv "
                   "{ tmem S^T | dP^T | dV | dK; }",
-                  "    kernel K2b parallel_bwd_dq_kernel cta 320 grid q_tiles x b*heads "
+                  "    kernel K2b parallel_bwd_dq_kernel cta 576 (16 row warps) grid q_tiles x b*heads "
                   "{ tmem S | dP | dQ | Q^A | dO^A; 64-key column halves; }",
                   "  }"]
     lines.append("}")
