@@ -43,11 +43,26 @@ int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o
 }
 
 namespace {
+// KV splits per (batch, value half): one CTA per SM (TMEM / smem), so the step time is
+// waves x blocks-per-CTA; pick the split count minimising it (plus a fixed per-CTA cost of
+// ~4 key blocks for the Q load, pipeline fill and partial-O write), e.g. B=16 on 148 SMs gives
+// 9 splits = 288 CTAs in two waves rather than 10 = 320 CTAs in three.
 int decode_splits(const af_mla_desc* d) {
-  const int ctas_per_split = d->batch * 2;
-  int splits = (2 * sm_count() + ctas_per_split - 1) / ctas_per_split;  // ~2 waves of CTAs
-  splits = std::max(1, std::min(splits, (d->seq_k + MlaTile<true>::kN - 1) / MlaTile<true>::kN));
-  return splits;
+  const int sms = sm_count();
+  const int blocks = (d->seq_k + MlaTile<true>::kN - 1) / MlaTile<true>::kN;
+  const int max_splits = std::max(1, std::min(blocks, 8 * sms / (2 * d->batch) + 1));
+  int best = 1;
+  long best_cost = -1;
+  for (int s = 1; s <= max_splits; ++s) {
+    const long ctas = 2L * d->batch * s;
+    const long waves = (ctas + sms - 1) / sms;
+    const long cost = waves * ((blocks + s - 1) / s + 4);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
 }
 }  // namespace
 

@@ -86,8 +86,12 @@ AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float
     const float dp0 = __uint_as_float(dr[e]), dp1 = __uint_as_float(dr[e + 1]);
     float ds0, ds1;
     if constexpr (kFamily == kFamilySoftmax) {
-      ds0 = p0 * (dp0 - (kRowDelta ? del_row : del_col[e]));
-      ds1 = p1 * (dp1 - (kRowDelta ? del_row : del_col[e + 1]));
+      // ds = p (dP - delta): FADD2 + FMUL2 per pair
+      const float2 t = fadd2(make_float2(dp0, dp1),
+                             kRowDelta ? splat2(-del_row) : make_float2(-del_col[e], -del_col[e + 1]));
+      const float2 d2 = fmul2(make_float2(p0, p1), t);
+      ds0 = d2.x;
+      ds1 = d2.y;
       if constexpr (kAct == kActSoftcap) {
         ds0 *= bf16_lo(gk[e / 2]);
         ds1 *= bf16_hi(gk[e / 2]);
@@ -383,13 +387,17 @@ __global__ void __launch_bounds__(kKvThreads, 1)
           if (fullblk) {
 #pragma unroll
             for (int e = 0; e < 32; e += 4) {
+              // x = s * scale - lse: one FFMA2 per pair (the negation is an operand modifier)
               const float4 l4 = *reinterpret_cast<const float4*>(lse_s + c2 * 32 + e);
-              pk[c2 * 16 + e / 2] =
-                  pack_bf16(bwd_exp2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x), e),
-                            bwd_exp2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y), e));
-              pk[c2 * 16 + e / 2 + 1] =
-                  pack_bf16(bwd_exp2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z), e + 2),
-                            bwd_exp2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w), e + 2));
+              const float2 sc2 = splat2(p.scale_log2);
+              const float2 x01 =
+                  ffma2(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2,
+                        make_float2(-l4.x, -l4.y));
+              const float2 x23 =
+                  ffma2(make_float2(__uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3])), sc2,
+                        make_float2(-l4.z, -l4.w));
+              pk[c2 * 16 + e / 2] = pack_bf16(bwd_exp2(x01.x, e), bwd_exp2(x01.y, e));
+              pk[c2 * 16 + e / 2 + 1] = pack_bf16(bwd_exp2(x23.x, e + 2), bwd_exp2(x23.y, e + 2));
             }
           } else {
 #pragma unroll
@@ -783,10 +791,11 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         } else if constexpr (kFamily == kFamilySoftmax) {
           if (fullblk) {
 #pragma unroll
-            for (int e = 0; e < 32; e += 2)
-              pk[c2 * 16 + e / 2] =
-                  pack_bf16(bwd_exp2(fmaf(__uint_as_float(sr[e]), p.scale_log2, -l2), e),
-                            bwd_exp2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l2), e));
+            for (int e = 0; e < 32; e += 2) {
+              const float2 x = ffma2(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])),
+                                     splat2(p.scale_log2), splat2(-l2));
+              pk[c2 * 16 + e / 2] = pack_bf16(bwd_exp2(x.x, e), bwd_exp2(x.y, e));
+            }
           } else {
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {

@@ -131,3 +131,11 @@ extern "C" int af_parallel_fwd(const af_parallel_desc* d, const void* q, const v
   set_error("bf16 parallel forward: head dims (%d, %d) not instantiated", d->d_qk, d->d_v);
   return AF_ERR_UNSUPPORTED;
 }
+
+#ifdef AF_FWD_TRACE
+extern "C" int af_debug_fwd_trace(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, af::g_fwd_trace, n * sizeof(unsigned long long)) == cudaSuccess
+             ? 0
+             : 1;
+}
+#endif

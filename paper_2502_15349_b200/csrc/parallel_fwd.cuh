@@ -21,6 +21,26 @@
 
 namespace af {
 
+// Developer timeline trace (-DAF_FWD_TRACE): SM clock stamps of one CTA's row warps / MMA warp,
+// read back with af_debug_fwd_trace.  Compiled out of the product build.
+#ifdef AF_FWD_TRACE
+__device__ unsigned long long g_fwd_trace[9 * 64 * 6 + 1];
+#define AF_TRACE(slot, n, ev)                                                              \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && blockIdx.y == 37 && lane_id() == 0 && (n) < 64)                \
+      g_fwd_trace[((slot) * 64 + (n)) * 6 + (ev)] = clock64();                             \
+  } while (0)
+#else
+#define AF_TRACE(slot, n, ev) \
+  do {                        \
+  } while (0)
+#endif
+#ifndef AF_FWD_TREEMAX
+#define AF_FWD_TREEMAX 1
+#endif
+#ifndef AF_FWD_EARLY_P
+#define AF_FWD_EARLY_P 1
+#endif
 #ifndef AF_EXP2_POLY_MASK
 #define AF_EXP2_POLY_MASK 14  // column pairs with (c & mask) == 0 use exp2_poly: 14 -> 12.5 %
 #endif
@@ -39,18 +59,22 @@ struct FwdSmem {
   static constexpr int kVOff = kKOff + kStages * kKBytes;
   static constexpr int kBarOff = kVOff + kStages * kVBytes;
   // barriers: q_full, k_full[S], k_empty[S], v_full[S], v_empty[S], s_full[2], p_full[2], o_done[2]
-  static constexpr int kNumBars = 1 + 4 * kStages + 6;
+  static constexpr int kNumBars = 1 + 4 * kStages + 8;  // + p_half[2]
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kRowSumOff = kTmemSlotOff + 16;  // [2 tiles][2 halves][128] fp32
-  static constexpr int kTotal = kRowSumOff + 2 * 2 * 128 * 4 + 1024;  // + alignment slack
+  static constexpr int kRowMaxOff = kRowSumOff + 2 * 2 * 128 * 4;  // [2 bufs][2][2][128] fp32
+  static constexpr int kTotal = kRowMaxOff + 2 * 2 * 2 * 128 * 4 + 1024;  // + alignment slack
 };
 
-// Non-softmax families have no running row max, so each score row is split over two warps
-// (64 key columns each; 16 row warps): twice the warps to hide the SFU / issue latency of the
-// activation, with only the abssum row sum combined once at the end.  Softmax keeps one warp per
-// row (its max / rescale protocol is per row).
+// Each score row is split over two warps (64 key columns each; 16 row warps): twice the warps
+// per scheduler to hide the SFU / issue latency of the row epilogue, which otherwise leaves the
+// tensor pipe waiting for P.  Softmax exchanges the block row max between the two warps of a row
+// once per key block (named barrier per warp pair); row sums are combined once at the end.
+#ifndef AF_FWD_SOFTMAX_SPLIT
+#define AF_FWD_SOFTMAX_SPLIT 1  // swept: 2 (16 row warps) is no faster for softmax
+#endif
 __host__ __device__ constexpr int fwd_row_split(int family) {
-  return family == kFamilySoftmax ? 1 : 2;
+  return family == kFamilySoftmax ? AF_FWD_SOFTMAX_SPLIT : 2;
 }
 __host__ __device__ constexpr int fwd_threads(int family) {
   return 32 * (8 * fwd_row_split(family) + 2);
@@ -130,8 +154,10 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
   uint64_t* s_full = v_empty + kStages;
   uint64_t* p_full = s_full + 2;
   uint64_t* o_done = p_full + 2;
+  uint64_t* p_half = o_done + 2;  // first 64 keys of P published (one-warp softmax rows)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
   float* sRowSum = reinterpret_cast<float*>(smem + L::kRowSumOff);
+  float* sRowMax = reinterpret_cast<float*>(smem + L::kRowMaxOff);
   constexpr int kSplit = fwd_row_split(kFamily);
   constexpr int kTmaWarp = 8 * kSplit, kMmaWarp = 8 * kSplit + 1;
 
@@ -161,6 +187,7 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
       mbar_init(&s_full[t], 1);
       mbar_init(&p_full[t], 4 * kSplit);  // one arrival per row warp
       mbar_init(&o_done[t], 1);
+      mbar_init(&p_half[t], 4);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tm_q);
@@ -219,16 +246,33 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
         }
         mma_commit(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int n) {
+      // PV over key slices [k_lo, k_hi) of the block (16 keys per MMA)
+      auto issue_pv_part = [&](int t, int n, int k_lo, int k_hi) {
         const int s = n % kStages;
         const uint32_t d_tmem = tmem + 2 * kBlockN + t * DV;
         const uint32_t p_tmem = tmem + t * kBlockN;
 #pragma unroll
-        for (int kk = 0; kk < kBlockN / 16; ++kk) {
+        for (int kk = k_lo; kk < k_hi; ++kk) {
           const uint64_t bdesc =
               make_sdesc(sv_addr + s * L::kVBytes + kk * 16 * 128, kBlockN * 128, 1024);
           mma_ts(d_tmem, p_tmem + (kSplit == 2 ? fwd_split_col(kk) : kk * 8), bdesc, idesc_o,
                  (n > 0 || kk > 0) ? 1u : 0u);
+        }
+      };
+      // One-warp softmax rows publish P in two halves: the first half of PV starts while the
+      // row warps are still exponentiating the second half.
+      auto wait_p_and_pv = [&](int t, int n) {
+        if constexpr (kSplit == 1 && AF_FWD_EARLY_P) {
+          mbar_wait(&p_half[t], n & 1);
+          tc_fence_after();
+          issue_pv_part(t, n, 0, kBlockN / 32);
+          mbar_wait(&p_full[t], n & 1);
+          tc_fence_after();
+          issue_pv_part(t, n, kBlockN / 32, kBlockN / 16);
+        } else {
+          mbar_wait(&p_full[t], n & 1);
+          tc_fence_after();
+          issue_pv_part(t, n, 0, kBlockN / 16);
         }
         mma_commit(&o_done[t]);
       };
@@ -245,17 +289,16 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
         const int s1 = (n + 1) % kStages;
         const uint32_t ph1 = ((n + 1) / kStages) & 1;
         mbar_wait(&v_full[s], ph);
-        mbar_wait(&p_full[0], n & 1);
-        tc_fence_after();
-        issue_pv(0, n);
+        AF_TRACE(8, n, 0);
+        wait_p_and_pv(0, n);
+        AF_TRACE(8, n, 1);
         if (more) {
           mbar_wait(&k_full[s1], ph1);
           tc_fence_after();
           issue_s(0, n + 1);
         }
-        mbar_wait(&p_full[1], n & 1);
-        tc_fence_after();
-        issue_pv(1, n);
+        wait_p_and_pv(1, n);
+        AF_TRACE(8, n, 2);
         mma_commit(&v_empty[s]);
         if (more) {
           issue_s(1, n + 1);
@@ -277,6 +320,108 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
     const float slope = (p.slope != nullptr) ? p.slope[h] : 0.0f;
     const float fi = static_cast<float>(i);
     float l_run = 0.0f;
+    float m_run = -INFINITY;  // softmax: running max (log2 units), identical in both row halves
+    const int pair_bar = 3 + t * 4 + wq;  // named barrier of the two warps sharing these rows
+    if constexpr (kFamily == kFamilySoftmax) {
+      constexpr bool kCap = kAct == kActSoftcap;
+      const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
+      for (int n = 0; n < nk; ++n) {
+        const int c0 = (band.jb_lo + n) * kBlockN;
+        const int cb = c0 + ch * 64;
+        mbar_wait(&s_full[t], n & 1);
+        tc_fence_after();
+        uint32_t sr[64];
+        tmem_ld32(s_tmem, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        tmem_ld32(s_tmem + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        tmem_ld_wait();
+        float* s = reinterpret_cast<float*>(sr);
+        const bool full = block_fully_kept(p.mask, r0, c0, p.seq_k);
+        const bool fast = !kCap && full && p.scale_log2 > 0.0f;
+        float bmax = -INFINITY;
+        if (fast) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) bmax = fmaxf(bmax, s[c]);
+          bmax *= p.scale_log2;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            const float x = kCap ? cap_out * tanh_precise(cap_in * s[c]) : s[c] * p.scale_log2;
+            s[c] = (full || kept(p.mask, i, cb + c, p.seq_k)) ? x : -INFINITY;
+            bmax = fmaxf(bmax, s[c]);
+          }
+        }
+        // block row max over both halves (double-buffered slot: the partner's next write goes
+        // to the other buffer, and the one after that follows its read of this one)
+        float* mx = sRowMax + (n & 1) * 512 + t * 256;
+        mx[ch * 128 + row] = bmax;
+        named_bar_sync(pair_bar, 64);
+        bmax = fmaxf(bmax, mx[(1 - ch) * 128 + row]);
+        const float m_new = fmaxf(m_run, bmax);
+        const bool need = (m_new - m_run) > 8.0f;  // lazy rescale, as in the one-warp path
+        float factor = 1.0f;
+        if (need) {
+          factor = (m_run == -INFINITY) ? 0.0f : ex2(m_run - m_new);
+          m_run = m_new;
+        }
+        const float m_use = (m_run == -INFINITY) ? 0.0f : m_run;
+        // P in two 32-column chunks, each stored as soon as it is packed (keeps the live
+        // register set at the S row plus 16 packed words)
+        float lsum;
+        if (fast) {
+          const float2 sc2 = splat2(p.scale_log2), nm2 = splat2(-m_use);
+          float2 ls2[2] = {splat2(0.0f), splat2(0.0f)};
+#pragma unroll
+          for (int hc = 0; hc < 2; ++hc) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int c = hc * 32; c < hc * 32 + 32; c += 2) {
+              const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
+              const bool poly = (c & AF_EXP2_POLY_MASK) == 0;
+              const float2 e = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+              ls2[(c / 2) & 1] = fadd2(ls2[(c / 2) & 1], e);
+              pk[(c / 2) % 16] = pack_bf16(e.x, e.y);
+            }
+            tmem_st16(s_tmem + hc * 16, pk);
+          }
+          lsum = (ls2[0].x + ls2[1].x) + (ls2[0].y + ls2[1].y);
+        } else {
+          lsum = 0.0f;
+#pragma unroll
+          for (int hc = 0; hc < 2; ++hc) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int c = hc * 32; c < hc * 32 + 32; c += 2) {
+              const float e0 = ex2(s[c] - m_use);
+              const float e1 = ex2(s[c + 1] - m_use);
+              lsum += e0 + e1;
+              pk[(c / 2) % 16] = pack_bf16(e0, e1);
+            }
+            tmem_st16(s_tmem + hc * 16, pk);
+          }
+        }
+        l_run = l_run * factor + lsum;
+        tmem_st_wait();
+        // correction of this warp's O columns (only rows whose max moved by > 2^8)
+        if (n > 0 && __any_sync(0xffffffffu, need)) {
+          mbar_wait(&o_done[t], (n - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < DV / 64; ++c) {
+            uint32_t orr[32];
+            tmem_ld32(o_tmem + c * 32, orr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              orr[e] = __float_as_uint(__uint_as_float(orr[e]) * factor);
+            tmem_st32(o_tmem + c * 32, orr);
+          }
+          tmem_st_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&p_full[t]);
+      }
+    } else
     for (int n = 0; n < nk; ++n) {
       const int c0 = (band.jb_lo + n) * kBlockN;
       const int cb = c0 + ch * 64;
@@ -334,6 +479,15 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
     }
     // ───────────── epilogue: O (this warp's DV/2 columns), abssum row statistic ─────────────
     float inv = 1.0f;
+    if constexpr (kFamily == kFamilySoftmax) {
+      sRowSum[(t * 2 + ch) * 128 + row] = l_run;
+      named_bar_sync(pair_bar, 64);
+      const float total = sRowSum[t * 2 * 128 + row] + sRowSum[(t * 2 + 1) * 128 + row];
+      inv = (total == 0.0f) ? 0.0f : 1.0f / total;
+      if (ch == 0 && p.lse != nullptr && i < p.seq_q)
+        p.lse[(static_cast<int64_t>(b) * p.heads_q + h) * p.seq_q + i] =
+            (total == 0.0f) ? -INFINITY : (m_run * kLn2 + logf(total));
+    }
     if constexpr (kFamily == kFamilyAbssum) {
       sRowSum[(t * 2 + ch) * 128 + row] = l_run;
       named_bar_sync(1 + t, 256);
@@ -392,12 +546,14 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
     for (int n = 0; n < nk; ++n) {
       const int c0 = (band.jb_lo + n) * kBlockN;
       mbar_wait(&s_full[t], n & 1);
+      AF_TRACE(t * 4 + wq, n, 0);
       tc_fence_after();
       uint32_t sr[kBlockN];
 #pragma unroll
       for (int c = 0; c < kBlockN / 32; ++c)
         tmem_ld32(s_tmem + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
       tmem_ld_wait();
+      AF_TRACE(t * 4 + wq, n, 1);
       float* s = reinterpret_cast<float*>(sr);
       const bool full = block_fully_kept(p.mask, r0, c0, p.seq_k);
 
@@ -410,8 +566,17 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
         const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
         float bmax = -INFINITY;
         if (fast) {
+#if AF_FWD_TREEMAX
+          // four independent FMNMX3 chains (a single chain is 64 dependent max ops)
+          float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int c = 0; c < kBlockN; c += 2)
+            mx4[(c / 2) & 3] = fmaxf(mx4[(c / 2) & 3], fmaxf(s[c], s[c + 1]));
+          bmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+#else
 #pragma unroll
           for (int c = 0; c < kBlockN; ++c) bmax = fmaxf(bmax, s[c]);
+#endif
           bmax *= p.scale_log2;
         } else {
 #pragma unroll
@@ -430,49 +595,70 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
           m_run = m_new;
         }
         const float m_use = (m_run == -INFINITY) ? 0.0f : m_run;
-        float lsum = 0.0f;
-        uint32_t pk[kBlockN / 2];
-        if (fast) {
+        AF_TRACE(t * 4 + wq, n, 2);
+        // P in two 64-key halves; the first is published (p_half) before the second is
+        // exponentiated, so the MMA warp runs half of PV under the row warps' second half.
+        // The O correction (only rows whose max moved by > 2^8) precedes the first publish: PV(n)
+        // must accumulate onto the rescaled O, and PV(n-1) has completed (S(n) was issued behind
+        // it); it runs after half of the S row is dead, to keep the register peak down.
+        auto publish = [&](int hh, const uint32_t (&pk)[kBlockN / 4]) {
+          tmem_st32(s_tmem + hh * 32, pk);
+          tmem_st_wait();
+          if (hh == 0 && n > 0 && __any_sync(0xffffffffu, need)) {
+            mbar_wait(&o_done[t], (n - 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < DV / 32; ++c) {
+              uint32_t orr[32];
+              tmem_ld32(o_tmem + c * 32, orr);
+              tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < kBlockN; c += 2) {
-            const float x0 = fmaf(s[c], p.scale_log2, -m_use);
-            const float x1 = fmaf(s[c + 1], p.scale_log2, -m_use);
-            const bool poly = (c & AF_EXP2_POLY_MASK) == 0;  // default: c % 16 in {0, 1}, 12.5 % (swept: 25 % and 6 % are slower)
-            const float e0 = poly ? exp2_poly(x0) : ex2(x0);
-            const float e1 = poly ? exp2_poly(x1) : ex2(x1);
-            lsum += e0 + e1;
-            pk[c / 2] = pack_bf16(e0, e1);
+              for (int e = 0; e < 32; ++e)
+                orr[e] = __float_as_uint(__uint_as_float(orr[e]) * factor);
+              tmem_st32(o_tmem + c * 32, orr);
+            }
+            tmem_st_wait();
+          }
+          if (hh == 0 && AF_FWD_EARLY_P) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane_id() == 0) mbar_arrive(&p_half[t]);
+            AF_TRACE(t * 4 + wq, n, 3);
+          }
+        };
+        float2 ls2[2] = {splat2(0.0f), splat2(0.0f)};
+        if (fast) {
+          // packed pairs: one FFMA2 for the scale/max fold, FADD2 row sums (two chains); an
+          // eighth of the exponentials on the FMA pipe (exp2_poly2)
+          const float2 sc2 = splat2(p.scale_log2), nm2 = splat2(-m_use);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t pk[kBlockN / 4];
+#pragma unroll
+            for (int c = hh * (kBlockN / 2); c < (hh + 1) * (kBlockN / 2); c += 2) {
+              const float2 x = ffma2(make_float2(s[c], s[c + 1]), sc2, nm2);
+              const bool poly = (c & AF_EXP2_POLY_MASK) == 0;  // default: c % 16 in {0, 1}
+              const float2 e = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+              ls2[(c / 2) & 1] = fadd2(ls2[(c / 2) & 1], e);
+              pk[(c / 2) % (kBlockN / 4)] = pack_bf16(e.x, e.y);
+            }
+            publish(hh, pk);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < kBlockN; c += 2) {
-            const float e0 = ex2(s[c] - m_use);
-            const float e1 = ex2(s[c + 1] - m_use);
-            lsum += e0 + e1;
-            pk[c / 2] = pack_bf16(e0, e1);
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t pk[kBlockN / 4];
+#pragma unroll
+            for (int c = hh * (kBlockN / 2); c < (hh + 1) * (kBlockN / 2); c += 2) {
+              const float2 e = make_float2(ex2(s[c] - m_use), ex2(s[c + 1] - m_use));
+              ls2[(c / 2) & 1] = fadd2(ls2[(c / 2) & 1], e);
+              pk[(c / 2) % (kBlockN / 4)] = pack_bf16(e.x, e.y);
+            }
+            publish(hh, pk);
           }
         }
-        l_run = l_run * factor + lsum;
-#pragma unroll
-        for (int c = 0; c < kBlockN / 64; ++c)
-          tmem_st32(s_tmem + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[c * 32]));
-        tmem_st_wait();
-        // Correction of the O accumulator (only rows whose max moved by > 2^8).
-        if (n > 0 && __any_sync(0xffffffffu, need)) {
-          mbar_wait(&o_done[t], (n - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < DV / 32; ++c) {
-            uint32_t orr[32];
-            tmem_ld32(o_tmem + c * 32, orr);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              orr[e] = __float_as_uint(__uint_as_float(orr[e]) * factor);
-            tmem_st32(o_tmem + c * 32, orr);
-          }
-          tmem_st_wait();
-        }
+        l_run = l_run * factor + ((ls2[0].x + ls2[1].x) + (ls2[0].y + ls2[1].y));
+        AF_TRACE(t * 4 + wq, n, 4);
       } else if constexpr (kFamily == kFamilyAbssum) {
         // s = tau q.k gamma^(i-j) on the kept band (slope = log2 gamma); l_run = sum |s|
         uint32_t pk[kBlockN / 2];
@@ -517,6 +703,7 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&p_full[t]);
+      AF_TRACE(t * 4 + wq, n, 5);
     }
 
     // ───────────── epilogue: O / l, LSE ─────────────

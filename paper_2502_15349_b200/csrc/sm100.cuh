@@ -43,8 +43,22 @@ AF_DEVICE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit (up to the hint, in
+// ns) instead of re-issuing the probe, leaving issue slots to the warps doing row work.
+#ifndef AF_MBAR_SUSPEND_NS
+#define AF_MBAR_SUSPEND_NS 0  // swept: 1000 ns and 0x989680 are no faster than a plain probe loop
+#endif
 AF_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if AF_MBAR_SUSPEND_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "n"(AF_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
@@ -52,6 +66,7 @@ AF_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 AF_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -263,6 +278,24 @@ AF_DEVICE float exp2_poly(float x) {
   const float p = fmaf(fmaf(fmaf(0.05286731570959091f, f, 0.242152139544487f), f,
                             0.6935868263244629f), f, 0.9999627470970154f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+// Packed fp32 pairs (FFMA2 / FADD2 / FMUL2 on sm_100): one issue slot for two lanes' worth of
+// row-epilogue arithmetic — the softmax row warps are issue-bound, not FMA-throughput-bound.
+AF_DEVICE float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+AF_DEVICE float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+AF_DEVICE float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+AF_DEVICE float2 splat2(float a) { return make_float2(a, a); }
+// exp2_poly on a pair, packed (same rounding as two exp2_poly calls)
+AF_DEVICE float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.0f);
+  x.y = fmaxf(x.y, -127.0f);
+  const float2 t = fadd2(x, splat2(12582912.0f));
+  const float2 f = ffma2(fadd2(t, splat2(-12582912.0f)), splat2(-1.0f), x);
+  const float2 q = ffma2(ffma2(ffma2(splat2(0.05286731570959091f), f, splat2(0.242152139544487f)),
+                               f, splat2(0.6935868263244629f)),
+                         f, splat2(0.9999627470970154f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
 // tanh(y) = 1 - 2 / (1 + 2^(2 y log2 e)): absolute error ~1e-7 over the whole range (the
 // soft-cap multiplies it by the cap, so absolute — not relative — accuracy is what matters);
