@@ -13,7 +13,9 @@
 // A reads — the S GEMM at N = 64 is otherwise bound by re-reading Q from smem every tile),
 // columns [256, 576) stay in smem (80 KB), which leaves room for a 2-stage ring of 64-key latent
 // tiles (72 KB each).  TMEM: S double buffer [0,128) (P packed in place) | O half [128,384) |
-// Q[:, 0:256] packed bf16 [384,512).
+// Q[:, 0:256] packed bf16 [384,512).  Decode (32-key tiles) uses only [0,64) for S and puts
+// Q[:, 256:384] at [64,128): 24 of the 36 QK^T k-steps read no smem A, Q smem is 48 KB and the
+// latent ring runs 4 stages.
 // Warps: 0-3 softmax rows (one row per thread, FA4-style lazy rescale), 4 TMA, 5 MMA.
 #pragma once
 #include <cuda.h>
@@ -29,6 +31,9 @@ constexpr int kMlaHalf = 256;
 // keys per latent tile and ring depth: prefill (KV reused from L2 across heads, compute bound)
 // 64-key tiles x 2 stages; decode (KV streamed once from HBM) 32-key tiles x 4 stages, i.e. three
 // tiles of prefetch distance, to hide the HBM latency behind the S / softmax / PV chain.
+#ifndef AF_MLA_DECODE_QT
+#define AF_MLA_DECODE_QT 384
+#endif
 #ifndef AF_MLA_PREFILL_N
 #define AF_MLA_PREFILL_N 64
 #endif
@@ -36,9 +41,11 @@ template <bool kDecode>
 struct MlaTile {
   static constexpr int kN = kDecode ? 32 : AF_MLA_PREFILL_N;
   static constexpr int kStages = kDecode ? 4 : (AF_MLA_PREFILL_N == 32 ? 4 : 2);
+  // Q columns [0, kQT) held in TMEM as TS-MMA A operand; decode's 32-key S double buffer leaves
+  // TMEM columns [64, 128) free for Q columns [256, 384), so fewer S MMAs stream Q from smem
+  static constexpr int kQT = kDecode ? AF_MLA_DECODE_QT : 256;
 };
 constexpr int kMlaN = 64;     // prefill tile (split lengths of decode are multiples of both)
-constexpr int kMlaQT = 256;   // Q columns [0, 256) live in TMEM (TS MMA), [256, 576) in smem
 
 struct MlaParams {
   int batch, heads, seq_q, seq_k;
@@ -61,11 +68,11 @@ struct MlaParams {
 // Shared memory: Q columns [256, 576) as 5 boxes [128 rows][64] (80 KB) + a 2-stage ring of
 // 64-key latent tiles (9 boxes [64 keys][64] = 72 KB each).  TMEM (512 columns): S double buffer
 // [0, 128) (P packed in place) | O half [128, 384) | Q columns [0, 256) packed bf16 [384, 512).
-template <int kN, int kSt>
+template <int kN, int kSt, int kQT>
 struct MlaSmem {
   static constexpr int kQBox = 128 * 128;
   static constexpr int kKBox = kN * 128;
-  static constexpr int kQBytes = 5 * kQBox;
+  static constexpr int kQBytes = (576 - kQT) / 64 * kQBox;
   static constexpr int kKBytes = 9 * kKBox;
   static constexpr int kQOff = 0;
   static constexpr int kKOff = kQBytes;
@@ -82,7 +89,10 @@ __global__ void __launch_bounds__(192, 1)
                    const __grid_constant__ CUtensorMap tm_kv, const MlaParams p) {
   constexpr int kN = MlaTile<kDecode>::kN;
   constexpr int kSt = MlaTile<kDecode>::kStages;
-  using L = MlaSmem<kN, kSt>;
+  constexpr int kQT = MlaTile<kDecode>::kQT;
+  constexpr int kQB = (kMlaDqk - kQT) / 64;  // Q boxes of 64 columns in smem
+  static_assert(kQT == 256 || (kDecode && kQT == 384 && 2 * kN <= 64), "TMEM map");
+  using L = MlaSmem<kN, kSt, kQT>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + L::kQOff;
   uint8_t* sK = smem + L::kKOff;
@@ -139,12 +149,14 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   constexpr uint32_t kColO = 128, kColQ = 384;
+  // TMEM column of the packed Q chunk c (64 Q columns = 32 packed TMEM columns)
+  auto q_tcol = [](int c) -> uint32_t { return c < 4 ? kColQ + c * 32 : 64 + (c - 4) * 32; };
 
   if (warp == 4) {
     if (elect_one() && nk > 0) {
       mbar_expect_tx(q_full, L::kQBytes);
-      for (int c = 0; c < 5; ++c) {
-        const int col = kMlaQT + c * 64;
+      for (int c = 0; c < kQB; ++c) {
+        const int col = kQT + c * 64;
         if constexpr (kDecode)
           tma_load_4d(sQ + c * L::kQBox, &tm_q, q_full, col, 0, b, 0);
         else
@@ -172,13 +184,13 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_after();
         const uint32_t kb = aK + st * L::kKBytes;
 #pragma unroll
-        for (int kk = 0; kk < kMlaQT / 16; ++kk)  // Q columns [0, 256) from TMEM
-          mma_ts(tmem + s * kN, tmem + kColQ + kk * 8,
+        for (int kk = 0; kk < kQT / 16; ++kk)  // Q columns [0, kQT) from TMEM
+          mma_ts(tmem + s * kN, tmem + q_tcol(kk / 4) + (kk % 4) * 8,
                  make_sdesc(kb + (kk / 4) * L::kKBox + (kk % 4) * 32, 0, 1024), id_s, kk > 0);
 #pragma unroll
-        for (int kk = kMlaQT / 16; kk < kMlaDqk / 16; ++kk)  // columns [256, 576) from smem
+        for (int kk = kQT / 16; kk < kMlaDqk / 16; ++kk)  // columns [kQT, 576) from smem
           mma_ss(tmem + s * kN,
-                 make_sdesc(aQ + (kk / 4 - 4) * L::kQBox + (kk % 4) * 32, 0, 1024),
+                 make_sdesc(aQ + (kk / 4 - kQT / 64) * L::kQBox + (kk % 4) * 32, 0, 1024),
                  make_sdesc(kb + (kk / 4) * L::kKBox + (kk % 4) * 32, 0, 1024), id_s, 1u);
         mma_commit(&s_full[s]);
       };
@@ -213,7 +225,7 @@ __global__ void __launch_bounds__(192, 1)
           kDecode ? p.q + b * p.q_sb + static_cast<int64_t>(live ? row : 0) * p.q_ss
                   : p.q + b * p.q_sb + h * p.q_sh + static_cast<int64_t>(live ? i : 0) * p.q_ss;
 #pragma unroll
-      for (int c = 0; c < kMlaQT / 64; ++c) {
+      for (int c = 0; c < kQT / 64; ++c) {
         uint32_t w[32];
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
@@ -224,7 +236,7 @@ __global__ void __launch_bounds__(192, 1)
           w[v * 4 + 2] = x.z;
           w[v * 4 + 3] = x.w;
         }
-        tmem_st32(tmem + lane_base + kColQ + c * 32, w);
+        tmem_st32(tmem + lane_base + q_tcol(c), w);
       }
       tmem_st_wait();
       tc_fence_before();

@@ -5,8 +5,8 @@
 
 namespace af {
 
-using PrefillSmem = MlaSmem<MlaTile<false>::kN, MlaTile<false>::kStages>;
-using DecodeSmem = MlaSmem<MlaTile<true>::kN, MlaTile<true>::kStages>;
+using PrefillSmem = MlaSmem<MlaTile<false>::kN, MlaTile<false>::kStages, MlaTile<false>::kQT>;
+using DecodeSmem = MlaSmem<MlaTile<true>::kN, MlaTile<true>::kStages, MlaTile<true>::kQT>;
 
 int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o, float* lse,
                 cudaStream_t s) {
