@@ -22,6 +22,8 @@ through its C ABI (``runtime.py``); if the library or a GPU is missing the call 
 
 from __future__ import annotations
 
+import contextlib
+import contextvars
 import math
 from dataclasses import dataclass
 
@@ -34,6 +36,33 @@ from .plan import (FAMILY_ABSSUM, FAMILY_SOFTMAX, LinearPlan, ParallelPlan, plan
 from .spec import AttentionSpec, Pattern, from_reference
 
 _BF16 = torch.bfloat16
+
+
+# Output-buffer reuse for repeated same-shape calls (HostPipeline slots): inside
+# ``reuse_buffers(cache)`` the executors' output / workspace tensors come from ``cache`` (keyed by
+# allocation site) instead of fresh allocations; the caller owns the ordering of reuse.
+_REUSE: contextvars.ContextVar = contextvars.ContextVar("af_reuse_buffers", default=None)
+
+
+@contextlib.contextmanager
+def reuse_buffers(cache: dict):
+    token = _REUSE.set(cache)
+    try:
+        yield cache
+    finally:
+        _REUSE.reset(token)
+
+
+def _empty(key: str, shape, dtype, device) -> torch.Tensor:
+    cache = _REUSE.get()
+    shape = tuple(int(x) for x in shape)
+    if cache is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    t = cache.get(key)
+    if t is None or tuple(t.shape) != shape or t.dtype != dtype or t.device != torch.device(device):
+        t = torch.empty(shape, dtype=dtype, device=device)
+        cache[key] = t
+    return t
 
 
 def _spec(spec) -> AttentionSpec:
@@ -249,8 +278,8 @@ def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: 
     pad = _padded_dim(spec, precision)
     if pad is not None:
         q, k, v = _pad_last(q, pad), _pad_last(k, pad), _pad_last(v, pad)
-    o = torch.empty(d.batch, d.heads, d.seq_q, v.shape[-1], device=q.device, dtype=dtype)
-    lse = (torch.empty(d.batch, d.heads, d.seq_q, device=q.device, dtype=torch.float32)
+    o = _empty("fwd.o", (d.batch, d.heads, d.seq_q, v.shape[-1]), dtype, q.device)
+    lse = (_empty("fwd.lse", (d.batch, d.heads, d.seq_q), torch.float32, q.device)
            if plan.has_lse else None)
     # Value dims above the kernel's 128 (softmax-diff's 256) run as 128-wide value slices: the
     # normalised scores P do not depend on V, so each slice is exact (S is recomputed per slice)
@@ -310,8 +339,8 @@ def _parallel_backward_mapped(spec, plan, arrays: dict, o, lse, dout) -> dict:
         dout = dout.contiguous()
         o = o.contiguous()
     _check_shape(dout, (d.batch, d.heads, d.seq_q, d.d_v), "dout")
-    dq = torch.empty_like(q, memory_format=torch.contiguous_format)
-    dk = torch.empty(k.shape, device=k.device, dtype=_BF16)
+    dq = _empty("bwd.dq", q.shape, q.dtype, q.device)
+    dk = _empty("bwd.dk", k.shape, _BF16, k.device)
     if spec.kv_shared:
         # MLA lowering: V aliases K[..., :d_v]; the kernel writes dK + [dV, 0] into dk
         if q.stride() != dq.stride() or k.stride() != dk.stride():
@@ -319,14 +348,14 @@ def _parallel_backward_mapped(spec, plan, arrays: dict, o, lse, dout) -> dict:
         v = k[..., : d.d_v]
         dv = dk[..., : d.d_v]
     else:
-        dv = torch.empty(d.batch, d.kv_heads, d.seq_k, d.d_v, device=k.device, dtype=_BF16)
+        dv = _empty("bwd.dv", (d.batch, d.kv_heads, d.seq_k, d.d_v), _BF16, k.device)
         # dq/dk/dv are written with the q/k/v strides of the descriptor: use contiguous copies
         if q.stride() != dq.stride() or k.stride() != dk.stride() or v.stride() != dv.stride():
             q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     desc = _desc(plan, q, k, v, o, slope, rt.AF_DTYPE_BF16)
     L = rt.lib()
     ws_n = L.af_parallel_bwd_workspace(desc)
-    ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
+    ws = _empty("bwd.ws", (ws_n,), torch.uint8, q.device)
     if plan.family in (FAMILY_SOFTMAX, FAMILY_ABSSUM) and lse is None:
         raise InputError("softmax / abssum backward needs the forward row statistic")
     rt.check(L.af_parallel_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
@@ -430,7 +459,7 @@ def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = Fa
     plan = plan_linear(spec, chunk)
     q, k, v = _linear_qkv(plan, arrays)
     d = spec.dims
-    o = torch.empty(d.batch, d.heads, d.seq_q, v.shape[-1], device=q.device, dtype=_BF16)
+    o = _empty("lin.o", (d.batch, d.heads, d.seq_q, v.shape[-1]), _BF16, q.device)
     state = (torch.empty(d.batch, d.heads, q.shape[-1], v.shape[-1], device=q.device,
                          dtype=torch.float32) if return_state else None)
     desc, _keep = _linear_desc(plan, arrays, q, k, v, o)
@@ -495,7 +524,9 @@ def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 128) ->
     dout = _as(dout, _BF16).contiguous()
     _check_shape(dout, (d.batch, d.heads, d.seq_q, d.d_v), "dout")
     dout = _pad_last(dout, v.shape[-1]).contiguous()
-    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    dq = _empty("lin.dq", q.shape, q.dtype, q.device)
+    dk = _empty("lin.dk", k.shape, k.dtype, k.device)
+    dv = _empty("lin.dv", v.shape, v.dtype, v.device)
     # dout / dq use the o / q stride slots of the descriptor (all contiguous here)
     desc, keep = _linear_desc(plan, arrays, q, k, v, dout)
     extras = spec.extras_by_name()
@@ -508,7 +539,7 @@ def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 128) ->
     dgate = grads_x.get(plan.k_gate) if plan.k_gate is not None else None
     L = rt.lib()
     ws_n = L.af_linear_bwd_workspace(desc)
-    ws = torch.empty(ws_n, device=q.device, dtype=torch.uint8)
+    ws = _empty("lin.ws", (ws_n,), torch.uint8, q.device)
     rt.check(L.af_linear_bwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
                              dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
                              rt.C.cast(dfac, rt.C.c_void_p), rt.ptr(dgate), ws.data_ptr(), ws_n,

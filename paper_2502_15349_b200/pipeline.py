@@ -11,8 +11,9 @@ work into unit chunks and runs three CUDA streams:
     d2h  : copy chunk c-1's outputs back into the caller's pinned host tensors
 
 Host→device and device→host use separate copy engines, so in steady state the step costs
-max(H2D, kernels, D2H) per chunk instead of their sum.  Device input slots are double-buffered;
-output tensors come from the caching allocator and are ``record_stream``-ed onto the d2h stream.
+max(H2D, kernels, D2H) per chunk instead of their sum.  Device input and output slots are
+double-buffered and persistent across calls (``api.reuse_buffers``): chunk c+2 writes slot
+c % 2 only after chunk c's inputs are consumed and its outputs copied out.
 The call is stream-ordered with the caller's current stream on both ends (its events bracket the
 whole pipeline).
 """
@@ -95,6 +96,7 @@ class HostPipeline:
         self.comp = torch.cuda.Stream(self.device)
         self.d2h = torch.cuda.Stream(self.device)
         self._slots: list[dict] = [{}, {}]
+        self._obufs: list[dict] = [{}, {}]  # per-slot output / workspace buffers (api reuse)
 
     # device slot tensor for one host slice (reused across calls of the same shape)
     def _slot(self, s: int, name: str, like: torch.Tensor) -> torch.Tensor:
@@ -147,6 +149,7 @@ class HostPipeline:
         kv_names = {"k", "v"}
         in_ready = [torch.cuda.Event() for _ in self.units]
         comp_done = [torch.cuda.Event() for _ in self.units]
+        out_read = [torch.cuda.Event() for _ in self.units]
         host_out = out
         for c, unit in enumerate(self.units):
             s = c % 2
@@ -169,7 +172,12 @@ class HostPipeline:
                     ddo.copy_(hs, non_blocking=True)
                 in_ready[c].record(self.h2d)
             self.comp.wait_event(in_ready[c])
-            with torch.cuda.stream(self.comp):
+            if c >= 2:
+                self.comp.wait_event(out_read[c - 2])  # slot s outputs copied out
+            # outputs and workspaces come from the slot's persistent buffers: no per-chunk
+            # allocation on the host path (fresh 100 MB-class allocations per chunk made the
+            # enqueue, not the copies, the bound)
+            with torch.cuda.stream(self.comp), api.reuse_buffers(self._obufs[s]):
                 res = self._run_unit(dev, ddo)
                 comp_done[c].record(self.comp)
             if host_out is None:
@@ -182,6 +190,7 @@ class HostPipeline:
                     t.record_stream(self.d2h)
                     _slice(host_out[name], self.spec, unit, name in kv_names and
                            self.spec.dims.heads_kv is not None).copy_(t, non_blocking=True)
+                out_read[c].record(self.d2h)
         end = torch.cuda.Event()
         end.record(self.d2h)
         caller.wait_event(end)
