@@ -30,14 +30,23 @@ from .plan import plan_linear, plan_parallel
 from .spec import AttentionSpec, Pattern
 
 
+# unit modes: -1 a batch range; 0 a KV-head group range of batch 0; 1 a query-head range of
+# batch 0 with the shared latent KV (MLA) copied whole and its gradient summed over the chunks
+_BATCH, _KV_GROUP, _HEADS_SHARED_KV = -1, 0, 1
+
+
 def _chunks(spec: AttentionSpec, max_chunks: int) -> list[tuple[int, int, int]]:
-    """(batch index | -1 for a batch range, lo, hi): batch ranges when B > 1, else KV-head
-    group ranges of the single batch element."""
+    """(mode, lo, hi): batch ranges when B > 1; else KV-head group ranges of the single batch
+    element, or query-head ranges when one latent KV head is shared by all heads (MLA)."""
     d = spec.dims
     if d.batch > 1:
         n = min(max_chunks, d.batch)
         bounds = [round(i * d.batch / n) for i in range(n + 1)]
-        return [(-1, bounds[i], bounds[i + 1]) for i in range(n)]
+        return [(_BATCH, bounds[i], bounds[i + 1]) for i in range(n)]
+    if spec.kv_shared and d.kv_heads == 1 and d.heads > 1:
+        n = min(max_chunks, d.heads)
+        bounds = [round(i * d.heads / n) for i in range(n + 1)]
+        return [(_HEADS_SHARED_KV, bounds[i], bounds[i + 1]) for i in range(n)]
     g = d.kv_heads
     n = min(max_chunks, g)
     bounds = [round(i * g / n) for i in range(n + 1)]
@@ -47,8 +56,10 @@ def _chunks(spec: AttentionSpec, max_chunks: int) -> list[tuple[int, int, int]]:
 def _sub_spec(spec: AttentionSpec, unit) -> AttentionSpec:
     b, lo, hi = unit
     d = spec.dims
-    if b < 0:
+    if b == _BATCH:
         return replace(spec, dims=replace(d, batch=hi - lo))
+    if b == _HEADS_SHARED_KV:
+        return replace(spec, dims=replace(d, heads=hi - lo))
     r = d.heads // d.kv_heads
     heads_kv = None if d.heads_kv is None else hi - lo
     return replace(spec, dims=replace(d, batch=1, heads=(hi - lo) * r, heads_kv=heads_kv))
@@ -58,8 +69,10 @@ def _slice(t: torch.Tensor, spec: AttentionSpec, unit, kv: bool) -> torch.Tensor
     """Slice a [B|1, H|1, ...] host tensor to one unit chunk."""
     b, lo, hi = unit
     d = spec.dims
-    if b < 0:
+    if b == _BATCH:
         return t[lo:hi] if t.shape[0] > 1 else t
+    if b == _HEADS_SHARED_KV:
+        return t if kv or t.shape[1] == 1 else t[:, lo:hi]
     r = 1 if kv else d.heads // d.kv_heads
     t = t[0:1]
     return t[:, lo * r: hi * r] if t.shape[1] > 1 else t
@@ -92,6 +105,9 @@ class HostPipeline:
         if len(units) > 1 and not _same_lowering(self.spec, _sub_spec(self.spec, units[0])):
             units = [(-1, 0, self.spec.dims.batch)]  # one chunk: the spec itself
         self.units = units
+        # gradients of the shared latent KV: per-chunk partials summed on the device
+        self._summed = {"k"} if units[0][0] == _HEADS_SHARED_KV else set()
+        self._acc: dict = {}
         self.h2d = torch.cuda.Stream(self.device)
         self.comp = torch.cuda.Stream(self.device)
         self.d2h = torch.cuda.Stream(self.device)
@@ -114,8 +130,11 @@ class HostPipeline:
             if t is None:
                 continue
             shape = list(t.shape)
-            if self.units[0][0] < 0:
+            if self.units[0][0] == _BATCH:
                 shape[0] = d.batch
+            elif self.units[0][0] == _HEADS_SHARED_KV:
+                if name not in self._summed:
+                    shape[1] = d.heads
             else:
                 kv = name in ("k", "v") and d.heads_kv is not None
                 shape[1] = d.kv_heads if kv else d.heads
@@ -179,18 +198,37 @@ class HostPipeline:
             # enqueue, not the copies, the bound)
             with torch.cuda.stream(self.comp), api.reuse_buffers(self._obufs[s]):
                 res = self._run_unit(dev, ddo)
+                for name in self._summed & res.keys():
+                    acc = self._acc.get(name)
+                    if acc is None or acc.shape != res[name].shape:
+                        acc = self._acc[name] = torch.empty(res[name].shape, dtype=torch.float32,
+                                                            device=self.device)
+                    if c == 0:
+                        acc.copy_(res[name])
+                    else:
+                        acc.add_(res[name])
                 comp_done[c].record(self.comp)
             if host_out is None:
                 host_out = self._outputs_like(res)
             self.d2h.wait_event(comp_done[c])
             with torch.cuda.stream(self.d2h):
                 for name, t in res.items():
-                    if t is None:
+                    if t is None or name in self._summed:
                         continue
                     t.record_stream(self.d2h)
                     _slice(host_out[name], self.spec, unit, name in kv_names and
                            self.spec.dims.heads_kv is not None).copy_(t, non_blocking=True)
                 out_read[c].record(self.d2h)
+        if self._summed & res.keys():
+            with torch.cuda.stream(self.comp):
+                summed = {n: self._acc[n].to(host_out[n].dtype) for n in self._summed & res.keys()}
+                done = torch.cuda.Event()
+                done.record(self.comp)
+            self.d2h.wait_event(done)
+            with torch.cuda.stream(self.d2h):
+                for n, t in summed.items():
+                    t.record_stream(self.d2h)
+                    host_out[n].copy_(t, non_blocking=True)
         end = torch.cuda.Event()
         end.record(self.d2h)
         caller.wait_event(end)

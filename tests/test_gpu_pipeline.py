@@ -56,3 +56,27 @@ def test_pipeline_rejects_device_inputs():
     spec = S.builtin("softmax", batch=1, heads=1, seq=64, d_qk=64, d_v=64)
     with pytest.raises(af.InputError):
         HostPipeline(spec)({"q": torch.zeros(1, 1, 64, 64, device="cuda")})
+
+
+def test_mla_pipeline_head_chunks():
+    """B = 1 MLA (one latent KV head shared by all heads) chunks over query heads: O, LSE and dQ
+    are bitwise the device API's; the latent-KV gradient is the fp32 sum of the per-chunk
+    (bf16) partials, so it matches within bf16 rounding of the partials."""
+    from paper_2502_15349_b200.configs import mla
+    spec = mla(1, 16, 256, 256, causal=True)
+    host = {"q": _rand(1, 16, 256, 576).pin_memory(), "k": _rand(1, 1, 256, 576).pin_memory()}
+    hdo = _rand(1, 16, 256, 512).pin_memory()
+    pipe = HostPipeline(spec, max_chunks=4)
+    assert len(pipe.units) == 4
+    out = pipe(host, hdo)
+    out2 = pipe(host, hdo)  # second call reuses the slot buffers and the accumulator
+    torch.cuda.synchronize()
+    dev = {k: v.cuda() for k, v in host.items()}
+    o, lse = af.parallel_forward(spec, dev)
+    g = af.parallel_backward(spec, dev, o, lse, hdo.cuda())
+    assert torch.equal(out["o"], o.cpu()) and torch.equal(out["lse"], lse.cpu())
+    assert torch.equal(out["q"], g["q"].cpu())
+    ref = g["k"].float().cpu()
+    err = (out["k"].float() - ref).norm() / ref.norm()
+    assert err < 1e-2, err
+    assert torch.equal(out2["k"], out["k"])
