@@ -30,35 +30,39 @@ from .plan import plan_linear, plan_parallel
 from .spec import AttentionSpec, Pattern
 
 
-# unit modes: -1 a batch range; 0 a KV-head group range of batch 0; 1 a query-head range of
-# batch 0 with the shared latent KV (MLA) copied whole and its gradient summed over the chunks
+# unit = (mode, b, lo, hi): mode _BATCH is the batch range [lo, hi); _KV_GROUP the KV-head group
+# range [lo, hi) of batch element b (with its query heads); _HEADS_SHARED_KV the query-head range
+# [lo, hi) of batch element 0 with the shared latent KV (MLA) copied whole and its gradient summed
+# over the chunks
 _BATCH, _KV_GROUP, _HEADS_SHARED_KV = -1, 0, 1
 
 
-def _chunks(spec: AttentionSpec, max_chunks: int) -> list[tuple[int, int, int]]:
-    """(mode, lo, hi): batch ranges when B > 1; else KV-head group ranges of the single batch
-    element, or query-head ranges when one latent KV head is shared by all heads (MLA)."""
+def _ranges(n_items: int, n: int) -> list[tuple[int, int]]:
+    bounds = [round(i * n_items / n) for i in range(n + 1)]
+    return [(bounds[i], bounds[i + 1]) for i in range(n)]
+
+
+def _chunks(spec: AttentionSpec, max_chunks: int) -> list[tuple[int, int, int, int]]:
+    """Batch ranges when B ≥ max_chunks; else (batch, KV-head group) units so that small batches
+    still fill the pipeline (its fill / drain is one chunk's copies); query-head ranges when one
+    latent KV head is shared by all heads (MLA, B = 1)."""
     d = spec.dims
-    if d.batch > 1:
-        n = min(max_chunks, d.batch)
-        bounds = [round(i * d.batch / n) for i in range(n + 1)]
-        return [(_BATCH, bounds[i], bounds[i + 1]) for i in range(n)]
-    if spec.kv_shared and d.kv_heads == 1 and d.heads > 1:
-        n = min(max_chunks, d.heads)
-        bounds = [round(i * d.heads / n) for i in range(n + 1)]
-        return [(_HEADS_SHARED_KV, bounds[i], bounds[i + 1]) for i in range(n)]
-    g = d.kv_heads
-    n = min(max_chunks, g)
-    bounds = [round(i * g / n) for i in range(n + 1)]
-    return [(0, bounds[i], bounds[i + 1]) for i in range(n)]
+    if d.batch >= max_chunks or (d.batch > 1 and d.kv_heads == 1):
+        return [(_BATCH, 0, lo, hi) for lo, hi in _ranges(d.batch, min(max_chunks, d.batch))]
+    if d.batch == 1 and spec.kv_shared and d.kv_heads == 1 and d.heads > 1:
+        return [(_HEADS_SHARED_KV, 0, lo, hi)
+                for lo, hi in _ranges(d.heads, min(max_chunks, d.heads))]
+    per_b = min(d.kv_heads, max(1, round(max_chunks / d.batch)))
+    return [(_KV_GROUP, b, lo, hi) for b in range(d.batch)
+            for lo, hi in _ranges(d.kv_heads, per_b)]
 
 
 def _sub_spec(spec: AttentionSpec, unit) -> AttentionSpec:
-    b, lo, hi = unit
+    mode, _, lo, hi = unit
     d = spec.dims
-    if b == _BATCH:
+    if mode == _BATCH:
         return replace(spec, dims=replace(d, batch=hi - lo))
-    if b == _HEADS_SHARED_KV:
+    if mode == _HEADS_SHARED_KV:
         return replace(spec, dims=replace(d, heads=hi - lo))
     r = d.heads // d.kv_heads
     heads_kv = None if d.heads_kv is None else hi - lo
@@ -67,14 +71,14 @@ def _sub_spec(spec: AttentionSpec, unit) -> AttentionSpec:
 
 def _slice(t: torch.Tensor, spec: AttentionSpec, unit, kv: bool) -> torch.Tensor:
     """Slice a [B|1, H|1, ...] host tensor to one unit chunk."""
-    b, lo, hi = unit
+    mode, b, lo, hi = unit
     d = spec.dims
-    if b == _BATCH:
+    if mode == _BATCH:
         return t[lo:hi] if t.shape[0] > 1 else t
-    if b == _HEADS_SHARED_KV:
+    if mode == _HEADS_SHARED_KV:
         return t if kv or t.shape[1] == 1 else t[:, lo:hi]
     r = 1 if kv else d.heads // d.kv_heads
-    t = t[0:1]
+    t = t[b:b + 1] if t.shape[0] > 1 else t
     return t[:, lo * r: hi * r] if t.shape[1] > 1 else t
 
 
@@ -96,14 +100,14 @@ class HostPipeline:
     return them.  ``out`` may pass preallocated pinned host tensors (same keys) to avoid
     allocating pinned memory per call."""
 
-    def __init__(self, spec, device=None, max_chunks: int = 8, precision: str = "bf16"):
+    def __init__(self, spec, device=None, max_chunks: int = 16, precision: str = "bf16"):
         self.spec = api._spec(spec)
         self.precision = precision
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
                        else torch.device(device))
         units = _chunks(self.spec, max_chunks)
         if len(units) > 1 and not _same_lowering(self.spec, _sub_spec(self.spec, units[0])):
-            units = [(-1, 0, self.spec.dims.batch)]  # one chunk: the spec itself
+            units = [(_BATCH, 0, 0, self.spec.dims.batch)]  # one chunk: the spec itself
         self.units = units
         # gradients of the shared latent KV: per-chunk partials summed on the device
         self._summed = {"k"} if units[0][0] == _HEADS_SHARED_KV else set()
@@ -137,6 +141,7 @@ class HostPipeline:
                     shape[1] = d.heads
             else:
                 kv = name in ("k", "v") and d.heads_kv is not None
+                shape[0] = d.batch
                 shape[1] = d.kv_heads if kv else d.heads
             out[name] = torch.empty(shape, dtype=t.dtype).pin_memory()
         return out

@@ -58,7 +58,7 @@ for key in sys.argv[1:] or ["cfg2"]:
         print(f"{key}: {name} {tot / 1e6:.0f} MB each way: {ms:.1f} ms "
               f"({tot / ms / 1e6:.1f} GB/s per direction)", flush=True)
     import time
-    for chunks in (4, 8):
+    for chunks in (8, 16, 32):
         pipe = HostPipeline(spec, max_chunks=chunks)
         out = pipe(host, hdo)
         ms = timed(lambda: pipe(host, hdo, out=out))
