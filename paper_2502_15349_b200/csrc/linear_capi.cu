@@ -86,7 +86,7 @@ int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
   }
   dim3 grid(d->batch * d->heads * (a.dvv / kLinVB));
   ::af::note_launch();
-  kern<<<grid, kLinThreads, L::kTotal, s>>>(tq, tk, tv, p);
+  kern<<<grid, lin_threads(DK), L::kTotal, s>>>(tq, tk, tv, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
 }

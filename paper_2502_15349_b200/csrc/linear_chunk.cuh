@@ -110,11 +110,15 @@ AF_DEVICE uint4* swz_row(uint8_t* base, int r, int g) {
 
 // Warp roles: 0-7 chunk-row warps (two per TMEM lane quarter), 8-11 output warps (one per lane
 // quarter: O = s_out (OI + cp Q H) of chunk n runs while the row warps already work on chunk n+1;
-// OI and QH are double-buffered in TMEM), 12 TMA producer, 13 TMEM allocator + MMA issuer.
-constexpr int kLinThreads = 448;
+// OI and QH are double-buffered in TMEM), 12 per-step decay scan, 13 TMEM allocator + MMA issuer,
+// 14 TMA loader of Q/K, 15 TMA loader of V.  The loaders run ahead of the scan by the ring depths
+// (a single producer issuing the loads behind the scan left V late: ncu's top stall was the row
+// warps waiting on vfull; cfg5b fwd 0.473 -> 0.448 ms).
+// DK = 256 (single-stage Q/K ring) keeps the loads in warp 12 and runs without warps 14-15.
+__host__ __device__ constexpr int lin_threads(int dk) { return dk == 128 ? 512 : 448; }
 
 template <int DK, bool kReverse, bool kFac>
-__global__ void __launch_bounds__(kLinThreads, 1)
+__global__ void __launch_bounds__(lin_threads(DK), 1)
     linear_chunk_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
                         const __grid_constant__ CUtensorMap tm_v, const LinearParams p) {
@@ -122,6 +126,10 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   static_assert(DK == 128 || DK == 256, "DK");
   constexpr int kHalves = DK / 128;
   constexpr int kStages = L::kStages;
+  // DK = 128 (two-stage Q/K ring): dedicated loader warps run ahead of the scan; DK = 256 (one
+  // stage) keeps the loads behind the scan in warp 12 (measured: the loaders' spinning cost more
+  // than the run-ahead gained there)
+  constexpr bool kSplitLoad = lin_threads(DK) == 512;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + L::kQOff;
   uint8_t* sK = smem + L::kKOff;
@@ -219,7 +227,6 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     for (int n = 0; n < nchunks; ++n) {
       const int c = kReverse ? nchunks - 1 - n : n;
       const int t0 = c * kLinChunk;
-      const int st = n % kStages;
       const int pb = n & 1;
       __syncwarp();
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -266,24 +273,50 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       if (lane == 0) sFlag[pb] = fac ? 1 : 0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&scan_ready[pb]);
-      // Q, K, V of chunk n (after the scan: the scan never waits on the ring)
-      if (elect_one()) {
-        mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
-        mbar_expect_tx(&full[st], 2 * L::kQBytes);
-        for (int x = 0; x < DK / 64; ++x) {
-          tma_load_4d(sQ + st * L::kQBytes + x * (kLinChunk * 128), &tm_q, &full[st], x * 64, t0,
-                      h, b);
-          tma_load_4d(sK + st * L::kQBytes + x * (kLinChunk * 128), &tm_k, &full[st], x * 64, t0,
-                      h, b);
+      if constexpr (!kSplitLoad) {  // Q, K, V of chunk n behind its scan (single-stage Q/K ring)
+        if (elect_one()) {
+          const int st = n % kStages;
+          mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
+          mbar_expect_tx(&full[st], 2 * L::kQBytes);
+          for (int x = 0; x < DK / 64; ++x) {
+            tma_load_4d(sQ + st * L::kQBytes + x * (kLinChunk * 128), &tm_q, &full[st], x * 64,
+                        t0, h, b);
+            tma_load_4d(sK + st * L::kQBytes + x * (kLinChunk * 128), &tm_k, &full[st], x * 64,
+                        t0, h, b);
+          }
+          const int sv = n % kVSt;
+          mbar_wait(&vempty[sv], ((n / kVSt) & 1) ^ 1);
+          mbar_expect_tx(&vfull[sv], L::kVBytes);
+          tma_load_4d(sV + sv * L::kVBytes, &tm_v, &vfull[sv], vb * kLinVB, t0, h, b);
         }
-        const int sv = n % kVSt;
-        mbar_wait(&vempty[sv], ((n / kVSt) & 1) ^ 1);
-        mbar_expect_tx(&vfull[sv], L::kVBytes);
-        tma_load_4d(sV + sv * L::kVBytes, &tm_v, &vfull[sv], vb * kLinVB, t0, h, b);
+        __syncwarp();
       }
-      __syncwarp();
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+  } else if (warp == 14 || warp == 15) {
+    // ───────────── TMA loaders: Q/K ring (warp 14), V ring (warp 15) ─────────────
+    if (kSplitLoad && elect_one()) {
+      for (int n = 0; n < nchunks; ++n) {
+        const int c = kReverse ? nchunks - 1 - n : n;
+        const int t0 = c * kLinChunk;
+        if (warp == 14) {
+          const int st = n % kStages;
+          mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
+          mbar_expect_tx(&full[st], 2 * L::kQBytes);
+          for (int x = 0; x < DK / 64; ++x) {
+            tma_load_4d(sQ + st * L::kQBytes + x * (kLinChunk * 128), &tm_q, &full[st], x * 64,
+                        t0, h, b);
+            tma_load_4d(sK + st * L::kQBytes + x * (kLinChunk * 128), &tm_k, &full[st], x * 64,
+                        t0, h, b);
+          }
+        } else {
+          const int sv = n % kVSt;
+          mbar_wait(&vempty[sv], ((n / kVSt) & 1) ^ 1);
+          mbar_expect_tx(&vfull[sv], L::kVBytes);
+          tma_load_4d(sV + sv * L::kVBytes, &tm_v, &vfull[sv], vb * kLinVB, t0, h, b);
+        }
+      }
+    }
   } else if (warp == 13) {
     // ───────────── MMA issuer:  S | QH | H update | OI ─────────────
     if (elect_one()) {
@@ -417,7 +450,6 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       const int c = kReverse ? nchunks - 1 - n : n;
       const int t = c * kLinChunk + r;
       const uint32_t ph = n & 1;
-      const int st = n % kStages;
       const bool live = t < p.seq;
       (void)live;
       // (a) the producer warp's scan of log2 a for this chunk
