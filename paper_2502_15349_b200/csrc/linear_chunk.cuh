@@ -31,7 +31,7 @@ namespace af {
 
 #ifdef AF_TRACE
 // Developer timeline of CTA 0: g_lin_trace[event][chunk] = clock64().
-__device__ long long g_lin_trace[16][128];
+__device__ long long g_lin_trace[24][128];
 #define AF_LT(ev, n)                                                                  \
   do {                                                                                \
     if (blockIdx.x == 0 && (n) < 128) g_lin_trace[ev][n] = clock64();                 \
@@ -43,6 +43,16 @@ __device__ long long g_lin_trace[16][128];
 #endif
 
 constexpr int kLinChunk = 128;
+// Waits of warps that idle for long stretches (row warps between chunks, output warps, loaders):
+// with a back-off they stop taking issue slots from the scan warp on their SMSP.
+#ifndef AF_LIN_IDLE_SLEEP
+#define AF_LIN_IDLE_SLEEP 1
+#endif
+#if AF_LIN_IDLE_SLEEP
+#define LIN_IDLE_WAIT(bar, par) mbar_wait_sleep(bar, par)
+#else
+#define LIN_IDLE_WAIT(bar, par) mbar_wait(bar, par)
+#endif
 constexpr int kLinVB = 64;  // value columns per CTA
 
 // Per-step fp32 tensor with element strides [b, h, s] (0 = broadcast axis).
@@ -81,15 +91,17 @@ struct LinSmem {
   static constexpr int kVOff = kKOff + kStages * kQBytes;
   static constexpr int kVwOff = kVOff + kVStages * kVBytes;
   static constexpr int kHbOff = kVwOff + kVBytes;
-  static constexpr int kLOff = kHbOff + DK * kLinVB * 2;  // [2][128] cumsum log2 a, per parity
-  static constexpr int kUOff = kLOff + 2 * kLinChunk * 4;  // [2][128] key/value-side scale
-  static constexpr int kRawOff = kUOff + 2 * kLinChunk * 4;  // [3][128] raw factors (cp.async)
-  static constexpr int kCpOff = kRawOff + 3 * kLinChunk * 4;  // [2][128] per-row output decay
-  // [2][128] column factor e^{-+L_u} u_u of the factorised decay and [2] per-chunk flags
-  static constexpr int kEcOff = kCpOff + 2 * kLinChunk * 4;
-  static constexpr int kFlagOff = kEcOff + 2 * kLinChunk * 4;
-  // ring: full[S], empty[S]; s_full qh_full oi_full[2] h_full scan_ready[2] (1 arrival) |
-  // p_ready vw_ready h_scaled hb_ready scan_free[2] (8 row warps) | oi_empty[2] cp_ready[2] (4)
+  // per row warp [8][128]: in-chunk cumsum of log2 a, key/value-side scale, and the column
+  // factor e^{-+L_u} u_u of the factorised decay (each row warp scans the chunk itself)
+  static constexpr int kLOff = kHbOff + DK * kLinVB * 2;
+  static constexpr int kUOff = kLOff + 8 * kLinChunk * 4;
+  static constexpr int kEcOff = kUOff + 8 * kLinChunk * 4;
+  static constexpr int kRawOff = kEcOff + 8 * kLinChunk * 4;  // [2][3][128] raw factors
+  static constexpr int kCpOff = kRawOff + 2 * 3 * kLinChunk * 4;  // [2][128] per-row output decay
+  static constexpr int kFlagOff = kCpOff + 2 * kLinChunk * 4;
+  // ring: full[S], empty[S]; s_full qh_full oi_full[2] h_full scan_ready[2] (raw factors of the
+  // chunk landed; 1 arrival) | p_ready vw_ready h_scaled hb_ready scan_free[2] (raw factors read;
+  // 8 row warps) | oi_empty[2] cp_ready[2] (4)
   static constexpr int kBarOff = kFlagOff + 16;
   static constexpr int kNumBars = 2 * kStages + 17 + 2 * kVStages;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
@@ -136,12 +148,11 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
   uint8_t* sV = smem + L::kVOff;
   uint8_t* sVw = smem + L::kVwOff;
   uint8_t* sHb = smem + L::kHbOff;
-  float* sLb = reinterpret_cast<float*>(smem + L::kLOff);  // in-chunk cumsum of log2 a [2][128]
-  float* sUb = reinterpret_cast<float*>(smem + L::kUOff);  // key/value-side scale [2][128]
+  float* sLb = reinterpret_cast<float*>(smem + L::kLOff);  // [8 row warps][128]
+  float* sUb = reinterpret_cast<float*>(smem + L::kUOff);  // [8 row warps][128]
   float* sRaw = reinterpret_cast<float*>(smem + L::kRawOff);
   float* sCp = reinterpret_cast<float*>(smem + L::kCpOff);
-  float* sEcb = reinterpret_cast<float*>(smem + L::kEcOff);
-  int* sFlag = reinterpret_cast<int*>(smem + L::kFlagOff);
+  float* sEcb = reinterpret_cast<float*>(smem + L::kEcOff);  // [8 row warps][128]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* full = bars;                 // Q, K, V of one chunk landed (one tx barrier)
   uint64_t* empty = bars + kStages;      // the chunk's Q, K, V may be overwritten
@@ -198,81 +209,38 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
   constexpr uint32_t kColS = 0, kColOI = 128, kColQH = 256, kColH = 384;
 
   if (warp == 12) {
-    // ───────────── producer warp: TMA ring + the per-step decay scan ─────────────
-    // The raw per-step factors of chunk n+1 are fetched with cp.async while chunk n is handed out
-    // (plain loads would be waited on by every later barrier of the issuing warp), then
-    // log2 a, its in-chunk inclusive cumsum and the key-side scale go to sL/sU[n % 2].
+    // ───────────── producer warp: raw per-step factors (+ the TMA ring at DK = 256) ─────────────
+    // The raw factors of chunk n go to sRaw[n % 2] with cp.async (up to two chunks ahead of the
+    // row warps, which scan them themselves: a separate scan warp sat on the critical path, its
+    // few hundred instructions starved of issue slots by the busy warps of its SMSP).
     const int lane = static_cast<int>(lane_id());
     const int nraw = p.nfac + (p.u_scale.ptr != nullptr ? 1 : 0);
-    auto fetch_raw = [&](int n) {
+    for (int n = 0; n < nchunks; ++n) {
       const int c = kReverse ? nchunks - 1 - n : n;
+      const int t0 = c * kLinChunk;
+      const int pb = n & 1;
+      if (n >= 2) LIN_IDLE_WAIT(&scan_free[pb], ((n >> 1) - 1) & 1);  // rows done with chunk n-2
+      float* raw = sRaw + pb * 3 * kLinChunk;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int rr = lane * 4 + j;
-        const int t = c * kLinChunk + rr;
-        if (n < nchunks && t < p.seq) {
+        const int t = t0 + rr;
+        if (t < p.seq) {
           for (int f = 0; f < nraw; ++f) {
             const StepTensor& ts = f < p.nfac ? p.fac[f] : p.u_scale;
             const float* src = ts.ptr + b * ts.sb + h * ts.sh + t * ts.ss;
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                             smem_u32(sRaw + f * kLinChunk + rr)),
+                             smem_u32(raw + f * kLinChunk + rr)),
                          "l"(src)
                          : "memory");
           }
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    fetch_raw(0);
-    for (int n = 0; n < nchunks; ++n) {
-      const int c = kReverse ? nchunks - 1 - n : n;
-      const int t0 = c * kLinChunk;
-      const int pb = n & 1;
-      __syncwarp();
       asm volatile("cp.async.wait_group 0;" ::: "memory");
-      float x[4], us[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int rr = lane * 4 + j;
-        const bool live = t0 + rr < p.seq;
-        x[j] = 0.0f;
-        us[j] = 1.0f;
-        if (live) {
-          x[j] = p.log_const * kLog2e_;
-          for (int f = 0; f < p.nfac; ++f) x[j] += __log2f(sRaw[f * kLinChunk + rr]);
-          if (p.u_scale.ptr != nullptr) us[j] = sRaw[p.nfac * kLinChunk + rr];
-        }
-      }
-      __syncwarp();
-      fetch_raw(n + 1);  // sRaw consumed: prefetch the next chunk
-      x[1] += x[0];
-      x[2] += x[1];
-      x[3] += x[2];
-      float tot = x[3];
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const float y = __shfl_up_sync(0xffffffffu, tot, off);
-        if (lane >= off) tot += y;
-      }
-      const float excl = tot - x[3];
-      // Factorised decay D[i,u] = e^{L_i} e^{-L_u} (reverse: e^{-L_i} e^{L_u}) when every |L| of
-      // the chunk stays below 2^100: one multiply per element instead of an ex2.
-      float amax = fmaxf(fabsf(excl + x[0]), fabsf(excl + x[3]));
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1)
-        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-      const bool fac = kFac && amax <= 100.0f;
-      if (n >= 2) mbar_wait(&scan_free[pb], ((n >> 1) - 1) & 1);  // chunk n-2 done with sL[pb]
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float lj = excl + x[j];
-        sLb[pb * kLinChunk + lane * 4 + j] = lj;
-        sUb[pb * kLinChunk + lane * 4 + j] = us[j];
-        sEcb[pb * kLinChunk + lane * 4 + j] = fac ? exp2f(kReverse ? lj : -lj) * us[j] : 0.0f;
-      }
-      if (lane == 0) sFlag[pb] = fac ? 1 : 0;
       __syncwarp();
       if (lane == 0) mbar_arrive(&scan_ready[pb]);
+      if (lane == 0) AF_LT(15, n);
       if constexpr (!kSplitLoad) {  // Q, K, V of chunk n behind its scan (single-stage Q/K ring)
         if (elect_one()) {
           const int st = n % kStages;
@@ -301,7 +269,7 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
         const int t0 = c * kLinChunk;
         if (warp == 14) {
           const int st = n % kStages;
-          mbar_wait(&empty[st], ((n / kStages) & 1) ^ 1);
+          LIN_IDLE_WAIT(&empty[st], ((n / kStages) & 1) ^ 1);
           mbar_expect_tx(&full[st], 2 * L::kQBytes);
           for (int x = 0; x < DK / 64; ++x) {
             tma_load_4d(sQ + st * L::kQBytes + x * (kLinChunk * 128), &tm_q, &full[st], x * 64,
@@ -311,7 +279,7 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
           }
         } else {
           const int sv = n % kVSt;
-          mbar_wait(&vempty[sv], ((n / kVSt) & 1) ^ 1);
+          LIN_IDLE_WAIT(&vempty[sv], ((n / kVSt) & 1) ^ 1);
           mbar_expect_tx(&vfull[sv], L::kVBytes);
           tma_load_4d(sV + sv * L::kVBytes, &tm_v, &vfull[sv], vb * kLinVB, t0, h, b);
         }
@@ -386,10 +354,10 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
       const int t = c * kLinChunk + r;
       const uint32_t ph = n & 1;
       const bool live = t < p.seq;
-      mbar_wait(&cp_ready[ph], (n >> 1) & 1);
+      LIN_IDLE_WAIT(&cp_ready[ph], (n >> 1) & 1);
       const float cp = sCp[ph * kLinChunk + r];
       const float rs = (p.o_rowscale.ptr != nullptr && live) ? p.o_rowscale.at(b, h, t) : 1.0f;
-      mbar_wait(&oi_full[ph], (n >> 1) & 1);
+      LIN_IDLE_WAIT(&oi_full[ph], (n >> 1) & 1);
       if (warp == 8 && lane_id() == 0) AF_LT(9, n);
       tc_fence_after();
 #pragma unroll 1
@@ -453,14 +421,60 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
       const bool live = t < p.seq;
       (void)live;
       // (a) the producer warp's scan of log2 a for this chunk
-      const float* sL = sLb + ph * kLinChunk;
-      const float* sU = sUb + ph * kLinChunk;
-      const float* sEc = sEcb + ph * kLinChunk;
-      mbar_wait(&scan_ready[ph], (n >> 1) & 1);
+      float* sL = sLb + warp * kLinChunk;
+      float* sU = sUb + warp * kLinChunk;
+      float* sEc = sEcb + warp * kLinChunk;
+      LIN_IDLE_WAIT(&scan_ready[ph], (n >> 1) & 1);
       if (threadIdx.x == 0) AF_LT(14, n);
+      bool fac;
+      {  // this warp's scan of the chunk: L = in-chunk inclusive cumsum of log2 a, per position
+        const int lane = static_cast<int>(lane_id());
+        const float* raw = sRaw + ph * 3 * kLinChunk;
+        const int t0 = c * kLinChunk;
+        float x[4], us[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int rr = lane * 4 + j;
+          x[j] = 0.0f;
+          us[j] = 1.0f;
+          if (t0 + rr < p.seq) {
+            x[j] = p.log_const * kLog2e_;
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+              if (f < p.nfac) x[j] += __log2f(raw[f * kLinChunk + rr]);
+            if (p.u_scale.ptr != nullptr) us[j] = raw[p.nfac * kLinChunk + rr];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&scan_free[ph]);  // raw factors of this chunk read
+        x[1] += x[0];
+        x[2] += x[1];
+        x[3] += x[2];
+        float tot = x[3];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float y = __shfl_up_sync(0xffffffffu, tot, off);
+          if (lane >= off) tot += y;
+        }
+        const float excl = tot - x[3];
+        // Factorised decay D[i,u] = e^{L_i} e^{-L_u} (reverse: e^{-L_i} e^{L_u}) when every |L|
+        // of the chunk stays below 2^100: one multiply per element instead of an ex2.
+        float amax = fmaxf(fabsf(excl + x[0]), fabsf(excl + x[3]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+          amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+        fac = kFac && amax <= 100.0f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float lj = excl + x[j];
+          sL[lane * 4 + j] = lj;
+          sU[lane * 4 + j] = us[j];
+          if (fac) sEc[lane * 4 + j] = exp2f(kReverse ? lj : -lj) * us[j];
+        }
+        __syncwarp();
+      }
       const float l_r = sL[r];
       const float l_last = sL[kLinChunk - 1];
-      const bool fac = kFac && sFlag[ph] != 0;
       const float er = fac ? exp2f(kReverse ? -l_r : l_r) : 0.0f;
       const float g = exp2f(l_last);
       const float cp = kReverse ? exp2f(l_last - l_r) : exp2f(l_r);
@@ -568,8 +582,6 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
         tmem_st32(tmem + lane_base + kColS + half * 64, pk);  // packed: see split_col_lin
         tmem_st_wait();
       }
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&scan_free[ph]);  // last read of sL / sU of this chunk
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(p_ready);

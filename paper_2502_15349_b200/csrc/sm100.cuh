@@ -45,6 +45,9 @@ AF_DEVICE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 // try_wait with a suspend-time hint: a waiting warp sleeps in the barrier unit (up to the hint, in
 // ns) instead of re-issuing the probe, leaving issue slots to the warps doing row work.
+#ifndef AF_MBAR_SLEEP_NS
+#define AF_MBAR_SLEEP_NS 64
+#endif
 #ifndef AF_MBAR_SUSPEND_NS
 #define AF_MBAR_SUSPEND_NS 0  // swept: 1000 ns and 0x989680 are no faster than a plain probe loop
 #endif
@@ -71,6 +74,13 @@ AF_DEVICE bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 AF_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// Wait with a nanosleep back-off: for warps that idle for long stretches (they would otherwise
+// keep re-issuing the probe and take issue slots from a latency-critical warp on their SMSP).
+AF_DEVICE void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+    __nanosleep(AF_MBAR_SLEEP_NS);
   }
 }
 
