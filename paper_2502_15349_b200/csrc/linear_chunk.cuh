@@ -446,6 +446,7 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
           }
         }
         __syncwarp();
+        if (threadIdx.x == 0) AF_LT(16, n);
         if (lane == 0) mbar_arrive(&scan_free[ph]);  // raw factors of this chunk read
         x[1] += x[0];
         x[2] += x[1];
@@ -457,6 +458,7 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
           if (lane >= off) tot += y;
         }
         const float excl = tot - x[3];
+        if (threadIdx.x == 0) AF_LT(17, n);
         // Factorised decay D[i,u] = e^{L_i} e^{-L_u} (reverse: e^{-L_i} e^{L_u}) when every |L|
         // of the chunk stays below 2^100: one multiply per element instead of an ex2.
         float amax = fmaxf(fabsf(excl + x[0]), fabsf(excl + x[3]));
@@ -473,12 +475,14 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
         }
         __syncwarp();
       }
+      if (threadIdx.x == 0) AF_LT(18, n);
       const float l_r = sL[r];
       const float l_last = sL[kLinChunk - 1];
       const float er = fac ? exp2f(kReverse ? -l_r : l_r) : 0.0f;
       const float g = exp2f(l_last);
       const float cp = kReverse ? exp2f(l_last - l_r) : exp2f(l_r);
       const float wgt = sU[r] * (kReverse ? exp2f(l_r) : exp2f(l_last - l_r));
+      if (threadIdx.x == 0) AF_LT(19, n);
       if (half == 0) {  // hand cp to the output warps (sCp[ph] is free once chunk n-2 is out)
         if (n >= 2) mbar_wait(&oi_empty[ph], ((n >> 1) - 1) & 1);
         sCp[ph * kLinChunk + r] = cp;

@@ -15,10 +15,14 @@ import paper_2502_15349_b200 as af  # noqa: E402
 from paper_2502_15349_b200 import runtime as rt  # noqa: E402
 
 key = sys.argv[1] if len(sys.argv) > 1 else "cfg5b"
+bwd = len(sys.argv) > 2 and sys.argv[2] == "bwd"  # trace the last chunk-kernel run of the VJP
 spec = bench.build_spec(key)
-arrays, _ = bench.device_inputs(spec, torch.device("cuda"), 0)
+arrays, dout = bench.device_inputs(spec, torch.device("cuda"), 0)
 for _ in range(3):
-    af.linear_forward(spec, arrays)
+    if bwd:
+        af.linear_backward(spec, arrays, dout)
+    else:
+        af.linear_forward(spec, arrays)
 torch.cuda.synchronize()
 buf = np.zeros((24, 128), dtype=np.int64)
 fn = rt.lib().af_debug_lin_trace_read
@@ -30,9 +34,8 @@ names = {15: "scan: scan_ready arrive", 14: "rows: scan_ready passed", 4: "rows:
          7: "rows: s_full passed", 8: "rows: P written", 11: "rows: h_full+qh_full passed",
          12: "rows: bf16 H written", 0: "mma: Q/K full", 1: "mma: hb_ready+oi_empty",
          3: "mma: vw+h_scaled", 2: "mma: p_ready+vfull", 9: "out: oi_full passed",
-         10: "out: O written", 16: "scan: loop top", 17: "scan: raw landed",
-         18: "scan: computed", 19: "scan: scan_free passed",
-         20: "scan: log2 done", 21: "scan: prefetch issued", 22: "scan: cumsum done"}
+         10: "out: O written", 16: "rows: log2 done", 17: "rows: cumsum done",
+         18: "rows: scan stored", 19: "rows: row factors done"}
 ss = range(8, 56)
 base = buf[14]
 period = np.mean([buf[14, n + 1] - buf[14, n] for n in ss])
