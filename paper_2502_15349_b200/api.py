@@ -58,10 +58,11 @@ def _empty(key: str, shape, dtype, device) -> torch.Tensor:
     shape = tuple(int(x) for x in shape)
     if cache is None:
         return torch.empty(shape, dtype=dtype, device=device)
-    t = cache.get(key)
-    if t is None or tuple(t.shape) != shape or t.dtype != dtype or t.device != torch.device(device):
+    ck = (key, shape, dtype, str(device))  # several chunk widths may share one cache
+    t = cache.get(ck)
+    if t is None:
         t = torch.empty(shape, dtype=dtype, device=device)
-        cache[key] = t
+        cache[ck] = t
     return t
 
 

@@ -120,11 +120,12 @@ class HostPipeline:
 
     # device slot tensor for one host slice (reused across calls of the same shape)
     def _slot(self, s: int, name: str, like: torch.Tensor) -> torch.Tensor:
-        t = self._slots[s].get(name)
-        if t is None or t.shape != like.shape or t.dtype != like.dtype:
+        key = (name, tuple(like.shape), like.dtype)  # ramp units of several widths coexist
+        t = self._slots[s].get(key)
+        if t is None:
             with torch.cuda.stream(self.h2d):
                 t = torch.empty(like.shape, dtype=like.dtype, device=self.device)
-            self._slots[s][name] = t
+            self._slots[s][key] = t
         return t
 
     def _outputs_like(self, dev_out: dict) -> dict:
