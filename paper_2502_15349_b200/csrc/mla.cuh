@@ -18,12 +18,28 @@
 // latent ring runs 4 stages.
 // Warps: 0-3 softmax rows (one row per thread, FA4-style lazy rescale), 4 TMA, 5 MMA.
 #pragma once
+#include <climits>
 #include <cuda.h>
 #include "params.h"
 #include "sm100.cuh"
 #include "parallel_fwd.cuh"
 
 namespace af {
+
+// Developer timeline (-DAF_MLA_TRACE): SM-clock stamps of CTA 0 (the heaviest causal prefill
+// tile, value half 0) per key tile, read back with af_debug_mla_trace.
+#ifdef AF_MLA_TRACE
+__device__ long long g_mla_trace[10][128];
+#define MLA_TRACE(ev, n)                                                              \
+  do {                                                                                \
+    if (!kDecode && blockIdx.x == 0 && lane_id() == 0 && (n) < 128)                   \
+      g_mla_trace[ev][n] = clock64();                                                 \
+  } while (0)
+#else
+#define MLA_TRACE(ev, n) \
+  do {                   \
+  } while (0)
+#endif
 
 constexpr int kMlaDqk = 576;
 constexpr int kMlaDv = 512;
@@ -165,6 +181,7 @@ __global__ void __launch_bounds__(192, 1)
       for (int n = 0; n < nk; ++n) {
         const int s = n % kSt;
         mbar_wait(&k_empty[s], ((n / kSt) & 1) ^ 1);
+        MLA_TRACE(0, n);
         mbar_expect_tx(&k_full[s], L::kKBytes);
         const int j0 = kv_lo + n * kN;
         for (int c = 0; c < 9; ++c)
@@ -181,6 +198,7 @@ __global__ void __launch_bounds__(192, 1)
         const int s = n & 1;  // TMEM S buffer
         const int st = n % kSt;
         mbar_wait(&k_full[st], (n / kSt) & 1);
+        MLA_TRACE(1, n);
         tc_fence_after();
         const uint32_t kb = aK + st * L::kKBytes;
 #pragma unroll
@@ -203,6 +221,7 @@ __global__ void __launch_bounds__(192, 1)
         const int st = n % kSt;
         if (n + 1 < nk) issue_s(n + 1);
         mbar_wait(p_ready, n & 1);
+        MLA_TRACE(2, n);
         tc_fence_after();
         // V = latent columns [256*half, +256): boxes 4*half .. 4*half+3 of the tile, MN-major
         const uint32_t vbase = aK + st * L::kKBytes + half * 4 * L::kKBox;
@@ -248,6 +267,7 @@ __global__ void __launch_bounds__(192, 1)
       const int s = n & 1;
       const int j0 = kv_lo + n * kN;
       mbar_wait(&s_full[s], (n >> 1) & 1);
+      MLA_TRACE(3, n);
       tc_fence_after();
       uint32_t sr[kN];
 #pragma unroll
@@ -255,16 +275,19 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld32(tmem + lane_base + s * kN + c * 32,
                   *reinterpret_cast<uint32_t(*)[32]>(&sr[c * 32]));
       tmem_ld_wait();
+      MLA_TRACE(5, n);
       float x[kN];
-      float bmax = -INFINITY;
       const bool full = (j0 + kN <= kv_hi) && (kDecode || !p.causal || j0 + kN - 1 <= q0);
+      // branch-free per element (a short-circuit keep test compiled to a branch + reconvergence
+      // per score and made this loop the prefill's critical path: ~3.7k clk per 64-key tile)
+      const int lim = full ? INT_MAX : min(kv_hi - j0, (kDecode || !p.causal) ? INT_MAX : i - j0 + 1);
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
       for (int e = 0; e < kN; ++e) {
-        bool keep = true;
-        if (!full) keep = (j0 + e < kv_hi) && (kDecode || !p.causal || j0 + e <= i);
-        x[e] = keep ? __uint_as_float(sr[e]) * p.scale_log2 : -INFINITY;
-        bmax = fmaxf(bmax, x[e]);
+        x[e] = (e < lim) ? __uint_as_float(sr[e]) * p.scale_log2 : -INFINITY;
+        mx4[e & 3] = fmaxf(mx4[e & 3], x[e]);
       }
+      const float bmax = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float m_new = fmaxf(m_run, bmax);
       const bool need = (m_new - m_run) > 8.0f;
       float factor = 1.0f;
@@ -273,6 +296,7 @@ __global__ void __launch_bounds__(192, 1)
         m_run = m_new;
       }
       const float m_use = (m_run == -INFINITY) ? 0.0f : m_run;
+      MLA_TRACE(6, n);
       uint32_t pk[kN / 2];
       float lsum = 0.0f;
 #pragma unroll
@@ -282,11 +306,13 @@ __global__ void __launch_bounds__(192, 1)
         pk[e / 2] = pack_bf16(e0, e1);
       }
       l_run = l_run * factor + lsum;
+      MLA_TRACE(7, n);
       if constexpr (kN == 64)
         tmem_st32(tmem + lane_base + s * kN, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
       else
         tmem_st16(tmem + lane_base + s * kN, *reinterpret_cast<uint32_t(*)[16]>(&pk[0]));
       tmem_st_wait();
+      MLA_TRACE(8, n);
       if (n > 0 && __any_sync(0xffffffffu, need)) {
         mbar_wait(o_done, (n - 1) & 1);
         tc_fence_after();
@@ -304,6 +330,7 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(p_ready);
+      MLA_TRACE(4, n);
     }
     // ───────────── epilogue ─────────────
     if (nk > 0) {

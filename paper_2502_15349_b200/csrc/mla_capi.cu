@@ -146,3 +146,9 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
 }
+
+#ifdef AF_MLA_TRACE
+extern "C" int af_debug_mla_trace(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, af::g_mla_trace, sizeof(af::g_mla_trace)));
+}
+#endif
