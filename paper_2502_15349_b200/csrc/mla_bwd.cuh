@@ -241,10 +241,13 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
           const int j = k0 + cb + e + x;
-          const bool keep = full_blk || kept(p.mask, i, j, p.seq_k);
-          const float pe = keep ? ex2(fmaf(__uint_as_float(sr[e + x]), p.scale_log2, -l2)) : 0.0f;
+          const bool keep = full_blk | kept(p.mask, i, j, p.seq_k);
+          // ex2(-inf) = 0: masked scores without a branch around the MUFU op; dS' is selected
+          // (not multiplied by the zero) since dP of a masked position need not be finite
+          const float pe =
+              ex2(keep ? fmaf(__uint_as_float(sr[e + x]), p.scale_log2, -l2) : -INFINITY);
           pv[x] = pe;
-          dv[x] = pe * (__uint_as_float(dr[e + x]) - dl) * p.scale;
+          dv[x] = keep ? pe * (__uint_as_float(dr[e + x]) - dl) * p.scale : 0.0f;
         }
         pw[e / 2] = pack_bf16(pv[0], pv[1]);
         dw[e / 2] = pack_bf16(dv[0], dv[1]);

@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
               const int i = q0 + cb + c2 * 32 + e + x;
-              const bool keep = fullblk || (kept(p.mask, i, j, p.seq_k) && i < p.seq_q);
+              const bool keep = fullblk | (kept(p.mask, i, j, p.seq_k) & (i < p.seq_q));
               const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
               pv[x] = keep ? ex2(fmaf(cap_out, t, -lse_s[c2 * 32 + e + x])) : 0.0f;
               gv[x] = cap_g * fmaf(-t, t, 1.0f);
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
               const int i = q0 + cb + c2 * 32 + e + x;
-              const bool keep = fullblk || (kept(p.mask, i, j, p.seq_k) && i < p.seq_q);
+              const bool keep = fullblk | (kept(p.mask, i, j, p.seq_k) & (i < p.seq_q));
               const float rc = norm ? rcp_approx(fmaxf(lse_s[c2 * 32 + e + x], 1.0f)) : 1.0f;
               const float m = ex2(static_cast<float>(i - j) * slope);
               const float z = __uint_as_float(sr[e + x]) * p.scale * m;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
 #pragma unroll
               for (int x = 0; x < 2; ++x) {
                 const int i = q0 + cb + c2 * 32 + e + x;
-                const bool keep = kept(p.mask, i, j, p.seq_k) && i < p.seq_q;
+                const bool keep = kept(p.mask, i, j, p.seq_k) & (i < p.seq_q);
                 pv[x] = keep ? ex2(fmaf(__uint_as_float(sr[e + x]), p.scale_log2,
                                         -lse_s[c2 * 32 + e + x]))
                              : 0.0f;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
                 const int i = q0 + cb + c2 * 32 + e + x;
                 const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
                                      zb - slope * static_cast<float>(e + x));
-                const bool keep = kept(p.mask, i, j, p.seq_k) && i < p.seq_q;
+                const bool keep = kept(p.mask, i, j, p.seq_k) & (i < p.seq_q);
                 const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
                 bits |= (keep && g) ? (1u << (e + x)) : 0u;
                 pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             float pv[2], gv[2];
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
-              const bool keep = fullblk || kept(p.mask, i, jb + e + x, p.seq_k);
+              const bool keep = fullblk | kept(p.mask, i, jb + e + x, p.seq_k);
               const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
               pv[x] = keep ? ex2(fmaf(cap_out, t, -l2)) : 0.0f;
               gv[x] = cap_g * fmaf(-t, t, 1.0f);
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 #pragma unroll
             for (int x = 0; x < 2; ++x) {
               const int jj = jb + e + x;
-              const bool keep = live && (fullblk || kept(p.mask, i, jj, p.seq_k));
+              const bool keep = live & (fullblk | kept(p.mask, i, jj, p.seq_k));
               const float m = ex2(static_cast<float>(i - jj) * slope);
               const float z = __uint_as_float(sr[e + x]) * p.scale * m;
               pv[x] = keep ? z * rc : 0.0f;
@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
               for (int x = 0; x < 2; ++x) {
                 const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
                                      zb + slope * static_cast<float>(e + x));
-                const bool keep = live && kept(p.mask, i, jb + e + x, p.seq_k);
+                const bool keep = live & kept(p.mask, i, jb + e + x, p.seq_k);
                 const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
                 bits |= (keep && g) ? (1u << (e + x)) : 0u;
                 pv[x] = keep ? apply_act<kAct>(z) : 0.0f;

@@ -15,6 +15,7 @@
 // packed bf16, and the MMA warp consumes P straight from TMEM (A-from-TMEM) for O_t += P V.
 // The two query tiles ping-pong so the tensor pipe runs tile 1's MMAs while tile 0's row math runs.
 #pragma once
+#include <climits>
 #include <cuda.h>
 #include "params.h"
 #include "sm100.cuh"
@@ -109,11 +110,12 @@ AF_DEVICE bool block_fully_kept(const MaskParams& m, int r0, int c0, int seq_k) 
   if (m.window > 0 && (r0 + kBlockM - 1) + m.diag_offset - c0 >= m.window) return false;
   return true;
 }
+// Branch-free band test: keep iff lo <= j < hi, with the row's bounds loop-invariant so unrolled
+// callers hoist them (short-circuit forms compiled to a branch + reconvergence per score).
 AF_DEVICE bool kept(const MaskParams& m, int i, int j, int seq_k) {
-  bool k = j < seq_k;
-  if (m.causal) k = k && (j <= i + m.diag_offset);
-  if (m.window > 0) k = k && (i + m.diag_offset - j < m.window);
-  return k;
+  const int hi = m.causal ? min(seq_k, i + m.diag_offset + 1) : seq_k;
+  const int lo = m.window > 0 ? i + m.diag_offset - m.window + 1 : INT_MIN;
+  return (j >= lo) & (j < hi);
 }
 
 template <int kAct>
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
 #pragma unroll
           for (int c = 0; c < 64; ++c) {
             const float x = kCap ? cap_out * tanh_precise(cap_in * s[c]) : s[c] * p.scale_log2;
-            s[c] = (full || kept(p.mask, i, cb + c, p.seq_k)) ? x : -INFINITY;
+            s[c] = (full | kept(p.mask, i, cb + c, p.seq_k)) ? x : -INFINITY;
             bmax = fmaxf(bmax, s[c]);
           }
         }
@@ -582,7 +584,7 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
 #pragma unroll
           for (int c = 0; c < kBlockN; ++c) {
             const float x = kCap ? cap_out * tanh_precise(cap_in * s[c]) : s[c] * p.scale_log2;
-            s[c] = (full || kept(p.mask, i, c0 + c, p.seq_k)) ? x : -INFINITY;
+            s[c] = (full | kept(p.mask, i, c0 + c, p.seq_k)) ? x : -INFINITY;
             bmax = fmaxf(bmax, s[c]);
           }
         }
