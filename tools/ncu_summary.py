@@ -30,7 +30,10 @@ def summarize(rep):
         for k, m in KEYS.items():
             if m not in d:
                 continue
-            v = float(d[m].replace(",", ""))
+            try:
+                v = float(d[m].replace(",", ""))
+            except ValueError:  # "no data" for metrics a short kernel did not report
+                continue
             if k.endswith("_bytes"):
                 v *= SCALE.get(u[m], 1.0)
             rec[k] = v

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-end evidence on one GPU box: bench lines for every config (with the CPU baseline), the
 # cfg2 launch list, and --set full captures of the dominant kernels.  TAG names the files.
-TAG=${TAG:-r01e}
+TAG=${TAG:-r01g}
 O=gpurun_out
 mkdir -p $O
 timeout 1500 python bench.py --config all > $O/bench_${TAG}_all.log 2>&1

@@ -1,4 +1,4 @@
-O=gpurun_out; TAG=r01e
+O=gpurun_out; TAG=${TAG:-r01g}
 timeout 900 ncu --set full --clock-control none --import-source on -c 8 -k regex:"mla_" -o $O/prof_cfg4a_${TAG} -f python bench.py --config cfg4a --steps 1 --warmup 0 --no-cpu > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none -c 8 -k regex:"linear_" -o $O/prof_cfg5a_${TAG} -f python bench.py --config cfg5a --steps 1 --warmup 0 --no-cpu > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none -c 8 -k regex:"linear_" -o $O/prof_cfg5b_${TAG} -f python bench.py --config cfg5b --steps 1 --warmup 0 --no-cpu > /dev/null 2>&1
