@@ -8,14 +8,14 @@
 //   decode  : rows = the 128 heads of one query token (seq_q = 1, unmasked — SURVEY §0), grid
 //             over (batch, key split, value half); splits are merged by mla_combine_kernel.
 // Budget: the fp32 O accumulator of 128 rows x 512 would fill all of TMEM, so each CTA owns one
-// 256-wide value half (the two halves recompute S; 1.53x the QK^T work).  Q (128 x 576 bf16,
-// 144 KB) is split: columns [0, 256) sit in TMEM as the A operand of TS MMAs (no shared-memory
-// A reads — the S GEMM at N = 64 is otherwise bound by re-reading Q from smem every tile),
-// columns [256, 576) stay in smem (80 KB), which leaves room for a 2-stage ring of 64-key latent
-// tiles (72 KB each).  TMEM: S double buffer [0,128) (P packed in place) | O half [128,384) |
-// Q[:, 0:256] packed bf16 [384,512).  Decode (32-key tiles) uses only [0,64) for S and puts
-// Q[:, 256:384] at [64,128): 24 of the 36 QK^T k-steps read no smem A, Q smem is 48 KB and the
-// latent ring runs 4 stages.
+// 256-wide value half (the two halves recompute S; 1.53x the QK^T work).  Both prefill and decode
+// stream 32-key latent tiles (36 KB, 4-stage ring): the S double buffer then takes TMEM [0,64)
+// only, so Q (128 x 576 bf16) columns [0, 384) sit in TMEM as the A operand of TS MMAs
+// ([384,512) and [64,128); no shared-memory A re-reads — at N = 32 the S GEMM is otherwise bound
+// by re-reading Q from smem every tile) and only Q[:, 384:576] (48 KB) stays in smem.
+// TMEM: S double buffer [0,64) (P packed in place) | Q[:, 256:384] [64,128) | O half [128,384) |
+// Q[:, 0:256] [384,512).  (64-key prefill tiles — AF_MLA_PREFILL_N=64 — keep Q[:, 0:256] in TMEM
+// and a 2-stage ring; measured 9 + 10 % slower once the softmax rows stopped branching.)
 // Warps: 0-3 softmax rows (one row per thread, FA4-style lazy rescale), 4 TMA, 5 MMA.
 #pragma once
 #include <climits>
@@ -50,8 +50,11 @@ constexpr int kMlaHalf = 256;
 #ifndef AF_MLA_DECODE_QT
 #define AF_MLA_DECODE_QT 384
 #endif
+#ifndef AF_MLA_PREFILL_QT
+#define AF_MLA_PREFILL_QT 384  // 32-key prefill tiles leave TMEM [64,128) free for Q[:, 256:384]
+#endif
 #ifndef AF_MLA_PREFILL_N
-#define AF_MLA_PREFILL_N 64
+#define AF_MLA_PREFILL_N 32  // swept after the branch-free softmax: 32 beats 64 by ~9 %
 #endif
 template <bool kDecode>
 struct MlaTile {
@@ -59,7 +62,8 @@ struct MlaTile {
   static constexpr int kStages = kDecode ? 4 : (AF_MLA_PREFILL_N == 32 ? 4 : 2);
   // Q columns [0, kQT) held in TMEM as TS-MMA A operand; decode's 32-key S double buffer leaves
   // TMEM columns [64, 128) free for Q columns [256, 384), so fewer S MMAs stream Q from smem
-  static constexpr int kQT = kDecode ? AF_MLA_DECODE_QT : 256;
+  static constexpr int kQT = kDecode ? AF_MLA_DECODE_QT
+                                     : (AF_MLA_PREFILL_N == 32 ? AF_MLA_PREFILL_QT : 256);
 };
 constexpr int kMlaN = 64;     // prefill tile (split lengths of decode are multiples of both)
 
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(192, 1)
   constexpr int kSt = MlaTile<kDecode>::kStages;
   constexpr int kQT = MlaTile<kDecode>::kQT;
   constexpr int kQB = (kMlaDqk - kQT) / 64;  // Q boxes of 64 columns in smem
-  static_assert(kQT == 256 || (kDecode && kQT == 384 && 2 * kN <= 64), "TMEM map");
+  static_assert(kQT == 256 || (kQT == 384 && 2 * kN <= 64), "TMEM map");
   using L = MlaSmem<kN, kSt, kQT>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sQ = smem + L::kQOff;

@@ -51,15 +51,16 @@ def _parallel(spec: AttentionSpec) -> list[str]:
         if d.seq_q == 1:
             lines += ["  kernel K3 mla_fwd_kernel<decode> cta 192 (4 softmax warps, TMA, MMA) "
                       "grid batch x splits x value_half;",
-                      "  buffer q bf16[heads x 576]: cols [0,256) tmem (TS MMA A), [256,576) smem;",
+                      "  buffer q bf16[heads x 576]: cols [0,384) tmem (TS MMA A), [384,576) smem;",
                       "  buffer kv bf16[32 keys x 576] ring stages=4 (tma box 64x32, swizzle128);",
-                      "  tmem S[0,64) double | O_half[128,384) | Q[384,512);",
+                      "  tmem S[0,64) double | Q[64,128) | O_half[128,384) | Q[384,512);",
                       "  combine mla_combine_kernel (LSE-weighted split merge);"]
         else:
             lines += ["  kernel K3 mla_fwd_kernel<prefill> cta 192 grid q_tiles x heads x "
                       "value_half;",
-                      "  buffer kv bf16[64 keys x 576] ring stages=2;",
-                      "  tmem S[0,128) double | O_half[128,384) | Q[384,512);"]
+                      "  buffer q bf16[128 x 576]: cols [0,384) tmem (TS MMA A), [384,576) smem;",
+                      "  buffer kv bf16[32 keys x 576] ring stages=4;",
+                      "  tmem S[0,64) double | Q[64,128) | O_half[128,384) | Q[384,512);"]
     else:
         dv_k = min(dv, 128)
         stages = 1 if dq > 128 else 2
