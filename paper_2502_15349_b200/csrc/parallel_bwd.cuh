@@ -29,6 +29,30 @@
 
 namespace af {
 
+// Developer timeline (-DAF_BWD_TRACE): SM-clock stamps of one K2b CTA, read back with
+// af_debug_bwd_trace.  Compiled out of the product build.
+#ifdef AF_BWD_TRACE
+__device__ long long g_bwd_trace[10][256];
+#define BWD_TRACE(ev, n)                                                                    \
+  do {                                                                                      \
+    if (blockIdx.x == 0 && blockIdx.y == 37 && lane_id() == 0 && (n) < 256)                \
+      g_bwd_trace[ev][n] = clock64();                                                       \
+  } while (0)
+__device__ long long g_bwd2a_trace[6][512];
+#define BWD2A_TRACE(ev, n)                                                                  \
+  do {                                                                                      \
+    if (blockIdx.x == 40 && blockIdx.y == 5 && lane_id() == 0 && (n) < 512)                \
+      g_bwd2a_trace[ev][n] = clock64();                                                     \
+  } while (0)
+#else
+#define BWD2A_TRACE(ev, n) \
+  do {                     \
+  } while (0)
+#define BWD_TRACE(ev, n) \
+  do {                   \
+  } while (0)
+#endif
+
 #ifndef AF_BWD_POLY_MASK
 #define AF_BWD_POLY_MASK 6  // fully-kept tiles: pairs with (e & mask) == 0 use exp2_poly (25 %; swept: 12.5 % 13.4 ms, 25 % 13.3 ms, 100 % 14.9 ms, none 14.0 ms)
 #endif
@@ -118,6 +142,13 @@ AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float
 
 // ═══════════════════════════════ K2a: dK, dV ═══════════════════════════════
 
+// dS^T of K2a in shared memory instead of TMEM, so dP of the next tile can be issued ahead of dK:
+// parity-green but measured slower (cfg2 bwd 12.6-12.9 -> 13.1-13.2 ms; tools/trace_bwd.py) —
+// with one 32 KB buffer (no smem for two) the rows wait for dK of the previous tile before
+// writing, which costs more than the earlier dP saves.  Off.
+#ifndef AF_K2A_DS_SMEM
+#define AF_K2A_DS_SMEM 0
+#endif
 template <int D, int DV>
 struct BwdKVSmem {
   static constexpr int kStages = 2;
@@ -131,9 +162,13 @@ struct BwdKVSmem {
   static constexpr int kOOff = kQOff + kStages * kQBytes;
   static constexpr int kLseOff = kOOff + kStages * kOBytes;
   static constexpr int kDeltaOff = kLseOff + kStages * kBlockM * 4;
-  static constexpr int kBarOff = kDeltaOff + kStages * kBlockM * 4;
-  // kv_full, full[S], empty[S], s_full, dp_full, p_ready, ds_ready, acc_full
-  static constexpr int kNumBars = 1 + 2 * kStages + 5;
+  // dS^T [128 keys][128 queries] bf16, K-major SW128 (A operand of dK += dS^T Q): kept in smem so
+  // dP of the next tile can be issued before dK of this one (TMEM would alias it)
+  static constexpr int kDsOff = AF_K2A_DS_SMEM ? ((kDeltaOff + kStages * kBlockM * 4 + 1023) & ~1023)
+                                               : kDeltaOff + kStages * kBlockM * 4;
+  static constexpr int kBarOff = kDsOff + (AF_K2A_DS_SMEM ? kBlockN * kBlockM * 2 : 0);
+  // kv_full, full[S], empty[S], s_full, dp_full, p_ready, ds_ready, acc_full, ds_free
+  static constexpr int kNumBars = 1 + 2 * kStages + 6;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -169,6 +204,8 @@ __global__ void __launch_bounds__(kKvThreads, 1)
   uint64_t* p_ready = dp_full + 1;
   uint64_t* ds_ready = p_ready + 1;
   uint64_t* acc_full = ds_ready + 1;
+  uint64_t* ds_free = acc_full + 1;  // dK of the previous tile has read sDS
+  uint8_t* sDS = smem + L::kDsOff;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -199,6 +236,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
     mbar_init(p_ready, kRW);
     mbar_init(ds_ready, kRW);
     mbar_init(acc_full, 1);
+    mbar_init(ds_free, 1);
     fence_barrier_init();
   }
   if (warp == kMmaW) tmem_alloc<512>(tmem_slot);
@@ -287,6 +325,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
       for (int n = 0; n < niter; ++n) {
         const int s = n % kStages;
         mbar_wait(p_ready, n & 1);
+        BWD2A_TRACE(0, n);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kBlockM / 16; ++kk)
@@ -298,14 +337,30 @@ __global__ void __launch_bounds__(kKvThreads, 1)
           issue_s(n + 1);
         }
         mbar_wait(ds_ready, n & 1);
+        BWD2A_TRACE(1, n);
         tc_fence_after();
+        if constexpr (AF_K2A_DS_SMEM) {
+          // dS^T lives in smem: dP of the next tile goes first (the row warps start on it while
+          // the pipe runs dK of this tile)
+          if (n + 1 < niter) issue_dp(n + 1);
+          const uint32_t aDS = smem_u32(sDS);
 #pragma unroll
-        for (int kk = 0; kk < kBlockM / 16; ++kk)
-          mma_ts(tmem + kColDK, tmem + kColDP + (kCpw * (kk / (kCpw / 16)) + 8 * (kk % (kCpw / 16))),
-                 make_sdesc(aQ + s * L::kQBytes + kk * 16 * 128, kBlockM * 128, 1024), id_dk,
-                 (n > 0 || kk > 0));
-        mma_commit(&empty[s]);
-        if (n + 1 < niter) issue_dp(n + 1);
+          for (int kk = 0; kk < kBlockM / 16; ++kk)
+            mma_ss(tmem + kColDK, kmajor(aDS, kk, kBlockN),
+                   make_sdesc(aQ + s * L::kQBytes + kk * 16 * 128, kBlockM * 128, 1024), id_dk,
+                   (n > 0 || kk > 0));
+          mma_commit(ds_free);
+          mma_commit(&empty[s]);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < kBlockM / 16; ++kk)
+            mma_ts(tmem + kColDK,
+                   tmem + kColDP + (kCpw * (kk / (kCpw / 16)) + 8 * (kk % (kCpw / 16))),
+                   make_sdesc(aQ + s * L::kQBytes + kk * 16 * 128, kBlockM * 128, 1024), id_dk,
+                   (n > 0 || kk > 0));
+          mma_commit(&empty[s]);
+          if (n + 1 < niter) issue_dp(n + 1);
+        }
       }
       mma_commit(acc_full);
     }
@@ -337,6 +392,7 @@ __global__ void __launch_bounds__(kKvThreads, 1)
       const float* del_s = sDelta + s * kBlockM + cb;
 
       mbar_wait(s_full, n & 1);
+      if (warp == 0) BWD2A_TRACE(2, n);
       tc_fence_after();
       uint32_t pk[16 * kNP];
       uint32_t gk[16 * kNP];  // soft-cap derivative factors (kActSoftcap only)
@@ -457,8 +513,10 @@ __global__ void __launch_bounds__(kKvThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(p_ready);
+      if (warp == 0) BWD2A_TRACE(3, n);
 
       mbar_wait(dp_full, n & 1);
+      if (warp == 0) BWD2A_TRACE(4, n);
       tc_fence_after();
       uint32_t dsk[16 * kNP];
 #pragma unroll
@@ -469,14 +527,29 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         make_ds<kFamily, kAct, false>(pk + c2 * 16, dr, del_s + c2 * 32, 0.0f, gmask[c2],
                                       dsk + c2 * 16, gk + c2 * 16);
       }
-      if constexpr (kNP == 2)
-        tmem_st32(tmem + lane_base + kColDP + pcol, *reinterpret_cast<uint32_t(*)[32]>(dsk));
-      else
-        tmem_st16(tmem + lane_base + kColDP + pcol, *reinterpret_cast<uint32_t(*)[16]>(dsk));
-      tmem_st_wait();
-      tc_fence_before();
+      if constexpr (AF_K2A_DS_SMEM) {
+        static_assert(kNP == 1, "dS^T smem slice is 32 query columns per warp");
+        // this row's 32 query columns of dS^T: four 16-byte granules of the K-major SW128 tile
+        if (n > 0) mbar_wait(ds_free, (n - 1) & 1);
+        uint8_t* box = sDS + (cb / 64) * (kBlockN * 128);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int g = (cb % 64) / 8 + q;
+          *reinterpret_cast<uint4*>(box + row * 128 + ((g ^ (row & 7)) << 4)) =
+              make_uint4(dsk[q * 4], dsk[q * 4 + 1], dsk[q * 4 + 2], dsk[q * 4 + 3]);
+        }
+        fence_proxy_async_smem();
+      } else {
+        if constexpr (kNP == 2)
+          tmem_st32(tmem + lane_base + kColDP + pcol, *reinterpret_cast<uint32_t(*)[32]>(dsk));
+        else
+          tmem_st16(tmem + lane_base + kColDP + pcol, *reinterpret_cast<uint32_t(*)[16]>(dsk));
+        tmem_st_wait();
+        tc_fence_before();
+      }
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(ds_ready);
+      if (warp == 0) BWD2A_TRACE(5, n);
     }
     // ───────────── epilogue: slices 0-1 store dV rows, slices 2-3 store dK rows ─────────────
     if (niter > 0) {
@@ -666,6 +739,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         const bool more = n + 1 < nk;
         for (int x = 0; x < 2; ++x) {
           mbar_wait(&ds_ready[x], n & 1);
+          BWD_TRACE(x, n);
           tc_fence_after();
 #pragma unroll
           for (int k4 = 0; k4 < 4; ++k4) {
@@ -683,6 +757,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
               tc_fence_after();
             }
             issue_sdp(n + 1, x);
+            BWD_TRACE(2 + x, n);
           }
         }
       }
@@ -743,6 +818,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const int c0 = (band.jb_lo + n) * kBlockN;
       const bool fullblk = tile_fully_kept(p.mask, q0, c0, p.seq_q, p.seq_k);
       mbar_wait(&s_full[half], n & 1);
+      if (warp % 8 == 0) BWD_TRACE(4 + half, n);
       tc_fence_after();
       uint32_t pk[16 * kNP];
       uint32_t gk[16 * kNP];  // soft-cap derivative factors (kActSoftcap only)
@@ -841,6 +917,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         gmask[c2] = bits;
       }
       mbar_wait(&dp_full[half], n & 1);
+      if (warp % 8 == 0) BWD_TRACE(6 + half, n);
       tc_fence_after();
       uint32_t dsk[16 * kNP];
 #pragma unroll
@@ -860,6 +937,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&ds_ready[half]);
+      if (warp % 8 == 0) BWD_TRACE(8 + half, n);
     }
     // ───────────── epilogue: dQ = tau * acc (bf16); each warp stores D/4 columns ─────────────
     if (nk > 0) {

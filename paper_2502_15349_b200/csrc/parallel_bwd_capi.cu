@@ -172,3 +172,13 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
   if (d->d_qk == 128) return dispatch_bwd<128, 128>(a);
   return dispatch_bwd<64, 64>(a);
 }
+
+#ifdef AF_BWD_TRACE
+extern "C" int af_debug_bwd_trace(void* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, af::g_bwd_trace, sizeof(af::g_bwd_trace)));
+}
+extern "C" int af_debug_bwd2a_trace(void* host) {
+  return static_cast<int>(
+      cudaMemcpyFromSymbol(host, af::g_bwd2a_trace, sizeof(af::g_bwd2a_trace)));
+}
+#endif
