@@ -29,10 +29,13 @@ namespace af {
 // Developer timeline (-DAF_MLA_TRACE): SM-clock stamps of CTA 0 (the heaviest causal prefill
 // tile, value half 0) per key tile, read back with af_debug_mla_trace.
 #ifdef AF_MLA_TRACE
+#ifndef AF_MLA_TRACE_DECODE
+#define AF_MLA_TRACE_DECODE 0  // 1: trace the decode kernel (batch 0, split 0, value half 0)
+#endif
 __device__ long long g_mla_trace[10][128];
 #define MLA_TRACE(ev, n)                                                              \
   do {                                                                                \
-    if (!kDecode && blockIdx.x == 0 && lane_id() == 0 && (n) < 128)                   \
+    if (kDecode == AF_MLA_TRACE_DECODE && blockIdx.x == 0 && lane_id() == 0 && (n) < 128) \
       g_mla_trace[ev][n] = clock64();                                                 \
   } while (0)
 #else
