@@ -331,11 +331,13 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
         const int c0 = (band.jb_lo + n) * kBlockN;
         const int cb = c0 + ch * 64;
         mbar_wait(&s_full[t], n & 1);
+        if (ch == 0) AF_TRACE(t * 4 + wq, n, 0);
         tc_fence_after();
         uint32_t sr[64];
         tmem_ld32(s_tmem, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
         tmem_ld32(s_tmem + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
         tmem_ld_wait();
+        if (ch == 0) AF_TRACE(t * 4 + wq, n, 1);
         float* s = reinterpret_cast<float*>(sr);
         const bool full = block_fully_kept(p.mask, r0, c0, p.seq_k);
         const bool fast = !kCap && full && p.scale_log2 > 0.0f;
@@ -358,6 +360,7 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
         mx[ch * 128 + row] = bmax;
         named_bar_sync(pair_bar, 64);
         bmax = fmaxf(bmax, mx[(1 - ch) * 128 + row]);
+        if (ch == 0) AF_TRACE(t * 4 + wq, n, 2);
         const float m_new = fmaxf(m_run, bmax);
         const bool need = (m_new - m_run) > 8.0f;  // lazy rescale, as in the one-warp path
         float factor = 1.0f;
@@ -403,6 +406,7 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
         }
         l_run = l_run * factor + lsum;
         tmem_st_wait();
+        if (ch == 0) AF_TRACE(t * 4 + wq, n, 3);
         // correction of this warp's O columns (only rows whose max moved by > 2^8)
         if (n > 0 && __any_sync(0xffffffffu, need)) {
           mbar_wait(&o_done[t], (n - 1) & 1);
@@ -422,6 +426,7 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
         tc_fence_before();
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&p_full[t]);
+        if (ch == 0) AF_TRACE(t * 4 + wq, n, 5);
       }
     } else
     for (int n = 0; n < nk; ++n) {

@@ -27,7 +27,7 @@ assert lib.af_debug_fwd_trace(buf, len(buf)) == 0
 t = np.array(buf[:9 * 64 * 6], dtype=np.int64).reshape(9, 64, 6)
 rows, mma = t[:8], t[8]
 ss = slice(8, 56)
-names = ["S wait->ldtm", "ldtm->max", "max->P half 0", "->P half 1 stored", "->published"]
+names = ["S wait->ldtm", "ldtm->max", "max->P half 0 (split: ->P stored)", "->P half 1 stored", "->published"]
 for w in (0, 4):
     d = np.diff(rows[w, ss, :], axis=1).mean(axis=0)
     print(f"tile{w // 4} warp0:", ", ".join(f"{n} {v:.0f}" for n, v in zip(names, d)))
