@@ -11,7 +11,7 @@ import bench  # noqa: E402
 import paper_2502_15349_b200 as af  # noqa: E402
 from paper_2502_15349_b200 import runtime as rt  # noqa: E402
 
-spec = bench.build_spec("cfg2")
+spec = bench.build_spec(sys.argv[1] if len(sys.argv) > 1 else "cfg2")
 arrays, dout = bench.device_inputs(spec, torch.device("cuda"), 0)
 for _ in range(2):
     o, lse = af.parallel_forward(spec, arrays)
