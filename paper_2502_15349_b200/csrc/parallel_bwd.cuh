@@ -663,6 +663,27 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 
   constexpr int kRW = kDqRowWarps, kTmaW = kRW, kMmaW = kRW + 1;
   constexpr int kCpw = kBlockN / (kRW / 4);  // score columns per row warp (32)
+  // Row warps fetch their Q / dO slice and row statistics before the CTA set-up (barrier init,
+  // TMEM allocation): the global-load latency hides behind it instead of following it.
+  uint32_t qw[D / 8], ow[DV / 8];
+  float l2 = INFINITY, dl = 0.0f;
+  if (warp < kRW) {
+    const int sub = warp / 4;
+    const int i = q0 + (warp % 4) * 32 + static_cast<int>(lane_id());
+    const bool live = i < p.seq_q;
+    load_row_words<D / 8>(q + b * q_sb + h * q_sh + static_cast<int64_t>(live ? i : 0) * q_ss +
+                              sub * (D / 4),
+                          live, qw);
+    load_row_words<DV / 8>(dout + b * do_sb + h * do_sh +
+                               static_cast<int64_t>(live ? i : 0) * do_ss + sub * (DV / 4),
+                           live, ow);
+    const int64_t srow =
+        (static_cast<int64_t>(b) * p.heads_q + h) * seq_q_pad + (live ? i : q0);
+    if (live) {
+      l2 = lse2[srow];  // +inf -> P = 0
+      dl = delta[srow];
+    }
+  }
   if (warp == kTmaW && lane_id() == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -779,36 +800,19 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // lane quarter each write a quarter of the packed words (D/8 of Q^A, DV/8 of dO^A).
     {
       static_assert(kRW == 16, "parking split assumes four warps per lane quarter");
-      const __nv_bfloat16* qrow =
-          q + b * q_sb + h * q_sh + static_cast<int64_t>(live ? i : 0) * q_ss + sub * (D / 4);
-      const __nv_bfloat16* orow = dout + b * do_sb + h * do_sh +
-                                  static_cast<int64_t>(live ? i : 0) * do_ss + sub * (DV / 4);
-      if constexpr (D == 128) {
-        uint32_t w[16];
-        load_row_words<16>(qrow, live, w);
-        tmem_st16(tmem + lane_base + kColQA + sub * 16, w);
-      } else {
-        uint32_t w[8];
-        load_row_words<8>(qrow, live, w);
-        tmem_st8(tmem + lane_base + kColQA + sub * 8, w);
-      }
-      if constexpr (DV == 128) {
-        uint32_t w[16];
-        load_row_words<16>(orow, live, w);
-        tmem_st16(tmem + lane_base + kColOA + sub * 16, w);
-      } else {
-        uint32_t w[8];
-        load_row_words<8>(orow, live, w);
-        tmem_st8(tmem + lane_base + kColOA + sub * 8, w);
-      }
+      if constexpr (D == 128)
+        tmem_st16(tmem + lane_base + kColQA + sub * 16, qw);
+      else
+        tmem_st8(tmem + lane_base + kColQA + sub * 8, qw);
+      if constexpr (DV == 128)
+        tmem_st16(tmem + lane_base + kColOA + sub * 16, ow);
+      else
+        tmem_st8(tmem + lane_base + kColOA + sub * 8, ow);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(qa_ready);
     }
-    const int64_t srow = (static_cast<int64_t>(b) * p.heads_q + h) * seq_q_pad + (live ? i : q0);
-    const float l2 = live ? lse2[srow] : INFINITY;  // +inf -> P = 0
-    const float dl = live ? delta[srow] : 0.0f;
     float slope = 0.0f;
     if constexpr (kFamily != kFamilySoftmax) {
       if (p.slope != nullptr) slope = p.slope[h];
