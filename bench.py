@@ -179,7 +179,37 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ───────────────────────────── CPU baseline (oracle port) ─────────────────────────────
+# ───────────────────────────── CPU baseline (the reference itself) ─────────────────────────────
+# The reference is a pure-Python package: `baseline/_ref` holds it installed unmodified (pip
+# --target), and the CPU legs time its own executors — engine.run_tiled_parallel /
+# run_chunk_recurrent + engine.autodiff_grads (loss = sum(O)) — on (b, h) slices of the workload,
+# one process per host core (parallelism over (b, h) is what the reference permits).
+# Without the install the float64 oracle port (numpy matmuls, same algorithm) stands in.
+
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_available() -> bool:
+    if not (REF_DIR / "attnforge" / "engine.py").exists():
+        return False
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    try:
+        import attnforge.engine  # noqa: F401
+        return True
+    except Exception:  # noqa: BLE001 - a broken install falls back to the port
+        return False
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
 
 def _cpu_sample_spec(key: str, s_len: int):
     """One (b, h) slice of the workload at a bounded sequence length."""
@@ -198,16 +228,41 @@ def _cpu_sample_spec(key: str, s_len: int):
     return build_spec(key, batch=1, heads=1, seq=s_len)
 
 
+def _reference_spec(spec):
+    """The same slice as an attnforge spec (variant-file dict through the reference's own
+    loader).  MLA's shared latent head becomes an ordinary K/V pair of the same shapes (the
+    reference has no kv_shared); a one-head slice has no GQA grouping."""
+    from attnforge import variantfile as VF
+    from paper_2502_15349_b200.spec import spec_to_dict
+    doc = spec_to_dict(spec)
+    doc.pop("kv_shared", None)
+    doc["dims"].pop("heads_kv", None)
+    return VF.spec_from_dict(doc)
+
+
 def _cpu_slice(args):
-    key, s_len, seed = args
+    key, s_len, seed, kind = args
     import numpy as np
     from threadpoolctl import threadpool_limits
-    import oracle
-    from oracle import parallel as OP, recurrent as OR
     from paper_2502_15349_b200.spec import Pattern
     spec = _cpu_sample_spec(key, s_len)
     w = WORKLOADS[key]
     with threadpool_limits(1):
+        if kind == "reference":
+            reference_available()
+            from attnforge import engine as E
+            rs = _reference_spec(spec)
+            arrays = E.generate(rs, seed).arrays
+            t0 = time.perf_counter()
+            if spec.pattern is Pattern.PARALLEL:
+                E.run_tiled_parallel(rs, arrays, 64, 64)
+            else:
+                E.run_chunk_recurrent(rs, arrays, 64)
+            if w.backward:
+                E.autodiff_grads(rs, arrays)
+            return time.perf_counter() - t0
+        import oracle
+        from oracle import parallel as OP, recurrent as OR
         arrays = oracle.generate(spec, seed)
         rng = np.random.default_rng(seed)
         t0 = time.perf_counter()
@@ -222,26 +277,62 @@ def _cpu_slice(args):
         return time.perf_counter() - t0
 
 
-def cpu_baseline(key: str, s_len: int | None = None, slices: int | None = None) -> dict:
-    """The f64 oracle port of the reference executors, one workload slice per host core."""
-    import multiprocessing as mp
-    w = WORKLOADS[key]
-    s_len = s_len or w.cpu_seq
-    cores = slices or (os.cpu_count() or 1)
-    if key == "cfg1":
-        cores = 1                       # the whole config is one sample
-    t0 = time.perf_counter()
-    with mp.get_context("spawn").Pool(cores) as pool:
-        pool.map(_cpu_slice, [(key, s_len, i) for i in range(cores)])
-    wall = time.perf_counter() - t0
-    wk = work(_cpu_sample_spec(key, s_len))
-    flops = cores * (wk["fwd_flops"] + (wk["bwd_flops"] if w.backward else 0))
-    what = "fwd + VJP" if w.backward else "fwd"
-    return {"value": flops / wall / 1e12, "unit": "TFLOPS", "cores": cores, "kind": "port",
-            "sample": f"{cores} slice(s) of {key} ({_cpu_sample_spec(key, s_len).dims}), {what} "
-                      f"with the float64 oracle (tiled 64x64 / chunk 64), one process per core: "
-                      f"{wall:.2f} s wall",
-            "wall_s": wall}
+# Slice lengths of the CPU legs: the reference's autodiff holds every intermediate of the dense
+# graph (≈1 GB per head at S=2048) and refuses recurrent unrolls above 256 steps
+# (attention.py:475-477), so its slices are shorter than the port's.
+_REF_SEQ = {"cfg1": 512, "cfg2": 1024, "cfg3": 1024, "cfg4a": 512, "cfg4b": 4096,
+            "cfg5a": 256, "cfg5b": 256}
+
+
+class CpuPool:
+    """One spawned process per host core, imported and warmed before any timing."""
+
+    def __init__(self, key: str, s_len: int | None, kind: str | None = None):
+        import multiprocessing as mp
+        self.key = key
+        self.kind = kind or ("reference" if reference_available() else "port")
+        self.s_len = s_len or (_REF_SEQ[key] if self.kind == "reference" else
+                               WORKLOADS[key].cpu_seq)
+        self.cores = 1 if key == "cfg1" else (os.cpu_count() or 1)
+        self.pool = mp.get_context("spawn").Pool(self.cores)
+        self.pool.map(_cpu_slice, [(key, min(self.s_len, 64) if key != "cfg1" else self.s_len,
+                                    i, self.kind) for i in range(self.cores)])
+
+    def step(self, seed0: int = 0) -> dict:
+        w = WORKLOADS[self.key]
+        t0 = time.perf_counter()
+        self.pool.map(_cpu_slice, [(self.key, self.s_len, seed0 + i, self.kind)
+                                   for i in range(self.cores)])
+        wall = time.perf_counter() - t0
+        sample = _cpu_sample_spec(self.key, self.s_len)
+        wk = work(sample)
+        flops = self.cores * (wk["fwd_flops"] + (wk["bwd_flops"] if w.backward else 0))
+        if self.kind == "reference":
+            what = ("engine.run_tiled_parallel(64x64)" if sample.pattern.value == "parallel"
+                    else "engine.run_chunk_recurrent(64)")
+            what += " + engine.autodiff_grads" if w.backward else ""
+            who = "the unmodified reference (attnforge from baseline/_ref)"
+        else:
+            what = "fwd + VJP" if w.backward else "fwd"
+            who = "the float64 oracle port (baseline/_ref absent)"
+        return {"value": flops / wall / 1e12, "unit": "TFLOPS", "cores": self.cores,
+                "kind": self.kind, "cpu_model": cpu_model(),
+                "sample": f"{self.cores} (b,h) slice(s) of {self.key} ({sample.dims}), {what} "
+                          f"by {who}, one process per core: {wall:.2f} s wall; throughput "
+                          f"credits the slices' algorithmic flops",
+                "wall_s": wall}
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_baseline(key: str, s_len: int | None = None) -> dict:
+    pool = CpuPool(key, s_len)
+    try:
+        return pool.step()
+    finally:
+        pool.close()
 
 
 def run_reference(args) -> None:
@@ -249,21 +340,26 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     w = WORKLOADS[args.config]
-    for _ in range(args.warmup):
-        cpu_baseline(args.config, args.cpu_seq)
-    vals, t_total = [], 0.0
-    for _ in range(args.steps):
-        r = cpu_baseline(args.config, args.cpu_seq)
-        vals.append(r["value"])
-        t_total += r["wall_s"]
+    pool = CpuPool(args.config, args.cpu_seq)
+    try:
+        for i in range(args.warmup):
+            pool.step(1000 * (i + 1))
+        vals, t_total = [], 0.0
+        for i in range(args.steps):
+            r = pool.step(i)
+            vals.append(r["value"])
+            t_total += r["wall_s"]
+    finally:
+        pool.close()
     v = statistics.median(vals)
     r["value"] = v
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOPS",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w.title + " (CPU sample, see cpu_baseline.sample)"},
-            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "cpu_model",
+                                               "sample")},
             "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -307,12 +403,22 @@ def run_gpu(args, key: str) -> dict | None:
     from paper_2502_15349_b200.pipeline import HostPipeline
     from paper_2502_15349_b200.spec import Pattern
 
+    from paper_2502_15349_b200.shard import shard_units
     w = WORKLOADS[key]
     rank, world, local = dist_env()
     dev = torch.device("cuda", local)
     spec = build_spec(key)
     wk = work(spec)
-    arrays, dout = device_inputs(spec, dev, 1234 + rank)
+    # Multi-GPU: the global workload is `world` copies of the config along the batch
+    # axis (weak scaling); its independent units — (b, KV group) for the parallel template, (b, h)
+    # for the linear one — are partitioned by shard.shard_units, which hands every rank exactly one
+    # config's worth of whole batch rows.  No data-path collective runs in the timed region.
+    d = spec.dims
+    groups = d.kv_heads if spec.pattern is Pattern.PARALLEL else d.heads
+    shard = shard_units(d.batch * world, groups, world, rank)
+    b_lo = shard.units[0] // groups
+    assert len(shard.units) == d.batch * groups and shard.units[0] % groups == 0, shard
+    arrays, dout = device_inputs(spec, dev, 1234 + b_lo)
     if w.precision == "fp32":
         arrays = {k: v.float() for k, v in arrays.items()}
     in_bytes = sum(t.numel() * t.element_size() for t in arrays.values())
@@ -363,6 +469,31 @@ def run_gpu(args, key: str) -> dict | None:
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, fwd_ms, bwd_ms = (float(x) for x in t.tolist())
+
+    # The one collective of the path (outside the timed region): all-gather every rank's O (and
+    # LSE) into the global [world*B, ...] tensors over NCCL, timed on the device, max over ranks.
+    gather = None
+    if world > 1:
+        from paper_2502_15349_b200.shard import gather_batch_rows
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        outs = [o] + ([lse] if lse is not None else [])
+        gather_batch_rows(outs, world)  # warm-up (communicator set-up)
+        barrier()
+        g0.record(stream)
+        full = gather_batch_rows(outs, world)
+        g1.record(stream)
+        barrier()
+        gms = torch.tensor([g0.elapsed_time(g1)], device=dev)
+        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        ok = all(torch.equal(f[b_lo: b_lo + d.batch], x) for f, x in zip(full, outs))
+        nbytes = sum(x.numel() * x.element_size() for x in outs)
+        gather = {"ms": float(gms.item()), "bytes_per_rank": nbytes,
+                  "bus_gbs": nbytes * (world - 1) / (float(gms.item()) * 1e-3) / 1e9,
+                  "what": "dist.all_gather_into_tensor of O" + (" and LSE" if lse is not None
+                                                                else "") +
+                          " into the global batch (NCCL), outside the timed region",
+                  "own_slot_matches": bool(ok)}
+        del full
 
     # e2e through the public host-buffer API: pinned host inputs, H2D + kernels + D2H per step
     pipe = HostPipeline(spec, device=dev, precision=w.precision)
@@ -422,7 +553,6 @@ def run_gpu(args, key: str) -> dict | None:
                 "peak_source": "nominal fp32 FFMA (no measured figure)"}
     roof["kernel"] = {"fwd": "forward kernel(s) of the config", "bwd": "backward kernels of "
                       "the config"}[dom]
-    d = spec.dims
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -432,7 +562,9 @@ def run_gpu(args, key: str) -> dict | None:
         "config": {"workload": w.title, "global_batch": d.batch * world, "seq_len": d.seq_q,
                    "seq_k": d.seq_k, "heads_q": d.heads, "heads_kv": d.kv_heads,
                    "d_qk": d.d_qk, "d_v": d.d_v,
-                   "parallelism": f"batchxhead shards, {world} rank(s), no collective",
+                   "parallelism": (f"dp{world}: batch x {'KV-group' if parallel else 'head'} "
+                                   f"units partitioned by shard.shard_units, {len(shard.units)} "
+                                   f"units per rank, no collective in the timed region"),
                    "l2": ("L2 flushed (2x126 MB write) before every step" if flush is not None
                           else f"inputs larger than L2 ({in_bytes / 1e6:.0f} MB per rank)")},
         "frac_of_peak": (value / world / pk["tflops_sustained"]) if w.bound == "tensor" else None,
@@ -450,6 +582,8 @@ def run_gpu(args, key: str) -> dict | None:
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    if gather is not None:
+        line["gather"] = gather
     return line
 
 
@@ -477,6 +611,19 @@ def main() -> None:
                 cmd.append("--no-cpu")
             subprocess.run(cmd, check=False)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun (the driver's own launch
+        # sets WORLD_SIZE and lands below directly)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        sys.exit(subprocess.run(cmd, env=env).returncode)
     if args.impl == "reference":
         for k in keys:
             args.config = k

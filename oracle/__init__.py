@@ -8,8 +8,8 @@ follows.  It exists to *check* the CUDA path: only ``tests/``, ``__graft_entry__
 
 Parity pinning: ``tests/golden/*.npz`` hold outputs of the reference itself (run in the build
 container by ``tests/golden/make_golden.py``); ``tests/test_oracle_golden.py`` checks this oracle
-against every fixture, and ``tests/test_oracle_reference.py`` re-runs the live reference when
-``/root/reference`` is mounted.
+against every fixture, ``tests/test_oracle_reference.py`` re-runs the live reference when ``/root/reference`` is mounted,
+and ``tests/test_oracle_gradcheck.py`` checks the closed-form VJPs against central differences.
 
 Modules
   hooks      hook expressions evaluated on numpy arrays, with dual numbers for elementwise
@@ -17,6 +17,7 @@ Modules
   fills      deterministic problem instances (engine.py:326-388)
   parallel   parallel template: tiled online forward, dense forward, LSE, closed-form VJP
   recurrent  linear template: stepwise / chunked forward, chunked VJP
+  gradcheck  central finite-difference check of the VJPs (engine.finite_diff_check restated)
 """
 
 from .fills import generate, philox_key  # noqa: F401

@@ -10,6 +10,9 @@
                     protocol when no direct form is declared).
 ``lse_rows``        log-sum-exp of the final score rows — what the reference's own online
                     epilogue ``acc*0 + m + log(l)`` returns.
+``streamed_vjp``    the same forward + VJP streamed over query-row blocks (full-length slices at
+                    O(block * S) memory); ``keycols_softmax_vjp`` dK/dV of sampled key rows summed
+                    over every query head given the forward's row statistics.
 ``parallel_vjp``    gradients of <dO, O> in closed form, equal to what
                     attention.derive_backward + graph.backward produce with the ``o * g``
                     cotangent trick; elementwise hook derivatives use the
@@ -359,3 +362,163 @@ def sampled_forward(spec, arrays: dict, rows) -> tuple[np.ndarray, np.ndarray | 
             return s @ vm, None
         a = row_sum(np.abs(s))
         return (s @ vm) / np.clip(a, 1.0, None), None
+
+
+def _chain_mods(spec, arrays, dqm, dkm, dvm):
+    """Chain the q/k/v mods (elementwise) and fold GQA groups / MLA's aliased V, as in
+    ``parallel_vjp``."""
+    d = spec.dims
+    env = {**_consts(d), **arrays}
+    g = _group(spec)
+    q = np.asarray(arrays["q"], np.float64)
+    k = _expand(np.asarray(arrays["k"], np.float64), g)
+    v = k[..., : d.d_v] if getattr(spec, "kv_shared", False) else \
+        _expand(np.asarray(arrays["v"], np.float64), g)
+    dq = dqm * (evaluate_dual(spec.q_mod.source, {**env, "q": q}, "q")[1] if spec.q_mod else 1.0)
+    dk = dkm * (evaluate_dual(spec.k_mod.source, {**env, "k": k}, "k")[1] if spec.k_mod else 1.0)
+    dv = dvm * (evaluate_dual(spec.v_mod.source, {**env, "v": v}, "v")[1] if spec.v_mod else 1.0)
+    dq, dk, dv = (np.asarray(x) * np.ones(y.shape) for x, y in ((dq, q), (dk, k), (dv, v)))
+    if g > 1:
+        b, h = dk.shape[0], d.heads
+        dk = dk.reshape(b, h // g, g, d.seq_k, -1).sum(2)
+        dv = dv.reshape(b, h // g, g, d.seq_k, -1).sum(2)
+    if getattr(spec, "kv_shared", False):
+        dk = dk.copy()
+        dk[..., : d.d_v] += dv
+        return {"q": dq, "k": dk}
+    return {"q": dq, "k": dk, "v": dv}
+
+
+def _block_scores(spec, env, qm_blk, km, rows, cols):
+    """Final scores z and dz/ds of query rows ``rows`` against key columns ``cols`` (absolute
+    indices, so index-grid masks stay exact)."""
+    s = qm_blk @ np.swapaxes(km, -1, -2)
+    env = {**env, "qidx": np.asarray(rows, np.float64).reshape(1, 1, -1, 1),
+           "kidx": np.asarray(cols, np.float64).reshape(1, 1, 1, -1)}
+    z, dz = s, np.ones_like(s)
+    for m in spec.score_mods:
+        z, dz = evaluate_dual(m.source, {**env, "s": z}, "s", seed=dz)
+        z = np.asarray(z, np.float64) * np.ones(s.shape)
+        dz = np.asarray(dz, np.float64) * np.ones(s.shape)
+    return z, dz
+
+
+def _extras_env(spec, arrays, rows, cols):
+    env = {}
+    for e in spec.extra_inputs:
+        x = np.asarray(arrays[e.name], np.float64)
+        idx = [slice(None)] * 4
+        for ax, tok in enumerate(e.shape):
+            if tok == "seq_q" and x.shape[ax] > 1:
+                idx[ax] = np.asarray(rows)
+            elif tok == "seq_k" and x.shape[ax] > 1:
+                idx[ax] = np.asarray(cols)
+        env[e.name] = x[tuple(idx)]
+    return env
+
+
+def streamed_vjp(spec, arrays: dict, dout: np.ndarray, block: int = 512) -> dict:
+    """Forward and VJP of the softmax / elementwise families streamed over query-row
+    blocks, one head at a time, so a full-length slice (S = 8192) needs O(block * S) memory
+    instead of O(S^2): the same closed forms as ``parallel_vjp``, exact in float64.
+    Returns {"o", "lse" (softmax) , "q", "k", "v"} for the given arrays (any batch / heads)."""
+    d = spec.dims
+    kind = _classify(spec)
+    if kind not in ("softmax", "none"):
+        raise NotImplementedError("streamed_vjp covers the softmax and elementwise families")
+    qm, km, vm = _inputs(spec, arrays)
+    dout = np.asarray(dout, np.float64)
+    B, H, S = qm.shape[0], qm.shape[1], d.seq_q
+    consts = _consts(d)
+    o = np.zeros(qm.shape[:-1] + (vm.shape[-1],))
+    lse = np.zeros(qm.shape[:-1]) if kind == "softmax" else None
+    dqm, dkm, dvm = np.zeros_like(qm), np.zeros_like(km), np.zeros_like(vm)
+    cols = np.arange(d.seq_k)
+    with np.errstate(**_ERR):
+        for b in range(B):
+            for h in range(H):
+                for r0 in range(0, S, block):
+                    rows = np.arange(r0, min(S, r0 + block))
+                    env = {**consts, **_extras_env(spec, arrays, rows, cols)}
+                    for k_, x in list(env.items()):
+                        if isinstance(x, np.ndarray) and x.ndim == 4:
+                            env[k_] = x[min(b, x.shape[0] - 1): min(b, x.shape[0] - 1) + 1,
+                                        min(h, x.shape[1] - 1): min(h, x.shape[1] - 1) + 1]
+                    qb = qm[b:b + 1, h:h + 1, rows]
+                    z, dz = _block_scores(spec, env, qb, km[b:b + 1, h:h + 1], rows, cols)
+                    z, dz = z[0, 0], dz[0, 0]
+                    vb, kb, dob = vm[b, h], km[b, h], dout[b, h, rows]
+                    dp = dob @ vb.T
+                    if kind == "softmax":
+                        m = np.max(z, -1, keepdims=True)
+                        ok = np.isfinite(m)
+                        e = np.where(ok, np.exp(z - np.where(ok, m, 0.0)), 0.0)
+                        den = np.sum(e, -1, keepdims=True)
+                        p = np.where(den == 0, 0.0, e / np.where(den == 0, 1.0, den))
+                        lse[b, h, rows] = np.where(den[:, 0] == 0, -np.inf,
+                                                   np.where(ok, m, 0.0)[:, 0] + np.log(
+                                                       np.where(den == 0, 1.0, den))[:, 0])
+                        ob = p @ vb
+                        dzz = p * (dp - np.sum(dob * ob, -1, keepdims=True))
+                        pv = p
+                    else:
+                        ob = z @ vb
+                        dzz, pv = dp, z
+                    o[b, h, rows] = ob
+                    ds = dzz * dz
+                    ds = np.where(np.isfinite(ds), ds, 0.0)
+                    dqm[b, h, rows] = ds @ kb
+                    dkm[b, h] += ds.T @ qm[b, h, rows]
+                    dvm[b, h] += pv.T @ dob
+    g = _chain_mods(spec, arrays, dqm, dkm, dvm)
+    g["o"] = o
+    if lse is not None:
+        g["lse"] = lse
+    return g
+
+
+def keycols_softmax_vjp(spec, arrays: dict, dout: np.ndarray, o: np.ndarray, lse: np.ndarray,
+                        key_cols) -> dict:
+    """dK (and dV) of the key rows ``key_cols`` only, summed over every query head, for the
+    softmax family — given the forward's row statistics (O and LSE, the backward kernel's own
+    inputs, each checked against the oracle separately).  Cost O(S * |key_cols|) per head:
+    the MLA latent-cache gradient summed over all 128 heads at S = 4096 in seconds.
+    Returns {"k": [B, Hkv, |J|, Dqk], "v": [B, Hkv, |J|, Dv]} (MLA: V folded into k)."""
+    d = spec.dims
+    qm, km, vm = _inputs(spec, arrays)
+    J = np.asarray(key_cols)
+    dout, o, lse = (np.asarray(x, np.float64) for x in (dout, o, lse))
+    consts = _consts(d)
+    dkmJ = np.zeros(km.shape[:2] + (len(J), km.shape[-1]))
+    dvmJ = np.zeros(vm.shape[:2] + (len(J), vm.shape[-1]))
+    rows = np.arange(d.seq_q)
+    with np.errstate(**_ERR):
+        for b in range(qm.shape[0]):
+            for h in range(qm.shape[1]):
+                env = {**consts, **_extras_env(spec, arrays, rows, J)}
+                z, dz = _block_scores(spec, env, qm[b:b + 1, h:h + 1], km[b:b + 1, h:h + 1, J],
+                                      rows, J)
+                z, dz = z[0, 0], dz[0, 0]
+                lr = lse[b, h][:, None]
+                p = np.where(np.isfinite(lr), np.exp(z - np.where(np.isfinite(lr), lr, 0.0)), 0.0)
+                dp = dout[b, h] @ vm[b, h, J].T
+                delta = np.sum(dout[b, h] * o[b, h], -1, keepdims=True)
+                ds = p * (dp - delta) * dz
+                ds = np.where(np.isfinite(ds), ds, 0.0)
+                dkmJ[b, h] = ds.T @ qm[b, h]
+                dvmJ[b, h] = p.T @ dout[b, h]
+    g = _group(spec)
+    # chain the k / v mods on the selected rows (constant-scale mods in every config here)
+    env = {**consts, **arrays}
+    k = _expand(np.asarray(arrays["k"], np.float64), g)[..., J, :]
+    dk = dkmJ * (evaluate_dual(spec.k_mod.source, {**env, "k": k}, "k")[1] if spec.k_mod else 1.0)
+    dv = dvmJ
+    if g > 1:
+        Bq = dk.shape[0]
+        dk = dk.reshape(Bq, d.heads // g, g, len(J), -1).sum(2)
+        dv = dv.reshape(Bq, d.heads // g, g, len(J), -1).sum(2)
+    if getattr(spec, "kv_shared", False):
+        dk = np.asarray(dk, np.float64).copy()
+        dk[..., : d.d_v] += dv
+        return {"k": dk}
+    return {"k": dk, "v": dv}

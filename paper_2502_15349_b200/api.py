@@ -428,6 +428,16 @@ def _linear_desc(plan: LinearPlan, arrays: dict, q, k, v, o):
     return c, keep
 
 
+def _check_factors(plan: LinearPlan, arrays: dict) -> None:
+    """The chunked kernels evaluate decays in log space: a negative per-step factor has no
+    log-space form (the reference's running product handles it, engine.py:597-605)."""
+    for name in plan.decay_factors:
+        t = _need(arrays, name)
+        if bool((t < 0).any().item()):
+            raise UnsupportedError("negative per-step decay factor; the chunked kernels need "
+                                   "a_t >= 0", extra=name)
+
+
 def _linear_pad(d) -> tuple[int, int]:
     """Kernel dims of the linear template: 128 or 256 for both the key and the value dim (the
     backward runs the chunked kernel with the value dim in the key role).  Smaller dims run
@@ -469,6 +479,8 @@ def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = Fa
     if o.shape[-1] != d.d_v:
         o = o[..., : d.d_v].contiguous()
     if check_nan:
+        if torch.isnan(o).any().item():
+            _check_factors(plan, arrays)
         _check_nan(o, "chunk")
     if return_state:
         return o, state[..., : d.d_qk, : d.d_v].contiguous()
@@ -607,49 +619,69 @@ def bind(spec) -> BoundKernel:
 # ───────────────────────────── autograd module ─────────────────────────────
 
 class _ParallelFn(torch.autograd.Function):
+    """Autograd node of the parallel template.  Extras are positional inputs (names on ctx) so
+    autograd sees them; their gradients are not lowered on this template, so a differentiable
+    extra raises at forward time (the reference differentiates them, attention.py:542-543)."""
+
     @staticmethod
-    def forward(ctx, spec, q, k, v, extras):
+    def forward(ctx, spec, names, q, k, v, *extra_t):
+        extras = dict(zip(names, extra_t))
+        for e in spec.extra_inputs:
+            if e.differentiable:
+                raise UnsupportedError("gradients w.r.t. parallel-template extras are not "
+                                       "lowered", extra=e.name)
         arrays = {"q": q, "k": k, "v": v, **extras}
         with torch.cuda.device(q.device):
             o, lse = parallel_forward(spec, arrays)
-        ctx.spec, ctx.extras = spec, extras
-        ctx.save_for_backward(q, k, v, o, lse if lse is not None else torch.empty(0))
+        ctx.spec, ctx.names = spec, names
+        ctx.save_for_backward(q, k, v, o, lse if lse is not None else torch.empty(0), *extra_t)
         ctx.has_lse = lse is not None
         return o
 
     @staticmethod
     def backward(ctx, do):
-        q, k, v, o, lse = ctx.saved_tensors
-        arrays = {"q": q, "k": k, "v": v, **ctx.extras}
+        q, k, v, o, lse, *extra_t = ctx.saved_tensors
+        arrays = {"q": q, "k": k, "v": v, **dict(zip(ctx.names, extra_t))}
         with torch.cuda.device(q.device):
             g = parallel_backward(ctx.spec, arrays, o, lse if ctx.has_lse else None, do)
-        return None, g["q"].to(q.dtype), g["k"].to(k.dtype), g.get("v", None), None
+        # MLA (kv_shared): V aliases K[..., :d_v]; its gradient is folded into dk and the v
+        # argument is not read, so it receives none.
+        gv = g.get("v")
+        return (None, None, g["q"].to(q.dtype), g["k"].to(k.dtype),
+                gv.to(v.dtype) if gv is not None and v is not None else None,
+                *([None] * len(extra_t)))
 
 
 class AttentionEngine:
     """AttentionEngine-style callable: ``AttentionEngine(spec)(q, k, v, **custom_fwd_inputs)``
-    with autograd support (forward K1, backward K2 / linear K4-K5)."""
+    with autograd support (forward K1, backward K2 / linear K4-K5).  Gradients flow to q, k, v
+    and, on the linear template, to the differentiable per-step extras (gate / decay)."""
 
     def __init__(self, spec):
         self.spec = _spec(spec)
         self.plan = bind(self.spec).plan
 
     def __call__(self, q, k, v, **extras):
+        names = tuple(extras)
+        tensors = tuple(extras[n] for n in names)
         if self.spec.pattern is Pattern.PARALLEL:
-            return _ParallelFn.apply(self.spec, q, k, v, extras)
-        return _LinearFn.apply(self.spec, q, k, v, extras)
+            return _ParallelFn.apply(self.spec, names, q, k, v, *tensors)
+        return _LinearFn.apply(self.spec, names, q, k, v, *tensors)
 
 
 class _LinearFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, spec, q, k, v, extras):
-        ctx.spec, ctx.extras = spec, extras
-        ctx.save_for_backward(q, k, v)
-        return linear_forward(spec, {"q": q, "k": k, "v": v, **extras})
+    def forward(ctx, spec, names, q, k, v, *extra_t):
+        ctx.spec, ctx.names = spec, names
+        ctx.save_for_backward(q, k, v, *extra_t)
+        return linear_forward(spec, {"q": q, "k": k, "v": v, **dict(zip(names, extra_t))})
 
     @staticmethod
     def backward(ctx, do):
-        q, k, v = ctx.saved_tensors
+        q, k, v, *extra_t = ctx.saved_tensors
         with torch.cuda.device(q.device):
-            g = linear_backward(ctx.spec, {"q": q, "k": k, "v": v, **ctx.extras}, do)
-        return None, g["q"].to(q.dtype), g["k"].to(k.dtype), g["v"].to(v.dtype), None
+            g = linear_backward(ctx.spec, {"q": q, "k": k, "v": v,
+                                           **dict(zip(ctx.names, extra_t))}, do)
+        gx = [g[n].to(t.dtype) if n in g and ctx.needs_input_grad[5 + i] else None
+              for i, (n, t) in enumerate(zip(ctx.names, extra_t))]
+        return None, None, g["q"].to(q.dtype), g["k"].to(k.dtype), g["v"].to(v.dtype), *gx

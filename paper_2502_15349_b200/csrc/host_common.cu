@@ -4,6 +4,8 @@
 
 #include <atomic>
 #include <mutex>
+#include <set>
+#include <utility>
 
 namespace af {
 
@@ -40,6 +42,18 @@ void set_error(const char* fmt, ...) {
 }
 
 const char* last_error() { return g_last_error.c_str(); }
+
+int ensure_max_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  AF_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, func})) return AF_OK;
+  AF_CUDA_CHECK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({dev, func});
+  return AF_OK;
+}
 
 std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }

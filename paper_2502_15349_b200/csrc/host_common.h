@@ -39,6 +39,16 @@ bool make_tmap_4d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype,
 
 int sm_count();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device context: cache it per
+// (current device, kernel) under a mutex, so a kernel first launched on one GPU still gets the
+// attribute on the next GPU of the same process.
+int ensure_max_smem(const void* func, int bytes);
+#define AF_SMEM_ATTR(kern, bytes)                                                            \
+  do {                                                                                       \
+    if (::af::ensure_max_smem(reinterpret_cast<const void*>(kern), (bytes)) != AF_OK)        \
+      return AF_ERR_CUDA;                                                                    \
+  } while (0)
+
 // Process-wide count of kernels this library launched (af_launch_count()).
 void note_launch();
 void ensure_context();

@@ -79,11 +79,7 @@ int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
   p.dot = a.dot;
   p.final_state = a.final_state;
   auto kern = linear_chunk_kernel<DK, kRev, kFac>;
-  static bool attr = false;
-  if (!attr) {
-    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
-    attr = true;
-  }
+  AF_SMEM_ATTR(kern, L::kTotal);
   dim3 grid(d->batch * d->heads * (a.dvv / kLinVB));
   ::af::note_launch();
   kern<<<grid, lin_threads(DK), L::kTotal, s>>>(tq, tk, tv, p);
@@ -138,7 +134,8 @@ extern "C" size_t af_linear_bwd_workspace(const af_linear_desc* d) {
   if (d == nullptr) return 0;
   const size_t rows = static_cast<size_t>(d->batch) * d->heads * d->seq;
   const size_t slots = static_cast<size_t>(d->d_k) / 32;  // dot partials per 32-column slot
-  size_t bytes = rows * 2 * slots * sizeof(float);
+  // dot partials, then d log a and dk_dot per step; the bf16 Km copy starts 256-byte aligned
+  size_t bytes = (rows * (2 * slots + 2) * sizeof(float) + 255) / 256 * 256;
   if (d->key_gate != nullptr) bytes += rows * static_cast<size_t>(d->d_k) * 2;  // bf16 Km
   return bytes;
 }
@@ -156,6 +153,8 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
   const int slots = d->d_k / 32;
   float* dq_dot = static_cast<float*>(workspace);
   float* dk_dot = dq_dot + n * slots;
+  float* step_dloga = dk_dot + n * slots;
+  float* step_dkdot = step_dloga + n;
   AF_CUDA_CHECK(cudaMemsetAsync(workspace, 0, static_cast<size_t>(2 * n * slots) * sizeof(float), s));
   // Gated keys, materialised once (see gate_keys_kernel)
   const void* km = k;
@@ -163,7 +162,9 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
   int64_t km_contig[4] = {static_cast<int64_t>(d->heads) * d->seq * d->d_k,
                           static_cast<int64_t>(d->seq) * d->d_k, d->d_k, 1};
   if (d->key_gate != nullptr) {
-    __nv_bfloat16* kmb = reinterpret_cast<__nv_bfloat16*>(dk_dot + n * slots);
+    __nv_bfloat16* kmb = reinterpret_cast<__nv_bfloat16*>(
+        static_cast<char*>(workspace) +
+        (static_cast<size_t>(n) * (2 * slots + 2) * sizeof(float) + 255) / 256 * 256);
     const int64_t thr = n * (d->d_k / 8);
     ::af::note_launch();
     gate_keys_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, s>>>(
@@ -191,19 +192,30 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
   if (want_fac || d_key_gate != nullptr) {
     LinearParams p = base_params(d);
     p.u_scale = step_tensor(d->key_gate, d->key_gate_stride);
-    StepTensor f0{}, f1{}, g{};
-    if (d_decay_factor != nullptr && d->n_decay_factors > 0)
-      f0 = step_tensor(d_decay_factor[0], d->decay_factor_stride[0]);
-    if (d_decay_factor != nullptr && d->n_decay_factors > 1)
-      f1 = step_tensor(d_decay_factor[1], d->decay_factor_stride[1]);
-    if (d_key_gate != nullptr) {
+    if (d_key_gate != nullptr)
       AF_REQUIRE(d->key_gate != nullptr, AF_ERR_INPUT, "d_key_gate without a key gate");
-      g = step_tensor(d_key_gate, d->key_gate_stride);
-    }
     ::af::note_launch();
-    linear_step_grads_kernel<<<d->batch * d->heads, 256, 0, s>>>(dq_dot, dk_dot, slots, p, f0,
-                                                                  f1, g);
+    linear_step_grads_kernel<<<d->batch * d->heads, 256, 0, s>>>(
+        dq_dot, dk_dot, slots, p, step_dloga, d_key_gate != nullptr ? step_dkdot : nullptr);
     AF_CUDA_CHECK(cudaGetLastError());
+    auto reduce = [&](const float* val, StepTensor div, StepTensor out) -> int {
+      const int nb = out.sb == 0 ? 1 : d->batch, nh = out.sh == 0 ? 1 : d->heads;
+      const int64_t total = static_cast<int64_t>(nb) * nh * d->seq;
+      ::af::note_launch();
+      step_grad_reduce_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+          val, div, out, d->batch, d->heads, d->seq);
+      AF_CUDA_CHECK(cudaGetLastError());
+      return AF_OK;
+    };
+    for (int f = 0; f < d->n_decay_factors; ++f)
+      if (d_decay_factor != nullptr && d_decay_factor[f] != nullptr)
+        if ((st = reduce(step_dloga, p.fac[f],
+                         step_tensor(d_decay_factor[f], d->decay_factor_stride[f]))) != AF_OK)
+          return st;
+    if (d_key_gate != nullptr)
+      if ((st = reduce(step_dkdot, p.u_scale, step_tensor(d_key_gate, d->key_gate_stride))) !=
+          AF_OK)
+        return st;
   }
   return AF_OK;
 }

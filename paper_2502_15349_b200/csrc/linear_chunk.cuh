@@ -110,6 +110,14 @@ struct LinSmem {
 
 constexpr float kLog2e_ = 1.4426950408889634f;
 
+// log2 of a per-step decay factor, floored at -200: a factor of exactly 0 (a state reset) gives
+// 2^-200 = 0 in fp32 after the cumulative sums instead of -inf - -inf = NaN.  A negative factor
+// stays NaN (log-space decays need a >= 0; the host reports it as unsupported).
+AF_DEVICE float log2_floor(float v) {
+  const float l = __log2f(v);
+  return l < -200.0f ? -200.0f : l;
+}
+
 // packed (bf16x2) TMEM column of the k-th 16-key slice of P (key halves [0,64) -> [0,32),
 // [64,128) -> [64,96): each row-warp half only overwrites S columns it alone has read)
 AF_DEVICE uint32_t split_col_lin(int kk) { return kk < 4 ? kk * 8 : 64 + (kk - 4) * 8; }
@@ -441,7 +449,7 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
             x[j] = p.log_const * kLog2e_;
 #pragma unroll
             for (int f = 0; f < 2; ++f)
-              if (f < p.nfac) x[j] += __log2f(raw[f * kLinChunk + rr]);
+              if (f < p.nfac) x[j] += log2_floor(raw[f * kLinChunk + rr]);
             if (p.u_scale.ptr != nullptr) us[j] = raw[p.nfac * kLinChunk + rr];
           }
         }
@@ -645,16 +653,16 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
 }
 
 // Per-step gradients (SURVEY A.4 restated):  d log a_t = sum_{s>=t} (dq_dot_s - dk_dot_s)
-// where dq_dot = Qm . dQm, dk_dot = Km . dKm;  d fac_f += d log a / fac_f;
-// d gate += dk_dot / gate (k_mod = k * gate: dL/dgate = k . dKm).  One block per (b, h) sequence; outputs accumulate with
-// the strides of the corresponding input (broadcast axes sum via atomics).
+// where dq_dot = Qm . dQm, dk_dot = Km . dKm.  One block per (b, h) sequence writes d log a_t and
+// dk_dot_t (both [B, H, S] fp32); step_grad_reduce_kernel then forms d fac_f = d log a / fac_f and
+// d gate = dk_dot / gate (k_mod = k * gate: dL/dgate = k . dKm) and sums broadcast axes in a fixed
+// order — no atomics, bitwise deterministic.
 __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
                                          const float* __restrict__ dk_dot, int slots,
-                                         LinearParams p, StepTensor dfac0, StepTensor dfac1,
-                                         StepTensor dgate) {
+                                         LinearParams p, float* __restrict__ dloga_out,
+                                         float* __restrict__ dkdot_out) {
   __shared__ float part[32];
   const int bh = blockIdx.x;
-  const int b = bh / p.heads, h = bh % p.heads;
   const int64_t base = static_cast<int64_t>(bh) * p.seq;
   const int seq = p.seq;
   const int64_t rows = static_cast<int64_t>(p.batch) * p.heads * p.seq;
@@ -683,16 +691,28 @@ __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
   for (int w2 = w + 1; w2 < static_cast<int>(blockDim.x >> 5); ++w2) acc += part[w2];
   for (int t = t1 - 1; t >= t0; --t) {
     acc += val(t);
-    const float dloga = acc;
-    const StepTensor* df[2] = {&dfac0, &dfac1};
-    for (int f = 0; f < p.nfac; ++f)
-      if (df[f]->ptr != nullptr)
-        atomicAdd(const_cast<float*>(df[f]->ptr) + b * df[f]->sb + h * df[f]->sh + t * df[f]->ss,
-                  dloga / p.fac[f].at(b, h, t));
-    if (dgate.ptr != nullptr)
-      atomicAdd(const_cast<float*>(dgate.ptr) + b * dgate.sb + h * dgate.sh + t * dgate.ss,
-                dot(dk_dot, t) / p.u_scale.at(b, h, t));
+    dloga_out[base + t] = acc;
+    if (dkdot_out != nullptr) dkdot_out[base + t] = dot(dk_dot, t);
   }
+}
+
+// out[b', h', t] += sum over the broadcast axes of out (stride 0) of val[b, h, t] / div(b, h, t),
+// in ascending (b, h) order.  val is [B, H, S] fp32; one thread per output element.
+__global__ void step_grad_reduce_kernel(const float* __restrict__ val, StepTensor div,
+                                        StepTensor out, int batch, int heads, int seq) {
+  const int nb = out.sb == 0 ? 1 : batch, nh = out.sh == 0 ? 1 : heads;
+  const int64_t total = static_cast<int64_t>(nb) * nh * seq;
+  const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (gid >= total) return;
+  const int t = static_cast<int>(gid % seq);
+  const int hh = static_cast<int>((gid / seq) % nh);
+  const int bb = static_cast<int>(gid / (static_cast<int64_t>(seq) * nh));
+  float acc = 0.0f;
+  for (int b = (out.sb == 0 ? 0 : bb); b < (out.sb == 0 ? batch : bb + 1); ++b)
+    for (int h = (out.sh == 0 ? 0 : hh); h < (out.sh == 0 ? heads : hh + 1); ++h)
+      acc += val[(static_cast<int64_t>(b) * heads + h) * seq + t] / div.at(b, h, t);
+  float* dst = const_cast<float*>(out.ptr) + bb * out.sb + hh * out.sh + t * out.ss;
+  *dst += acc;
 }
 
 // Km = bf16(k * gate): the backward uses one rounded copy of the gated keys in every pass so the

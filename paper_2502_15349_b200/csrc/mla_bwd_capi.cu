@@ -38,12 +38,6 @@ MatLayout mat_layout(const af_parallel_desc* d, bool shared) {
   return l;
 }
 
-template <typename K>
-int set_smem(K kern, int bytes) {
-  AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  return AF_OK;
-}
-
 // 3-D bf16 tensor map [outer][rows][cols] (cols contiguous) as a 4-D map with a unit batch.
 bool tmap_3d(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t outer,
              int box_cols, int box_rows) {
@@ -58,11 +52,7 @@ int launch_gemm(const CUtensorMap& a1, const CUtensorMap& a2, const CUtensorMap&
                 const CUtensorMap& b2, const MlaBwdParams& p, int n0, unsigned grid,
                 cudaStream_t s) {
   auto kern = mla_bwd_gemm_kernel<kMode, N>;
-  static bool attr = false;
-  if (!attr) {
-    if (set_smem(kern, MlaGemmSmem<N>::kTotal) != AF_OK) return AF_ERR_CUDA;
-    attr = true;
-  }
+  AF_SMEM_ATTR(kern, MlaGemmSmem<N>::kTotal);
   ::af::note_launch();
   kern<<<grid, 192, MlaGemmSmem<N>::kTotal, s>>>(a1, a2, b1, b2, p, n0);
   AF_CUDA_CHECK(cudaGetLastError());
@@ -148,11 +138,7 @@ int run_materialized(const af_parallel_desc* d, const void* q, const void* k, co
                       kShared ? d->k_stride : d->v_stride, 64, 128, true))
       return AF_ERR_INPUT;
     auto kern = mla_bwd_scores_kernel<D, DV, kShared>;
-    static bool attr = false;
-    if (!attr) {
-      if (set_smem(kern, SL::kTotal) != AF_OK) return AF_ERR_CUDA;
-      attr = true;
-    }
+    AF_SMEM_ATTR(kern, SL::kTotal);
     ::af::note_launch();
     kern<<<static_cast<unsigned>(k_tiles * bhs), 320, SL::kTotal, s>>>(tq, tdo, tk, tv, p);
     AF_CUDA_CHECK(cudaGetLastError());
@@ -195,8 +181,32 @@ bool materialized_bwd_dims(const af_parallel_desc* d) {
          (d->d_qk == 128 && d->d_v == 256);
 }
 
+// The materialised path holds two bf16 [b*H, q_pad, k_pad] score buffers: it runs over chunks
+// of the batch whose workspace fits kMatBudget, so the scratch stays bounded at any batch size
+// (e.g. softmax-diff 128/256 at B8 H32 S8192 would need ~68 GB in one pass).  A single batch
+// element above the budget is unsupported.
+constexpr size_t kMatBudget = size_t(24) << 30;
+
+int mat_batch_chunk(const af_parallel_desc* d) {
+  af_parallel_desc c = *d;
+  const bool shared = d->d_qk == 576 && d->d_v == 512;
+  int lo = 1;
+  for (int b = d->batch; b >= 1; b = (b == 1 ? 0 : (b + 1) / 2)) {
+    c.batch = b;
+    if (mat_layout(&c, shared).total <= kMatBudget) {
+      lo = b;
+      break;
+    }
+    if (b == 1) return 0;
+  }
+  return lo;
+}
+
 size_t mla_bwd_workspace(const af_parallel_desc* d) {
-  return mat_layout(d, d->d_qk == 576 && d->d_v == 512).total;
+  const int chunk = mat_batch_chunk(d);
+  af_parallel_desc c = *d;
+  c.batch = chunk > 0 ? chunk : 1;
+  return mat_layout(&c, d->d_qk == 576 && d->d_v == 512).total;
 }
 
 int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void* v, const void* o,
@@ -210,16 +220,45 @@ int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void*
   AF_REQUIRE(d->k_stride[3] == 1 && d->q_stride[3] == 1 && d->o_stride[3] == 1 &&
                  d->v_stride[3] == 1,
              AF_ERR_INPUT, "feature stride must be 1");
-  if (d->d_qk == 576 && d->d_v == 512) {
-    AF_REQUIRE(d->heads_kv == 1, AF_ERR_UNSUPPORTED, "MLA backward needs one latent KV head");
-    return run_materialized<576, 512, true>(d, q, k, v, o, lse, dout, dq, dk, dv, workspace, s);
+  const int chunk = mat_batch_chunk(d);
+  AF_REQUIRE(chunk > 0, AF_ERR_UNSUPPORTED,
+             "materialised backward: one batch element needs more than %zu GB of score scratch "
+             "(heads %d, seq %d x %d)", kMatBudget >> 30, d->heads_q, d->seq_q, d->seq_k);
+  auto off = [](const void* p, int64_t elems, int bytes) {
+    return p == nullptr ? nullptr
+                        : static_cast<const void*>(static_cast<const char*>(p) + elems * bytes);
+  };
+  for (int b0 = 0; b0 < d->batch; b0 += chunk) {
+    af_parallel_desc c = *d;
+    c.batch = std::min(chunk, d->batch - b0);
+    const void* q_ = off(q, b0 * d->q_stride[0], 2);
+    const void* k_ = off(k, b0 * d->k_stride[0], 2);
+    const void* v_ = off(v, b0 * d->v_stride[0], 2);
+    const void* o_ = off(o, b0 * d->o_stride[0], 2);
+    const void* do_ = off(dout, b0 * d->o_stride[0], 2);
+    const float* lse_ = static_cast<const float*>(
+        off(lse, static_cast<int64_t>(b0) * d->heads_q * d->seq_q, 4));
+    void* dq_ = const_cast<void*>(off(dq, b0 * d->q_stride[0], 2));
+    void* dk_ = const_cast<void*>(off(dk, b0 * d->k_stride[0], 2));
+    void* dv_ = const_cast<void*>(off(dv, b0 * d->v_stride[0], 2));
+    int st = AF_ERR_UNSUPPORTED;
+    if (d->d_qk == 576 && d->d_v == 512) {
+      AF_REQUIRE(d->heads_kv == 1, AF_ERR_UNSUPPORTED, "MLA backward needs one latent KV head");
+      st = run_materialized<576, 512, true>(&c, q_, k_, v_, o_, lse_, do_, dq_, dk_, dv_,
+                                            workspace, s);
+    } else if (d->d_qk == 192 && d->d_v == 128) {
+      st = run_materialized<192, 128, false>(&c, q_, k_, v_, o_, lse_, do_, dq_, dk_, dv_,
+                                             workspace, s);
+    } else if (d->d_qk == 128 && d->d_v == 256) {
+      st = run_materialized<128, 256, false>(&c, q_, k_, v_, o_, lse_, do_, dq_, dk_, dv_,
+                                             workspace, s);
+    } else {
+      set_error("materialised backward: head dims (%d, %d) not instantiated", d->d_qk, d->d_v);
+      return AF_ERR_UNSUPPORTED;
+    }
+    if (st != AF_OK) return st;
   }
-  if (d->d_qk == 192 && d->d_v == 128)
-    return run_materialized<192, 128, false>(d, q, k, v, o, lse, dout, dq, dk, dv, workspace, s);
-  if (d->d_qk == 128 && d->d_v == 256)
-    return run_materialized<128, 256, false>(d, q, k, v, o, lse, dout, dq, dk, dv, workspace, s);
-  set_error("materialised backward: head dims (%d, %d) not instantiated", d->d_qk, d->d_v);
-  return AF_ERR_UNSUPPORTED;
+  return AF_OK;
 }
 
 }  // namespace af

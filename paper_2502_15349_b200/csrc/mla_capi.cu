@@ -2,15 +2,6 @@
 // variant is softmax over one shared latent head with (Dqk, Dv) = (576, 512) and V = K[:, :512].
 #include "host_common.h"
 #include "mla.cuh"
-#include "mla_decode.cuh"
-
-#ifndef AF_MLA_DECODE_PAIR
-// Cluster-pair decode (QK^T split across the two value-half CTAs, partials exchanged through
-// DSMEM): parity-green but measured 2.2x slower (0.53 vs 0.24 ms at cfg4b) — the per-32-key-tile
-// exchange round trip sits on the softmax critical path.  Kept off as the starting point for a
-// pipelined exchange.
-#define AF_MLA_DECODE_PAIR 0
-#endif
 
 namespace af {
 
@@ -39,11 +30,7 @@ int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o
   p.o = o; p.o_sb = d->o_stride[0]; p.o_sh = d->o_stride[1]; p.o_ss = d->o_stride[2];
   p.lse = lse;
   auto kern = mla_fwd_kernel<false>;
-  static bool attr = false;
-  if (!attr) {
-    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PrefillSmem::kTotal));
-    attr = true;
-  }
+  AF_SMEM_ATTR(kern, PrefillSmem::kTotal);
   const int q_tiles = (d->seq_q + 127) / 128;
   ::af::note_launch();
   kern<<<q_tiles * d->batch * d->heads_q * 2, 192, PrefillSmem::kTotal, s>>>(tq, tkv, p);
@@ -118,24 +105,9 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
   float* part_lse = part_o + static_cast<size_t>(d->batch) * splits * d->heads * kMlaDv;
   p.part_o = part_o;
   p.part_lse = part_lse;
-  if (AF_MLA_DECODE_PAIR) {
-    auto kern = mla_decode_pair_kernel;
-    static bool attr = false;
-    if (!attr) {
-      AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         MlaDecSmem::kTotal));
-      attr = true;
-    }
-    ::af::note_launch();
-    kern<<<d->batch * splits * 2, 192, MlaDecSmem::kTotal, s>>>(tkv, p);
-  } else {
+  {
     auto kern = mla_fwd_kernel<true>;
-    static bool attr = false;
-    if (!attr) {
-      AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         DecodeSmem::kTotal));
-      attr = true;
-    }
+    AF_SMEM_ATTR(kern, DecodeSmem::kTotal);
     ::af::note_launch();
     kern<<<d->batch * splits * 2, 192, DecodeSmem::kTotal, s>>>(tq, tkv, p);
   }

@@ -33,11 +33,7 @@ int launch_bwd(const BwdLaunch& a) {
   {
     using L = BwdKVSmem<D, DV>;
     auto kern = parallel_bwd_dkdv_kernel<D, DV, kFamily, kAct>;
-    static bool attr = false;
-    if (!attr) {
-      AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
-      attr = true;
-    }
+    AF_SMEM_ATTR(kern, L::kTotal);
     dim3 grid((a.d->seq_k + kBlockN - 1) / kBlockN, a.d->batch * a.d->heads_kv);
     ::af::note_launch();
     kern<<<grid, kKvThreads, L::kTotal, a.s>>>(a.tq, a.tk, a.tv, a.tdo, a.p, a.lse2, a.delta,
@@ -47,11 +43,7 @@ int launch_bwd(const BwdLaunch& a) {
   {
     using L = BwdQSmem<D, DV>;
     auto kern = parallel_bwd_dq_kernel<D, DV, kFamily, kAct>;
-    static bool attr = false;
-    if (!attr) {
-      AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal));
-      attr = true;
-    }
+    AF_SMEM_ATTR(kern, L::kTotal);
     dim3 grid((a.d->seq_q + kBlockM - 1) / kBlockM, a.d->batch * a.d->heads_q);
     ::af::note_launch();
     kern<<<grid, kDqThreads, L::kTotal, a.s>>>(

@@ -2,15 +2,6 @@
 // tensor maps and dispatches the K1 instantiation for (head dims, hook family, activation).
 #include "host_common.h"
 #include "parallel_fwd.cuh"
-#include "parallel_fwd_1t.cuh"
-
-// K1t (parallel_fwd_1t.cuh): one query tile per CTA, P in its own TMEM columns.  Parity-green but
-// measured 16 % slower at cfg2 (4.9 vs 4.2 ms): with 128 rows per CTA the K/V stream doubles to
-// ~4.9 KB/clk of L2 -> SMEM, near the L2 throughput limit, so S(n+1) waits for its K tile
-// (tools/trace_fwd.py).  Kept off until K/V are shared by a 2-CTA cluster (TMA multicast).
-#ifndef AF_FWD_1T
-#define AF_FWD_1T 0
-#endif
 
 namespace af {
 namespace {
@@ -19,30 +10,10 @@ namespace {
 template <int D, int DV, int kFamily, int kAct>
 int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
                const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t stream) {
-  if constexpr (AF_FWD_1T && kFamily == kFamilySoftmax && kAct == kActIdentity && D <= 128) {
-    using L1 = Fwd1tSmem<D, DV>;
-    auto kern1 = parallel_fwd_1t_kernel<D, DV>;
-    static bool attr1 = false;
-    if (!attr1) {
-      AF_CUDA_CHECK(cudaFuncSetAttribute(kern1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         L1::kTotal));
-      attr1 = true;
-    }
-    dim3 grid1((d->seq_q + kBlockM - 1) / kBlockM, d->batch * d->heads_q);
-    ::af::note_launch();
-    kern1<<<grid1, kFwd1tThreads, L1::kTotal, stream>>>(tq, tk, tv, p);
-    AF_CUDA_CHECK(cudaGetLastError());
-    return AF_OK;
-  }
   constexpr int kStages = D > 128 ? 1 : 2;  // D = 192: two 48 KB Q tiles leave room for one stage
   using L = FwdSmem<D, DV, kStages>;
   auto kern = parallel_fwd_kernel<D, DV, kFamily, kAct, kStages>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    AF_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       L::kTotal));
-    attr_done = true;
-  }
+  AF_SMEM_ATTR(kern, L::kTotal);
   dim3 grid((d->seq_q + 2 * kBlockM - 1) / (2 * kBlockM), d->batch * d->heads_q);
   ::af::note_launch();
   kern<<<grid, fwd_threads(kFamily), L::kTotal, stream>>>(tq, tk, tv, p);

@@ -65,7 +65,16 @@ class Band:
 
     @property
     def kernel_window(self) -> int:
-        return 0 if self.window is None else self.window + self.diag_offset
+        """The kernels read window <= 0 as "no window": a lower key bound that reaches the
+        diagonal offset (e.g. ``where(kidx > qidx, s, -inf)``, keep j > i) is not lowered."""
+        if self.window is None:
+            return 0
+        w = self.window + self.diag_offset
+        if w <= 0:
+            raise UnsupportedError("mask keeps only keys above the diagonal (lower key bound "
+                                   "j > i - window with window + offset <= 0); not lowered",
+                                   window=self.window, diag_offset=self.diag_offset)
+        return w
 
 
 FM_NONE, FM_SILU, FM_SIGMOID, FM_RELU, FM_TANH, FM_EXP = range(6)
@@ -203,14 +212,15 @@ def _band_from_cond(cond: H.Cmp, consts: dict, band: Band) -> bool:
         op = "<" if op == ">" else "<="
     if op not in ("<", "<=") or a != -b or a == 0:
         return False
-    if op == "<":  # integer positions: x < 0  <=>  x <= -1
-        c += 1.0
-    # a*(i - j) + c <= 0
-    if a < 0:  # j <= i + c/a
-        up = math.floor(c / a + 1e-9)
+    # a*(i - j) + c (op) 0 over integer positions.  Strict bounds use ceil(.) - 1 so non-integer
+    # constants keep the reference's set (qidx - kidx < 2.5 keeps i - j <= 2).
+    if a < 0:  # j - i (op) c/a
+        t = c / a
+        up = (math.ceil(t - 1e-9) - 1) if op == "<" else math.floor(t + 1e-9)
         band.upper = up if band.upper is None else min(band.upper, up)
-    else:      # i - j <= -c/a  <=>  i - j < floor(-c/a) + 1
-        w = math.floor(-c / a + 1e-9) + 1
+    else:      # i - j (op) -c/a  →  keep i - j < w
+        t = -c / a
+        w = math.ceil(t - 1e-9) if op == "<" else math.floor(t + 1e-9) + 1
         band.window = w if band.window is None else min(band.window, w)
     return True
 
@@ -443,6 +453,12 @@ def _affine_score(e, consts: dict, extras: dict):
 
 
 def _plan_parallel(spec: AttentionSpec) -> ParallelPlan:
+    plan = _classify_parallel(spec)
+    plan.band.kernel_window  # noqa: B018 - raises for a band the kernels cannot express
+    return plan
+
+
+def _classify_parallel(spec: AttentionSpec) -> ParallelPlan:
     if spec.pattern is not Pattern.PARALLEL:
         raise InputError("variant is not a parallel-pattern variant", variant=spec.name)
     spec.validate()

@@ -55,3 +55,20 @@ def gather_outputs(local, shard: Shard, batch: int, groups: int, group=None):
         if units:
             out[units[0]: units[-1] + 1] = bufs[r][: len(units)]
     return out.reshape((batch, groups) + tuple(local.shape[1:]))
+
+
+def gather_batch_rows(tensors, world: int, group=None):
+    """All-gather equally sized per-rank outputs along dim 0 (the batch rows each rank owns,
+    ranks in order) with ``all_gather_into_tensor`` — one NCCL collective per tensor, written
+    straight into the global [world * B, ...] buffer."""
+    import torch
+    import torch.distributed as dist
+
+    out = []
+    for t in tensors:
+        t = t.contiguous()
+        full = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype,
+                           device=t.device)
+        dist.all_gather_into_tensor(full, t, group=group)
+        out.append(full)
+    return out

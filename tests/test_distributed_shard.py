@@ -54,3 +54,38 @@ def test_gloo_world2_gather_reassembles_every_unit():
     for _, full in results:
         assert full.shape == (batch, groups, 3, 2)
         assert torch.equal(full[..., 0, 0], want)
+
+
+def _rows_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2502_15349_b200.shard import gather_batch_rows
+    # bench.py's layout: every rank owns one config's worth of whole batch rows
+    batch, groups = 2, 3
+    shard = shard_units(batch * world, groups, world, rank)
+    b_lo = shard.units[0] // groups
+    o = torch.arange(batch * 4, dtype=torch.float32).reshape(batch, 4) + 100 * b_lo
+    lse = torch.full((batch, 2), float(b_lo))
+    full = gather_batch_rows([o, lse], world)
+    q.put((rank, b_lo, [f.clone() for f in full]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_bench_partition_gathers_batch_rows():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_rows_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sorted(b for _, b, _ in results) == [0, 2]
+    for _, _, (o, lse) in results:
+        assert o.shape == (4, 4) and lse.shape == (4, 2)
+        assert torch.equal(o[2:], torch.arange(8, dtype=torch.float32).reshape(2, 4) + 200)
+        assert torch.equal(lse[:, 0], torch.tensor([0.0, 0.0, 2.0, 2.0]))

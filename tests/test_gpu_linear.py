@@ -113,3 +113,51 @@ def test_prompt_state_then_decode_steps(name, dk, dv):
         assert nw(ot.double().cpu().numpy(), want[:, :, t:t + 1]) <= 2e-2, t
     _, state_full = af.linear_forward(full, to_dev(a), return_state=True)
     assert nw(state.double().cpu().numpy(), state_full.double().cpu().numpy()) <= 1e-2
+
+
+def test_broadcast_extra_gradient_is_deterministic_and_summed():
+    """A gate broadcast over the batch ([1, H, S, 1]): its gradient sums the per-(b, h) terms in a
+    fixed order (no atomics) — two calls agree bitwise and match the oracle's axis sum."""
+    from dataclasses import replace as dreplace
+    base = S.builtin("gated-retention", batch=3, heads=2, seq=300, d_qk=128, d_v=128)
+    spec = dreplace(base, extra_inputs=(dreplace(base.extra_inputs[0],
+                                                 shape=(1, "heads", "seq_k", 1),
+                                                 differentiable=True),))
+    arrays = oracle.generate(spec, seed=4)
+    assert arrays["gate"].shape == (1, 2, 300, 1)
+    dev = to_dev(arrays)
+    dout = torch.rand(3, 2, 300, 128, device="cuda").sub(0.5).to(torch.bfloat16)
+    g1 = af.linear_backward(spec, dev, dout)
+    g2 = af.linear_backward(spec, dev, dout)
+    assert torch.equal(g1["gate"], g2["gate"])
+    want = OR.chunk_vjp(spec, rounded(arrays), dout.double().cpu().numpy(), chunk=64)
+    assert nw(g1["gate"].double().cpu().numpy(), want["gate"]) <= 2e-2
+
+
+def test_autograd_engine_returns_extra_gradients():
+    """AttentionEngine(mamba2)(q, k, v, gate=, decay=): gate.grad / decay.grad are populated with
+    what linear_backward computes."""
+    spec = S.builtin("mamba2-ssm", batch=1, heads=2, seq=256, d_qk=128, d_v=128)
+    dev = to_dev(oracle.generate(spec, 1))
+    leaves = {n: t.clone().requires_grad_() for n, t in dev.items()}
+    out = af.AttentionEngine(spec)(leaves["q"], leaves["k"], leaves["v"], gate=leaves["gate"],
+                                   decay=leaves["decay"])
+    dout = torch.rand_like(out)
+    out.backward(dout)
+    g = af.linear_backward(spec, dev, dout)
+    for n in ("q", "k", "v", "gate", "decay"):
+        assert leaves[n].grad is not None, n
+        assert torch.equal(leaves[n].grad, g[n].to(leaves[n].dtype)), n
+
+
+def test_zero_decay_factor_resets_the_state_exactly():
+    """A per-step factor of exactly 0 (a state reset) stays finite in the log-space kernels and
+    matches the stepwise recurrence; a negative factor is reported as unsupported."""
+    spec = S.builtin("mamba2-ssm", batch=1, heads=2, seq=300, d_qk=128, d_v=128)
+    arrays = oracle.generate(spec, 2)
+    arrays["decay"][:, :, [0, 5, 130, 131, 299]] = 0.0
+    o = af.run_chunk_recurrent(spec, to_dev(arrays))
+    assert nw(o.double().cpu().numpy(), OR.step_forward(spec, rounded(arrays))) <= 2e-2
+    arrays["decay"][:, :, 7] = -0.5
+    with pytest.raises(af.UnsupportedError):
+        af.run_chunk_recurrent(spec, to_dev(arrays))

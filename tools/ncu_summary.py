@@ -15,6 +15,9 @@ KEYS = {
     "sm_clock_ghz": "sm__cycles_elapsed.avg.per_second",
 }
 SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+# gpu__time_duration is reported in ns, us (usecond), ms (msecond) or s depending on magnitude
+TO_MS = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0,
+         "s": 1e3, "second": 1e3}
 
 
 def summarize(rep):
@@ -36,6 +39,10 @@ def summarize(rep):
                 continue
             if k.endswith("_bytes"):
                 v *= SCALE.get(u[m], 1.0)
+            elif k == "duration_ms":
+                if u[m] not in TO_MS:
+                    raise ValueError(f"unknown duration unit {u[m]!r}")
+                v *= TO_MS[u[m]]
             rec[k] = v
         res.append(rec)
     return res
@@ -51,14 +58,16 @@ def launches(csv_path):
         name = r["Kernel Name"].split("(")[0].replace("void ", "")
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
-        v = v / 1e6 if unit in ("ns", "nsecond") else (v / 1e3 if unit in ("us", "usecond") else v)
+        v *= TO_MS[unit]
         tot.setdefault(name, []).append(v)
     return {k: {"launches": len(v), "ms_total": sum(v), "ms_avg": sum(v) / len(v)}
             for k, v in tot.items()}
 
 
 if __name__ == "__main__":
-    out = {}
+    head = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
+                          text=True).stdout.strip()
+    out = {"head": head}
     for rep in sys.argv[1:]:
         if rep.endswith(".csv"):
             out["launch_list"] = launches(rep)
