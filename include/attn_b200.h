@@ -141,6 +141,39 @@ enum { AF_FM_NONE = 0, AF_FM_SILU = 1, AF_FM_SIGMOID = 2, AF_FM_RELU = 3, AF_FM_
 int af_feature_map(int kind, int backward, const void* x, const void* dy, void* y, int64_t n,
                    void* stream);
 
+/* ---- elementwise hook programs (output_mod, general q/k/v mods) ---- */
+/* A hook expression compiled by the host (paper_2502_15349_b200/hookvm.py) into a postfix program
+ * evaluated per element of a [B, H, S, D] tensor in fp32 with a forward-mode dual number.
+ * Opcodes: 1 operand <k>, 2 const <i>, 3 index <axis>; 10 neg, 11 add, 12 sub, 13 mul, 14 div;
+ * 20 exp, 21 exp2, 22 log, 23 abs, 24 tanh, 25 sigmoid, 26 relu, 27 sqrt; 30 max, 31 min,
+ * 32 clamp, 33 where; 40 lt, 41 le, 42 gt, 43 ge, 44 eq, 45 ne.  Derivatives follow the reference
+ * adjoint rules (graph.py:481-569). */
+#define AF_HOOK_MAX_OPS 128
+#define AF_HOOK_MAX_CONSTS 32
+#define AF_HOOK_MAX_OPERANDS 8
+typedef struct af_hook_program {
+  int32_t n_ops;
+  int32_t ops[AF_HOOK_MAX_OPS];
+  int32_t n_consts;
+  float consts[AF_HOOK_MAX_CONSTS];
+} af_hook_program;
+
+/* A bf16 / fp32 tensor seen as [B, H, S, D] with element strides (0 = broadcast axis). */
+typedef struct af_hook_operand {
+  const void* ptr;
+  int32_t dtype;             /* AF_DTYPE_BF16 or AF_DTYPE_F32 */
+  int64_t stride[4];
+} af_hook_operand;
+
+/* out[i] = hook(operands)[i]  and/or  dout[i] = seed[i] * d hook / d operand[wrt] at i (seed NULL
+ * = 1) over the element grid `shape` [B, H, S, D].  Replaces the per-tile evaluation of
+ * output_mod (engine.py:502-504, 548-550) and of extra-reading q/k/v mods (engine.py:511-522); the
+ * derivative output gives the VJP through the hook (graph.py:436-591). */
+int af_hook_eval(const af_hook_program* prog, const int32_t* shape,
+                 const af_hook_operand* operands, int32_t n_operands, int32_t wrt,
+                 const af_hook_operand* seed, const af_hook_operand* out,
+                 const af_hook_operand* dout, void* stream);
+
 /* ---- diagnostics ---- */
 const char* af_status_string(int status);
 const char* af_last_error(void);      /* thread-local message of the last failing call */

@@ -24,14 +24,16 @@ from __future__ import annotations
 
 import contextlib
 import contextvars
+import dataclasses
 import math
 from dataclasses import dataclass
 
 import torch
 
+from . import hookvm
 from . import runtime as rt
 from .errors import InputError, NanError, ShapeError, UnsupportedError
-from .plan import (FAMILY_ABSSUM, FAMILY_SOFTMAX, LinearPlan, ParallelPlan, plan_linear,
+from .plan import (FAMILY_ABSSUM, FAMILY_SOFTMAX, FM_HOOK, LinearPlan, ParallelPlan, plan_linear,
                    plan_parallel)
 from .spec import AttentionSpec, Pattern, from_reference
 
@@ -128,6 +130,71 @@ def _maps(plan) -> tuple[int, int, int]:
     return getattr(plan, "q_map", 0), getattr(plan, "k_map", 0), getattr(plan, "v_map", 0)
 
 
+def _hook_tensors(plan, arrays: dict, **named) -> dict:
+    """Operands a compiled hook may read: the spec's extras (as given) plus ``named``."""
+    out = {e.name: arrays[e.name] for e in plan.spec.extra_inputs if e.name in arrays}
+    out.update(named)
+    return out
+
+
+def _mod(plan, var: str, x: torch.Tensor, arrays: dict) -> torch.Tensor:
+    """q_mod / k_mod / v_mod applied ahead of the template kernels: af_feature_map for its fixed
+    forms, a compiled hook program (af_hook_eval) for any other elementwise mod."""
+    kind = getattr(plan, f"{var}_map", 0)
+    if kind == FM_HOOK:
+        return hookvm.run_hook(plan.hooks[var], x.shape, _hook_tensors(plan, arrays, **{var: x}),
+                               out_dtype=_BF16)[0]
+    return _fmap(kind, x)
+
+
+def _hook_extra_grads(plan, key: str, shape, tensors: dict, seed: torch.Tensor,
+                      grads_x: dict) -> None:
+    """Accumulate seed * d hook / d extra (summed over the extra's broadcast axes) for every
+    differentiable extra the hook reads."""
+    hook = plan.hooks[key]
+    for e in plan.spec.extra_inputs:
+        if e.differentiable and hook.uses(e.name):
+            _, de = hookvm.run_hook(hook, shape, tensors, value=False, wrt=e.name, seed=seed)
+            de = hookvm.sum_to(de, tuple(tensors[e.name].shape))
+            grads_x[e.name] = de if e.name not in grads_x else grads_x[e.name] + de
+
+
+def _mod_vjp(plan, var: str, x: torch.Tensor, g: torch.Tensor, arrays: dict,
+             grads_x: dict) -> torch.Tensor:
+    """dL/dx from dL/d mod(x); extras read by a hook mod receive their gradient in grads_x."""
+    kind = getattr(plan, f"{var}_map", 0)
+    if kind == FM_HOOK:
+        tensors = _hook_tensors(plan, arrays, **{var: x})
+        _, dx = hookvm.run_hook(plan.hooks[var], x.shape, tensors, value=False, wrt=var, seed=g,
+                                deriv_dtype=_BF16)
+        _hook_extra_grads(plan, var, x.shape, tensors, g, grads_x)
+        return dx
+    return _fmap(kind, x, g)
+
+
+def _out_mod(plan, o: torch.Tensor, arrays: dict) -> torch.Tensor:
+    """output_mod on the full output (engine.py:502-504, 548-550, 613-615)."""
+    if "o" not in plan.hooks:
+        return o
+    return hookvm.run_hook(plan.hooks["o"], o.shape, _hook_tensors(plan, arrays, o=o),
+                           out_dtype=o.dtype)[0]
+
+
+def _out_mod_vjp(plan, o_inner: torch.Tensor, dout: torch.Tensor, arrays: dict,
+                 grads_x: dict) -> torch.Tensor:
+    tensors = _hook_tensors(plan, arrays, o=o_inner)
+    _, d = hookvm.run_hook(plan.hooks["o"], o_inner.shape, tensors, value=False, wrt="o",
+                           seed=dout, deriv_dtype=_BF16)
+    _hook_extra_grads(plan, "o", o_inner.shape, tensors, dout, grads_x)
+    return d
+
+
+def _hook_only_extras(plan) -> set:
+    """Differentiable extras read only by whole-tensor hooks (their gradients are lowered)."""
+    return {e.name for e in plan.spec.extra_inputs
+            if e.differentiable and any(h.uses(e.name) for h in plan.hooks.values())}
+
+
 # ───────────────────────────── parallel template ─────────────────────────────
 
 def _parallel_inputs(plan: ParallelPlan, arrays: dict, dtype):
@@ -156,7 +223,7 @@ def _parallel_inputs(plan: ParallelPlan, arrays: dict, dtype):
     if qm or km or vm:
         if dtype != _BF16 or plan.spec.kv_shared:
             raise UnsupportedError("feature maps run on the bf16 path of non-MLA variants only")
-        q, k, v = _fmap(qm, q), _fmap(km, k), _fmap(vm, v)
+        q, k, v = (_mod(plan, n, t, arrays) for n, t in (("q", q), ("k", k), ("v", v)))
     return _as(q, dtype), _as(k, dtype), _as(v, dtype), slope
 
 
@@ -259,9 +326,19 @@ def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: 
     ``precision="bf16"`` runs the tcgen05 kernel (K1) on bf16 inputs (fp32 inputs are rounded);
     ``"fp32"`` runs the exact-FFMA fp32 kernel (cfg1 parity path).  MLA variants (``kv_shared``,
     (Dqk, Dv) = (576, 512), one latent head) run K3: prefill, or the split-KV decode kernel when
-    seq_q == 1 and no mask applies."""
+    seq_q == 1 and no mask applies.  An ``output_mod`` runs on the full output afterwards
+    (af_hook_eval); the LSE is the template's own row statistic."""
     spec = _spec(spec)
     plan = plan_parallel(spec)
+    o, lse = _parallel_forward_core(spec, plan, arrays, precision)
+    if "o" in plan.hooks:
+        o = _out_mod(plan, o, arrays)
+    if check_nan:
+        _check_nan(o, "kernel")
+    return o, lse
+
+
+def _parallel_forward_core(spec, plan, arrays: dict, precision: str):
     d0 = spec.dims
     if (spec.kv_shared and precision == "bf16" and (d0.d_qk, d0.d_v) == (MLA_DQK, MLA_DV)
             and d0.seq_q == 1 and not plan.band.causal and plan.band.window is None):
@@ -270,8 +347,6 @@ def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: 
         _check_shape(q, (d0.batch, d0.heads, 1, MLA_DQK), "q")
         _check_shape(k, (d0.batch, 1, d0.seq_k, MLA_DQK), "k")
         o, lse = mla_decode(q[:, :, 0], k[:, 0], float(plan.scale))
-        if check_nan:
-            _check_nan(o, "kernel")
         return o.unsqueeze(2), lse.unsqueeze(2)
     dtype = _BF16 if precision == "bf16" else torch.float32
     q, k, v, slope = _parallel_inputs(plan, arrays, dtype)
@@ -295,8 +370,6 @@ def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: 
                  "af_parallel_fwd")
     if pad is not None:
         o = o[..., : d.d_v].contiguous()
-    if check_nan:
-        _check_nan(o, "kernel")
     return o, lse
 
 
@@ -315,15 +388,22 @@ def run_naive_parallel(spec, arrays: dict, **kw):
 
 def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tensor) -> dict:
     """VJP of ``parallel_forward`` for cotangent ``dout``: ``{"q": dq, "k": dk, "v": dv}`` (bf16;
-    dk/dv summed over each GQA group; for ``kv_shared`` the V gradient is folded into dk)."""
+    dk/dv summed over each GQA group; for ``kv_shared`` the V gradient is folded into dk), plus
+    the gradient of every differentiable extra read by a whole-tensor hook (q/k/v mod programs,
+    output_mod).  With an ``output_mod`` the template's own output is recomputed (``o`` is the
+    modified one) and ``dout`` is pulled back through the mod first."""
     spec = _spec(spec)
     plan = plan_parallel(spec)
-    maps = _maps(plan)
+    grads_x: dict = {}
+    if "o" in plan.hooks:
+        o, lse = _parallel_forward_core(spec, plan, arrays, "bf16")
+        dout = _out_mod_vjp(plan, o, dout, arrays, grads_x)
     g = _parallel_backward_mapped(spec, plan, arrays, o, lse, dout)
-    if any(maps):  # chain the feature maps: dL/dx = dL/df(x) * f'(x)
-        for name, kind in zip("qkv", maps):
-            if kind and name in g:
-                g[name] = _fmap(kind, _need(arrays, name), g[name])
+    for name, kind in zip("qkv", _maps(plan)):  # chain the q/k/v mods: dL/dx = dL/df(x) f'(x)
+        if kind and name in g:
+            g[name] = _mod_vjp(plan, name, _need(arrays, name), g[name], arrays, grads_x)
+    for name, t in grads_x.items():
+        g[name] = t.reshape(_need(arrays, name).shape).to(torch.float32)
     return g
 
 
@@ -454,8 +534,7 @@ def _linear_qkv(plan: LinearPlan, arrays: dict):
     _check_shape(q, (d.batch, d.heads, d.seq_q, d.d_qk), "q")
     _check_shape(k, (d.batch, d.heads, d.seq_k, d.d_qk), "k")
     _check_shape(v, (d.batch, d.heads, d.seq_k, d.d_v), "v")
-    qm, km, vm = _maps(plan)
-    q, k, v = _fmap(qm, q), _fmap(km, k), _fmap(vm, v)
+    q, k, v = (_mod(plan, n, t, arrays) for n, t in (("q", q), ("k", k), ("v", v)))
     pk, pv = _linear_pad(d)
     return (_pad_last(_as(q, _BF16), pk), _pad_last(_as(k, _BF16), pk),
             _pad_last(_as(v, _BF16), pv))
@@ -478,6 +557,8 @@ def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = Fa
                                     o.data_ptr(), rt.ptr(state), _stream()), "af_linear_fwd")
     if o.shape[-1] != d.d_v:
         o = o[..., : d.d_v].contiguous()
+    if "o" in plan.hooks:
+        o = _out_mod(plan, o, arrays)
     if check_nan:
         if torch.isnan(o).any().item():
             _check_factors(plan, arrays)
@@ -501,8 +582,8 @@ def linear_step(spec, arrays: dict, state: torch.Tensor) -> torch.Tensor:
     _check_shape(q, (d.batch, d.heads, 1, d.d_qk), "q")
     _check_shape(k, (d.batch, d.heads, 1, d.d_qk), "k")
     _check_shape(v, (d.batch, d.heads, 1, d.d_v), "v")
-    qm, km, vm = _maps(plan)
-    q, k, v = (_as(_fmap(m, t), _BF16).contiguous() for m, t in ((qm, q), (km, k), (vm, v)))
+    q, k, v = (_as(_mod(plan, n, t, arrays), _BF16).contiguous()
+               for n, t in (("q", q), ("k", k), ("v", v)))
     if state.dtype != torch.float32 or tuple(state.shape) != (d.batch, d.heads, d.d_qk, d.d_v) \
             or not state.is_contiguous() or not state.is_cuda:
         raise ShapeError("state must be contiguous fp32 [B,H,Dk,Dv] on the GPU",
@@ -511,7 +592,7 @@ def linear_step(spec, arrays: dict, state: torch.Tensor) -> torch.Tensor:
     desc, _keep = _linear_desc(plan, arrays, q, k, v, o)
     rt.check(rt.lib().af_linear_step(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                      state.data_ptr(), o.data_ptr(), _stream()), "af_linear_step")
-    return o
+    return _out_mod(plan, o, arrays)
 
 
 def run_chunk_recurrent(spec, arrays: dict, chunk: int = 64):
@@ -532,10 +613,14 @@ def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 128) ->
     enters a_t or k_mod (accumulated in-kernel with the extra's broadcast shape)."""
     spec = _spec(spec)
     plan = plan_linear(spec, chunk)
-    q, k, v = (t.contiguous() for t in _linear_qkv(plan, arrays))
     d = spec.dims
-    dout = _as(dout, _BF16).contiguous()
     _check_shape(dout, (d.batch, d.heads, d.seq_q, d.d_v), "dout")
+    hook_grads: dict = {}
+    if "o" in plan.hooks:  # pull dout back through output_mod at the template's own output
+        o_inner = linear_forward(dataclasses.replace(spec, output_mod=None), arrays, chunk)
+        dout = _out_mod_vjp(plan, o_inner, _as(dout, _BF16), arrays, hook_grads)
+    q, k, v = (t.contiguous() for t in _linear_qkv(plan, arrays))
+    dout = _as(dout, _BF16).contiguous()
     dout = _pad_last(dout, v.shape[-1]).contiguous()
     dq = _empty("lin.dq", q.shape, q.dtype, q.device)
     dk = _empty("lin.dk", k.shape, k.dtype, k.device)
@@ -559,11 +644,15 @@ def linear_backward(spec, arrays: dict, dout: torch.Tensor, chunk: int = 128) ->
                              _stream()), "af_linear_bwd")
     grads = {"q": dq[..., : d.d_qk], "k": dk[..., : d.d_qk], "v": dv[..., : d.d_v]}
     grads = {n: (t if t.is_contiguous() else t.contiguous()) for n, t in grads.items()}
-    for name, kind in zip("qkv", _maps(plan)):  # chain the feature maps
+    for name, kind in zip("qkv", _maps(plan)):  # chain the q/k/v mods
         if kind:
-            grads[name] = _fmap(kind, _need(arrays, name), grads[name])
+            grads[name] = _mod_vjp(plan, name, _need(arrays, name), grads[name], arrays,
+                                   hook_grads)
     for name, g in grads_x.items():
         grads[name] = g.reshape(_need(arrays, name).shape)
+    for name, g in hook_grads.items():
+        g = g.reshape(_need(arrays, name).shape).to(torch.float32)
+        grads[name] = grads[name] + g if name in grads else g
     return grads
 
 
@@ -577,11 +666,12 @@ def autodiff_grads(spec, arrays: dict, wrt=None, dout: torch.Tensor | None = Non
     if spec.pattern is Pattern.PARALLEL:
         o, lse = parallel_forward(spec, arrays)
         g = torch.ones_like(o) if dout is None else dout
-        grads = parallel_backward(spec, arrays, o, lse, g)
+        plan = plan_parallel(spec)
         for e in spec.extra_inputs:
-            if e.differentiable:
-                raise UnsupportedError("gradients w.r.t. parallel-template extras are not "
-                                       "lowered", extra=e.name)
+            if e.differentiable and e.name not in _hook_only_extras(plan):
+                raise UnsupportedError("gradients w.r.t. extras read by the fused score hooks "
+                                       "are not lowered", extra=e.name)
+        grads = parallel_backward(spec, arrays, o, lse, g)
     else:
         g = torch.ones(d.batch, d.heads, d.seq_q, d.d_v, device=_need(arrays, "q").device,
                        dtype=_BF16) if dout is None else dout
@@ -620,16 +710,18 @@ def bind(spec) -> BoundKernel:
 
 class _ParallelFn(torch.autograd.Function):
     """Autograd node of the parallel template.  Extras are positional inputs (names on ctx) so
-    autograd sees them; their gradients are not lowered on this template, so a differentiable
-    extra raises at forward time (the reference differentiates them, attention.py:542-543)."""
+    autograd sees them.  Extras read by whole-tensor hooks (q/k/v mod programs, output_mod) get
+    gradients; a differentiable extra read by the fused score hooks raises at forward time (the
+    reference differentiates it, attention.py:542-543; not lowered here)."""
 
     @staticmethod
     def forward(ctx, spec, names, q, k, v, *extra_t):
         extras = dict(zip(names, extra_t))
+        hook_only = _hook_only_extras(plan_parallel(spec))
         for e in spec.extra_inputs:
-            if e.differentiable:
-                raise UnsupportedError("gradients w.r.t. parallel-template extras are not "
-                                       "lowered", extra=e.name)
+            if e.differentiable and e.name not in hook_only:
+                raise UnsupportedError("gradients w.r.t. extras read by the fused score hooks "
+                                       "are not lowered", extra=e.name)
         arrays = {"q": q, "k": k, "v": v, **extras}
         with torch.cuda.device(q.device):
             o, lse = parallel_forward(spec, arrays)
@@ -647,9 +739,10 @@ class _ParallelFn(torch.autograd.Function):
         # MLA (kv_shared): V aliases K[..., :d_v]; its gradient is folded into dk and the v
         # argument is not read, so it receives none.
         gv = g.get("v")
+        gx = [g[n].to(t.dtype) if n in g and ctx.needs_input_grad[5 + i] else None
+              for i, (n, t) in enumerate(zip(ctx.names, extra_t))]
         return (None, None, g["q"].to(q.dtype), g["k"].to(k.dtype),
-                gv.to(v.dtype) if gv is not None and v is not None else None,
-                *([None] * len(extra_t)))
+                gv.to(v.dtype) if gv is not None and v is not None else None, *gx)
 
 
 class AttentionEngine:

@@ -43,6 +43,7 @@ __device__ long long g_lin_trace[24][128];
 #endif
 
 constexpr int kLinChunk = 128;
+constexpr int kRawRing = 4;  // chunks of raw per-step factors in flight (producer warp)
 // Waits of warps that idle for long stretches (row warps between chunks, output warps, loaders):
 // with a back-off they stop taking issue slots from the scan warp on their SMSP.
 #ifndef AF_LIN_IDLE_SLEEP
@@ -91,13 +92,13 @@ struct LinSmem {
   static constexpr int kVOff = kKOff + kStages * kQBytes;
   static constexpr int kVwOff = kVOff + kVStages * kVBytes;
   static constexpr int kHbOff = kVwOff + kVBytes;
-  // per row warp [8][128]: in-chunk cumsum of log2 a, key/value-side scale, and the column
-  // factor e^{-+L_u} u_u of the factorised decay (each row warp scans the chunk itself)
+  // [2 chunks in flight][128]: in-chunk cumsum of log2 a, key/value-side scale, and the column
+  // factor e^{-+L_u} u_u of the factorised decay — scanned by the producer warp one chunk ahead
   static constexpr int kLOff = kHbOff + DK * kLinVB * 2;
-  static constexpr int kUOff = kLOff + 8 * kLinChunk * 4;
-  static constexpr int kEcOff = kUOff + 8 * kLinChunk * 4;
-  static constexpr int kRawOff = kEcOff + 8 * kLinChunk * 4;  // [2][3][128] raw factors
-  static constexpr int kCpOff = kRawOff + 2 * 3 * kLinChunk * 4;  // [2][128] per-row output decay
+  static constexpr int kUOff = kLOff + 2 * kLinChunk * 4;
+  static constexpr int kEcOff = kUOff + 2 * kLinChunk * 4;
+  static constexpr int kRawOff = kEcOff + 2 * kLinChunk * 4;  // [kRawRing][3][128] raw factors
+  static constexpr int kCpOff = kRawOff + kRawRing * 3 * kLinChunk * 4;  // [2][128] output decay
   static constexpr int kFlagOff = kCpOff + 2 * kLinChunk * 4;
   // ring: full[S], empty[S]; s_full qh_full oi_full[2] h_full scan_ready[2] (raw factors of the
   // chunk landed; 1 arrival) | p_ready vw_ready h_scaled hb_ready scan_free[2] (raw factors read;
@@ -156,11 +157,12 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
   uint8_t* sV = smem + L::kVOff;
   uint8_t* sVw = smem + L::kVwOff;
   uint8_t* sHb = smem + L::kHbOff;
-  float* sLb = reinterpret_cast<float*>(smem + L::kLOff);  // [8 row warps][128]
-  float* sUb = reinterpret_cast<float*>(smem + L::kUOff);  // [8 row warps][128]
+  float* sLb = reinterpret_cast<float*>(smem + L::kLOff);  // [2][128]
+  float* sUb = reinterpret_cast<float*>(smem + L::kUOff);  // [2][128]
   float* sRaw = reinterpret_cast<float*>(smem + L::kRawOff);
   float* sCp = reinterpret_cast<float*>(smem + L::kCpOff);
-  float* sEcb = reinterpret_cast<float*>(smem + L::kEcOff);  // [8 row warps][128]
+  float* sEcb = reinterpret_cast<float*>(smem + L::kEcOff);  // [2][128]
+  volatile int* sFac = reinterpret_cast<volatile int*>(smem + L::kFlagOff);  // [2]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* full = bars;                 // Q, K, V of one chunk landed (one tx barrier)
   uint64_t* empty = bars + kStages;      // the chunk's Q, K, V may be overwritten
@@ -217,36 +219,96 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
   constexpr uint32_t kColS = 0, kColOI = 128, kColQH = 256, kColH = 384;
 
   if (warp == 12) {
-    // ───────────── producer warp: raw per-step factors (+ the TMA ring at DK = 256) ─────────────
-    // The raw factors of chunk n go to sRaw[n % 2] with cp.async (up to two chunks ahead of the
-    // row warps, which scan them themselves: a separate scan warp sat on the critical path, its
-    // few hundred instructions starved of issue slots by the busy warps of its SMSP).
+    // ───────────── producer warp: per-step decay scan (+ the TMA ring at DK = 256) ─────────────
+    // Chunk n's raw factors land by cp.async; this warp then scans them — L = in-chunk inclusive
+    // cumsum of log2 a, the key/value-side scale u and, when the chunk's |L| stays below 2^100,
+    // the column factors e^{-+L_u} u_u of the factorised decay — into the shared [n % 2] arrays,
+    // one chunk ahead of the row warps (traced: a scan inside every row warp put ~2.5k clk of
+    // dependent LDS / MUFU / SHFL latency on the ~6k-clk chunk period).
     const int lane = static_cast<int>(lane_id());
     const int nraw = p.nfac + (p.u_scale.ptr != nullptr ? 1 : 0);
+    // raw factors run kRawRing - 1 chunks ahead of the scan (cp.async groups; only this warp
+    // reads them): traced, a load issued one chunk ahead still took ~3.5k clk to land under the
+    // TMA traffic and held the rows back by ~1.3k clk per chunk
+    auto load_raw = [&](int m) {
+      if (m < nchunks) {
+        const int cm = kReverse ? nchunks - 1 - m : m;
+        float* raw = sRaw + (m % kRawRing) * 3 * kLinChunk;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int rr = lane * 4 + j;
+          const int t = cm * kLinChunk + rr;
+          if (t < p.seq) {
+            for (int f = 0; f < nraw; ++f) {
+              const StepTensor& ts = f < p.nfac ? p.fac[f] : p.u_scale;
+              const float* src = ts.ptr + b * ts.sb + h * ts.sh + t * ts.ss;
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                               smem_u32(raw + f * kLinChunk + rr)),
+                           "l"(src)
+                           : "memory");
+            }
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count)
+    };
+    for (int m = 0; m < kRawRing - 1; ++m) load_raw(m);
     for (int n = 0; n < nchunks; ++n) {
       const int c = kReverse ? nchunks - 1 - n : n;
       const int t0 = c * kLinChunk;
       const int pb = n & 1;
-      if (n >= 2) LIN_IDLE_WAIT(&scan_free[pb], ((n >> 1) - 1) & 1);  // rows done with chunk n-2
-      float* raw = sRaw + pb * 3 * kLinChunk;
+      load_raw(n + kRawRing - 1);  // its slot held chunk n-1, already scanned by this warp
+      asm volatile("cp.async.wait_group %0;" ::"n"(kRawRing - 1) : "memory");
+      __syncwarp();
+      if (lane == 0) AF_LT(17, n);
+      const float* raw = sRaw + (n % kRawRing) * 3 * kLinChunk;
+      {
+        float x[4], us[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int rr = lane * 4 + j;
-        const int t = t0 + rr;
-        if (t < p.seq) {
-          for (int f = 0; f < nraw; ++f) {
-            const StepTensor& ts = f < p.nfac ? p.fac[f] : p.u_scale;
-            const float* src = ts.ptr + b * ts.sb + h * ts.sh + t * ts.ss;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                             smem_u32(raw + f * kLinChunk + rr)),
-                         "l"(src)
-                         : "memory");
+        for (int j = 0; j < 4; ++j) {
+          const int rr = lane * 4 + j;
+          x[j] = 0.0f;
+          us[j] = 1.0f;
+          if (t0 + rr < p.seq) {
+            x[j] = p.log_const * kLog2e_;
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+              if (f < p.nfac) x[j] += log2_floor(raw[f * kLinChunk + rr]);
+            if (p.u_scale.ptr != nullptr) us[j] = raw[p.nfac * kLinChunk + rr];
           }
         }
+        x[1] += x[0];
+        x[2] += x[1];
+        x[3] += x[2];
+        float tot = x[3];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float y = __shfl_up_sync(0xffffffffu, tot, off);
+          if (lane >= off) tot += y;
+        }
+        const float excl = tot - x[3];
+        // Factorised decay D[i,u] = e^{L_i} e^{-L_u} (reverse: e^{-L_i} e^{L_u}) when every |L|
+        // of the chunk stays below 2^100: one multiply per element instead of an ex2.
+        float amax = fmaxf(fabsf(excl + x[0]), fabsf(excl + x[3]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+          amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+        const bool fac = kFac && amax <= 100.0f;
+        if (n >= 2) LIN_IDLE_WAIT(&scan_free[pb], ((n >> 1) - 1) & 1);  // chunk n-2 fully read
+        if (lane == 0) AF_LT(16, n);
+        float* sL = sLb + pb * kLinChunk;
+        float* sU = sUb + pb * kLinChunk;
+        float* sEc = sEcb + pb * kLinChunk;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float lj = excl + x[j];
+          sL[lane * 4 + j] = lj;
+          sU[lane * 4 + j] = us[j];
+          if (fac) sEc[lane * 4 + j] = exp2f(kReverse ? lj : -lj) * us[j];
+        }
+        if (lane == 0) sFac[pb] = fac ? 1 : 0;
+        __syncwarp();
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncwarp();
       if (lane == 0) mbar_arrive(&scan_ready[pb]);
       if (lane == 0) AF_LT(15, n);
       if constexpr (!kSplitLoad) {  // Q, K, V of chunk n behind its scan (single-stage Q/K ring)
@@ -428,61 +490,13 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
       const uint32_t ph = n & 1;
       const bool live = t < p.seq;
       (void)live;
-      // (a) the producer warp's scan of log2 a for this chunk
-      float* sL = sLb + warp * kLinChunk;
-      float* sU = sUb + warp * kLinChunk;
-      float* sEc = sEcb + warp * kLinChunk;
+      // (a) the producer warp's scan of this chunk (shared [n % 2] arrays)
+      const float* sL = sLb + ph * kLinChunk;
+      const float* sU = sUb + ph * kLinChunk;
+      const float* sEc = sEcb + ph * kLinChunk;
       LIN_IDLE_WAIT(&scan_ready[ph], (n >> 1) & 1);
       if (threadIdx.x == 0) AF_LT(14, n);
-      bool fac;
-      {  // this warp's scan of the chunk: L = in-chunk inclusive cumsum of log2 a, per position
-        const int lane = static_cast<int>(lane_id());
-        const float* raw = sRaw + ph * 3 * kLinChunk;
-        const int t0 = c * kLinChunk;
-        float x[4], us[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int rr = lane * 4 + j;
-          x[j] = 0.0f;
-          us[j] = 1.0f;
-          if (t0 + rr < p.seq) {
-            x[j] = p.log_const * kLog2e_;
-#pragma unroll
-            for (int f = 0; f < 2; ++f)
-              if (f < p.nfac) x[j] += log2_floor(raw[f * kLinChunk + rr]);
-            if (p.u_scale.ptr != nullptr) us[j] = raw[p.nfac * kLinChunk + rr];
-          }
-        }
-        __syncwarp();
-        if (threadIdx.x == 0) AF_LT(16, n);
-        if (lane == 0) mbar_arrive(&scan_free[ph]);  // raw factors of this chunk read
-        x[1] += x[0];
-        x[2] += x[1];
-        x[3] += x[2];
-        float tot = x[3];
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const float y = __shfl_up_sync(0xffffffffu, tot, off);
-          if (lane >= off) tot += y;
-        }
-        const float excl = tot - x[3];
-        if (threadIdx.x == 0) AF_LT(17, n);
-        // Factorised decay D[i,u] = e^{L_i} e^{-L_u} (reverse: e^{-L_i} e^{L_u}) when every |L|
-        // of the chunk stays below 2^100: one multiply per element instead of an ex2.
-        float amax = fmaxf(fabsf(excl + x[0]), fabsf(excl + x[3]));
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1)
-          amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-        fac = kFac && amax <= 100.0f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float lj = excl + x[j];
-          sL[lane * 4 + j] = lj;
-          sU[lane * 4 + j] = us[j];
-          if (fac) sEc[lane * 4 + j] = exp2f(kReverse ? lj : -lj) * us[j];
-        }
-        __syncwarp();
-      }
+      const bool fac = sFac[ph] != 0;
       if (threadIdx.x == 0) AF_LT(18, n);
       const float l_r = sL[r];
       const float l_last = sL[kLinChunk - 1];
@@ -596,7 +610,10 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive(p_ready);
+      if (lane_id() == 0) {
+        mbar_arrive(p_ready);
+        mbar_arrive(&scan_free[ph]);  // this chunk's scan arrays read (last use: P)
+      }
       if (threadIdx.x == 0) AF_LT(8, n);
       // (f) bf16 copy of the updated state (this half's columns) for the next chunk's Q H —
       //     after Q H of this chunk has read the previous copy

@@ -78,6 +78,7 @@ class Band:
 
 
 FM_NONE, FM_SILU, FM_SIGMOID, FM_RELU, FM_TANH, FM_EXP = range(6)
+FM_HOOK = 99  # any other elementwise mod: a compiled hook program (hookvm.py / af_hook_eval)
 _FM_BY_FUNC = {"sigmoid": FM_SIGMOID, "relu": FM_RELU, "tanh": FM_TANH, "exp": FM_EXP}
 
 
@@ -101,6 +102,8 @@ class ParallelPlan:
     decay_extra: str | None = None
     decay_gammas: tuple = ()
     normalize: bool = False
+    # compiled whole-tensor hooks: "q"/"k"/"v" for FM_HOOK mods, "o" for output_mod
+    hooks: dict = field(default_factory=dict)
 
     @property
     def has_lse(self) -> bool:
@@ -121,6 +124,7 @@ class LinearPlan:
     k_map: int = FM_NONE
     v_map: int = FM_NONE
     decay_hint: bool = False              # mild constant decay fills: factorised-decay kernel
+    hooks: dict = field(default_factory=dict)  # as ParallelPlan.hooks
 
 
 # ───────────────────────────── helpers ─────────────────────────────
@@ -164,8 +168,21 @@ def _feature_map(fn, var: str, consts: dict) -> tuple[int, float]:
         for x, y in ((e.lhs, e.rhs), (e.rhs, e.lhs)):
             if is_var(x) and isinstance(y, H.Fn) and y.func == "sigmoid" and is_var(y.args[0]):
                 return FM_SILU, 1.0
-    raise UnsupportedError(f"{var}_mod is neither a compile-time scalar nor a supported "
-                           "elementwise feature map", source=fn.source)
+    return FM_HOOK, 1.0
+
+
+def _compile_mods(spec: AttentionSpec, maps: dict, consts: dict) -> dict:
+    """Hook programs for the FM_HOOK q/k/v mods and for output_mod (hookvm.compile_hook; the
+    inputs a hook may read are its own tensor, the spec's extras and the dims constants)."""
+    from . import hookvm
+    extras = [e.name for e in spec.extra_inputs]
+    hooks = {}
+    for var in "qkv":
+        if maps.get(f"{var}_map") == FM_HOOK:
+            hooks[var] = hookvm.compile_hook(getattr(spec, f"{var}_mod"), [var] + extras, consts)
+    if spec.output_mod is not None:
+        hooks["o"] = hookvm.compile_hook(spec.output_mod, ["o"] + extras, consts)
+    return hooks
 
 
 def _linear_in_index(e, consts: dict):
@@ -467,12 +484,10 @@ def _classify_parallel(spec: AttentionSpec) -> ParallelPlan:
     k_map, k_sc = _feature_map(spec.k_mod, "k", consts)
     v_map, v_sc = _feature_map(spec.v_mod, "v", consts)
     scale = q_sc * k_sc
-    if v_sc != 1.0:
-        raise UnsupportedError("v_mod scaling is not lowered", source=spec.v_mod.source)
+    if v_sc != 1.0:  # o is linear in v: a scalar v_mod becomes a one-op hook program
+        v_map = FM_HOOK
     maps = dict(q_map=q_map, k_map=k_map, v_map=v_map)
-    if spec.output_mod is not None:
-        raise UnsupportedError("output_mod is not lowered on the parallel template yet",
-                               source=spec.output_mod.source)
+    maps["hooks"] = _compile_mods(spec, maps, consts)
     band = Band()
     plain, mask_vals = [], []
     seen_mask = False
@@ -680,38 +695,28 @@ def _plan_linear(spec: AttentionSpec, chunk: int = 64) -> LinearPlan:
             raise UnsupportedError("per-step scale is not a product of extras and constants",
                                    factor=H.to_source(f))
     k_gate = None
+    k_map, k_sc = FM_NONE, 1.0
     if spec.k_mod is not None:
         e = spec.k_mod.expr
-        ok = False
         if isinstance(e, H.BinOp) and e.op == "*":
             for x, y in ((e.lhs, e.rhs), (e.rhs, e.lhs)):
                 if isinstance(x, H.Name) and x.name == "k" and isinstance(y, H.Name) \
-                        and y.name in extras:
-                    k_gate, ok = y.name, True
-        if not ok:
-            k_map_, k_sc = _feature_map(spec.k_mod, "k", consts)
-            if k_map_ == FM_NONE:
-                raise UnsupportedError("k_mod must be k * <per-step extra> or an elementwise "
-                                       "feature map on the linear template",
-                                       source=spec.k_mod.source)
-            if k_sc != 1.0:
-                raise UnsupportedError("scaled k feature maps are not lowered",
-                                       source=spec.k_mod.source)
-    k_map = FM_NONE if k_gate is not None or spec.k_mod is None else \
-        _feature_map(spec.k_mod, "k", consts)[0]
+                        and y.name in extras and tuple(extras[y.name].shape)[2:] == ("seq_k", 1):
+                    k_gate = y.name  # a per-step key gate: applied inside the kernels
+        if k_gate is None:
+            k_map, k_sc = _feature_map(spec.k_mod, "k", consts)
     v_map, v_scale = _feature_map(spec.v_mod, "v", consts)
-    if spec.output_mod is not None:
-        raise UnsupportedError("output_mod is not lowered on the linear template yet",
-                               source=spec.output_mod.source)
     q_map, q_scale = _feature_map(spec.q_mod, "q", consts)
-    # o is linear in v: a scalar v_mod folds into the output scale
+    maps = dict(q_map=q_map, k_map=k_map, v_map=v_map)
+    hooks = _compile_mods(spec, maps, consts)
     hint = 0.5 <= const and all(
         extras[nm].fill == "constant_decay"
         and all(0.5 <= float(g) <= 1.0 for g in extras[nm].fill_params.get("gamma", [0.0]))
         for nm in names)
-    return LinearPlan(spec, q_scale=q_scale * v_scale, decay_factors=tuple(names),
+    # o is linear in q, k and v: scalar mods fold into the output scale
+    return LinearPlan(spec, q_scale=q_scale * v_scale * k_sc, decay_factors=tuple(names),
                       decay_const=const, k_gate=k_gate, chunk=chunk, q_map=q_map, k_map=k_map,
-                      v_map=v_map, decay_hint=hint)
+                      v_map=v_map, decay_hint=hint, hooks=hooks)
 
 
 # ───────────────────────────── plan cache ─────────────────────────────

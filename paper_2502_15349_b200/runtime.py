@@ -73,6 +73,7 @@ SIGNATURES: dict[str, tuple] = {
     "af_mla_decode_workspace": (C.c_size_t, [C.POINTER(MlaDesc)]),
     "af_mla_decode": (C.c_int, [C.POINTER(MlaDesc), P, P, P, P, P, C.c_size_t, P]),
     "af_feature_map": (C.c_int, [C.c_int, C.c_int, P, P, P, C.c_int64, P]),
+    "af_hook_eval": (C.c_int, [P, P, P, C.c_int32, C.c_int32, P, P, P, P]),
     "af_status_string": (C.c_char_p, [C.c_int]),
     "af_last_error": (C.c_char_p, []),
     "af_device_sm_count": (C.c_int, []),

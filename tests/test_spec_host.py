@@ -178,8 +178,15 @@ def test_feature_maps_recognised():
     for src, kind in (("relu(q)", P.FM_RELU), ("sigmoid(q) * q", P.FM_SILU), ("exp(q)", P.FM_EXP),
                       ("tanh(q)", P.FM_TANH), ("q * 0.5", P.FM_NONE)):
         assert P._feature_map(S.mod(src, "q"), "q", consts)[0] == kind
-    with pytest.raises(E.UnsupportedError):
-        P._feature_map(S.mod("q * q", "q"), "q", consts)
+    # any other elementwise mod becomes a compiled hook program (af_hook_eval)
+    assert P._feature_map(S.mod("q * q", "q"), "q", consts)[0] == P.FM_HOOK
+    from paper_2502_15349_b200 import hookvm
+    h = hookvm.compile_hook(S.mod("q * sigmoid(w) + qidx / seqq", "q"), ["q", "w"], consts)
+    assert h.operands == ("q", "w") and h.ops[-1] == 11  # ... add
+    with pytest.raises(E.UnsupportedError):  # reductions are not elementwise
+        hookvm.compile_hook(S.mod("q - reduceMax(q)", "q"), ["q"], consts)
+    with pytest.raises(E.UnsupportedError):  # unknown names
+        hookvm.compile_hook(S.mod("q * z", "q"), ["q"], consts)
 
 
 def test_every_reference_fixture_lowers():

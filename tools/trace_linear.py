@@ -34,7 +34,7 @@ names = {15: "scan: scan_ready arrive", 14: "rows: scan_ready passed", 4: "rows:
          7: "rows: s_full passed", 8: "rows: P written", 11: "rows: h_full+qh_full passed",
          12: "rows: bf16 H written", 0: "mma: Q/K full", 1: "mma: hb_ready+oi_empty",
          3: "mma: vw+h_scaled", 2: "mma: p_ready+vfull", 9: "out: oi_full passed",
-         10: "out: O written", 16: "rows: log2 done", 17: "rows: cumsum done",
+         10: "out: O written", 16: "prod: scan_free passed", 17: "prod: raw landed",
          18: "rows: scan stored", 19: "rows: row factors done"}
 ss = range(8, 56)
 base = buf[14]
