@@ -96,11 +96,15 @@ typedef struct af_linear_desc {
                                 variant (still checked per chunk at run time); 0: generic */
 } af_linear_desc;
 
+/* Bytes of device scratch af_linear_fwd needs (the per-chunk decay scan shared by the passes). */
+size_t af_linear_fwd_workspace(const af_linear_desc* desc);
+
 /* o_t = q_scale * q_t h_t,  h_t = a_t h_{t-1} + (k_t * gate_t)^T v_t,  h_0 = 0.
  * final_state (may be NULL): fp32 [B, H, d_k, d_v] receives h_S, the state after the last token.
  * Replaces engine.run_chunk_recurrent (engine.py:554). */
 int af_linear_fwd(const af_linear_desc* desc, const void* q, const void* k, const void* v,
-                  void* o, float* final_state, void* stream);
+                  void* o, float* final_state, void* workspace, size_t workspace_bytes,
+                  void* stream);
 
 /* One generation step (desc->seq == 1): state <- a_t state + (k_t * gate_t)^T v_t (fp32
  * [B, H, d_k, d_v], in place), o_t = q_scale * q_t state.  The body of engine.run_step_recurrent
@@ -173,6 +177,26 @@ int af_hook_eval(const af_hook_program* prog, const int32_t* shape,
                  const af_hook_operand* operands, int32_t n_operands, int32_t wrt,
                  const af_hook_operand* seed, const af_hook_operand* out,
                  const af_hook_operand* dout, void* stream);
+
+/* ---- materialised tier of the parallel template (engine.run_naive_parallel on the GPU) ---- */
+/* For variants the fused kernels do not lower: S = Qm Km^T and O = P Vm are plain GEMMs, the
+ * score hooks run through af_hook_eval over [B, H, Sq, Sk], and these apply the recognised row
+ * normalisation to contiguous fp32 score rows [rows, n]. */
+enum { AF_ROWNORM_NONE = 0, AF_ROWNORM_SOFTMAX = 1, AF_ROWNORM_ABSSUM = 2 };
+
+/* p = rownorm(z); stat = LSE (softmax; -inf for fully-masked rows) or the row abs-sum (abssum).
+ * attention.py:556-586. */
+int af_rownorm_fwd(int32_t kind, const float* z, float* p, float* stat, int64_t rows, int64_t n,
+                   void* stream);
+
+/* dz = d rownorm / dz applied to dp, given rowdot = <dO, O> per row (graph.py:436-591 rules). */
+int af_rownorm_bwd(int32_t kind, const float* z, const float* p, const float* dp,
+                   const float* rowdot, const float* stat, float* dz, int64_t rows, int64_t n,
+                   void* stream);
+
+/* out[b, h, s] = sum_d a[b, h, s, d] * b[b, h, s, d] (the softmax VJP's row term). */
+int af_rowdot(const af_hook_operand* a, const af_hook_operand* b, const int32_t* shape,
+              float* out, void* stream);
 
 /* ---- diagnostics ---- */
 const char* af_status_string(int status);

@@ -553,8 +553,11 @@ def linear_forward(spec, arrays: dict, chunk: int = 128, *, check_nan: bool = Fa
     state = (torch.empty(d.batch, d.heads, q.shape[-1], v.shape[-1], device=q.device,
                          dtype=torch.float32) if return_state else None)
     desc, _keep = _linear_desc(plan, arrays, q, k, v, o)
-    rt.check(rt.lib().af_linear_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                                    o.data_ptr(), rt.ptr(state), _stream()), "af_linear_fwd")
+    L = rt.lib()
+    ws_n = L.af_linear_fwd_workspace(desc)
+    ws = _empty("lin.fws", (ws_n,), torch.uint8, q.device)
+    rt.check(L.af_linear_fwd(desc, q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                             rt.ptr(state), ws.data_ptr(), ws_n, _stream()), "af_linear_fwd")
     if o.shape[-1] != d.d_v:
         o = o[..., : d.d_v].contiguous()
     if "o" in plan.hooks:

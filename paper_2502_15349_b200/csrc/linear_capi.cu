@@ -6,6 +6,28 @@
 namespace af {
 namespace {
 
+// Scratch of the decay scan shared by every template pass of one call.
+struct ScanBufs {
+  float* lcum = nullptr;
+  float* ucum = nullptr;
+  int* cflag = nullptr;
+};
+
+size_t scan_bytes(const af_linear_desc* d) {
+  const size_t units = static_cast<size_t>(d->batch) * d->heads * ((d->seq + 127) / 128);
+  const size_t vec = units * kLinChunk * sizeof(float);
+  return (2 * vec + units * sizeof(int) + 255) / 256 * 256;
+}
+
+ScanBufs scan_layout(const af_linear_desc* d, void* base) {
+  const size_t units = static_cast<size_t>(d->batch) * d->heads * ((d->seq + 127) / 128);
+  ScanBufs s;
+  s.lcum = static_cast<float*>(base);
+  s.ucum = d->key_gate != nullptr ? s.lcum + units * kLinChunk : nullptr;
+  s.cflag = reinterpret_cast<int*>(s.lcum + 2 * units * kLinChunk);
+  return s;
+}
+
 struct LaArgs {
   const void* q;
   const void* k;
@@ -24,6 +46,7 @@ struct LaArgs {
   float* dot;
   bool reverse;
   float* final_state = nullptr;
+  ScanBufs scan{};
 };
 
 StepTensor step_tensor(const float* ptr, const int64_t* st) {
@@ -78,6 +101,9 @@ int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
   }
   p.dot = a.dot;
   p.final_state = a.final_state;
+  p.lcum = a.scan.lcum;
+  p.ucum = a.u_gate ? a.scan.ucum : nullptr;  // the pass's own key/value-side scale
+  p.cflag = a.scan.cflag;
   auto kern = linear_chunk_kernel<DK, kRev, kFac>;
   AF_SMEM_ATTR(kern, L::kTotal);
   dim3 grid(d->batch * d->heads * (a.dvv / kLinVB));
@@ -92,17 +118,24 @@ int run_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
     set_error("linear template: value dim %d is not a multiple of %d", a.dvv, kLinVB);
     return AF_ERR_UNSUPPORTED;
   }
-  const bool fac = d->decay_hint != 0;
-  if (a.dqk == 128) {
-    if (fac) return a.reverse ? launch_la<128, true, true>(d, a, s) : launch_la<128, false, true>(d, a, s);
-    return a.reverse ? launch_la<128, true, false>(d, a, s) : launch_la<128, false, false>(d, a, s);
-  }
-  if (a.dqk == 256) {
-    if (fac) return a.reverse ? launch_la<256, true, true>(d, a, s) : launch_la<256, false, true>(d, a, s);
-    return a.reverse ? launch_la<256, true, false>(d, a, s) : launch_la<256, false, false>(d, a, s);
-  }
+  // decay factorisation is decided per 32-key group at run time (desc->decay_hint is advisory)
+  if (a.dqk == 128)
+    return a.reverse ? launch_la<128, true, true>(d, a, s) : launch_la<128, false, true>(d, a, s);
+  if (a.dqk == 256)
+    return a.reverse ? launch_la<256, true, true>(d, a, s) : launch_la<256, false, true>(d, a, s);
   set_error("linear template: key dim %d not instantiated (128, 256)", a.dqk);
   return AF_ERR_UNSUPPORTED;
+}
+
+int run_scan(const af_linear_desc* d, const ScanBufs& sb, cudaStream_t s) {
+  LinearParams p = base_params(d);
+  p.u_scale = step_tensor(d->key_gate, d->key_gate_stride);
+  const int64_t warps = static_cast<int64_t>(d->batch) * d->heads * ((d->seq + 127) / 128);
+  ::af::note_launch();
+  linear_decay_scan_kernel<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(
+      p, sb.lcum, sb.ucum, sb.cflag);
+  AF_CUDA_CHECK(cudaGetLastError());
+  return AF_OK;
 }
 
 int validate_linear(const af_linear_desc* d) {
@@ -120,14 +153,24 @@ int validate_linear(const af_linear_desc* d) {
 }  // namespace
 }  // namespace af
 
+extern "C" size_t af_linear_fwd_workspace(const af_linear_desc* d) {
+  return d == nullptr ? 0 : af::scan_bytes(d);
+}
+
 extern "C" int af_linear_fwd(const af_linear_desc* d, const void* q, const void* k, const void* v,
-                             void* o, float* final_state, void* stream) {
+                             void* o, float* final_state, void* workspace,
+                             size_t workspace_bytes, void* stream) {
   using namespace af;
   int st = validate_linear(d);
   if (st != AF_OK) return st;
+  AF_REQUIRE(workspace != nullptr && workspace_bytes >= scan_bytes(d), AF_ERR_INPUT,
+             "workspace too small (%zu < %zu)", workspace_bytes, scan_bytes(d));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const ScanBufs sb = scan_layout(d, workspace);
+  if ((st = run_scan(d, sb, s)) != AF_OK) return st;
   LaArgs a{q, k, v, d->q_stride, d->k_stride, d->v_stride, d->d_k, d->d_v, o, d->o_stride,
-           d->q_scale, true, false, nullptr, nullptr, nullptr, false, final_state};
-  return run_la(d, a, reinterpret_cast<cudaStream_t>(stream));
+           d->q_scale, true, false, nullptr, nullptr, nullptr, false, final_state, sb};
+  return run_la(d, a, s);
 }
 
 extern "C" size_t af_linear_bwd_workspace(const af_linear_desc* d) {
@@ -137,7 +180,8 @@ extern "C" size_t af_linear_bwd_workspace(const af_linear_desc* d) {
   // dot partials, then d log a and dk_dot per step; the bf16 Km copy starts 256-byte aligned
   size_t bytes = (rows * (2 * slots + 2) * sizeof(float) + 255) / 256 * 256;
   if (d->key_gate != nullptr) bytes += rows * static_cast<size_t>(d->d_k) * 2;  // bf16 Km
-  return bytes;
+  bytes = (bytes + 255) / 256 * 256;
+  return bytes + af::scan_bytes(d);
 }
 
 extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void* k, const void* v,
@@ -155,7 +199,7 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
   float* dk_dot = dq_dot + n * slots;
   float* step_dloga = dk_dot + n * slots;
   float* step_dkdot = step_dloga + n;
-  AF_CUDA_CHECK(cudaMemsetAsync(workspace, 0, static_cast<size_t>(2 * n * slots) * sizeof(float), s));
+  // (every dot partial slot of every live step is stored exactly once: no clearing needed)
   // Gated keys, materialised once (see gate_keys_kernel)
   const void* km = k;
   const int64_t* km_st = d->k_stride;
@@ -174,21 +218,30 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
     km = kmb;
     km_st = km_contig;
   }
-  // dq = q_scale * LA_fwd(q=dO, k=V, v=Km)                 dq_dot = q . dq   (= Qm . dQm)
-  LaArgs a1{dout, v, km, d->o_stride, d->v_stride, km_st, d->d_v, d->d_k, dq, d->q_stride,
-            d->q_scale, false, false, q, d->q_stride, dq_dot, false};
-  if ((st = run_la(d, a1, s)) != AF_OK) return st;
-  // dKm = q_scale * LA_rev(q=V, k=dO, v=Q); dk = gate*dKm   dk_dot = Km . dKm
-  LaArgs a2{v, dout, q, d->v_stride, d->o_stride, d->q_stride, d->d_v, d->d_k, dk, d->k_stride,
-            d->q_scale, false, true, km, km_st, dk_dot, true};
-  if ((st = run_la(d, a2, s)) != AF_OK) return st;
-  // dV = q_scale * LA_rev(q=Km, k=Q, v=dO)
-  LaArgs a3{km, q, dout, km_st, d->q_stride, d->o_stride, d->d_k, d->d_v, dv, d->v_stride,
-            d->q_scale, false, false, nullptr, nullptr, nullptr, true};
-  if ((st = run_la(d, a3, s)) != AF_OK) return st;
+  size_t scan_off = (static_cast<size_t>(n) * (2 * slots + 2) * sizeof(float) + 255) / 256 * 256;
+  if (d->key_gate != nullptr)
+    scan_off = (scan_off + static_cast<size_t>(n) * d->d_k * 2 + 255) / 256 * 256;
+  const ScanBufs sb = scan_layout(d, static_cast<char*>(workspace) + scan_off);
+  if ((st = run_scan(d, sb, s)) != AF_OK) return st;
   const bool want_fac = d_decay_factor != nullptr &&
                         ((d->n_decay_factors > 0 && d_decay_factor[0] != nullptr) ||
                          (d->n_decay_factors > 1 && d_decay_factor[1] != nullptr));
+  // the per-step dot products feed only the decay / gate gradients: skipped (no re-read of q
+  // and Km) when none is requested
+  const bool want_dots = want_fac || d_key_gate != nullptr;
+  // dq = q_scale * LA_fwd(q=dO, k=V, v=Km)                 dq_dot = q . dq   (= Qm . dQm)
+  LaArgs a1{dout, v, km, d->o_stride, d->v_stride, km_st, d->d_v, d->d_k, dq, d->q_stride,
+            d->q_scale, false, false, want_dots ? q : nullptr, d->q_stride, dq_dot, false, nullptr,
+            sb};
+  if ((st = run_la(d, a1, s)) != AF_OK) return st;
+  // dKm = q_scale * LA_rev(q=V, k=dO, v=Q); dk = gate*dKm   dk_dot = Km . dKm
+  LaArgs a2{v, dout, q, d->v_stride, d->o_stride, d->q_stride, d->d_v, d->d_k, dk, d->k_stride,
+            d->q_scale, false, true, want_dots ? km : nullptr, km_st, dk_dot, true, nullptr, sb};
+  if ((st = run_la(d, a2, s)) != AF_OK) return st;
+  // dV = q_scale * LA_rev(q=Km, k=Q, v=dO)
+  LaArgs a3{km, q, dout, km_st, d->q_stride, d->o_stride, d->d_k, d->d_v, dv, d->v_stride,
+            d->q_scale, false, false, nullptr, nullptr, nullptr, true, nullptr, sb};
+  if ((st = run_la(d, a3, s)) != AF_OK) return st;
   if (want_fac || d_key_gate != nullptr) {
     LinearParams p = base_params(d);
     p.u_scale = step_tensor(d->key_gate, d->key_gate_stride);

@@ -79,6 +79,10 @@ struct LinearParams {
   float* final_state;   // optional fp32 [B, H, dqk, dv]: the state after the last token (forward)
   float* dot;           // [dv/32 slots][B, H, S] fp32: one partial per 32-column slot, summed
                         // in slot order by linear_step_grads_kernel (deterministic)
+  // the decay scan of linear_decay_scan_kernel, [B*H][nchunks][128] (padded tail: a = 1, u = 1)
+  const float* lcum;    // in-chunk inclusive cumsum of log2 a
+  const float* ucum;    // key/value-side scale u (k_mod gate); null when absent
+  const int* cflag;     // [B*H][nchunks]: 1 when every |L| of the chunk is <= 100
 };
 
 template <int DK>
@@ -103,7 +107,7 @@ struct LinSmem {
   // ring: full[S], empty[S]; s_full qh_full oi_full[2] h_full scan_ready[2] (raw factors of the
   // chunk landed; 1 arrival) | p_ready vw_ready h_scaled hb_ready scan_free[2] (raw factors read;
   // 8 row warps) | oi_empty[2] cp_ready[2] (4)
-  static constexpr int kBarOff = kFlagOff + 16;
+  static constexpr int kBarOff = kFlagOff + 32;
   static constexpr int kNumBars = 2 * kStages + 17 + 2 * kVStages;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
@@ -117,6 +121,56 @@ constexpr float kLog2e_ = 1.4426950408889634f;
 AF_DEVICE float log2_floor(float v) {
   const float l = __log2f(v);
   return l < -200.0f ? -200.0f : l;
+}
+
+// The per-step decay scan, once per call for every chunk in parallel (one warp per (b, h, chunk)):
+// L = in-chunk inclusive cumsum of log2 a_t (a_t = e^{log_const} prod_f fac_f[t]), the key/value
+// scale u_t, and a per-chunk flag for the factorised-decay path (every |L| <= 100).  Traced inside
+// the chunk kernel this serial LDS / MUFU / SHFL chain held a whole chunk period (~1.8k clk of a
+// single latency-bound warp); here it runs ahead of every template pass that shares the decay
+// (the forward, and all three passes of the backward).
+__global__ void linear_decay_scan_kernel(const LinearParams p, float* __restrict__ lcum,
+                                         float* __restrict__ ucum, int* __restrict__ cflag) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const int nchunks = (p.seq + kLinChunk - 1) / kLinChunk;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+  if (gw >= static_cast<int64_t>(p.batch) * p.heads * nchunks) return;
+  const int c = static_cast<int>(gw % nchunks);
+  const int bh = static_cast<int>(gw / nchunks);
+  const int b = bh / p.heads, h = bh % p.heads;
+  float x[4], us[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int t = c * kLinChunk + lane * 4 + j;
+    x[j] = 0.0f;
+    us[j] = 1.0f;
+    if (t < p.seq) {
+      x[j] = p.log_const * kLog2e_;
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+        if (f < p.nfac) x[j] += log2_floor(p.fac[f].at(b, h, t));
+      if (p.u_scale.ptr != nullptr) us[j] = p.u_scale.at(b, h, t);
+    }
+  }
+  x[1] += x[0];
+  x[2] += x[1];
+  x[3] += x[2];
+  float tot = x[3];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, tot, off);
+    if (lane >= off) tot += y;
+  }
+  const float excl = tot - x[3];
+  float amax = fmaxf(fabsf(excl + x[0]), fabsf(excl + x[3]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  reinterpret_cast<float4*>(lcum + gw * kLinChunk)[lane] =
+      make_float4(excl + x[0], excl + x[1], excl + x[2], excl + x[3]);
+  if (ucum != nullptr)
+    reinterpret_cast<float4*>(ucum + gw * kLinChunk)[lane] = make_float4(us[0], us[1], us[2], us[3]);
+  if (lane == 0) cflag[gw] = amax <= 100.0f ? 1 : 0;
 }
 
 // packed (bf16x2) TMEM column of the k-th 16-key slice of P (key halves [0,64) -> [0,32),
@@ -162,7 +216,7 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
   float* sRaw = reinterpret_cast<float*>(smem + L::kRawOff);
   float* sCp = reinterpret_cast<float*>(smem + L::kCpOff);
   float* sEcb = reinterpret_cast<float*>(smem + L::kEcOff);  // [2][128]
-  volatile int* sFac = reinterpret_cast<volatile int*>(smem + L::kFlagOff);  // [2]
+  volatile int* sFac = reinterpret_cast<volatile int*>(smem + L::kFlagOff);  // [2][4 groups]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* full = bars;                 // Q, K, V of one chunk landed (one tx barrier)
   uint64_t* empty = bars + kStages;      // the chunk's Q, K, V may be overwritten
@@ -227,28 +281,28 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
     // dependent LDS / MUFU / SHFL latency on the ~6k-clk chunk period).
     const int lane = static_cast<int>(lane_id());
     const int nraw = p.nfac + (p.u_scale.ptr != nullptr ? 1 : 0);
-    // raw factors run kRawRing - 1 chunks ahead of the scan (cp.async groups; only this warp
-    // reads them): traced, a load issued one chunk ahead still took ~3.5k clk to land under the
-    // TMA traffic and held the rows back by ~1.3k clk per chunk
+    // the precomputed scan (linear_decay_scan_kernel) of chunk n lands in ring slot n % kRawRing
+    // by cp.async, kRawRing - 1 chunks ahead; this warp turns it into the shared [n % 2] arrays
+    // the row warps read (L, u and the column factors of the factorised decay)
+    const int bhx = b * p.heads + h;
     auto load_raw = [&](int m) {
       if (m < nchunks) {
         const int cm = kReverse ? nchunks - 1 - m : m;
+        const int64_t g = static_cast<int64_t>(bhx) * nchunks + cm;
         float* raw = sRaw + (m % kRawRing) * 3 * kLinChunk;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int rr = lane * 4 + j;
-          const int t = cm * kLinChunk + rr;
-          if (t < p.seq) {
-            for (int f = 0; f < nraw; ++f) {
-              const StepTensor& ts = f < p.nfac ? p.fac[f] : p.u_scale;
-              const float* src = ts.ptr + b * ts.sb + h * ts.sh + t * ts.ss;
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                               smem_u32(raw + f * kLinChunk + rr)),
-                           "l"(src)
-                           : "memory");
-            }
-          }
-        }
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(raw + lane * 4)),
+                     "l"(p.lcum + g * kLinChunk + lane * 4)
+                     : "memory");
+        if (p.ucum != nullptr)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                           smem_u32(raw + kLinChunk + lane * 4)),
+                       "l"(p.ucum + g * kLinChunk + lane * 4)
+                       : "memory");
+        if (lane == 0)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                           smem_u32(raw + 2 * kLinChunk)),
+                       "l"(p.cflag + g)
+                       : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count)
     };
@@ -257,43 +311,34 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
       const int c = kReverse ? nchunks - 1 - n : n;
       const int t0 = c * kLinChunk;
       const int pb = n & 1;
-      load_raw(n + kRawRing - 1);  // its slot held chunk n-1, already scanned by this warp
+      load_raw(n + kRawRing - 1);  // its slot held chunk n-1, already consumed by this warp
       asm volatile("cp.async.wait_group %0;" ::"n"(kRawRing - 1) : "memory");
       __syncwarp();
       if (lane == 0) AF_LT(17, n);
       const float* raw = sRaw + (n % kRawRing) * 3 * kLinChunk;
       {
-        float x[4], us[4];
+        const float4 l4 = reinterpret_cast<const float4*>(raw)[lane];
+        const float4 u4 = p.ucum != nullptr ? reinterpret_cast<const float4*>(raw + kLinChunk)[lane]
+                                            : make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+        const float lj4[4] = {l4.x, l4.y, l4.z, l4.w};
+        const float us[4] = {u4.x, u4.y, u4.z, u4.w};
+        // Factorised decay per 32-key group g (base index b_g: the group's first key, reverse:
+        // its last): D[i,u] = 2^{L_i - L_bg} * 2^{L_bg - L_u} (reverse: 2^{L_bg - L_i} *
+        // 2^{L_u - L_bg}).  The column factor 2^{+-(L_bg - L_u)} u_u is built here; the row
+        // warps multiply by their one row factor per group — an ex2 per element only in groups
+        // whose decay spans more than 2^100 (the column factor would leave fp32's range).  Row
+        // factors of kept pairs are <= 1, so nothing overflows; underflow only drops terms
+        // below 2^-26 of the diagonal's.
+        const int gl = lane & ~7;  // first lane of this lane's 32-key group
+        const float base = kReverse ? __shfl_sync(0xffffffffu, lj4[3], gl + 7)
+                                    : __shfl_sync(0xffffffffu, lj4[0], gl);
+        float dmax = 0.0f;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int rr = lane * 4 + j;
-          x[j] = 0.0f;
-          us[j] = 1.0f;
-          if (t0 + rr < p.seq) {
-            x[j] = p.log_const * kLog2e_;
+        for (int j = 0; j < 4; ++j) dmax = fmaxf(dmax, fabsf(lj4[j] - base));
 #pragma unroll
-            for (int f = 0; f < 2; ++f)
-              if (f < p.nfac) x[j] += log2_floor(raw[f * kLinChunk + rr]);
-            if (p.u_scale.ptr != nullptr) us[j] = raw[p.nfac * kLinChunk + rr];
-          }
-        }
-        x[1] += x[0];
-        x[2] += x[1];
-        x[3] += x[2];
-        float tot = x[3];
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const float y = __shfl_up_sync(0xffffffffu, tot, off);
-          if (lane >= off) tot += y;
-        }
-        const float excl = tot - x[3];
-        // Factorised decay D[i,u] = e^{L_i} e^{-L_u} (reverse: e^{-L_i} e^{L_u}) when every |L|
-        // of the chunk stays below 2^100: one multiply per element instead of an ex2.
-        float amax = fmaxf(fabsf(excl + x[0]), fabsf(excl + x[3]));
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1)
-          amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
-        const bool fac = kFac && amax <= 100.0f;
+        for (int off = 1; off < 8; off <<= 1)
+          dmax = fmaxf(dmax, __shfl_xor_sync(0xffffffffu, dmax, off));
+        const bool gfac = dmax <= 100.0f;
         if (n >= 2) LIN_IDLE_WAIT(&scan_free[pb], ((n >> 1) - 1) & 1);  // chunk n-2 fully read
         if (lane == 0) AF_LT(16, n);
         float* sL = sLb + pb * kLinChunk;
@@ -301,12 +346,12 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
         float* sEc = sEcb + pb * kLinChunk;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float lj = excl + x[j];
+          const float lj = lj4[j];
           sL[lane * 4 + j] = lj;
           sU[lane * 4 + j] = us[j];
-          if (fac) sEc[lane * 4 + j] = exp2f(kReverse ? lj : -lj) * us[j];
+          if (gfac) sEc[lane * 4 + j] = exp2f(kReverse ? lj - base : base - lj) * us[j];
         }
-        if (lane == 0) sFac[pb] = fac ? 1 : 0;
+        if (lane == gl) sFac[pb * 4 + (lane >> 3)] = gfac ? 1 : 0;
         __syncwarp();
       }
       if (lane == 0) mbar_arrive(&scan_ready[pb]);
@@ -496,11 +541,9 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
       const float* sEc = sEcb + ph * kLinChunk;
       LIN_IDLE_WAIT(&scan_ready[ph], (n >> 1) & 1);
       if (threadIdx.x == 0) AF_LT(14, n);
-      const bool fac = sFac[ph] != 0;
       if (threadIdx.x == 0) AF_LT(18, n);
       const float l_r = sL[r];
       const float l_last = sL[kLinChunk - 1];
-      const float er = fac ? exp2f(kReverse ? -l_r : l_r) : 0.0f;
       const float g = exp2f(l_last);
       const float cp = kReverse ? exp2f(l_last - l_r) : exp2f(l_r);
       const float wgt = sU[r] * (kReverse ? exp2f(l_r) : exp2f(l_last - l_r));
@@ -569,8 +612,9 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
           }
           uint32_t sr[32];
           tmem_ld32(tmem + lane_base + kColS + u0, sr);
-          tmem_ld_wait();
-          if (fac) {
+          if (sFac[ph * 4 + (u0 >> 5)] != 0) {
+            const float er = exp2f(kReverse ? sL[u0 + 31] - l_r : l_r - sL[u0]);
+            tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < 32; e += 4) {
               const int u = u0 + e;
@@ -587,6 +631,7 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
             }
             continue;
           }
+          tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
             const int u = u0 + e;

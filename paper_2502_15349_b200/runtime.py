@@ -20,6 +20,7 @@ AF_OK, AF_ERR_INPUT, AF_ERR_SHAPE, AF_ERR_UNSUPPORTED, AF_ERR_NAN, AF_ERR_CUDA =
 AF_FAMILY_SOFTMAX, AF_FAMILY_ELEMENTWISE, AF_FAMILY_ABSSUM = 0, 1, 2
 AF_ACT_IDENTITY, AF_ACT_SIGMOID, AF_ACT_RELU, AF_ACT_RELU2 = 0, 1, 2, 3
 AF_DTYPE_BF16, AF_DTYPE_F32 = 0, 1
+AF_ROWNORM_NONE, AF_ROWNORM_SOFTMAX, AF_ROWNORM_ABSSUM = 0, 1, 2
 AF_FM_NONE, AF_FM_SILU, AF_FM_SIGMOID, AF_FM_RELU, AF_FM_TANH, AF_FM_EXP = range(6)
 
 I64x4 = C.c_int64 * 4
@@ -65,7 +66,8 @@ SIGNATURES: dict[str, tuple] = {
     "af_parallel_bwd_workspace": (C.c_size_t, [C.POINTER(ParallelDesc)]),
     "af_parallel_bwd": (C.c_int, [C.POINTER(ParallelDesc), P, P, P, P, P, P, P, P, P, P,
                                   C.c_size_t, P]),
-    "af_linear_fwd": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P]),
+    "af_linear_fwd_workspace": (C.c_size_t, [C.POINTER(LinearDesc)]),
+    "af_linear_fwd": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P, C.c_size_t, P]),
     "af_linear_step": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P]),
     "af_linear_bwd_workspace": (C.c_size_t, [C.POINTER(LinearDesc)]),
     "af_linear_bwd": (C.c_int, [C.POINTER(LinearDesc), P, P, P, P, P, P, P, P, P, P, C.c_size_t,
@@ -74,6 +76,9 @@ SIGNATURES: dict[str, tuple] = {
     "af_mla_decode": (C.c_int, [C.POINTER(MlaDesc), P, P, P, P, P, C.c_size_t, P]),
     "af_feature_map": (C.c_int, [C.c_int, C.c_int, P, P, P, C.c_int64, P]),
     "af_hook_eval": (C.c_int, [P, P, P, C.c_int32, C.c_int32, P, P, P, P]),
+    "af_rownorm_fwd": (C.c_int, [C.c_int32, P, P, P, C.c_int64, C.c_int64, P]),
+    "af_rownorm_bwd": (C.c_int, [C.c_int32, P, P, P, P, P, P, C.c_int64, C.c_int64, P]),
+    "af_rowdot": (C.c_int, [P, P, P, P, P]),
     "af_status_string": (C.c_char_p, [C.c_int]),
     "af_last_error": (C.c_char_p, []),
     "af_device_sm_count": (C.c_int, []),
