@@ -30,6 +30,7 @@ from dataclasses import dataclass
 
 import torch
 
+from . import generic
 from . import hookvm
 from . import runtime as rt
 from .errors import InputError, NanError, ShapeError, UnsupportedError
@@ -189,6 +190,20 @@ def _out_mod_vjp(plan, o_inner: torch.Tensor, dout: torch.Tensor, arrays: dict,
     return d
 
 
+def _check_extra_grads(spec, arrays) -> None:
+    """Differentiable extras get gradients on the materialised tier and through whole-tensor hook
+    programs; one read by a fused kernel's score epilogue (a relative-position slope, the
+    declared decay mask) raises — its gradient is not lowered there."""
+    route, plan = route_parallel(spec, arrays)
+    if route == "generic":
+        return
+    hook_only = _hook_only_extras(plan)
+    for e in spec.extra_inputs:
+        if e.differentiable and e.name not in hook_only:
+            raise UnsupportedError("gradients w.r.t. extras read by the fused score hooks are "
+                                   "not lowered", extra=e.name)
+
+
 def _hook_only_extras(plan) -> set:
     """Differentiable extras read only by whole-tensor hooks (their gradients are lowered)."""
     return {e.name for e in plan.spec.extra_inputs
@@ -320,6 +335,41 @@ def mla_decode(q: torch.Tensor, kv: torch.Tensor, scale: float):
     return o, lse
 
 
+def _fused_dims(spec, plan, precision: str) -> bool:
+    """Head dims the fused kernels are instantiated for (directly, zero-padded, as 128-wide value
+    slices, or as MLA)."""
+    d = spec.dims
+    if spec.kv_shared:
+        return (d.d_qk, d.d_v) == (MLA_DQK, MLA_DV) and d.kv_heads == 1 and precision == "bf16"
+    if precision != "bf16":
+        return d.d_qk <= 128 and d.d_v <= 128
+    dims = (d.d_qk, d.d_v)
+    return (dims in _KERNEL_DIMS or max(dims) <= 128 or dims == (128, 256))
+
+
+def route_parallel(spec, arrays: dict | None = None, precision: str = "bf16"):
+    """("fused", ParallelPlan) when the fused kernels lower the variant at these dims (and, for
+    the abssum family, the decay mask is its declared fill); otherwise ("generic", GenericPlan)
+    — the materialised tier (generic.py) — which raises UnsupportedError for what neither
+    lowers."""
+    spec = _spec(spec)
+    try:
+        plan = plan_parallel(spec)
+    except UnsupportedError as fused_err:
+        try:
+            return "generic", generic.plan_generic(spec)
+        except UnsupportedError:
+            raise fused_err from None
+    if not _fused_dims(spec, plan, precision):
+        return "generic", generic.plan_generic(spec)
+    if plan.family == FAMILY_ABSSUM and arrays is not None and plan.decay_extra in arrays:
+        try:
+            _check_decay_mask(plan, arrays[plan.decay_extra], arrays[plan.decay_extra].device)
+        except UnsupportedError:
+            return "generic", generic.plan_generic(spec)
+    return "fused", plan
+
+
 def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: bool = False):
     """Forward of the parallel template → ``(O [B,H,Sq,Dv], LSE [B,H,Sq] fp32 or None)``.
 
@@ -329,7 +379,12 @@ def parallel_forward(spec, arrays: dict, *, precision: str = "bf16", check_nan: 
     seq_q == 1 and no mask applies.  An ``output_mod`` runs on the full output afterwards
     (af_hook_eval); the LSE is the template's own row statistic."""
     spec = _spec(spec)
-    plan = plan_parallel(spec)
+    route, plan = route_parallel(spec, arrays, precision)
+    if route == "generic":
+        o, lse = generic.forward(plan, arrays, _BF16 if precision == "bf16" else torch.float32)
+        if check_nan:
+            _check_nan(o, "materialised")
+        return o, lse
     o, lse = _parallel_forward_core(spec, plan, arrays, precision)
     if "o" in plan.hooks:
         o = _out_mod(plan, o, arrays)
@@ -393,7 +448,9 @@ def parallel_backward(spec, arrays: dict, o: torch.Tensor, lse, dout: torch.Tens
     output_mod).  With an ``output_mod`` the template's own output is recomputed (``o`` is the
     modified one) and ``dout`` is pulled back through the mod first."""
     spec = _spec(spec)
-    plan = plan_parallel(spec)
+    route, plan = route_parallel(spec, arrays)
+    if route == "generic":
+        return generic.backward(plan, arrays, dout)
     grads_x: dict = {}
     if "o" in plan.hooks:
         o, lse = _parallel_forward_core(spec, plan, arrays, "bf16")
@@ -669,11 +726,7 @@ def autodiff_grads(spec, arrays: dict, wrt=None, dout: torch.Tensor | None = Non
     if spec.pattern is Pattern.PARALLEL:
         o, lse = parallel_forward(spec, arrays)
         g = torch.ones_like(o) if dout is None else dout
-        plan = plan_parallel(spec)
-        for e in spec.extra_inputs:
-            if e.differentiable and e.name not in _hook_only_extras(plan):
-                raise UnsupportedError("gradients w.r.t. extras read by the fused score hooks "
-                                       "are not lowered", extra=e.name)
+        _check_extra_grads(spec, arrays)
         grads = parallel_backward(spec, arrays, o, lse, g)
     else:
         g = torch.ones(d.batch, d.heads, d.seq_q, d.d_v, device=_need(arrays, "q").device,
@@ -705,7 +758,7 @@ class BoundKernel:
 
 def bind(spec) -> BoundKernel:
     spec = _spec(spec)
-    plan = plan_parallel(spec) if spec.pattern is Pattern.PARALLEL else plan_linear(spec)
+    plan = route_parallel(spec)[1] if spec.pattern is Pattern.PARALLEL else plan_linear(spec)
     return BoundKernel(spec, plan)
 
 
@@ -720,11 +773,7 @@ class _ParallelFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, spec, names, q, k, v, *extra_t):
         extras = dict(zip(names, extra_t))
-        hook_only = _hook_only_extras(plan_parallel(spec))
-        for e in spec.extra_inputs:
-            if e.differentiable and e.name not in hook_only:
-                raise UnsupportedError("gradients w.r.t. extras read by the fused score hooks "
-                                       "are not lowered", extra=e.name)
+        _check_extra_grads(spec, {"q": q, "k": k, "v": v, **extras})
         arrays = {"q": q, "k": k, "v": v, **extras}
         with torch.cuda.device(q.device):
             o, lse = parallel_forward(spec, arrays)

@@ -59,9 +59,11 @@ class CompiledHook:
 
 def compile_hook(fn, inputs, consts: dict, *, index_names=("qidx",)) -> CompiledHook:
     """Compile a ``ModificationFn`` (or bare AST) over tensor names ``inputs`` (in operand order;
-    only the ones the expression reads become operands).  ``index_names`` map to the element's
-    sequence coordinate.  Raises ``UnsupportedError`` for reductions or programs beyond the
+    only the ones the expression reads become operands).  ``index_names`` map to an element
+    coordinate: a sequence of names (all the row axis, 2) or a {name: axis} dict (score grids:
+    qidx -> 2, kidx -> 3).  Raises ``UnsupportedError`` for reductions or programs beyond the
     kernel's limits."""
+    axes = dict(index_names) if isinstance(index_names, dict) else {n: 2 for n in index_names}
     expr = H.fold(getattr(fn, "expr", fn), consts)
     source = getattr(fn, "source", H.to_source(expr))
     ops: list[int] = []
@@ -80,8 +82,8 @@ def compile_hook(fn, inputs, consts: dict, *, index_names=("qidx",)) -> Compiled
             ops.extend((OP_CONST, cvals.index(e.value)))
             push()
         elif isinstance(e, H.Name):
-            if e.name in index_names:
-                ops.extend((OP_INDEX, 2))
+            if e.name in axes:
+                ops.extend((OP_INDEX, axes[e.name]))
             elif e.name in inputs:
                 if e.name not in used:
                     used.append(e.name)

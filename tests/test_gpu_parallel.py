@@ -228,15 +228,17 @@ def test_autograd_module_matches_backward():
 
 
 def test_unlowered_variant_raises_not_falls_back():
+    """What neither the fused kernels nor the materialised tier lower raises (no CPU path): an
+    online row normalisation that is neither softmax nor abssum-clamp."""
+    from dataclasses import replace
     spec = S.with_causal_mask(S.builtin("retention-parallel", heads=2, seq=128, d_qk=64, d_v=64))
     arrays = to_dev(oracle.generate(spec, 0))
-    af.run_tiled_parallel(spec, arrays)  # the declared causal decay mask lowers ...
-    arrays["mask"] = torch.rand_like(arrays["mask"])  # ... an arbitrary materialised one does not
+    af.run_tiled_parallel(spec, arrays)  # the declared causal decay mask lowers (fused)
+    base = S.builtin("softmax", heads=2, seq=128, d_qk=64, d_v=64)
+    odd = replace(base, rownorm=replace(base.rownorm, epilogue=S.ModificationFn(
+        "acc / (l + 1)", "acc", allow_reduce=True)))
     with pytest.raises(af.UnsupportedError):
-        af.run_tiled_parallel(spec, arrays)
-    spec = S.builtin("softmax", heads=2, seq=128, d_qk=320, d_v=320)  # no kernel for 320
-    with pytest.raises(af.UnsupportedError):
-        af.parallel_forward(spec, to_dev(oracle.generate(spec, 0)))
+        af.parallel_forward(odd, to_dev(oracle.generate(base, 0)))
 
 
 def test_run_tiled_parallel_accepts_reference_signature():
