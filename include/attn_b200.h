@@ -56,6 +56,11 @@ typedef struct af_parallel_desc {
                                 abssum family: cap_a = 1 divides rows by clamp(sum|z|, 1, inf)
                                 (retention-parallel), 0 leaves them unnormalised; lse then
                                 receives the row abs-sum                                     */
+  /* tile configuration (0 = the library's default; schedule.py's measured mode picks others,
+   * replacing the reference's analytic tile scheduler, scheduling.py:256-266) */
+  int32_t kv_stages;         /* K1 K/V ring depth for head dims <= 128: 1 or 2 (default 2)   */
+  int32_t head_groups;       /* materialised backward: query-head chunks of the key-side GEMMs
+                                (default: enough CTAs for ~4 waves)                          */
 } af_parallel_desc;
 
 /* O = template_forward(q, k, v); lse[b,h,i] = log-sum-exp of row i (softmax family, may be NULL).
@@ -126,6 +131,7 @@ int af_linear_bwd(const af_linear_desc* desc, const void* q, const void* k, cons
 typedef struct af_mla_desc {
   int32_t batch, heads, seq_k, d_qk, d_v;
   float scale;
+  int32_t splits;            /* KV splits per (batch, value half); 0 = minimise waves x blocks */
 } af_mla_desc;
 
 size_t af_mla_decode_workspace(const af_mla_desc* desc);

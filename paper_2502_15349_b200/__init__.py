@@ -20,7 +20,8 @@ from .plan import plan_parallel, plan_linear, ParallelPlan, LinearPlan
 from .api import (parallel_forward, parallel_backward, run_tiled_parallel, run_naive_parallel,
                   linear_forward, linear_backward, linear_step, run_chunk_recurrent, run_step_recurrent,
                   autodiff_grads, bind, AttentionEngine, mla_decode)
-from . import api
+from . import api, generic, hookvm, schedule
 from .emit import code_generation
+from .schedule import make_scheduling_task, measure_factory, tile_config_scheduling
 
 __all__ = [n for n in dir() if not n.startswith("_")]

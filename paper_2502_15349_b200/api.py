@@ -69,6 +69,28 @@ def _empty(key: str, shape, dtype, device) -> torch.Tensor:
     return t
 
 
+_TUNE: contextvars.ContextVar = contextvars.ContextVar("af_tuning", default=None)
+
+
+@contextlib.contextmanager
+def tuned(config: dict):
+    """Launch with an explicit tile configuration (schedule.Candidate fields) inside the block —
+    what the measured scheduler's ``measure`` uses to time one candidate."""
+    token = _TUNE.set(dict(config))
+    try:
+        yield
+    finally:
+        _TUNE.reset(token)
+
+
+def _tuning(spec) -> dict:
+    t = _TUNE.get()
+    if t is not None:
+        return t
+    from . import schedule
+    return schedule.tuning(spec)
+
+
 def _spec(spec) -> AttentionSpec:
     return spec if isinstance(spec, AttentionSpec) else from_reference(spec)
 
@@ -259,6 +281,8 @@ def _desc(plan: ParallelPlan, q, k, v, o, slope, dtype_code: int) -> rt.Parallel
     c.cap_a, c.cap_b = float(plan.cap_a), float(plan.cap_b)
     if plan.family == FAMILY_ABSSUM:  # cap_a = 1: rows divided by clamp(sum |s|, 1, inf)
         c.cap_a, c.cap_b = (1.0 if plan.normalize else 0.0), 0.0
+    t = _tuning(plan.spec)
+    c.kv_stages, c.head_groups = int(t.get("kv_stages", 0)), int(t.get("head_groups", 0))
     return c
 
 
@@ -311,7 +335,7 @@ def _pad_last(t: torch.Tensor, n: int) -> torch.Tensor:
     return t if t.shape[-1] == n else torch.nn.functional.pad(t, (0, n - t.shape[-1]))
 
 
-def mla_decode(q: torch.Tensor, kv: torch.Tensor, scale: float):
+def mla_decode(q: torch.Tensor, kv: torch.Tensor, scale: float, splits: int = 0):
     """K3 decode: softmax attention of every head of one query token over a shared latent cache.
 
     q [B, H, 576] bf16, kv [B, Sk, 576] bf16 (V = kv[..., :512]) → (O [B, H, 512] bf16,
@@ -325,6 +349,7 @@ def mla_decode(q: torch.Tensor, kv: torch.Tensor, scale: float):
     B, H, _ = q.shape
     c = rt.MlaDesc()
     c.batch, c.heads, c.seq_k, c.d_qk, c.d_v, c.scale = B, H, kv.shape[1], MLA_DQK, MLA_DV, scale
+    c.splits = int(splits)
     o = torch.empty(B, H, MLA_DV, device=q.device, dtype=_BF16)
     lse = torch.empty(B, H, device=q.device, dtype=torch.float32)
     L = rt.lib()
@@ -401,7 +426,8 @@ def _parallel_forward_core(spec, plan, arrays: dict, precision: str):
         k = _need(arrays, "k")
         _check_shape(q, (d0.batch, d0.heads, 1, MLA_DQK), "q")
         _check_shape(k, (d0.batch, 1, d0.seq_k, MLA_DQK), "k")
-        o, lse = mla_decode(q[:, :, 0], k[:, 0], float(plan.scale))
+        o, lse = mla_decode(q[:, :, 0], k[:, 0], float(plan.scale),
+                            int(_tuning(spec).get("splits", 0)))
         return o.unsqueeze(2), lse.unsqueeze(2)
     dtype = _BF16 if precision == "bf16" else torch.float32
     q, k, v, slope = _parallel_inputs(plan, arrays, dtype)

@@ -27,7 +27,8 @@ MatLayout mat_layout(const af_parallel_desc* d, bool shared) {
   const int64_t k_tiles = l.k_pad / 128;
   const int64_t units = k_tiles * d->batch * d->heads_kv;
   const int64_t group = d->heads_q / d->heads_kv;
-  const int64_t want = (4 * sm_count() + units - 1) / units;
+  const int64_t want =
+      d->head_groups > 0 ? d->head_groups : (4 * sm_count() + units - 1) / units;
   l.groups = std::max<int64_t>(1, std::min<int64_t>(want, group));
   l.part_width = shared ? d->d_qk : std::max(d->d_qk, d->d_v);
   l.stats = static_cast<size_t>(l.rows) * 2 * sizeof(float);

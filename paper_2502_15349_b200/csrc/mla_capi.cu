@@ -46,6 +46,7 @@ namespace {
 int decode_splits(const af_mla_desc* d) {
   const int sms = sm_count();
   const int blocks = (d->seq_k + MlaTile<true>::kN - 1) / MlaTile<true>::kN;
+  if (d->splits > 0) return std::min(d->splits, blocks);  // the measured scheduler's choice
   const int max_splits = std::max(1, std::min(blocks, 8 * sms / (2 * d->batch) + 1));
   int best = 1;
   long best_cost = -1;

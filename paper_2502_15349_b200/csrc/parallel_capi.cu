@@ -7,10 +7,9 @@ namespace af {
 namespace {
 
 
-template <int D, int DV, int kFamily, int kAct>
-int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
-               const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t stream) {
-  constexpr int kStages = D > 128 ? 1 : 2;  // D = 192: two 48 KB Q tiles leave room for one stage
+template <int D, int DV, int kFamily, int kAct, int kStages>
+int launch_fwd_stages(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
+                      const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t stream) {
   using L = FwdSmem<D, DV, kStages>;
   auto kern = parallel_fwd_kernel<D, DV, kFamily, kAct, kStages>;
   AF_SMEM_ATTR(kern, L::kTotal);
@@ -19,6 +18,21 @@ int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorM
   kern<<<grid, fwd_threads(kFamily), L::kTotal, stream>>>(tq, tk, tv, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
+}
+
+template <int D, int DV, int kFamily, int kAct>
+int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
+               const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t stream) {
+  // D = 192: two 48 KB Q tiles leave room for one stage; D <= 128 runs two unless the measured
+  // scheduler picked one (desc->kv_stages)
+  constexpr bool kTunable = (kFamily == kFamilySoftmax && kAct == kActIdentity) ||
+                            (kFamily == kFamilyElementwise && kAct == kActSigmoid);
+  if constexpr (D <= 128) {
+    if (kTunable && d->kv_stages == 1) return launch_fwd_stages<D, DV, kFamily, kAct, 1>(d, tq, tk, tv, p, stream);
+    return launch_fwd_stages<D, DV, kFamily, kAct, 2>(d, tq, tk, tv, p, stream);
+  } else {
+    return launch_fwd_stages<D, DV, kFamily, kAct, 1>(d, tq, tk, tv, p, stream);
+  }
 }
 
 template <int D, int DV>

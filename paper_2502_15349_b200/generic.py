@@ -81,8 +81,9 @@ def rownorm_kind(spec: AttentionSpec) -> int:
             return rt.AF_ROWNORM_SOFTMAX
         if is_online_abssum(rn, consts):
             return rt.AF_ROWNORM_ABSSUM
-        rn = rn.direct
-    if isinstance(rn, DirectRowNorm):
+        # run_tiled_parallel follows the online protocol (engine.py:481-489), not its `direct`
+        # twin: an unrecognised online form is not lowered even when a direct body exists
+    elif isinstance(rn, DirectRowNorm):
         if _direct_is_softmax(rn, consts):
             return rt.AF_ROWNORM_SOFTMAX
         if _direct_is_abssum(rn, consts):

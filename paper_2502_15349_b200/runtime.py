@@ -35,6 +35,7 @@ class ParallelDesc(C.Structure):
         ("family", C.c_int32), ("act", C.c_int32), ("scale", C.c_float),
         ("causal", C.c_int32), ("diag_offset", C.c_int32), ("window", C.c_int32),
         ("slope", C.c_void_p), ("bias", C.c_float), ("cap_a", C.c_float), ("cap_b", C.c_float),
+        ("kv_stages", C.c_int32), ("head_groups", C.c_int32),
     ]
 
 
@@ -55,7 +56,7 @@ class LinearDesc(C.Structure):
 class MlaDesc(C.Structure):
     _fields_ = [
         ("batch", C.c_int32), ("heads", C.c_int32), ("seq_k", C.c_int32), ("d_qk", C.c_int32),
-        ("d_v", C.c_int32), ("scale", C.c_float),
+        ("d_v", C.c_int32), ("scale", C.c_float), ("splits", C.c_int32),
     ]
 
 

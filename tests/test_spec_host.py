@@ -208,3 +208,27 @@ def test_emit_is_deterministic_for_every_fixture():
     from paper_2502_15349_b200 import configs
     for key, make in configs.CONFIGS.items():
         assert "tmem" in af.code_generation(make())
+
+
+def test_scheduling_task_candidates_and_analytic_mode():
+    """Measured scheduling (schedule.py) exposes the kernels' runtime tile configurations as
+    candidates; analytic mode returns the library default without touching a GPU."""
+    import paper_2502_15349_b200 as af
+    from paper_2502_15349_b200 import configs, schedule
+    t = schedule.make_scheduling_task(configs.cfg2(batch=1, heads=4, heads_kv=1, seq=1024))
+    assert t.kind == "k1" and [c.kv_stages for c in t.candidates] == [0, 1]
+    t = schedule.make_scheduling_task(configs.cfg4b(batch=2, seq_k=4096))
+    assert t.kind == "mla-decode" and any(c.splits == 8 for c in t.candidates)
+    t = schedule.make_scheduling_task(configs.cfg4a(heads=8, seq=256))
+    assert t.kind == "materialised-bwd" and len(t.candidates) > 1
+    plan = schedule.tile_config_scheduling(t, mode="analytic")
+    assert plan.candidate == schedule.Candidate() and plan.cost > 0
+    with pytest.raises(af.UnsupportedError):  # measured mode needs a measure callback
+        schedule.tile_config_scheduling(t, mode="measured")
+    calls = []
+    t.measure = lambda c: (calls.append(c), 1.0 if c.head_groups == 4 else 2.0)[1]
+    plan = schedule.tile_config_scheduling(t, mode="measured")
+    assert plan.candidate.head_groups == 4 and len(calls) == len(t.candidates)
+    assert schedule.tuning(t.spec)["head_groups"] == 4
+    schedule.clear()
+    assert schedule.tuning(t.spec) == {}
