@@ -87,7 +87,7 @@ int run_materialized(const af_parallel_desc* d, const void* q, const void* k, co
 
   {  // row statistics: LSE*log2e (+inf when fully masked / padded), D = rowsum(dO*O)
     const int threads = 256;
-    const unsigned blocks = static_cast<unsigned>((l.rows * 32 + threads - 1) / threads);
+    const unsigned blocks = static_cast<unsigned>((l.rows * (DV / 32) + threads - 1) / threads);
     ::af::note_launch();
     bwd_preprocess_kernel<DV><<<blocks, threads, 0, s>>>(
         static_cast<const __nv_bfloat16*>(o), static_cast<const __nv_bfloat16*>(dout), lse,

@@ -138,7 +138,8 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
 
   {
     const int threads = 256;
-    const unsigned blocks = static_cast<unsigned>((rows * 32 + threads - 1) / threads);
+    const int tpr = d->d_v == 128 ? 4 : 2;  // threads per row (DV / 32)
+    const unsigned blocks = static_cast<unsigned>((rows * tpr + threads - 1) / threads);
     auto pre = (d->d_v == 128) ? bwd_preprocess_kernel<128> : bwd_preprocess_kernel<64>;
     ::af::note_launch();
     pre<<<blocks, threads, 0, a.s>>>(static_cast<const __nv_bfloat16*>(o),
