@@ -121,9 +121,11 @@ AF_DEVICE bool kept(const MaskParams& m, int i, int j, int seq_k) {
 template <int kAct>
 AF_DEVICE float apply_act(float z) {
   if constexpr (kAct == kActSigmoid) {
-    // 1 / (1 + 2^(-z log2 e)): two MUFU ops (ex2, rcp.approx); __frcp_rn's IEEE fix-up path
-    // costs ~10x more and made the sigmoid variants SFU-latency bound.
-    return rcp_approx(1.0f + ex2(-z * kLog2e));
+    // 1 / (1 + 2^(-z log2 e)): one MUFU op (ex2) and the reciprocal on the FMA pipe (rcp_nr) —
+    // with rcp.approx as well the sigmoid row epilogue issued two MUFU ops per score, twice the
+    // tensor pipe's time per block (16 MUFU lanes / clk / SM); __frcp_rn's IEEE fix-up path is
+    // ~10x slower still.  -z log2 e is clamped at 126 so 1 + e stays in rcp_nr's range.
+    return rcp_nr(1.0f + ex2(fminf(-z * kLog2e, 126.0f)));
   } else if constexpr (kAct == kActRelu) {
     return fmaxf(z, 0.0f);
   } else if constexpr (kAct == kActRelu2) {
