@@ -530,21 +530,30 @@ def run_gpu(args, key: str) -> dict | None:
     value = world * step_flops / (ms * 1e-3) / 1e12
     dom = "bwd" if w.backward else "fwd"
     dom_ms = bwd_ms if w.backward else fwd_ms
-    traffic = None
+    traffic, traffic_src = None, None
     prof = ROOT / "profiles" / "roofline_traffic.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(key, {}).get(f"{dom}_dram_bytes_per_launch")
+        tdoc = json.loads(prof.read_text())
+        traffic = tdoc.get(key, {}).get(f"{dom}_dram_bytes_per_launch")
+        traffic_src = (f"profiles/roofline_traffic.json (ncu --set full, tag {tdoc.get('tag')}, "
+                       f"head {tdoc.get('head')}): DRAM read+write bytes of the step's {dom} "
+                       f"kernels")
     if w.bound == "hbm":
         achieved = wk[f"{dom}_bytes"] / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                 "algorithmic_bytes": wk[f"{dom}_bytes"],
                 "peak_source": f"{pk['source']} hbm_gbs"}
+        if w.backward:  # the forward's share, also HBM-bound
+            fa = wk["fwd_bytes"] / (fwd_ms * 1e-3) / 1e9
+            roof["fwd"] = {"achieved": fa, "frac": fa / pk["hbm_gbs"]}
     elif w.bound == "tensor":
         achieved = wk[f"{dom}_flops"] / (dom_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tflops_sustained"],
                 "unit": "TFLOP/s", "frac": achieved / pk["tflops_sustained"], "traffic": traffic,
-                "peak_source": f"{pk['source']} bf16_tflops_sustained"}
+                "peak_source": f"{pk['source']} bf16_tflops_sustained (the dominant kernel runs "
+                               f"inside a multi-kernel step)",
+                "peak_burst": pk["tflops_burst"], "frac_burst": achieved / pk["tflops_burst"]}
     else:  # exact fp32 FFMA path: nominal CUDA-core peak, 148 SMs x 128 FMA/clk x 1.965 GHz
         achieved = wk["fwd_flops"] / (fwd_ms * 1e-3) / 1e12
         peak = 148 * 128 * 2 * 1.965e9 / 1e12
@@ -553,6 +562,7 @@ def run_gpu(args, key: str) -> dict | None:
                 "peak_source": "nominal fp32 FFMA (no measured figure)"}
     roof["kernel"] = {"fwd": "forward kernel(s) of the config", "bwd": "backward kernels of "
                       "the config"}[dom]
+    roof["traffic_source"] = traffic_src
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

@@ -20,7 +20,10 @@ cases = {
     "K4/K5 Mamba2 128": configs.cfg5b(batch=1, heads=2, seq=300),
     "materialised tier (256/512)": af.builtin("retention-parallel", batch=1, heads=1, seq=64),
 }
-for name, spec in cases.items():
+only = sys.argv[1:]  # case indices (default: all)
+for idx, (name, spec) in enumerate(cases.items()):
+    if only and str(idx) not in only:
+        continue
     arrays, dout = bench.device_inputs(spec, dev, 0)
     if spec.pattern.value == "parallel":
         o, lse = af.parallel_forward(spec, arrays)
