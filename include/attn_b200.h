@@ -61,14 +61,20 @@ typedef struct af_parallel_desc {
   int32_t kv_stages;         /* K1 K/V ring depth for head dims <= 128: 1 or 2 (default 2)   */
   int32_t head_groups;       /* materialised backward: query-head chunks of the key-side GEMMs
                                 (default: enough CTAs for ~4 waves)                          */
+  int32_t bwd_mode;          /* backward kernels for head dims 128/128: AF_BWD_DEFAULT (fused),
+                                AF_BWD_SPLIT (K2a + K2b: S and dP recomputed, bitwise
+                                deterministic), AF_BWD_FUSED (one 5-GEMM kernel, dQ reduced
+                                through L2 in fp32: deterministic to fp32 rounding only)      */
 } af_parallel_desc;
+enum { AF_BWD_DEFAULT = 0, AF_BWD_SPLIT = 1, AF_BWD_FUSED = 2 };
 
 /* O = template_forward(q, k, v); lse[b,h,i] = log-sum-exp of row i (softmax family, may be NULL).
  * Replaces engine.run_tiled_parallel (engine.py:423) / lowering.ExecutablePlan.run (lowering.py:857). */
 int af_parallel_fwd(const af_parallel_desc* desc, const void* q, const void* k, const void* v,
                     void* o, float* lse, void* stream);
 
-/* Bytes of device scratch af_parallel_bwd needs (fp32 dQ accumulator + row statistics). */
+/* Bytes of device scratch af_parallel_bwd needs (row statistics; + the fp32 dQ accumulator on the
+ * fused path). */
 size_t af_parallel_bwd_workspace(const af_parallel_desc* desc);
 
 /* VJP of af_parallel_fwd for cotangent dO (bf16).  dq/dk/dv use the q/k/v strides of desc; dk/dv

@@ -283,7 +283,23 @@ def _desc(plan: ParallelPlan, q, k, v, o, slope, dtype_code: int) -> rt.Parallel
         c.cap_a, c.cap_b = (1.0 if plan.normalize else 0.0), 0.0
     t = _tuning(plan.spec)
     c.kv_stages, c.head_groups = int(t.get("kv_stages", 0)), int(t.get("head_groups", 0))
+    c.bwd_mode = rt.AF_BWD_SPLIT if _DETERMINISTIC[0] else int(t.get("bwd_mode", 0))
     return c
+
+
+# Bitwise-deterministic backward (the reference's SPEC.md:335 contract): the fused 5-GEMM backward
+# adds dQ partials of different key tiles in L2 arrival order (fp32), so it is reproducible to
+# fp32 rounding only; deterministic mode selects the split K2a/K2b kernels (S and dP recomputed).
+_DETERMINISTIC = [False]
+
+
+def use_deterministic_backward(flag: bool = True) -> None:
+    """Select the bitwise-deterministic backward kernels for every later call (default off)."""
+    _DETERMINISTIC[0] = bool(flag)
+
+
+def deterministic_backward() -> bool:
+    return _DETERMINISTIC[0]
 
 
 _MASK_CHECKED: dict = {}

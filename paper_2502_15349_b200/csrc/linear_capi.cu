@@ -234,9 +234,10 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
             d->q_scale, false, false, want_dots ? q : nullptr, d->q_stride, dq_dot, false, nullptr,
             sb};
   if ((st = run_la(d, a1, s)) != AF_OK) return st;
-  // dKm = q_scale * LA_rev(q=V, k=dO, v=Q); dk = gate*dKm   dk_dot = Km . dKm
+  // dKm = q_scale * LA_rev(q=V, k=dO, v=Q); dk = gate*dKm   dk_dot = k . dKm (raw keys)
   LaArgs a2{v, dout, q, d->v_stride, d->o_stride, d->q_stride, d->d_v, d->d_k, dk, d->k_stride,
-            d->q_scale, false, true, want_dots ? km : nullptr, km_st, dk_dot, true, nullptr, sb};
+            d->q_scale, false, true, want_dots ? k : nullptr, d->k_stride, dk_dot, true, nullptr,
+            sb};
   if ((st = run_la(d, a2, s)) != AF_OK) return st;
   // dV = q_scale * LA_rev(q=Km, k=Q, v=dO)
   LaArgs a3{km, q, dout, km_st, d->q_stride, d->o_stride, d->d_k, d->d_v, dv, d->v_stride,
@@ -266,7 +267,8 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
                          step_tensor(d_decay_factor[f], d->decay_factor_stride[f]))) != AF_OK)
           return st;
     if (d_key_gate != nullptr)
-      if ((st = reduce(step_dkdot, p.u_scale, step_tensor(d_key_gate, d->key_gate_stride))) !=
+      if ((st = reduce(step_dkdot, StepTensor{nullptr, 0, 0, 0},
+                       step_tensor(d_key_gate, d->key_gate_stride))) !=
           AF_OK)
         return st;
   }

@@ -714,11 +714,12 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
   }
 }
 
-// Per-step gradients (SURVEY A.4 restated):  d log a_t = sum_{s>=t} (dq_dot_s - dk_dot_s)
-// where dq_dot = Qm . dQm, dk_dot = Km . dKm.  One block per (b, h) sequence writes d log a_t and
-// dk_dot_t (both [B, H, S] fp32); step_grad_reduce_kernel then forms d fac_f = d log a / fac_f and
-// d gate = dk_dot / gate (k_mod = k * gate: dL/dgate = k . dKm) and sums broadcast axes in a fixed
-// order — no atomics, bitwise deterministic.
+// Per-step gradients (SURVEY A.4 restated):  d log a_t = sum_{s>=t} (dq_dot_s - u_s kdot_s)
+// where dq_dot = Qm . dQm and kdot = k . dKm over the raw (un-gated) keys, u the key gate
+// (Km . dKm = u k . dKm).  One block per (b, h) sequence writes d log a_t and kdot_t (both
+// [B, H, S] fp32); step_grad_reduce_kernel then forms d fac_f = d log a / fac_f and
+// d gate = kdot (k_mod = k * gate: dL/dgate = k . dKm, no division — finite at gate = 0) and sums
+// broadcast axes in a fixed order — no atomics, bitwise deterministic.
 __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
                                          const float* __restrict__ dk_dot, int slots,
                                          LinearParams p, float* __restrict__ dloga_out,
@@ -734,7 +735,11 @@ __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
     for (int sl = 0; sl < slots; ++sl) a += x[sl * rows + base + t];
     return a;
   };
-  auto val = [&](int t) { return dot(dq_dot, t) - dot(dk_dot, t); };
+  const int b = bh / p.heads, h = bh % p.heads;
+  auto val = [&](int t) {
+    const float u = p.u_scale.ptr != nullptr ? p.u_scale.at(b, h, t) : 1.0f;
+    return dot(dq_dot, t) - u * dot(dk_dot, t);
+  };
   const int per = (seq + blockDim.x - 1) / blockDim.x;
   const int t0 = threadIdx.x * per;
   const int t1 = min(seq, t0 + per);
@@ -758,7 +763,8 @@ __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
   }
 }
 
-// out[b', h', t] += sum over the broadcast axes of out (stride 0) of val[b, h, t] / div(b, h, t),
+// out[b', h', t] += sum over the broadcast axes of out (stride 0) of val[b, h, t] / div(b, h, t)
+// (div.ptr null: val itself),
 // in ascending (b, h) order.  val is [B, H, S] fp32; one thread per output element.
 __global__ void step_grad_reduce_kernel(const float* __restrict__ val, StepTensor div,
                                         StepTensor out, int batch, int heads, int seq) {
@@ -772,7 +778,9 @@ __global__ void step_grad_reduce_kernel(const float* __restrict__ val, StepTenso
   float acc = 0.0f;
   for (int b = (out.sb == 0 ? 0 : bb); b < (out.sb == 0 ? batch : bb + 1); ++b)
     for (int h = (out.sh == 0 ? 0 : hh); h < (out.sh == 0 ? heads : hh + 1); ++h)
-      acc += val[(static_cast<int64_t>(b) * heads + h) * seq + t] / div.at(b, h, t);
+      acc += div.ptr != nullptr ? val[(static_cast<int64_t>(b) * heads + h) * seq + t] /
+                                      div.at(b, h, t)
+                                : val[(static_cast<int64_t>(b) * heads + h) * seq + t];
   float* dst = const_cast<float*>(out.ptr) + bb * out.sb + hh * out.sh + t * out.ss;
   *dst += acc;
 }

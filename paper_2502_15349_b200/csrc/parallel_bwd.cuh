@@ -140,6 +140,117 @@ AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float
   }
 }
 
+// K2a / fused backward row math: P^T of one key row j against 32 consecutive query columns
+// [i0, i0 + 32) from the raw scores sr (fp32 bits), packed bf16 into pk[16]; gk[16] receives the
+// family's derivative factors (soft-cap, abssum); returns the keep / activation-gradient bits.
+template <int kFamily, int kAct>
+AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t (&sr)[32], int i0, int j,
+                               bool fullblk, float slope, const float* ls, uint32_t* pk,
+                               uint32_t* gk) {
+  uint32_t bits = 0u;
+  if constexpr (kFamily == kFamilySoftmax && kAct == kActSoftcap) {
+    const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
+    const float cap_g = p.cap_a * p.cap_b;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float pv[2], gv[2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int i = i0 + e + x;
+        const bool keep = fullblk | (kept(p.mask, i, j, p.seq_k) & (i < p.seq_q));
+        const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
+        pv[x] = keep ? ex2(fmaf(cap_out, t, -ls[e + x])) : 0.0f;
+        gv[x] = cap_g * fmaf(-t, t, 1.0f);
+      }
+      pk[e / 2] = pack_bf16(pv[0], pv[1]);
+      gk[e / 2] = pack_bf16(gv[0], gv[1]);
+    }
+  } else if constexpr (kFamily == kFamilyAbssum) {
+    const bool norm = p.cap_a != 0.0f;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) {
+      float pv[2], gv[2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int i = i0 + e + x;
+        const bool keep = fullblk | (kept(p.mask, i, j, p.seq_k) & (i < p.seq_q));
+        const float rc = norm ? rcp_approx(fmaxf(ls[e + x], 1.0f)) : 1.0f;
+        const float m = ex2(static_cast<float>(i - j) * slope);
+        const float z = __uint_as_float(sr[e + x]) * p.scale * m;
+        pv[x] = keep ? z * rc : 0.0f;
+        gv[x] = keep ? m * rc : 0.0f;
+        bits |= (z >= 0.0f) ? (1u << (e + x)) : 0u;
+      }
+      pk[e / 2] = pack_bf16(pv[0], pv[1]);
+      gk[e / 2] = pack_bf16(gv[0], gv[1]);
+    }
+  } else if constexpr (kFamily == kFamilySoftmax) {
+    if (fullblk) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 4) {
+        // x = s * scale - lse: one FFMA2 per pair (the negation is an operand modifier)
+        const float4 l4 = *reinterpret_cast<const float4*>(ls + e);
+        const float2 sc2 = splat2(p.scale_log2);
+        const float2 x01 =
+            ffma2(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2,
+                  make_float2(-l4.x, -l4.y));
+        const float2 x23 =
+            ffma2(make_float2(__uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3])), sc2,
+                  make_float2(-l4.z, -l4.w));
+        pk[e / 2] = pack_bf16(bwd_exp2(x01.x, e), bwd_exp2(x01.y, e));
+        pk[e / 2 + 1] = pack_bf16(bwd_exp2(x23.x, e + 2), bwd_exp2(x23.y, e + 2));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        float pv[2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          const int i = i0 + e + x;
+          const bool keep = kept(p.mask, i, j, p.seq_k) & (i < p.seq_q);
+          pv[x] = keep ? ex2(fmaf(__uint_as_float(sr[e + x]), p.scale_log2,
+                                  -ls[e + x]))
+                       : 0.0f;
+        }
+        pk[e / 2] = pack_bf16(pv[0], pv[1]);
+      }
+    }
+  } else {
+    const float zb = p.bias - slope * (static_cast<float>(i0) - static_cast<float>(j));
+    if (fullblk) {  // compact fast path: no per-element mask tests
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        const float z0 = fmaf(__uint_as_float(sr[e]), p.scale, zb - slope * static_cast<float>(e));
+        const float z1 = fmaf(__uint_as_float(sr[e + 1]), p.scale,
+                              zb - slope * static_cast<float>(e + 1));
+        if constexpr (kAct == kActRelu) {
+          bits |= (z0 >= 0.0f ? (1u << e) : 0u) | (z1 >= 0.0f ? (2u << e) : 0u);
+        } else {
+          bits |= 3u << e;
+        }
+        pk[e / 2] = pack_bf16(apply_act<kAct>(z0), apply_act<kAct>(z1));
+      }
+    } else {
+#pragma unroll 2
+      for (int e = 0; e < 32; e += 2) {
+        float pv[2];
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          const int i = i0 + e + x;
+          const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
+                               zb - slope * static_cast<float>(e + x));
+          const bool keep = kept(p.mask, i, j, p.seq_k) & (i < p.seq_q);
+          const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
+          bits |= (keep && g) ? (1u << (e + x)) : 0u;
+          pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
+        }
+        pk[e / 2] = pack_bf16(pv[0], pv[1]);
+      }
+    }
+  }
+  return bits;
+}
+
 // ═══════════════════════════════ K2a: dK, dV ═══════════════════════════════
 
 // dS^T of K2a in shared memory instead of TMEM, so dP of the next tile can be issued ahead of dK:
@@ -373,7 +484,6 @@ __global__ void __launch_bounds__(kKvThreads, 1)
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const int cb = sub * kCpw;
     const uint32_t pcol = cb;
-    const float fj = static_cast<float>(j);
     int hi_ = 0, qt_ = 0;
     for (int n = 0; n < niter; ++n) {
       const int s = n % kStages;
@@ -402,108 +512,8 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         uint32_t sr[32];
         tmem_ld32(tmem + lane_base + kColS + cb + c2 * 32, sr);
         tmem_ld_wait();
-        uint32_t bits = 0u;
-        if constexpr (kFamily == kFamilySoftmax && kAct == kActSoftcap) {
-          const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
-          const float cap_g = p.cap_a * p.cap_b;
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float pv[2], gv[2];
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-              const int i = q0 + cb + c2 * 32 + e + x;
-              const bool keep = fullblk | (kept(p.mask, i, j, p.seq_k) & (i < p.seq_q));
-              const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
-              pv[x] = keep ? ex2(fmaf(cap_out, t, -lse_s[c2 * 32 + e + x])) : 0.0f;
-              gv[x] = cap_g * fmaf(-t, t, 1.0f);
-            }
-            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
-            gk[c2 * 16 + e / 2] = pack_bf16(gv[0], gv[1]);
-          }
-        } else if constexpr (kFamily == kFamilyAbssum) {
-          const bool norm = p.cap_a != 0.0f;
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float pv[2], gv[2];
-#pragma unroll
-            for (int x = 0; x < 2; ++x) {
-              const int i = q0 + cb + c2 * 32 + e + x;
-              const bool keep = fullblk | (kept(p.mask, i, j, p.seq_k) & (i < p.seq_q));
-              const float rc = norm ? rcp_approx(fmaxf(lse_s[c2 * 32 + e + x], 1.0f)) : 1.0f;
-              const float m = ex2(static_cast<float>(i - j) * slope);
-              const float z = __uint_as_float(sr[e + x]) * p.scale * m;
-              pv[x] = keep ? z * rc : 0.0f;
-              gv[x] = keep ? m * rc : 0.0f;
-              bits |= (z >= 0.0f) ? (1u << (e + x)) : 0u;
-            }
-            pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
-            gk[c2 * 16 + e / 2] = pack_bf16(gv[0], gv[1]);
-          }
-        } else if constexpr (kFamily == kFamilySoftmax) {
-          if (fullblk) {
-#pragma unroll
-            for (int e = 0; e < 32; e += 4) {
-              // x = s * scale - lse: one FFMA2 per pair (the negation is an operand modifier)
-              const float4 l4 = *reinterpret_cast<const float4*>(lse_s + c2 * 32 + e);
-              const float2 sc2 = splat2(p.scale_log2);
-              const float2 x01 =
-                  ffma2(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), sc2,
-                        make_float2(-l4.x, -l4.y));
-              const float2 x23 =
-                  ffma2(make_float2(__uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3])), sc2,
-                        make_float2(-l4.z, -l4.w));
-              pk[c2 * 16 + e / 2] = pack_bf16(bwd_exp2(x01.x, e), bwd_exp2(x01.y, e));
-              pk[c2 * 16 + e / 2 + 1] = pack_bf16(bwd_exp2(x23.x, e + 2), bwd_exp2(x23.y, e + 2));
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              float pv[2];
-#pragma unroll
-              for (int x = 0; x < 2; ++x) {
-                const int i = q0 + cb + c2 * 32 + e + x;
-                const bool keep = kept(p.mask, i, j, p.seq_k) & (i < p.seq_q);
-                pv[x] = keep ? ex2(fmaf(__uint_as_float(sr[e + x]), p.scale_log2,
-                                        -lse_s[c2 * 32 + e + x]))
-                             : 0.0f;
-              }
-              pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
-            }
-          }
-        } else {
-          const float zb = p.bias - slope * (static_cast<float>(q0 + cb + c2 * 32) - fj);
-          if (fullblk) {  // compact fast path: no per-element mask tests
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const float z0 = fmaf(__uint_as_float(sr[e]), p.scale, zb - slope * static_cast<float>(e));
-              const float z1 = fmaf(__uint_as_float(sr[e + 1]), p.scale,
-                                    zb - slope * static_cast<float>(e + 1));
-              if constexpr (kAct == kActRelu) {
-                bits |= (z0 >= 0.0f ? (1u << e) : 0u) | (z1 >= 0.0f ? (2u << e) : 0u);
-              } else {
-                bits |= 3u << e;
-              }
-              pk[c2 * 16 + e / 2] = pack_bf16(apply_act<kAct>(z0), apply_act<kAct>(z1));
-            }
-          } else {
-#pragma unroll 2
-            for (int e = 0; e < 32; e += 2) {
-              float pv[2];
-#pragma unroll
-              for (int x = 0; x < 2; ++x) {
-                const int i = q0 + cb + c2 * 32 + e + x;
-                const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
-                                     zb - slope * static_cast<float>(e + x));
-                const bool keep = kept(p.mask, i, j, p.seq_k) & (i < p.seq_q);
-                const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
-                bits |= (keep && g) ? (1u << (e + x)) : 0u;
-                pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
-              }
-              pk[c2 * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
-            }
-          }
-        }
-        gmask[c2] = bits;
+        gmask[c2] = kv_rows_p32<kFamily, kAct>(p, sr, q0 + cb + c2 * 32, j, fullblk, slope,
+                                               lse_s + c2 * 32, pk + c2 * 16, gk + c2 * 16);
       }
       if constexpr (kNP == 2)
         tmem_st32(tmem + lane_base + kColS + pcol, *reinterpret_cast<uint32_t(*)[32]>(pk));

@@ -2,6 +2,7 @@
 // preprocess, K2a (dK, dV) and K2b (dQ) — stream-ordered, no atomics, deterministic.
 #include "host_common.h"
 #include "parallel_bwd.cuh"
+#include "parallel_bwd_fused.cuh"
 
 namespace af {
 int validate_parallel(const af_parallel_desc* d);
@@ -18,6 +19,9 @@ inline int64_t pad_q(int seq_q) { return ((seq_q + kBlockM - 1) / kBlockM) * kBl
 struct BwdLaunch {
   const af_parallel_desc* d;
   CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tq64, tdo64;  // 64-row query boxes (fused kernel)
+  bool fused;
+  float* dq_accum;
   ParallelBwdParams p;
   const void* q;
   const void* dout;
@@ -30,6 +34,28 @@ struct BwdLaunch {
 
 template <int D, int DV, int kFamily, int kAct>
 int launch_bwd(const BwdLaunch& a) {
+  if constexpr (D == 128) {
+    if (a.fused) {
+      using L = BwdFusedSmem<D, DV>;
+      const int64_t acc_bytes = static_cast<int64_t>(a.d->batch) * a.d->heads_q * a.pad * D * 4;
+      AF_CUDA_CHECK(cudaMemsetAsync(a.dq_accum, 0, acc_bytes, a.s));
+      auto kern = parallel_bwd_fused_kernel<D, DV, kFamily, kAct>;
+      AF_SMEM_ATTR(kern, L::kTotal);
+      dim3 grid((a.d->seq_k + kBlockN - 1) / kBlockN, a.d->batch * a.d->heads_kv);
+      ::af::note_launch();
+      kern<<<grid, kFusedThreads, L::kTotal, a.s>>>(a.tq64, a.tk, a.tv, a.tdo64, a.p, a.lse2,
+                                                    a.delta, a.pad, a.dq_accum);
+      AF_CUDA_CHECK(cudaGetLastError());
+      const int64_t rows = static_cast<int64_t>(a.d->batch) * a.d->heads_q * a.d->seq_q;
+      const int64_t threads = rows * (D / 8);
+      ::af::note_launch();
+      dq_convert_kernel<D><<<static_cast<unsigned>((threads + 255) / 256), 256, 0, a.s>>>(
+          a.dq_accum, static_cast<__nv_bfloat16*>(a.dq), a.d->q_stride[0], a.d->q_stride[1],
+          a.d->q_stride[2], a.d->heads_q, a.d->seq_q, a.pad, a.d->scale, rows);
+      AF_CUDA_CHECK(cudaGetLastError());
+      return AF_OK;
+    }
+  }
   {
     using L = BwdKVSmem<D, DV>;
     auto kern = parallel_bwd_dkdv_kernel<D, DV, kFamily, kAct>;
@@ -77,11 +103,24 @@ int dispatch_bwd(const BwdLaunch& a) {
 }  // namespace
 }  // namespace af
 
+namespace af {
+namespace {
+// The 5-GEMM kernel serves the 128/128 head dims unless the split (bitwise-deterministic) pair is
+// requested.
+bool use_fused_bwd(const af_parallel_desc* d) {
+  return d->d_qk == 128 && d->d_v == 128 && d->dtype == AF_DTYPE_BF16 && !is_mla(d) &&
+         d->bwd_mode != AF_BWD_SPLIT;
+}
+}  // namespace
+}  // namespace af
+
 extern "C" size_t af_parallel_bwd_workspace(const af_parallel_desc* d) {
   if (d == nullptr) return 0;
   if (af::materialized_bwd_dims(d)) return af::mla_bwd_workspace(d);
   const int64_t rows = static_cast<int64_t>(d->batch) * d->heads_q * af::pad_q(d->seq_q);
-  return static_cast<size_t>(rows) * 2 * sizeof(float);
+  size_t bytes = static_cast<size_t>(rows) * 2 * sizeof(float);
+  if (af::use_fused_bwd(d)) bytes += static_cast<size_t>(rows) * d->d_qk * sizeof(float);
+  return bytes;
 }
 
 extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const void* k,
@@ -120,6 +159,8 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
   float* delta = lse2 + rows;
   a.lse2 = lse2;
   a.delta = delta;
+  a.fused = use_fused_bwd(d);
+  a.dq_accum = a.fused ? delta + rows : nullptr;
   a.q = q;
   a.dout = dout;
   a.dq = dq;
@@ -134,6 +175,12 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
                     d->batch, d->v_stride, 64, kBlockN, true) ||
       !make_tmap_4d(&a.tdo, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d->d_v, d->seq_q,
                     d->heads_q, d->batch, d->o_stride, 64, kBlockM, true))
+    return AF_ERR_INPUT;
+  if (a.fused &&
+      (!make_tmap_4d(&a.tq64, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d->d_qk, d->seq_q,
+                     d->heads_q, d->batch, d->q_stride, 64, kFusedBM, true) ||
+       !make_tmap_4d(&a.tdo64, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d->d_v, d->seq_q,
+                     d->heads_q, d->batch, d->o_stride, 64, kFusedBM, true)))
     return AF_ERR_INPUT;
 
   {

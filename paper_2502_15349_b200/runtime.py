@@ -20,6 +20,7 @@ AF_OK, AF_ERR_INPUT, AF_ERR_SHAPE, AF_ERR_UNSUPPORTED, AF_ERR_NAN, AF_ERR_CUDA =
 AF_FAMILY_SOFTMAX, AF_FAMILY_ELEMENTWISE, AF_FAMILY_ABSSUM = 0, 1, 2
 AF_ACT_IDENTITY, AF_ACT_SIGMOID, AF_ACT_RELU, AF_ACT_RELU2 = 0, 1, 2, 3
 AF_DTYPE_BF16, AF_DTYPE_F32 = 0, 1
+AF_BWD_DEFAULT, AF_BWD_SPLIT, AF_BWD_FUSED = 0, 1, 2
 AF_ROWNORM_NONE, AF_ROWNORM_SOFTMAX, AF_ROWNORM_ABSSUM = 0, 1, 2
 AF_FM_NONE, AF_FM_SILU, AF_FM_SIGMOID, AF_FM_RELU, AF_FM_TANH, AF_FM_EXP = range(6)
 
@@ -35,7 +36,7 @@ class ParallelDesc(C.Structure):
         ("family", C.c_int32), ("act", C.c_int32), ("scale", C.c_float),
         ("causal", C.c_int32), ("diag_offset", C.c_int32), ("window", C.c_int32),
         ("slope", C.c_void_p), ("bias", C.c_float), ("cap_a", C.c_float), ("cap_b", C.c_float),
-        ("kv_stages", C.c_int32), ("head_groups", C.c_int32),
+        ("kv_stages", C.c_int32), ("head_groups", C.c_int32), ("bwd_mode", C.c_int32),
     ]
 
 

@@ -161,3 +161,21 @@ def test_zero_decay_factor_resets_the_state_exactly():
     arrays["decay"][:, :, 7] = -0.5
     with pytest.raises(af.UnsupportedError):
         af.run_chunk_recurrent(spec, to_dev(arrays))
+
+
+def test_zero_key_gate_has_finite_gradient():
+    """k_mod = k * gate with gate = 0 on some steps (padding masked through the gate): the gate
+    gradient is k . dKm from the raw keys — finite and equal to the oracle's — not dk_dot / gate."""
+    from dataclasses import replace as dreplace
+    base = S.builtin("gated-retention", batch=1, heads=2, seq=300, d_qk=128, d_v=128)
+    spec = dreplace(base, extra_inputs=(dreplace(base.extra_inputs[0], differentiable=True),))
+    arrays = oracle.generate(spec, seed=6)
+    arrays["gate"][:, :, [0, 1, 64, 200, 299]] = 0.0
+    dev = to_dev(arrays)
+    dout = torch.rand(1, 2, 300, 128, device="cuda").sub(0.5).to(torch.bfloat16)
+    g = af.linear_backward(spec, dev, dout)
+    assert bool(torch.isfinite(g["gate"]).all())
+    want = OR.chunk_vjp(spec, rounded(arrays), dout.double().cpu().numpy(), chunk=64)
+    assert nw(g["gate"].double().cpu().numpy(), want["gate"]) <= 2e-2
+    for n in ("q", "k", "v"):
+        assert nw(g[n].double().cpu().numpy(), want[n]) <= 2e-2, n

@@ -125,8 +125,24 @@ def test_bf16_forward_matches_oracle(case):
         assert_lse(lse, OP.lse_rows(spec, ref))
 
 
+@pytest.fixture
+def deterministic():
+    """Bitwise comparisons across calls need the split (K2a/K2b) backward: the fused 5-GEMM
+    kernel adds dQ partials in L2 arrival order (fp32)."""
+    af.api.use_deterministic_backward(True)
+    yield
+    af.api.use_deterministic_backward(False)
+
+
+@pytest.fixture(params=["fused", "split"])
+def bwd_mode(request):
+    af.api.use_deterministic_backward(request.param == "split")
+    yield request.param
+    af.api.use_deterministic_backward(False)
+
+
 @pytest.mark.parametrize("case", sorted(BF16_CASES))
-def test_bf16_backward_matches_oracle(case):
+def test_bf16_backward_matches_oracle(case, bwd_mode):
     spec = BF16_CASES[case]()
     arrays = oracle.generate(spec, seed=12)
     dev = to_dev(arrays)
@@ -199,7 +215,7 @@ def test_cfg2_full_size_sampled_rows():
         assert np.max(np.abs(lse[b, h, rows].double().cpu().numpy() - want_l[0, 0])) <= 1e-3
 
 
-def test_backward_s4096_gqa_group():
+def test_backward_s4096_gqa_group(bwd_mode):
     """Full-sequence backward at S4096 for one GQA group (4 q heads on 1 KV head)."""
     spec = spec_gqa("softmax", 1, 4, 1, 4096, 4096, 128)
     arrays = oracle.generate(spec, seed=21)
@@ -212,7 +228,7 @@ def test_backward_s4096_gqa_group():
         assert normwise(grads[k].double().cpu().numpy(), want[k]) <= 2e-2, k
 
 
-def test_autograd_module_matches_backward():
+def test_autograd_module_matches_backward(deterministic):
     spec = spec_gqa("softmax", 1, 4, 2, 256, 256, 128)
     arrays = oracle.generate(spec, seed=3)
     dev = to_dev(arrays)
@@ -250,7 +266,7 @@ def test_run_tiled_parallel_accepts_reference_signature():
     assert af.bind(spec).run(arrays).shape == o1.shape
 
 
-def test_bshd_strided_inputs_match_contiguous():
+def test_bshd_strided_inputs_match_contiguous(deterministic):
     """[B, S, H, D] activations passed as permuted views (element strides, unit feature stride)
     give the same results as contiguous [B, H, S, D] copies — forward and backward."""
     spec = spec_gqa("softmax", 2, 8, 2, 384, 384, 128)
@@ -275,3 +291,24 @@ def test_nan_inputs_raise_nan_error():
     dev["q"][0, 0, 5, 3] = float("nan")
     with pytest.raises(af.NanError):
         af.run_tiled_parallel(spec, dev)
+
+
+def test_fused_backward_matches_split_and_repeats():
+    """The fused 5-GEMM backward against the split (bitwise-deterministic) pair on the same inputs:
+    dK / dV are bitwise reproducible across repeated fused calls (no cross-CTA reduction), dQ to
+    fp32 rounding of the reduce-add order; both agree with each other to bf16 rounding."""
+    spec = spec_gqa("softmax", 2, 8, 2, 1000, 1000, 128)
+    dev = to_dev(oracle.generate(spec, seed=21))
+    o, lse = af.parallel_forward(spec, dev)
+    dout = torch.rand_like(o) * 2 - 1
+    g1 = af.parallel_backward(spec, dev, o, lse, dout)
+    g2 = af.parallel_backward(spec, dev, o, lse, dout)
+    assert torch.equal(g1["k"], g2["k"]) and torch.equal(g1["v"], g2["v"])
+    assert normwise(g1["q"].double().cpu(), g2["q"].double().cpu()) <= 1e-3
+    af.api.use_deterministic_backward(True)
+    try:
+        gs = af.parallel_backward(spec, dev, o, lse, dout)
+    finally:
+        af.api.use_deterministic_backward(False)
+    for n in "qkv":
+        assert normwise(g1[n].double().cpu(), gs[n].double().cpu()) <= 5e-3, n

@@ -16,8 +16,15 @@ def _rand(*shape, dtype=torch.bfloat16):
     return (torch.rand(*shape, generator=g) * 2 - 1).to(dtype)
 
 
+@pytest.fixture
+def deterministic():
+    af.api.use_deterministic_backward(True)
+    yield
+    af.api.use_deterministic_backward(False)
+
+
 @pytest.mark.parametrize("b,h,hkv,s", [(3, 8, 2, 512), (1, 8, 4, 384)])
-def test_parallel_pipeline_bitwise(b, h, hkv, s):
+def test_parallel_pipeline_bitwise(b, h, hkv, s, deterministic):
     spec = S.with_causal_mask(S.builtin("softmax", batch=b, heads=h, heads_kv=hkv, seq=s,
                                         d_qk=128, d_v=128))
     host = {"q": _rand(b, h, s, 128).pin_memory(), "k": _rand(b, hkv, s, 128).pin_memory(),
