@@ -98,13 +98,13 @@ AF_DEVICE void store_row_bf16(__nv_bfloat16* dst, const uint32_t (&r)[N], float 
   }
 }
 
-// dS from packed P and fp32 dP for 32 columns (both families)
+// dS from packed P and fp32 dP for NC (16 or 32) columns (both families)
 // (soft-capped softmax: gk holds the packed factor cap_a cap_b (1 - t^2) of d s'/d s)
-template <int kFamily, int kAct, bool kRowDelta>
-AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float* del_col,
+template <int kFamily, int kAct, bool kRowDelta, int NC = 32>
+AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t* dr, const float* del_col,
                        float del_row, uint32_t gmask, uint32_t* dsk, const uint32_t* gk) {
 #pragma unroll
-  for (int e = 0; e < 32; e += 2) {
+  for (int e = 0; e < NC; e += 2) {
     const uint32_t w = pk[e / 2];
     const float p0 = bf16_lo(w), p1 = bf16_hi(w);
     const float dp0 = __uint_as_float(dr[e]), dp1 = __uint_as_float(dr[e + 1]);
@@ -140,11 +140,12 @@ AF_DEVICE void make_ds(const uint32_t* pk, const uint32_t (&dr)[32], const float
   }
 }
 
-// K2a / fused backward row math: P^T of one key row j against 32 consecutive query columns
-// [i0, i0 + 32) from the raw scores sr (fp32 bits), packed bf16 into pk[16]; gk[16] receives the
-// family's derivative factors (soft-cap, abssum); returns the keep / activation-gradient bits.
-template <int kFamily, int kAct>
-AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t (&sr)[32], int i0, int j,
+// K2a / fused backward row math: P^T of one key row j against NC (16 or 32) consecutive query
+// columns [i0, i0 + NC) from the raw scores sr (fp32 bits), packed bf16 into pk[NC/2]; gk[NC/2]
+// receives the family's derivative factors (soft-cap, abssum); returns the keep /
+// activation-gradient bits.
+template <int kFamily, int kAct, int NC = 32>
+AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t* sr, int i0, int j,
                                bool fullblk, float slope, const float* ls, uint32_t* pk,
                                uint32_t* gk) {
   uint32_t bits = 0u;
@@ -152,7 +153,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t (&sr)[
     const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
     const float cap_g = p.cap_a * p.cap_b;
 #pragma unroll
-    for (int e = 0; e < 32; e += 2) {
+    for (int e = 0; e < NC; e += 2) {
       float pv[2], gv[2];
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
@@ -168,7 +169,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t (&sr)[
   } else if constexpr (kFamily == kFamilyAbssum) {
     const bool norm = p.cap_a != 0.0f;
 #pragma unroll
-    for (int e = 0; e < 32; e += 2) {
+    for (int e = 0; e < NC; e += 2) {
       float pv[2], gv[2];
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
@@ -187,7 +188,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t (&sr)[
   } else if constexpr (kFamily == kFamilySoftmax) {
     if (fullblk) {
 #pragma unroll
-      for (int e = 0; e < 32; e += 4) {
+      for (int e = 0; e < NC; e += 4) {
         // x = s * scale - lse: one FFMA2 per pair (the negation is an operand modifier)
         const float4 l4 = *reinterpret_cast<const float4*>(ls + e);
         const float2 sc2 = splat2(p.scale_log2);
@@ -202,7 +203,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t (&sr)[
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
+      for (int e = 0; e < NC; e += 2) {
         float pv[2];
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
@@ -219,7 +220,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t (&sr)[
     const float zb = p.bias - slope * (static_cast<float>(i0) - static_cast<float>(j));
     if (fullblk) {  // compact fast path: no per-element mask tests
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
+      for (int e = 0; e < NC; e += 2) {
         const float z0 = fmaf(__uint_as_float(sr[e]), p.scale, zb - slope * static_cast<float>(e));
         const float z1 = fmaf(__uint_as_float(sr[e + 1]), p.scale,
                               zb - slope * static_cast<float>(e + 1));
@@ -232,7 +233,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t (&sr)[
       }
     } else {
 #pragma unroll 2
-      for (int e = 0; e < 32; e += 2) {
+      for (int e = 0; e < NC; e += 2) {
         float pv[2];
 #pragma unroll
         for (int x = 0; x < 2; ++x) {

@@ -1,5 +1,7 @@
 // C-ABI entry points of the parallel-template backward: workspace sizing, the row-statistics
-// preprocess, K2a (dK, dV) and K2b (dQ) — stream-ordered, no atomics, deterministic.
+// preprocess, then either K2f (fused 5-GEMM kernel, dQ through an fp32 L2 reduce-add and a convert
+// pass; the default for 128/128 heads) or K2a (dK, dV) + K2b (dQ) — no atomics, bitwise
+// deterministic (AF_BWD_SPLIT, and every other head-dim pair).  Stream-ordered.
 #include "host_common.h"
 #include "parallel_bwd.cuh"
 #include "parallel_bwd_fused.cuh"
@@ -34,7 +36,7 @@ struct BwdLaunch {
 
 template <int D, int DV, int kFamily, int kAct>
 int launch_bwd(const BwdLaunch& a) {
-  if constexpr (D == 128) {
+  if constexpr (D == 128 && DV == 128) {
     if (a.fused) {
       using L = BwdFusedSmem<D, DV>;
       const int64_t acc_bytes = static_cast<int64_t>(a.d->batch) * a.d->heads_q * a.pad * D * 4;

@@ -3,23 +3,29 @@
 // Same VJP as K2a + K2b (parallel_bwd.cuh, the closed form of
 // attention.derive_backward / graph.py:481-569), but S and dP are computed once per (key tile,
 // query tile) pair: the key-tile-stationary CTA of K2a also forms dQ^T = K^T dS^T for the tile and
-// adds it into an fp32 accumulator in global memory with TMA bulk reduce-adds, so the recompute
-// of K2b (S = Q K^T, dP = dO V^T: 2 of K2's 7 GEMMs) disappears.  A small pass then scales the
-// accumulator into bf16 dQ.  fp32 reduce-adds from different key tiles land in L2 in arrival
-// order, so dQ is reproducible to fp32 rounding only (dK / dV stay bitwise deterministic); the
-// split K2a/K2b path remains available for bitwise-deterministic runs (desc.deterministic).
+// adds it into an fp32 accumulator in global memory with TMA bulk reduce-adds, so the
+// recompute of K2b (S = Q K^T, dP = dO V^T: 2 of K2's 7 GEMMs) disappears.  A small pass then
+// scales the accumulator into bf16 dQ.  fp32 reduce-adds from different key tiles land in L2 in
+// arrival order, so dQ is reproducible to fp32 rounding only (dK / dV stay bitwise deterministic);
+// the split K2a/K2b pair remains the bitwise-deterministic mode (desc.bwd_mode = AF_BWD_SPLIT).
 //
 // One CTA per (128-key tile, b, KV head); it loops over every query head of the GQA group and
-// every visible 64-row query tile (64 rather than 128 rows so all five accumulators fit TMEM
-// without aliasing: S^T x2 | dP^T | dQ^T | dV | dK = 64+64+64+64+128+128 columns).
-//   warps 0-7  row warps: lane quarter w%4, query columns [32*(w/4), +32) of the 64-row tile;
-//              P^T -> TMEM (A operand of dV), dS^T -> shared memory (A of dK, B of dQ^T)
-//   warps 8-11 dQ drain: one lane quarter (32 of the 128 d rows of dQ^T) each; TMEM -> smem
-//              staging -> cp.reduce.async.bulk .add.f32 into the accumulator
-//   warp 12    TMA producer (K/V once, Q/dO/LSE/delta ring of 3)
-//   warp 13    TMEM allocator + single-thread tcgen05.mma issuer
+// every visible 64-row query tile — 64 rather than 128 rows so all five accumulators fit TMEM
+// without aliasing (S^T x2 | dP^T | dQ^T | dV | dK = 64+64+64+64+128+128 columns) and no GEMM
+// waits on the dQ drain.
+//   warps 0-15  row warps: lane quarter w%4 (= key row), query columns [16*(w/4), +16);
+//               P^T -> TMEM (A operand of dV), dS^T -> TMEM over its own dP^T columns (A of
+//               dK) and shared memory (B operand of dQ^T)
+//   warps 16-19 dQ drain: one lane quarter (32 of the 128 d rows of dQ^T) each; TMEM -> smem
+//               staging -> cp.reduce.async.bulk .add.f32 (8 KB per warp and tile)
+//   warp 20     TMA producer (K/V once, Q/dO/LSE/delta ring of 3)
+//   warp 21     TMEM allocator + single-thread tcgen05.mma issuer
+// Shared-memory bandwidth (128 B/clk) is the budget this layout is cut to: the SS GEMMs read
+// 144 KB per 64-row tile, so dK takes dS^T from TMEM rather than smem (a 128-row-tile form with
+// dQ^T aliased over dP^T traced at 4.7k clk per tile against 2.6k of MMA: its smem traffic,
+// 512 KB per tile, set the pace).
 // Per query tile the tensor pipe runs S^T = K Q^T, dP^T = V dO^T (SS, N = 64), dV += P^T dO (TS),
-// dK += dS^T Q (SS), dQ^T = K^T dS^T (SS, MN-major A and B): 5 GEMMs of 128 x 64 x 128.
+// dK += dS^T Q (TS), dQ^T = K^T dS^T (SS, MN-major A and B).
 #pragma once
 #include <cuda.h>
 #include "params.h"
@@ -56,7 +62,10 @@ struct BwdFusedSmem {
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
 
-constexpr int kFusedRowWarps = 8;
+// Row warps: four per TMEM lane quarter, 16 query columns each.
+constexpr int kFusedRowWarps = 16;
+constexpr int kFusedCols = kFusedBM / (kFusedRowWarps / 4);  // query columns per row warp
+static_assert(kFusedCols == 16, "row-warp split");
 constexpr int kFusedThreads = 32 * (kFusedRowWarps + 4 + 2);
 
 // Query-row range [lo, hi) a key tile [k0, k0+128) is visible from (band mask), and whether a
@@ -93,7 +102,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   uint8_t* sQ = smem + L::kQOff;
   uint8_t* sO = smem + L::kOOff;
   uint8_t* sDS = smem + L::kDsOff;
-  float* sStg = reinterpret_cast<float*>(smem + L::kStgOff);
   float* sLse = reinterpret_cast<float*>(smem + L::kLseOff);
   float* sDelta = reinterpret_cast<float*>(smem + L::kDeltaOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -123,7 +131,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
   const int qt_hi = (qhi > qlo) ? (qhi + kFusedBM - 1) / kFusedBM : qt_lo;
   const int tiles_per_head = qt_hi - qt_lo;
   const int niter = tiles_per_head * group;
-  const int q_tiles64 = seq_q_pad / kFusedBM;
 
   constexpr int kRW = kFusedRowWarps, kDrainW0 = kRW, kTmaW = kRW + 4, kMmaW = kRW + 5;
   if (warp == kTmaW && lane_id() == 0) {
@@ -224,9 +231,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                  id_s, kk > 0);
         mma_commit(dp_full);
       };
-      // Pipe order: dV(n) | dP(n+1) dK(n) dQ^T(n) | S^T(n+2).  dP(n+1) goes first once the rows
-      // released dP^T(n) (ds_ready), so their dS(n+1) overlaps dK(n) / dQ^T(n) on the pipe; the
-      // S^T double buffer lets S^T(n+2) follow as soon as dV(n) has read P^T(n).
+      // Pipe order: dV(n) | dK(n) dP(n+1) dQ^T(n) | S^T(n+2).  dP(n+1) follows dK(n) (which reads
+      // dS^T(n) from the dP^T columns) so the rows' dS(n+1) overlaps dQ^T(n); the S^T double
+      // buffer lets S^T(n+2) follow as soon as dV(n) has read P^T(n).
       mbar_wait(kv_full, 0);
       wait_full(0);
       issue_s(0);
@@ -243,18 +250,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kFusedBM / 16; ++kk)
-          mma_ts(tmem + kColDV, tmem + kColS + buf * kFusedBM + 32 * (kk / 2) + 8 * (kk % 2),
+          mma_ts(tmem + kColDV, tmem + kColS + buf * kFusedBM + kFusedCols * kk,
                  make_sdesc(aO + s * L::kOBytes + kk * 16 * 128, kFusedBM * 128, 1024), id_dv,
                  (n > 0 || kk > 0));
         mbar_wait(&ds_ready[buf], ph2);
         tc_fence_after();
-        if (n + 1 < niter) issue_dp(n + 1);  // the rows have read dP^T(n) (before ds_ready)
         const uint32_t ds = aDS + buf * L::kDsBytes;
 #pragma unroll
-        for (int kk = 0; kk < kFusedBM / 16; ++kk)
-          mma_ss(tmem + kColDK, kmajor(ds, kk, kBlockN),
+        for (int kk = 0; kk < kFusedBM / 16; ++kk)  // A = packed dS^T over the dP^T columns
+          mma_ts(tmem + kColDK, tmem + kColDP + kFusedCols * kk,
                  make_sdesc(aQ + s * L::kQBytes + kk * 16 * 128, kFusedBM * 128, 1024), id_dk,
                  (n > 0 || kk > 0));
+        // dP^T(n+1) over dS^T(n): dK(n) reads it ahead on the in-order pipe, and the rows read
+        // dP^T(n) before ds_ready(n)
+        if (n + 1 < niter) issue_dp(n + 1);
         if (n > 0) {
           mbar_wait(dq_free, (n - 1) & 1);  // the drain warps have read dQ^T(n-1)
           tc_fence_after();
@@ -274,10 +283,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       mma_commit(acc_full);
     }
   } else if (warp >= kDrainW0) {
-    // ───────────── dQ drain: TMEM -> smem staging -> L2 reduce-add ─────────────
+    // ───────────── dQ drain: TMEM -> smem staging -> L2 bulk reduce-add ─────────────
+    // (red.global.add.v4.f32 straight from registers measured +3.5 ms over no reduce at cfg2,
+    // the TMA bulk reduce +1 ms: the per-SM reduce bursts queue behind each other in the LSU)
     const int wq = warp % 4;  // TMEM lane quarter = d rows [32 wq, 32 wq + 32)
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    float* stg = sStg + wq * (kFusedBM * 32);
+    const int lane = static_cast<int>(lane_id());
+    float* stg = reinterpret_cast<float*>(smem + L::kStgOff) + wq * (kFusedBM * 32);
+    const int q_tiles64 = seq_q_pad / kFusedBM;
     int hi_ = 0, qt_ = 0;
     for (int n = 0; n < niter; ++n) {
       const int h = hk * group + hi_;
@@ -294,12 +307,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) {
+      if (lane == 0) {
         mbar_arrive(dq_free);
         bulk_wait_read<0>();  // the previous reduce has finished reading the staging slice
       }
       __syncwarp();
-      const int lane = static_cast<int>(lane_id());
 #pragma unroll
       for (int q = 0; q < 32; ++q) stg[q * 32 + lane] = __uint_as_float(r0[q]);
 #pragma unroll
@@ -307,10 +319,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       fence_proxy_async_smem();
       __syncwarp();
 #ifndef AF_FUSED_NO_REDUCE  // developer ablation: drop the L2 reduce (dQ wrong) to time the rest
-      if (lane_id() == 0) {
-#else
-      if (false) {
-#endif
+      if (lane == 0) {
         float* dst = dq_accum +
                      dq_accum_offset(static_cast<int64_t>(b) * p.heads_q + h, q_tiles64, qt, wq, D);
         asm volatile(
@@ -319,17 +328,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
             : "memory");
         bulk_commit();
       }
+#endif
     }
-    if (lane_id() == 0) bulk_wait<0>();
+    if (lane == 0) bulk_wait<0>();
     __syncwarp();
   } else {
     // ───────────── key-row warps ─────────────
+    constexpr int NC = kFusedCols;
     const int wq = warp % 4;
-    const int sub = warp / 4;  // query columns [32 sub, 32 sub + 32) of the 64-row tile
+    const int sub = warp / 4;  // query columns [NC sub, NC sub + NC) of the 64-row tile
     const int row = wq * 32 + static_cast<int>(lane_id());
     const int j = k0 + row;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const int cb = sub * 32;
+    const int cb = sub * NC;
     int hi_ = 0, qt_ = 0;
     for (int n = 0; n < niter; ++n) {
       const int s = n % kStages;
@@ -351,16 +362,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       mbar_wait(&full[s], (n / kStages) & 1);  // LSE / delta of this stage (already complete)
       mbar_wait(&s_full[buf], ph2);
       tc_fence_after();
-      uint32_t pk[16], gk[16];
+      uint32_t pk[NC / 2], gk[NC / 2];
       uint32_t gmask;
       {
-        uint32_t sr[32];
-        tmem_ld32(tmem + lane_base + kColS + buf * kFusedBM + cb, sr);
+        uint32_t sr[NC];
+        tmem_ld16(tmem + lane_base + kColS + buf * kFusedBM + cb, sr);
         tmem_ld_wait();
-        gmask = kv_rows_p32<kFamily, kAct>(p, sr, q0 + cb, j, fullblk, slope, lse_s, pk, gk);
+        gmask = kv_rows_p32<kFamily, kAct, NC>(p, sr, q0 + cb, j, fullblk, slope, lse_s, pk, gk);
       }
-      tmem_st16(tmem + lane_base + kColS + buf * kFusedBM + cb,
-                *reinterpret_cast<uint32_t(*)[16]>(pk));
+      tmem_st8(tmem + lane_base + kColS + buf * kFusedBM + cb, pk);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -368,42 +378,47 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 
       mbar_wait(dp_full, n & 1);
       tc_fence_after();
-      uint32_t dsk[16];
+      uint32_t dsk[NC / 2];
       {
-        uint32_t dr[32];
-        tmem_ld32(tmem + lane_base + kColDP + cb, dr);
+        uint32_t dr[NC];
+        tmem_ld16(tmem + lane_base + kColDP + cb, dr);
         tmem_ld_wait();
-        make_ds<kFamily, kAct, false>(pk, dr, del_s, 0.0f, gmask, dsk, gk);
+        make_ds<kFamily, kAct, false, NC>(pk, dr, del_s, 0.0f, gmask, dsk, gk);
       }
-      // dS^T row (this key, 32 query columns) into the K-major SW128 tile of buffer `buf`
+      // packed dS^T over this warp's own dP^T columns (A operand of dK), and the same 16 query
+      // columns of this key row into the K-major SW128 tile of buffer `buf` (B operand of dQ^T)
+      tmem_st8(tmem + lane_base + kColDP + cb, dsk);
       if (n >= 2) mbar_wait(&ds_free[buf], ph2 ^ 1);
       uint8_t* box = sDS + buf * L::kDsBytes;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < NC / 8; ++q) {
         const int g = cb / 8 + q;
         *reinterpret_cast<uint4*>(box + row * 128 + ((g ^ (row & 7)) << 4)) =
             make_uint4(dsk[q * 4], dsk[q * 4 + 1], dsk[q * 4 + 2], dsk[q * 4 + 3]);
       }
       fence_proxy_async_smem();
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&ds_ready[buf]);
     }
-    // ───────────── epilogue: sub 0 stores dV rows, sub 1 stores dK rows ─────────────
+    // ───────────── epilogue: subs 0-1 store dV rows, subs 2-3 dK rows (half the columns each)
     if (niter > 0) {
       mbar_wait(acc_full, 0);
       tc_fence_after();
     }
     const bool live = j < p.seq_k;
-    const bool is_v = sub == 0;
-    const int ncol = is_v ? DV : D;
-    const uint32_t col0 = is_v ? kColDV : kColDK;
+    const bool is_v = sub < 2;
+    const int part = sub & 1;
+    const int ncol = (is_v ? DV : D) / 2;
+    const uint32_t col0 = (is_v ? kColDV : kColDK) + part * ncol;
     const float mul = is_v ? 1.0f : p.scale;
     __nv_bfloat16* dst =
-        is_v ? reinterpret_cast<__nv_bfloat16*>(p.dv) + b * p.dv_stride_b + hk * p.dv_stride_h +
-                   static_cast<int64_t>(live ? j : 0) * p.dv_stride_s
-             : reinterpret_cast<__nv_bfloat16*>(p.dk) + b * p.dk_stride_b + hk * p.dk_stride_h +
-                   static_cast<int64_t>(live ? j : 0) * p.dk_stride_s;
+        (is_v ? reinterpret_cast<__nv_bfloat16*>(p.dv) + b * p.dv_stride_b + hk * p.dv_stride_h +
+                    static_cast<int64_t>(live ? j : 0) * p.dv_stride_s
+              : reinterpret_cast<__nv_bfloat16*>(p.dk) + b * p.dk_stride_b + hk * p.dk_stride_h +
+                    static_cast<int64_t>(live ? j : 0) * p.dk_stride_s) +
+        part * ncol;
 #pragma unroll 1
     for (int c = 0; c < ncol / 32; ++c) {
       uint32_t r[32];

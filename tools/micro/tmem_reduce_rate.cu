@@ -134,10 +134,11 @@ int main() {
     }
   }
   }
-  for (int threads : {256, 512, 1024}) {
+  for (size_t footprint : {size_t(32) << 20, bytes})
+  for (int threads : {256, 1024}) {
     const int grid = 148 * 2;
     const int it = 2000;
-    const int slices = static_cast<int>(bytes / (size_t(grid) * threads * 16));
+    const int slices = static_cast<int>(footprint / (size_t(grid) * threads * 16));
     red_v4_kernel<<<grid, threads>>>(dst, 10, slices);
     cudaEventRecord(a);
     red_v4_kernel<<<grid, threads>>>(dst, it, slices);
@@ -145,7 +146,8 @@ int main() {
     cudaError_t e = cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
-    printf("red.global.add.v4.f32 %4d thr x 2 CTA/SM: %.0f GB/s (%s)\n", threads,
+    printf("red.global.add.v4.f32 footprint %5zu MB %4d thr x 2 CTA/SM: %.0f GB/s (%s)\n",
+           footprint >> 20, threads,
            double(grid) * it * threads * 16 / (ms * 1e-3) / 1e9, cudaGetErrorString(e));
   }
   return 0;

@@ -65,8 +65,14 @@ def launches(csv_path):
 
 
 if __name__ == "__main__":
+    import os
+    from pathlib import Path
     head = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
                           text=True).stdout.strip()
+    sha_file = Path(__file__).resolve().parents[1] / ".head_sha"  # written before a gpurun call
+    if not head and sha_file.exists():  # (the GPU box's copy of the repo has no .git)
+        head = sha_file.read_text().strip()
+    head = os.environ.get("AF_HEAD", head)
     out = {"head": head}
     for rep in sys.argv[1:]:
         if rep.endswith(".csv"):
