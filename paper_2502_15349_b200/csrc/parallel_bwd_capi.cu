@@ -215,6 +215,12 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
   return dispatch_bwd<64, 64>(a);
 }
 
+#ifdef AF_FUSED_TRACE
+extern "C" int af_debug_fused_trace(void* host) {
+  return static_cast<int>(
+      cudaMemcpyFromSymbol(host, af::g_fused_trace, sizeof(af::g_fused_trace)));
+}
+#endif
 #ifdef AF_BWD_TRACE
 extern "C" int af_debug_bwd_trace(void* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, af::g_bwd_trace, sizeof(af::g_bwd_trace)));

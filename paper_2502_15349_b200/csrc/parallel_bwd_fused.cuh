@@ -37,6 +37,20 @@ namespace af {
 
 constexpr int kFusedBM = 64;  // query rows per iteration
 
+// Developer timeline (-DAF_FUSED_TRACE): SM-clock stamps of one CTA's roles per iteration, read
+// back with af_debug_fused_trace (tools/trace_fused.py).  Compiled out of the product build.
+#ifdef AF_FUSED_TRACE
+__device__ long long g_fused_trace[16][512];
+#define FTRACE(ev, n)                                                                       \
+  do {                                                                                      \
+    if (blockIdx.x == 3 && blockIdx.y == 9 && (n) < 512) g_fused_trace[ev][n] = clock64();  \
+  } while (0)
+#else
+#define FTRACE(ev, n) \
+  do {                \
+  } while (0)
+#endif
+
 template <int D, int DV>
 struct BwdFusedSmem {
   static constexpr int kStages = 3;
@@ -178,6 +192,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           ++hi_;
         }
         mbar_wait(&empty[s], ph ^ 1);
+        FTRACE(12, n);
         mbar_expect_tx(&full[s], L::kQBytes + L::kOBytes + 2 * kFusedBM * 4);
         for (int c = 0; c < D / 64; ++c)
           tma_load_4d_hint(sQ + s * L::kQBytes + c * (kFusedBM * 128), &tm_q, &full[s], c * 64,
@@ -222,6 +237,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           mma_ss(tmem + col, kmajor(aK, kk, kBlockN), kmajor(aQ + s * L::kQBytes, kk, kFusedBM),
                  id_s, kk > 0);
         mma_commit(&s_full[n & 1]);
+        FTRACE(3, n);
       };
       auto issue_dp = [&](int n) {
         const int s = n % kStages;
@@ -230,6 +246,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           mma_ss(tmem + kColDP, kmajor(aV, kk, kBlockN), kmajor(aO + s * L::kOBytes, kk, kFusedBM),
                  id_s, kk > 0);
         mma_commit(dp_full);
+        FTRACE(1, n);
       };
       // Pipe order: dV(n) | dK(n) dP(n+1) dQ^T(n) | S^T(n+2).  dP(n+1) follows dK(n) (which reads
       // dS^T(n) from the dP^T columns) so the rows' dS(n+1) overlaps dQ^T(n); the S^T double
@@ -247,6 +264,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         const int buf = n & 1;
         const uint32_t ph2 = (n >> 1) & 1;
         mbar_wait(&p_ready[buf], ph2);
+        FTRACE(0, n);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kFusedBM / 16; ++kk)
@@ -254,6 +272,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                  make_sdesc(aO + s * L::kOBytes + kk * 16 * 128, kFusedBM * 128, 1024), id_dv,
                  (n > 0 || kk > 0));
         mbar_wait(&ds_ready[buf], ph2);
+        FTRACE(2, n);
         tc_fence_after();
         const uint32_t ds = aDS + buf * L::kDsBytes;
 #pragma unroll
@@ -300,6 +319,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         ++hi_;
       }
       mbar_wait_sleep(dq_full, n & 1);
+      if (lane == 0 && wq == 0) FTRACE(9, n);
       tc_fence_after();
       uint32_t r0[32], r1[32];
       tmem_ld32(tmem + lane_base + kColDQ, r0);
@@ -309,6 +329,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(dq_free);
+        if (wq == 0) FTRACE(10, n);
         bulk_wait_read<0>();  // the previous reduce has finished reading the staging slice
       }
       __syncwarp();
@@ -361,6 +382,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       const float* del_s = sDelta + s * kFusedBM + cb;
       mbar_wait(&full[s], (n / kStages) & 1);  // LSE / delta of this stage (already complete)
       mbar_wait(&s_full[buf], ph2);
+      if (warp == 0 && lane_id() == 0) FTRACE(4, n);
       tc_fence_after();
       uint32_t pk[NC / 2], gk[NC / 2];
       uint32_t gmask;
@@ -375,8 +397,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&p_ready[buf]);
+      if (warp == 0 && lane_id() == 0) FTRACE(5, n);
 
       mbar_wait(dp_full, n & 1);
+      if (warp == 0 && lane_id() == 0) FTRACE(6, n);
       tc_fence_after();
       uint32_t dsk[NC / 2];
       {
@@ -389,6 +413,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       // columns of this key row into the K-major SW128 tile of buffer `buf` (B operand of dQ^T)
       tmem_st8(tmem + lane_base + kColDP + cb, dsk);
       if (n >= 2) mbar_wait(&ds_free[buf], ph2 ^ 1);
+      if (warp == 0 && lane_id() == 0) FTRACE(7, n);
       uint8_t* box = sDS + buf * L::kDsBytes;
 #pragma unroll
       for (int q = 0; q < NC / 8; ++q) {
@@ -401,6 +426,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&ds_ready[buf]);
+      if (warp == 0 && lane_id() == 0) FTRACE(8, n);
     }
     // ───────────── epilogue: subs 0-1 store dV rows, subs 2-3 dK rows (half the columns each)
     if (niter > 0) {

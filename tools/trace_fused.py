@@ -24,11 +24,11 @@ fn = rt.lib().af_debug_fused_trace
 fn.restype = ctypes.c_int
 fn.argtypes = [ctypes.c_void_p]
 assert fn(buf.ctypes.data) == 0
-names = {0: "mma: dV(n) issued", 1: "mma: dP(n) issued", 2: "mma: ds_ready(n) passed",
+names = {0: "mma: p_ready(n) passed", 1: "mma: dP(n) issued", 2: "mma: ds_ready(n) passed",
          3: "mma: S(n) issued", 4: "rows: s_full(n) passed", 5: "rows: p_ready(n) arrived",
-         6: "rows: dp_full(n) passed", 7: "rows: ds_free(n-1) passed", 8: "rows: ds_ready(n) arrived",
-         9: "drain: dq_full(n) passed", 10: "drain: dq_free(n) arrived",
-         11: "drain: 2nd reduce(n) issued", 12: "tma: Q(n) issued", 13: "tma: dO(n) issued"}
+         6: "rows: dp_full(n) passed", 7: "rows: ds_free(n-2) passed",
+         8: "rows: ds_ready(n) arrived", 9: "drain: dq_full(n) passed",
+         10: "drain: dq_free(n) arrived", 12: "tma: Q/dO(n) issued"}
 nk = int((buf[4] > 0).sum())
 ss = range(8, max(9, nk - 8))
 base = buf[4]
