@@ -280,6 +280,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
           mma_ts(tmem + kColDK, tmem + kColDP + kFusedCols * kk,
                  make_sdesc(aQ + s * L::kQBytes + kk * 16 * 128, kFusedBM * 128, 1024), id_dk,
                  (n > 0 || kk > 0));
+        // stage s (Q, dO, LSE, delta of tile n) is free once dK(n) completes — its last reader
+        // (traced: releasing it after dQ^T(n) left S^T(n+2) waiting on its TMA load)
+        mma_commit(&empty[s]);
         // dP^T(n+1) over dS^T(n): dK(n) reads it ahead on the in-order pipe, and the rows read
         // dP^T(n) before ds_ready(n)
         if (n + 1 < niter) issue_dp(n + 1);
@@ -293,7 +296,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                  make_sdesc(ds + kk * 16 * 128, kBlockN * 128, 1024), id_dq, kk > 0);
         mma_commit(dq_full);
         mma_commit(&ds_free[buf]);
-        mma_commit(&empty[s]);
         if (n + 2 < niter) {  // into buffer `buf`: P^T(n) was consumed by dV(n) above
           wait_full(n + 2);
           issue_s(n + 2);
