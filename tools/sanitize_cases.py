@@ -12,18 +12,20 @@ from paper_2502_15349_b200 import configs  # noqa: E402
 
 dev = torch.device("cuda")
 cases = {
-    "K1/K2 softmax GQA causal": configs.cfg2(batch=1, heads=4, heads_kv=2, seq=384),
+    "K1/K2f softmax GQA causal": configs.cfg2(batch=1, heads=4, heads_kv=2, seq=384),
     "K1/K2 sigmoid relpos SWA": configs.cfg3(batch=1, heads=2, seq=512, window=200),
     "K3/K3b MLA prefill": configs.cfg4a(heads=2, seq=256),
     "K3 MLA decode": configs.cfg4b(batch=2, seq_k=1024),
     "K4/K5 RetNet 256": configs.cfg5a(batch=1, heads=1, seq=300),
     "K4/K5 Mamba2 128": configs.cfg5b(batch=1, heads=2, seq=300),
     "materialised tier (256/512)": af.builtin("retention-parallel", batch=1, heads=1, seq=64),
+    "K2a/K2b split (deterministic) backward": configs.cfg2(batch=1, heads=4, heads_kv=2, seq=384),
 }
 only = sys.argv[1:]  # case indices (default: all)
 for idx, (name, spec) in enumerate(cases.items()):
     if only and str(idx) not in only:
         continue
+    af.api.use_deterministic_backward(name.startswith("K2a/K2b"))
     arrays, dout = bench.device_inputs(spec, dev, 0)
     if spec.pattern.value == "parallel":
         o, lse = af.parallel_forward(spec, arrays)
