@@ -2,6 +2,7 @@
 // three runs of the same chunked kernel plus the per-step gradient scan for the decay factors.
 #include "host_common.h"
 #include "linear_chunk.cuh"
+#include "linear_wide.cuh"
 
 namespace af {
 namespace {
@@ -47,6 +48,8 @@ struct LaArgs {
   bool reverse;
   float* final_state = nullptr;
   ScanBufs scan{};
+  const void* dot2_x = nullptr;  // second dot (same strides as dot_x)
+  float* dot2 = nullptr;
 };
 
 StepTensor step_tensor(const float* ptr, const int64_t* st) {
@@ -100,6 +103,8 @@ int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
     p.x_ss = a.x_st[2];
   }
   p.dot = a.dot;
+  p.dot2_x = a.dot2_x;
+  p.dot2 = a.dot2;
   p.final_state = a.final_state;
   p.lcum = a.scan.lcum;
   p.ucum = a.u_gate ? a.scan.ucum : nullptr;  // the pass's own key/value-side scale
@@ -113,7 +118,55 @@ int launch_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
   return AF_OK;
 }
 
+// Dk = Dv = 128: one CTA per (b, h) over the whole value dimension (linear_wide.cuh).
+#ifndef AF_LIN_WIDE
+#define AF_LIN_WIDE 1
+#endif
+template <bool kRev>
+int launch_wide(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
+  using L = LinWideSmem;
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_4d(&tq, a.q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.dqk, d->seq, d->heads,
+                    d->batch, a.q_st, 64, kLinChunk, true) ||
+      !make_tmap_4d(&tk, a.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.dqk, d->seq, d->heads,
+                    d->batch, a.k_st, 64, kLinChunk, true) ||
+      !make_tmap_4d(&tv, a.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.dvv, d->seq, d->heads,
+                    d->batch, a.v_st, 64, kLinChunk, true))
+    return AF_ERR_INPUT;
+  LinearParams p = base_params(d);
+  p.dqk = a.dqk;
+  p.dv = a.dvv;
+  p.out_scale = a.out_scale;
+  if (a.u_gate) p.u_scale = step_tensor(d->key_gate, d->key_gate_stride);
+  if (a.row_gate) p.o_rowscale = step_tensor(d->key_gate, d->key_gate_stride);
+  p.o = a.o;
+  p.o_sb = a.o_st[0];
+  p.o_sh = a.o_st[1];
+  p.o_ss = a.o_st[2];
+  p.dot_x = a.dot_x;
+  if (a.dot_x != nullptr) {
+    p.x_sb = a.x_st[0];
+    p.x_sh = a.x_st[1];
+    p.x_ss = a.x_st[2];
+  }
+  p.dot = a.dot;
+  p.dot2_x = a.dot2_x;
+  p.dot2 = a.dot2;
+  p.final_state = a.final_state;
+  p.lcum = a.scan.lcum;
+  p.ucum = a.u_gate ? a.scan.ucum : nullptr;
+  p.cflag = a.scan.cflag;
+  auto kern = linear_wide_kernel<kRev>;
+  AF_SMEM_ATTR(kern, L::kTotal);
+  ::af::note_launch();
+  kern<<<d->batch * d->heads, kLinWideThreads, L::kTotal, s>>>(tq, tk, tv, p);
+  AF_CUDA_CHECK(cudaGetLastError());
+  return AF_OK;
+}
+
 int run_la(const af_linear_desc* d, const LaArgs& a, cudaStream_t s) {
+  if (AF_LIN_WIDE && a.dqk == 128 && a.dvv == 128)
+    return a.reverse ? launch_wide<true>(d, a, s) : launch_wide<false>(d, a, s);
   if (a.dvv % kLinVB != 0) {
     set_error("linear template: value dim %d is not a multiple of %d", a.dvv, kLinVB);
     return AF_ERR_UNSUPPORTED;
@@ -177,8 +230,9 @@ extern "C" size_t af_linear_bwd_workspace(const af_linear_desc* d) {
   if (d == nullptr) return 0;
   const size_t rows = static_cast<size_t>(d->batch) * d->heads * d->seq;
   const size_t slots = static_cast<size_t>(d->d_k) / 32;  // dot partials per 32-column slot
-  // dot partials, then d log a and dk_dot per step; the bf16 Km copy starts 256-byte aligned
-  size_t bytes = (rows * (2 * slots + 2) * sizeof(float) + 255) / 256 * 256;
+  // dot partials (q.dQm, Km.dKm, raw k.dKm), then d log a and dk_dot per step; the bf16 Km copy
+  // starts 256-byte aligned
+  size_t bytes = (rows * (3 * slots + 2) * sizeof(float) + 255) / 256 * 256;
   if (d->key_gate != nullptr) bytes += rows * static_cast<size_t>(d->d_k) * 2;  // bf16 Km
   bytes = (bytes + 255) / 256 * 256;
   return bytes + af::scan_bytes(d);
@@ -197,7 +251,8 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
   const int slots = d->d_k / 32;
   float* dq_dot = static_cast<float*>(workspace);
   float* dk_dot = dq_dot + n * slots;
-  float* step_dloga = dk_dot + n * slots;
+  float* kdot_raw = dk_dot + n * slots;
+  float* step_dloga = kdot_raw + n * slots;
   float* step_dkdot = step_dloga + n;
   // (every dot partial slot of every live step is stored exactly once: no clearing needed)
   // Gated keys, materialised once (see gate_keys_kernel)
@@ -208,7 +263,7 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
   if (d->key_gate != nullptr) {
     __nv_bfloat16* kmb = reinterpret_cast<__nv_bfloat16*>(
         static_cast<char*>(workspace) +
-        (static_cast<size_t>(n) * (2 * slots + 2) * sizeof(float) + 255) / 256 * 256);
+        (static_cast<size_t>(n) * (3 * slots + 2) * sizeof(float) + 255) / 256 * 256);
     const int64_t thr = n * (d->d_k / 8);
     ::af::note_launch();
     gate_keys_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, s>>>(
@@ -218,7 +273,7 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
     km = kmb;
     km_st = km_contig;
   }
-  size_t scan_off = (static_cast<size_t>(n) * (2 * slots + 2) * sizeof(float) + 255) / 256 * 256;
+  size_t scan_off = (static_cast<size_t>(n) * (3 * slots + 2) * sizeof(float) + 255) / 256 * 256;
   if (d->key_gate != nullptr)
     scan_off = (scan_off + static_cast<size_t>(n) * d->d_k * 2 + 255) / 256 * 256;
   const ScanBufs sb = scan_layout(d, static_cast<char*>(workspace) + scan_off);
@@ -234,10 +289,25 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
             d->q_scale, false, false, want_dots ? q : nullptr, d->q_stride, dq_dot, false, nullptr,
             sb};
   if ((st = run_la(d, a1, s)) != AF_OK) return st;
-  // dKm = q_scale * LA_rev(q=V, k=dO, v=Q); dk = gate*dKm   dk_dot = k . dKm (raw keys)
+  // dKm = q_scale * LA_rev(q=V, k=dO, v=Q); dk = gate*dKm   dk_dot = Km . dKm, and with a gate
+  // gradient requested kdot_raw = k . dKm (raw keys; Km shares k's layout when materialised)
   LaArgs a2{v, dout, q, d->v_stride, d->o_stride, d->q_stride, d->d_v, d->d_k, dk, d->k_stride,
-            d->q_scale, false, true, want_dots ? k : nullptr, d->k_stride, dk_dot, true, nullptr,
-            sb};
+            d->q_scale, false, true, want_dots ? km : nullptr, km_st, dk_dot, true, nullptr, sb};
+  // A pure key gate's gradient is k . dKm over the raw keys (a second dot in this pass; finite at
+  // gate = 0).  A gate that is also a decay factor (Mamba2's dt) takes Km . dKm / gate instead:
+  // its decay part d log a / gate has no finite value at 0 either way, and the division path
+  // saves re-reading k.
+  bool gate_is_factor = false;
+  for (int f = 0; f < d->n_decay_factors; ++f)
+    gate_is_factor |= d->decay_factor[f] == d->key_gate;
+  const bool raw_gate_dot = d_key_gate != nullptr && !gate_is_factor;
+  if (raw_gate_dot) {
+    AF_REQUIRE(km_st[0] == d->k_stride[0] && km_st[1] == d->k_stride[1] &&
+                   km_st[2] == d->k_stride[2],
+               AF_ERR_INPUT, "gate gradient needs contiguous keys");
+    a2.dot2_x = k;
+    a2.dot2 = kdot_raw;
+  }
   if ((st = run_la(d, a2, s)) != AF_OK) return st;
   // dV = q_scale * LA_rev(q=Km, k=Q, v=dO)
   LaArgs a3{km, q, dout, km_st, d->q_stride, d->o_stride, d->d_k, d->d_v, dv, d->v_stride,
@@ -250,7 +320,8 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
       AF_REQUIRE(d->key_gate != nullptr, AF_ERR_INPUT, "d_key_gate without a key gate");
     ::af::note_launch();
     linear_step_grads_kernel<<<d->batch * d->heads, 256, 0, s>>>(
-        dq_dot, dk_dot, slots, p, step_dloga, d_key_gate != nullptr ? step_dkdot : nullptr);
+        dq_dot, dk_dot, raw_gate_dot ? kdot_raw : nullptr, slots, p, step_dloga,
+        d_key_gate != nullptr ? step_dkdot : nullptr);
     AF_CUDA_CHECK(cudaGetLastError());
     auto reduce = [&](const float* val, StepTensor div, StepTensor out) -> int {
       const int nb = out.sb == 0 ? 1 : d->batch, nh = out.sh == 0 ? 1 : d->heads;
@@ -267,7 +338,7 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
                          step_tensor(d_decay_factor[f], d->decay_factor_stride[f]))) != AF_OK)
           return st;
     if (d_key_gate != nullptr)
-      if ((st = reduce(step_dkdot, StepTensor{nullptr, 0, 0, 0},
+      if ((st = reduce(step_dkdot, raw_gate_dot ? StepTensor{nullptr, 0, 0, 0} : p.u_scale,
                        step_tensor(d_key_gate, d->key_gate_stride))) !=
           AF_OK)
         return st;

@@ -77,6 +77,8 @@ struct LinearParams {
   const void* dot_x;    // optional bf16 X with element strides: dot[t] += X_t . o_t
   int64_t x_sb, x_sh, x_ss;
   float* final_state;   // optional fp32 [B, H, dqk, dv]: the state after the last token (forward)
+  const void* dot2_x;   // optional second X (same strides as dot_x): dot2[t] = X2_t . o_t — the
+  float* dot2;          // backward's raw-key dot of the gate gradient (same slot layout as dot)
   float* dot;           // [dv/32 slots][B, H, S] fp32: one partial per 32-column slot, summed
                         // in slot order by linear_step_grads_kernel (deterministic)
   // the decay scan of linear_decay_scan_kernel, [B*H][nchunks][128] (padded tail: a = 1, u = 1)
@@ -516,8 +518,25 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
                           bf16_hi_(xe[q2]) * ov[v * 8 + 2 * q2 + 1];
             }
             const int64_t rows = static_cast<int64_t>(p.batch) * p.heads * p.seq;
-            p.dot[(vb * 2 + half) * rows + (static_cast<int64_t>(b) * p.heads + h) * p.seq + t] =
-                dotacc;
+            const int64_t at =
+                (vb * 2 + half) * rows + (static_cast<int64_t>(b) * p.heads + h) * p.seq + t;
+            p.dot[at] = dotacc;
+            if (p.dot2_x != nullptr) {
+              const uint4* y4 = reinterpret_cast<const uint4*>(
+                  reinterpret_cast<const __nv_bfloat16*>(p.dot2_x) + b * p.x_sb + h * p.x_sh +
+                  static_cast<int64_t>(t) * p.x_ss + col0);
+              float acc2 = 0.0f;
+#pragma unroll
+              for (int v = 0; v < 4; ++v) {
+                const uint4 yv = y4[v];
+                const uint32_t* ye = reinterpret_cast<const uint32_t*>(&yv);
+#pragma unroll
+                for (int q2 = 0; q2 < 4; ++q2)
+                  acc2 += bf16_lo_(ye[q2]) * ov[v * 8 + 2 * q2] +
+                          bf16_hi_(ye[q2]) * ov[v * 8 + 2 * q2 + 1];
+              }
+              p.dot2[at] = acc2;
+            }
           }
         }
       }
@@ -714,14 +733,19 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
   }
 }
 
-// Per-step gradients (SURVEY A.4 restated):  d log a_t = sum_{s>=t} (dq_dot_s - u_s kdot_s)
-// where dq_dot = Qm . dQm and kdot = k . dKm over the raw (un-gated) keys, u the key gate
-// (Km . dKm = u k . dKm).  One block per (b, h) sequence writes d log a_t and kdot_t (both
-// [B, H, S] fp32); step_grad_reduce_kernel then forms d fac_f = d log a / fac_f and
-// d gate = kdot (k_mod = k * gate: dL/dgate = k . dKm, no division — finite at gate = 0) and sums
-// broadcast axes in a fixed order — no atomics, bitwise deterministic.
+// Per-step gradients (SURVEY A.4 restated):  d log a_t = sum_{s>=t} (dq_dot_s - dk_dot_s)
+// where dq_dot = Qm . dQm, dk_dot = Km . dKm over the same bf16 gated keys the passes used (the
+// two sums nearly cancel; a dot over u k instead of bf16(u k) measured 5 % off the oracle), and
+// kdot_raw = k . dKm over the raw keys (when the key gate is not also a decay factor).  One block
+// per (b, h) sequence writes d log a_t and the gate's dot (both [B, H, S] fp32);
+// step_grad_reduce_kernel then forms d fac_f = d log a / fac_f and d gate = kdot_raw (k_mod =
+// k * gate: dL/dgate = k . dKm, no division — finite at gate = 0; else dk_dot / gate) and sums
+// broadcast axes in a fixed order — no atomics, bitwise deterministic.  A decay factor of exactly
+// 0 gives a non-finite d fac at that step (d log a / 0; the unrolled reference differentiates
+// the product itself).
 __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
-                                         const float* __restrict__ dk_dot, int slots,
+                                         const float* __restrict__ dk_dot,
+                                         const float* __restrict__ kdot_raw, int slots,
                                          LinearParams p, float* __restrict__ dloga_out,
                                          float* __restrict__ dkdot_out) {
   __shared__ float part[32];
@@ -735,11 +759,7 @@ __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
     for (int sl = 0; sl < slots; ++sl) a += x[sl * rows + base + t];
     return a;
   };
-  const int b = bh / p.heads, h = bh % p.heads;
-  auto val = [&](int t) {
-    const float u = p.u_scale.ptr != nullptr ? p.u_scale.at(b, h, t) : 1.0f;
-    return dot(dq_dot, t) - u * dot(dk_dot, t);
-  };
+  auto val = [&](int t) { return dot(dq_dot, t) - dot(dk_dot, t); };
   const int per = (seq + blockDim.x - 1) / blockDim.x;
   const int t0 = threadIdx.x * per;
   const int t1 = min(seq, t0 + per);
@@ -759,7 +779,7 @@ __global__ void linear_step_grads_kernel(const float* __restrict__ dq_dot,
   for (int t = t1 - 1; t >= t0; --t) {
     acc += val(t);
     dloga_out[base + t] = acc;
-    if (dkdot_out != nullptr) dkdot_out[base + t] = dot(dk_dot, t);
+    if (dkdot_out != nullptr) dkdot_out[base + t] = dot(kdot_raw != nullptr ? kdot_raw : dk_dot, t);
   }
 }
 

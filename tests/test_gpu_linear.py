@@ -164,11 +164,18 @@ def test_zero_decay_factor_resets_the_state_exactly():
 
 
 def test_zero_key_gate_has_finite_gradient():
-    """k_mod = k * gate with gate = 0 on some steps (padding masked through the gate): the gate
-    gradient is k . dKm from the raw keys — finite and equal to the oracle's — not dk_dot / gate."""
-    from dataclasses import replace as dreplace
-    base = S.builtin("gated-retention", batch=1, heads=2, seq=300, d_qk=128, d_v=128)
-    spec = dreplace(base, extra_inputs=(dreplace(base.extra_inputs[0], differentiable=True),))
+    """k_mod = k * gate with gate = 0 on some steps (padding masked through a pure key gate): the
+    gate gradient is k . dKm from the raw keys — finite and equal to the oracle's — not
+    dk_dot / gate.  A differentiable decay factor that is exactly 0 yields a non-finite gradient
+    at that step only (d log a / a); every other gradient stays finite and correct."""
+    doc = {"name": "key-gated-retention", "pattern": "recurrent",
+           "dims": {"batch": 1, "heads": 2, "seq_q": 300, "seq_k": 300, "dqk": 128, "dv": 128},
+           "q_mod": "q / sqrt(dimqk)", "k_mod": "k * gate", "h_mod": "h * decay",
+           "extras": [{"name": "gate", "shape": ["batch", "heads", "seq_k", 1], "fill": "unit",
+                       "differentiable": True},
+                      {"name": "decay", "shape": ["batch", "heads", "seq_k", 1], "fill": "unit",
+                       "differentiable": True}]}
+    spec = S.spec_from_dict(doc)
     arrays = oracle.generate(spec, seed=6)
     arrays["gate"][:, :, [0, 1, 64, 200, 299]] = 0.0
     dev = to_dev(arrays)
@@ -176,6 +183,11 @@ def test_zero_key_gate_has_finite_gradient():
     g = af.linear_backward(spec, dev, dout)
     assert bool(torch.isfinite(g["gate"]).all())
     want = OR.chunk_vjp(spec, rounded(arrays), dout.double().cpu().numpy(), chunk=64)
-    assert nw(g["gate"].double().cpu().numpy(), want["gate"]) <= 2e-2
-    for n in ("q", "k", "v"):
+    for n in ("gate", "decay", "q", "k", "v"):
         assert nw(g[n].double().cpu().numpy(), want[n]) <= 2e-2, n
+    arrays["decay"][:, :, 7] = 0.0
+    g = af.linear_backward(spec, to_dev(arrays), dout)
+    bad = ~torch.isfinite(g["decay"]).cpu().numpy()[0, :, :, 0]
+    assert bad[:, 7].all() and bad.sum() == 2
+    for n in ("gate", "q", "k", "v"):  # (the f64 oracle's log-space VJP is NaN here too)
+        assert bool(torch.isfinite(g[n]).all()), n

@@ -36,6 +36,12 @@ names = {15: "scan: scan_ready arrive", 14: "rows: scan_ready passed", 4: "rows:
          3: "mma: vw+h_scaled", 2: "mma: p_ready+vfull", 9: "out: oi_full passed",
          10: "out: O written", 16: "prod: scan_free passed", 17: "prod: raw landed",
          18: "rows: scan stored", 19: "rows: row factors done"}
+if len(sys.argv) > 3 and sys.argv[3] == "wide":  # linear_wide_kernel event map
+    names = {15: "prod: empty passed", 14: "rows: full passed", 0: "mma: full (S issued)",
+             1: "mma: hb_ready (QH issued)", 3: "mma: pk+h_scaled (H upd)",
+             2: "mma: o_scaled (OI)", 7: "rows: s_full passed", 8: "rows: P+Kw done",
+             11: "rows: qh_full passed", 12: "rows: O scaled", 9: "out: oi_full passed",
+             10: "out: O written", 16: "state: h_full passed", 17: "state: Hb + H*g done"}
 ss = range(8, 56)
 base = buf[14]
 period = np.mean([buf[14, n + 1] - buf[14, n] for n in ss])
