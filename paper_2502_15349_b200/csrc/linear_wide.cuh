@@ -39,9 +39,9 @@ struct LinWideSmem {
   static constexpr int kLOff = kHbOff + kTile;                 // [2][128] in-chunk cumsum log2 a
   static constexpr int kUOff = kLOff + kStages * kLinChunk * 4;  // [2][128] key-side scale
   static constexpr int kBarOff = kUOff + kStages * kLinChunk * 4;
-  // full[2], empty[2], s_full, qh_full, pk_ready, o_scaled, h_full, hb_ready, h_scaled,
-  // oi_full[2], o_empty[2]
-  static constexpr int kNumBars = 2 * kStages + 7 + 4;
+  // full[2] (Q + scan arrays), empty[2] (Q), kfull[2], kempty[2], vfull[2], vempty[2], s_full,
+  // qh_full, pk_ready, o_scaled, h_full, hb_ready, h_scaled, oi_full[2], o_empty[2]
+  static constexpr int kNumBars = 6 * kStages + 7 + 4;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -63,9 +63,17 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
   float* sL = reinterpret_cast<float*>(smem + L::kLOff);
   float* sU = reinterpret_cast<float*>(smem + L::kUOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-  uint64_t* full = bars;
+  // Q, K and V rings with their own barriers, each slot released by its last reader (Q after
+  // Q Hb, K after the state update, V after P V) so the next loads start as early as possible
+  // (the kernel streams 128 KB per chunk and SM; one shared slot release after P V left the loads
+  // a chunk period behind)
+  uint64_t* full = bars;            // Q + the chunk's scan arrays
   uint64_t* empty = full + kSt;
-  uint64_t* s_full = empty + kSt;
+  uint64_t* kfull = empty + kSt;
+  uint64_t* kempty = kfull + kSt;
+  uint64_t* vfull = kempty + kSt;
+  uint64_t* vempty = vfull + kSt;
+  uint64_t* s_full = vempty + kSt;
   uint64_t* qh_full = s_full + 1;
   uint64_t* pk_ready = qh_full + 1;   // P in TMEM and Kw in smem (8 row warps)
   uint64_t* o_scaled = pk_ready + 1;  // Q Hb rows scaled by cp (8 row warps)
@@ -87,6 +95,10 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
     for (int s = 0; s < kSt; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+      mbar_init(&vfull[s], 1);
+      mbar_init(&vempty[s], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(qh_full, 1);
@@ -116,19 +128,15 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
         const int s = n % kSt;
         const int c = chunk_of(n);
         const int t0 = c * kLinChunk;
-        mbar_wait(&empty[s], ((n / kSt) & 1) ^ 1);
+        const uint32_t ph = ((n / kSt) & 1) ^ 1;
+        mbar_wait(&empty[s], ph);
         AF_LT(15, n);
         const int64_t g = (static_cast<int64_t>(bh) * nchunks + c) * kLinChunk;
         const uint32_t scan_bytes = kLinChunk * 4 * (p.ucum != nullptr ? 2 : 1);
-        mbar_expect_tx(&full[s], 3 * L::kTile + scan_bytes);
-        for (int x = 0; x < 2; ++x) {
+        mbar_expect_tx(&full[s], L::kTile + scan_bytes);
+        for (int x = 0; x < 2; ++x)
           tma_load_4d(sQ + s * L::kTile + x * (kLinChunk * 128), &tm_q, &full[s], x * 64, t0, h,
                       b);
-          tma_load_4d(sK + s * L::kTile + x * (kLinChunk * 128), &tm_k, &full[s], x * 64, t0, h,
-                      b);
-          tma_load_4d(sV + s * L::kTile + x * (kLinChunk * 128), &tm_v, &full[s], x * 64, t0, h,
-                      b);
-        }
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
             "[%3];" ::"r"(smem_u32(sL + s * kLinChunk)),
@@ -140,6 +148,16 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
               "[%3];" ::"r"(smem_u32(sU + s * kLinChunk)),
               "l"(p.ucum + g), "r"(kLinChunk * 4), "r"(smem_u32(&full[s]))
               : "memory");
+        mbar_wait(&kempty[s], ph);
+        mbar_expect_tx(&kfull[s], L::kTile);
+        for (int x = 0; x < 2; ++x)
+          tma_load_4d(sK + s * L::kTile + x * (kLinChunk * 128), &tm_k, &kfull[s], x * 64, t0, h,
+                      b);
+        mbar_wait(&vempty[s], ph);
+        mbar_expect_tx(&vfull[s], L::kTile);
+        for (int x = 0; x < 2; ++x)
+          tma_load_4d(sV + s * L::kTile + x * (kLinChunk * 128), &tm_v, &vfull[s], x * 64, t0, h,
+                      b);
       }
     }
   } else if (warp == kMmaW) {
@@ -159,6 +177,7 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
         const uint32_t qa = aQ + s * L::kTile, ka = aK + s * L::kTile, va = aV + s * L::kTile;
         const uint32_t o_tmem = tmem + kColO + ob * 128;
         mbar_wait(&full[s], (n / kSt) & 1);
+        mbar_wait(&kfull[s], (n / kSt) & 1);
         AF_LT(0, n);
         tc_fence_after();
 #pragma unroll
@@ -178,7 +197,10 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
         // state update once the row warps have scaled K by w (after S read it) and the state
         // warps have scaled H by this chunk's g
         mbar_wait(pk_ready, n & 1);
+        // Q (read by S and Q Hb, already issued) and the scan arrays (the row warps are past P)
+        mma_commit(&empty[s]);
         if (n > 0) mbar_wait(h_scaled, (n - 1) & 1);
+        mbar_wait(&vfull[s], (n / kSt) & 1);
         AF_LT(3, n);
         tc_fence_after();
 #pragma unroll
@@ -186,6 +208,7 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
           mma_ss(tmem + kColH, make_sdesc(ka + kk * 2048, kLinChunk * 128, 1024),
                  make_sdesc(va + kk * 2048, kLinChunk * 128, 1024), id_h, (n > 0 || kk > 0));
         mma_commit(h_full);
+        mma_commit(&kempty[s]);  // Kw: last read by the state update
         if (n > 0) {
           mbar_wait(o_scaled, (n - 1) & 1);
           tc_fence_after();
@@ -196,7 +219,7 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
           mma_ts(o_tmem, tmem + kColS + split_col_lin(kk),
                  make_sdesc(va + kk * 2048, kLinChunk * 128, 1024), id_oi, (n > 0 || kk > 0));
         mma_commit(&oi_full[ob]);
-        mma_commit(&empty[s]);  // Q, K, V of this chunk: last read by P V
+        mma_commit(&vempty[s]);  // V: last read by P V
       }
     }
   } else if (warp >= 12) {
