@@ -59,14 +59,16 @@ constexpr int kMlaHalf = 256;
 #ifndef AF_MLA_PREFILL_N
 #define AF_MLA_PREFILL_N 32  // swept after the branch-free softmax: 32 beats 64 by ~9 %
 #endif
+#ifndef AF_MLA_DECODE_N
+#define AF_MLA_DECODE_N 32
+#endif
 template <bool kDecode>
 struct MlaTile {
-  static constexpr int kN = kDecode ? 32 : AF_MLA_PREFILL_N;
-  static constexpr int kStages = kDecode ? 4 : (AF_MLA_PREFILL_N == 32 ? 4 : 2);
-  // Q columns [0, kQT) held in TMEM as TS-MMA A operand; decode's 32-key S double buffer leaves
-  // TMEM columns [64, 128) free for Q columns [256, 384), so fewer S MMAs stream Q from smem
-  static constexpr int kQT = kDecode ? AF_MLA_DECODE_QT
-                                     : (AF_MLA_PREFILL_N == 32 ? AF_MLA_PREFILL_QT : 256);
+  static constexpr int kN = kDecode ? AF_MLA_DECODE_N : AF_MLA_PREFILL_N;
+  static constexpr int kStages = kN == 32 ? 4 : 2;
+  // Q columns [0, kQT) held in TMEM as TS-MMA A operand; a 32-key S double buffer leaves TMEM
+  // columns [64, 128) free for Q columns [256, 384), so fewer S MMAs stream Q from smem
+  static constexpr int kQT = kN == 32 ? (kDecode ? AF_MLA_DECODE_QT : AF_MLA_PREFILL_QT) : 256;
 };
 constexpr int kMlaN = 64;     // prefill tile (split lengths of decode are multiples of both)
 
