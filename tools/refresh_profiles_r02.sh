@@ -16,7 +16,7 @@ fi
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $O/launches_${TAG}_cfg2.csv python bench.py --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
 for c in $CONFIGS; do
-  timeout 1200 ncu --set full --clock-control none -k regex:'af::' -o $R/prof_${c}_${TAG} -f \
+  timeout 1200 ncu --set full --clock-control none --kernel-name-base demangled -k regex:'af::' -o $R/prof_${c}_${TAG} -f \
     python tools/run_step_once.py $c > /dev/null 2>&1
   python tools/ncu_summary.py $R/prof_${c}_${TAG}.ncu-rep > $O/ncu_summary_${TAG}_${c}.json
 done
