@@ -319,7 +319,7 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
     if (d_key_gate != nullptr)
       AF_REQUIRE(d->key_gate != nullptr, AF_ERR_INPUT, "d_key_gate without a key gate");
     ::af::note_launch();
-    linear_step_grads_kernel<<<d->batch * d->heads, 256, 0, s>>>(
+    linear_step_grads_kernel<<<d->batch * d->heads, kStepGradThreads, 0, s>>>(
         dq_dot, dk_dot, raw_gate_dot ? kdot_raw : nullptr, slots, p, step_dloga,
         d_key_gate != nullptr ? step_dkdot : nullptr);
     AF_CUDA_CHECK(cudaGetLastError());
