@@ -21,14 +21,19 @@ for cfg in ("cfg1", "cfg2", "cfg3", "cfg4a", "cfg4b", "cfg5a", "cfg5b"):
     per, fwd, bwd = {}, 0.0, 0.0
     linear = cfg.startswith("cfg5")
     seen_chunk = 0
-    recs = [r for r in recs if "af::" in r["kernel"]]  # the library's kernels only
+    # the library's kernels only (the captures filter on the demangled "af::" name; the summary
+    # keeps ncu's function base name)
+    recs = [r for r in recs if "at::" not in r["kernel"] and "elementwise" not in r["kernel"]]
     for i, r in enumerate(recs):
         name = r["kernel"].split("(")[0].replace("void ", "").replace("af::", "")
+        name = name.split("<")[0].split("::")[-1] + ("<" + name.split("<", 1)[1] if "<" in name
+                                                        and "unnamed>" not in name else "")
         nbytes = r.get("dram_read_bytes", 0.0) + r.get("dram_write_bytes", 0.0)
         per[f"{name}#{i}"] = nbytes
         if linear:  # launch order: scan, forward chunk kernel | backward passes
-            is_fwd = seen_chunk == 0 and ("decay_scan" in name or "linear_chunk" in name)
-            if "linear_chunk" in name:
+            chunk = "linear_chunk" in name or "linear_wide" in name
+            is_fwd = seen_chunk == 0 and ("decay_scan" in name or chunk)
+            if chunk:
                 seen_chunk += 1
         else:
             is_fwd = name.startswith(FWD)
