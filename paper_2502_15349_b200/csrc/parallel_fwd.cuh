@@ -42,6 +42,9 @@ __device__ unsigned long long g_fwd_trace[9 * 64 * 6 + 1];
 #ifndef AF_FWD_EARLY_P
 #define AF_FWD_EARLY_P 1
 #endif
+#ifndef AF_SIGMOID_TANH
+#define AF_SIGMOID_TANH 1
+#endif
 #ifndef AF_EXP2_POLY_MASK
 #define AF_EXP2_POLY_MASK 14  // column pairs with (c & mask) == 0 use exp2_poly: 14 -> 12.5 %
 #endif
@@ -121,11 +124,19 @@ AF_DEVICE bool kept(const MaskParams& m, int i, int j, int seq_k) {
 template <int kAct>
 AF_DEVICE float apply_act(float z) {
   if constexpr (kAct == kActSigmoid) {
+#if AF_SIGMOID_TANH
+    // sigma(z) = 1/2 + tanh(z / 2) / 2: one MUFU op (tanh.approx, max rel. error ~2^-11, below
+    // bf16's 2^-8) and one FFMA — the 1 / (1 + 2^(-z log2 e)) form below spends the MUFU op on
+    // ex2 and ~7 FMA-pipe instructions on its reciprocal, and the sigmoid row epilogues are
+    // issue-bound (cfg3 K2f: P took 2.2k of a 3.7k-clk iteration).
+    return fmaf(0.5f, tanh_approx(0.5f * z), 0.5f);
+#else
     // 1 / (1 + 2^(-z log2 e)): one MUFU op (ex2) and the reciprocal on the FMA pipe (rcp_nr) —
     // with rcp.approx as well the sigmoid row epilogue issued two MUFU ops per score, twice the
     // tensor pipe's time per block (16 MUFU lanes / clk / SM); __frcp_rn's IEEE fix-up path is
     // ~10x slower still.  -z log2 e is clamped at 126 so 1 + e stays in rcp_nr's range.
     return rcp_nr(1.0f + ex2(fminf(-z * kLog2e, 126.0f)));
+#endif
   } else if constexpr (kAct == kActRelu) {
     return fmaxf(z, 0.0f);
   } else if constexpr (kAct == kActRelu2) {
