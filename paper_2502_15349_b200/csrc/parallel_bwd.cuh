@@ -232,7 +232,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t* sr, i
         pk[e / 2] = pack_bf16(apply_act<kAct>(z0), apply_act<kAct>(z1));
       }
     } else {
-#pragma unroll 2
+#pragma unroll  // fully: a partial unroll indexed pk through local memory
       for (int e = 0; e < NC; e += 2) {
         float pv[2];
 #pragma unroll
@@ -485,6 +485,8 @@ __global__ void __launch_bounds__(kKvThreads, 1)
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const int cb = sub * kCpw;
     const uint32_t pcol = cb;
+    int slope_h = -1;
+    float slope = 0.0f;
     int hi_ = 0, qt_ = 0;
     for (int n = 0; n < niter; ++n) {
       const int s = n % kStages;
@@ -495,9 +497,11 @@ __global__ void __launch_bounds__(kKvThreads, 1)
         ++hi_;
       }
       const bool fullblk = tile_fully_kept(p.mask, q0, k0, p.seq_q, p.seq_k);
-      float slope = 0.0f;
-      if constexpr (kFamily != kFamilySoftmax) {
-        if (p.slope != nullptr) slope = p.slope[h];
+      if constexpr (kFamily != kFamilySoftmax) {  // once per head of the group
+        if (h != slope_h) {
+          slope_h = h;
+          slope = p.slope != nullptr ? p.slope[h] : 0.0f;
+        }
       }
       const float* lse_s = sLse + s * kBlockM + cb;
       const float* del_s = sDelta + s * kBlockM + cb;
@@ -913,7 +917,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
               pk[c2 * 16 + e / 2] = pack_bf16(apply_act<kAct>(z0), apply_act<kAct>(z1));
             }
           } else {
-#pragma unroll 2
+#pragma unroll  // fully: a partial unroll indexed pk through local memory
             for (int e = 0; e < 32; e += 2) {
               float pv[2];
 #pragma unroll

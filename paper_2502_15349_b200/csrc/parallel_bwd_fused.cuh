@@ -364,6 +364,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     const int j = k0 + row;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const int cb = sub * NC;
+    int slope_h = -1;
+    float slope = 0.0f;
     int hi_ = 0, qt_ = 0;
     for (int n = 0; n < niter; ++n) {
       const int s = n % kStages;
@@ -376,9 +378,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
         ++hi_;
       }
       const bool fullblk = tile64_fully_kept(p.mask, q0, k0, p.seq_q, p.seq_k);
-      float slope = 0.0f;
-      if constexpr (kFamily != kFamilySoftmax) {
-        if (p.slope != nullptr) slope = p.slope[h];
+      if constexpr (kFamily != kFamilySoftmax) {  // once per head of the group
+        if (h != slope_h) {
+          slope_h = h;
+          slope = p.slope != nullptr ? p.slope[h] : 0.0f;
+        }
       }
       const float* lse_s = sLse + s * kFusedBM + cb;
       const float* del_s = sDelta + s * kFusedBM + cb;
