@@ -223,42 +223,46 @@ __global__ void __launch_bounds__(320, 1)
       if (lane_id() == 0) mbar_arrive(&stat_empty[t]);
       mbar_wait(&s_full[t], (n >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[64], dr[64];
-      tmem_ld32(tmem + lane_base + t * 256 + cb, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(tmem + lane_base + t * 256 + cb + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_ld32(tmem + lane_base + t * 256 + 128 + cb, *reinterpret_cast<uint32_t(*)[32]>(&dr[0]));
-      tmem_ld32(tmem + lane_base + t * 256 + 128 + cb + 32,
-                *reinterpret_cast<uint32_t(*)[32]>(&dr[32]));
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&acc_empty[t]);
+      // two 32-column halves (S and dP of one half live at a time: all 64 + 64 columns plus
+      // the packed outputs at once needed ~190 registers and spilled at the 168 cap)
       const bool full_blk = block_fully_kept(p.mask, q0, k0, p.seq_k) && q0 + 128 <= p.seq_q;
-      uint32_t pw[32], dw[32];
-#pragma unroll
-      for (int e = 0; e < 64; e += 2) {
-        float pv[2], dv[2];
-#pragma unroll
-        for (int x = 0; x < 2; ++x) {
-          const int j = k0 + cb + e + x;
-          const bool keep = full_blk | kept(p.mask, i, j, p.seq_k);
-          // ex2(-inf) = 0: masked scores without a branch around the MUFU op; dS' is selected
-          // (not multiplied by the zero) since dP of a masked position need not be finite
-          const float pe =
-              ex2(keep ? fmaf(__uint_as_float(sr[e + x]), p.scale_log2, -l2) : -INFINITY);
-          pv[x] = pe;
-          dv[x] = keep ? pe * (__uint_as_float(dr[e + x]) - dl) * p.scale : 0.0f;
-        }
-        pw[e / 2] = pack_bf16(pv[0], pv[1]);
-        dw[e / 2] = pack_bf16(dv[0], dv[1]);
-      }
       const int64_t off = (static_cast<int64_t>(bh) * p.q_pad + i) * p.k_pad + k0 + cb;
-      uint4* pd = reinterpret_cast<uint4*>(p.p + off);
-      uint4* dd = reinterpret_cast<uint4*>(p.ds + off);
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tmem + lane_base + t * 256 + cb + hf * 32, sr);
+        tmem_ld32(tmem + lane_base + t * 256 + 128 + cb + hf * 32, dr);
+        tmem_ld_wait();
+        if (hf == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&acc_empty[t]);
+        }
+        uint32_t pw[16], dw[16];
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        pd[v] = make_uint4(pw[v * 4], pw[v * 4 + 1], pw[v * 4 + 2], pw[v * 4 + 3]);
-        dd[v] = make_uint4(dw[v * 4], dw[v * 4 + 1], dw[v * 4 + 2], dw[v * 4 + 3]);
+        for (int e = 0; e < 32; e += 2) {
+          float pv[2], dv[2];
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            const int j = k0 + cb + hf * 32 + e + x;
+            const bool keep = full_blk | kept(p.mask, i, j, p.seq_k);
+            // ex2(-inf) = 0: masked scores without a branch around the MUFU op; dS' is selected
+            // (not multiplied by the zero) since dP of a masked position need not be finite
+            const float pe =
+                ex2(keep ? fmaf(__uint_as_float(sr[e + x]), p.scale_log2, -l2) : -INFINITY);
+            pv[x] = pe;
+            dv[x] = keep ? pe * (__uint_as_float(dr[e + x]) - dl) * p.scale : 0.0f;
+          }
+          pw[e / 2] = pack_bf16(pv[0], pv[1]);
+          dw[e / 2] = pack_bf16(dv[0], dv[1]);
+        }
+        uint4* pd = reinterpret_cast<uint4*>(p.p + off + hf * 32);
+        uint4* dd = reinterpret_cast<uint4*>(p.ds + off + hf * 32);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          pd[v] = make_uint4(pw[v * 4], pw[v * 4 + 1], pw[v * 4 + 2], pw[v * 4 + 3]);
+          dd[v] = make_uint4(dw[v * 4], dw[v * 4 + 1], dw[v * 4 + 2], dw[v * 4 + 3]);
+        }
       }
     }
   }
