@@ -197,9 +197,10 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
         // state update once the row warps have scaled K by w (after S read it) and the state
         // warps have scaled H by this chunk's g
         mbar_wait(pk_ready, n & 1);
-        // Q (read by S and Q Hb, already issued) and the scan arrays (the row warps are past P)
-        mma_commit(&empty[s]);
+        // Q (read by S and Q Hb, already issued) and the scan arrays: the row warps are past P
+        // and the state warps have scaled H by this chunk's g (read from this stage's sL)
         if (n > 0) mbar_wait(h_scaled, (n - 1) & 1);
+        mma_commit(&empty[s]);
         mbar_wait(&vfull[s], (n / kSt) & 1);
         AF_LT(3, n);
         tc_fence_after();

@@ -219,8 +219,6 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&stat_full[t], (n >> 1) & 1);
       const float l2 = sStat[t * 256 + row];
       const float dl = sStat[t * 256 + 128 + row];
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&stat_empty[t]);
       mbar_wait(&s_full[t], (n >> 1) & 1);
       tc_fence_after();
       // two 32-column halves (S and dP of one half live at a time: all 64 + 64 columns plus
@@ -264,6 +262,12 @@ __global__ void __launch_bounds__(320, 1)
           dd[v] = make_uint4(dw[v * 4], dw[v * 4 + 1], dw[v * 4 + 2], dw[v * 4 + 3]);
         }
       }
+      // release the statistics slot only after l2 / dl have been consumed (the stores above
+      // depend on them): an arrive right after the shared loads does not wait for them to
+      // return, and the producer's next bulk copy (async proxy) into this slot could land first
+      // — measured at cfg4a as whole 32 x 64 P / dS' blocks computed with the LSE of tile n+2
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&stat_empty[t]);
     }
   }
 

@@ -96,3 +96,17 @@ def test_cfg4a_full_shape_forward_and_backward():
     want = OP.keycols_softmax_vjp(spec, {"q": np64(arrays["q"]), "k": k}, np64(dout), np64(o),
                                   np64(lse), J)
     assert nw(np64(g["k"][:, :, J]), want["k"]) <= 2e-2
+
+
+def test_cfg4a_backward_is_bitwise_repeatable():
+    """The materialised MLA backward has no atomics (fixed-order group reduce), so repeated runs
+    must agree bit for bit.  At this shape a statistics-slot release that did not wait for its
+    shared loads let the next bulk copy land first (whole 32 x 64 P / dS' blocks computed with
+    another tile's LSE): every run differed in ~1500 blocks, dQ by up to 25 % on some heads."""
+    spec = configs.cfg4a()
+    arrays, dout = bench.device_inputs(spec, DEV, 0)
+    o, lse = af.parallel_forward(spec, arrays)
+    g0 = af.parallel_backward(spec, arrays, o, lse, dout)
+    for _ in range(4):
+        g = af.parallel_backward(spec, arrays, o, lse, dout)
+        assert torch.equal(g["q"], g0["q"]) and torch.equal(g["k"], g0["k"])
