@@ -19,7 +19,8 @@ from .spec import (AttentionSpec, Dims, ExtraInput, ModificationFn, DirectRowNor
 from .plan import plan_parallel, plan_linear, ParallelPlan, LinearPlan
 from .api import (parallel_forward, parallel_backward, run_tiled_parallel, run_naive_parallel,
                   linear_forward, linear_backward, linear_step, run_chunk_recurrent, run_step_recurrent,
-                  autodiff_grads, bind, AttentionEngine, mla_decode)
+                  autodiff_grads, bind, AttentionEngine, mla_decode, use_deterministic_backward,
+                  deterministic_backward)
 from . import api, generic, hookvm, schedule
 from .emit import code_generation
 from .schedule import make_scheduling_task, measure_factory, tile_config_scheduling
