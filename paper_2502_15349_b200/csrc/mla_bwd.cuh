@@ -7,10 +7,11 @@
 // Why not K2's fused key-/query-stationary kernels: a 128 x 576 fp32 accumulator (288 KB) does not
 // fit in TMEM (256 KB), and a 128-row Q/dO tile pair is 272 KB of shared memory.  Instead the
 // backward is split into dense tensor-core phases that each fit the SM:
-//   1. scores   (key-tile stationary, K tile resident in smem, Q/dO streamed in 64-column boxes):
-//               S = Q K^T, dP = dO V^T into double-buffered TMEM; row warps write
-//               P = exp(S tau - LSE) and dS' = tau P (dP - D) as bf16 tiles to HBM (only the
-//               causal blocks; padded rows/cols written as zeros).
+//   1. scores   (key-tile stationary, the key tile in TMEM as the MMA's A operand, Q/dO streamed
+//               in 64-column boxes through a 12-stage ring): S^T = K Q^T, dP^T = V dO^T; one
+//               thread per key row writes P^T = exp(S tau - LSE) and dS'^T = tau P (dP - D) as
+//               bf16 rows [B*H, k_pad, q_pad] to HBM (only the causal blocks; padded rows/cols
+//               written as zeros).
 //   2. dQ GEMM  (query-tile stationary): dQ[:, n0:n0+N] = dS' K[:, n0:n0+N], N = 512 then 64.
 //   3. dKV GEMM (key-tile stationary, one CTA per head group): dKV[:, n0:n0+N] =
 //               sum_{h in group, q tiles} dS'^T Q[:, n0:] + P^T dO[:, n0:] (dO only below 512);
@@ -53,19 +54,29 @@ template <int D, int DV, bool kShared>
 struct MlaScoresSmem {
   static constexpr int kBox = 128 * 128;              // [128 rows][64 bf16]
   static constexpr int kKB = D / 64, kVB = DV / 64;   // boxes per K / V row tile
-  // ring depth: whatever shared memory the resident K (and V) tile leaves (the streamed Q / dO
-  // boxes are consumed in ~256 cycles each, so the ring depth sets the bytes in flight)
-  static constexpr int kStages =
-      (225 * 1024 - (kKB + (kShared ? 0 : kVB)) * kBox - 4096) / kBox > 12
-          ? 12
-          : (225 * 1024 - (kKB + (kShared ? 0 : kVB)) * kBox - 4096) / kBox;
-  static constexpr int kKOff = 0;                     // the resident K (and V) tile
-  static constexpr int kVOff = kKOff + kKB * kBox;
-  static constexpr int kRingOff = kVOff + (kShared ? 0 : kVB) * kBox;  // streamed Q / dO boxes
-  static constexpr int kStatOff = kRingOff + kStages * kBox;  // [2][2][128] fp32
-  static constexpr int kBarOff = kStatOff + 2 * 2 * 128 * 4;
-  // k_full, full[S], empty[S], stat_full[2], stat_empty[2], s_full[2], acc_empty[2]
-  static constexpr int kNumBars = 1 + 2 * kStages + 8;
+  // The key tile's operand boxes live in TMEM (A of tcgen05.mma from TMEM: 32 columns per 64-wide
+  // box, eight slots over columns [256, 512)) — K boxes first, then (separate V) the V boxes.
+  // K boxes beyond the eight slots (MLA: the 64 rope columns) stay resident in shared memory.
+  static constexpr int kKT = kShared ? (kKB < 8 ? kKB : 8) : kKB;  // K boxes in TMEM
+  static constexpr int kKS = kKB - kKT;                             // K boxes in smem
+  static constexpr int kStg = kKT + (kShared ? 0 : kVB);            // boxes staged into TMEM
+  static_assert(kStg <= 8 && (!kShared || kVB <= kKT), "operand boxes must fit the TMEM slots");
+  // ring depth: all the shared memory the resident boxes leave (the streamed Q / dO boxes are
+  // consumed one per ~256 cycles, so the ring depth sets the bytes in flight)
+  static constexpr int kStagesFit = (225 * 1024 - kKS * kBox - 4608) / kBox;
+  static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
+  static_assert(kStages >= kStg + 2, "the staged operand boxes occupy the top ring slots");
+  static constexpr int kStgBase = kStages - kStg;     // first ring slot holding a staged box
+  static constexpr int kKsOff = 0;
+  static constexpr int kRingOff = kKsOff + kKS * kBox;
+  // row statistics (LSE*log2e, D) of a query tile: a ring of 4 — the producer loads tile n+2's
+  // while the rows may still be on tile n (with 2 slots it stalled the Q / dO stream behind them)
+  static constexpr int kStatSlots = 4;
+  static constexpr int kStatOff = kRingOff + kStages * kBox;  // [kStatSlots][2][128] fp32
+  static constexpr int kBarOff = kStatOff + kStatSlots * 2 * 128 * 4;
+  // k_full, k_ready, full[S], empty[S], stat_full[4], stat_empty[4], s_full, s_free, dp_full,
+  // dp_free
+  static constexpr int kNumBars = 2 + 2 * kStages + 2 * kStatSlots + 4;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -75,6 +86,12 @@ __host__ __device__ inline int mla_q_tile_lo(const MaskParams& m, int k0) {
   return m.causal ? max(0, k0 - m.diag_offset) / 128 : 0;
 }
 
+// Key-tile stationary, transposed: S^T = K Q^T and dP^T = V dO^T with the key tile as the A
+// operand read from TMEM, so shared memory holds (almost) only the ring of streamed Q / dO boxes —
+// twelve 16 KB stages in flight instead of four behind a 147 KB resident K tile (ncu at cfg4a:
+// the MMA warp waited on the ring 35x longer than it issued; tensor pipe 31 % active).
+// TMEM: S^T [0, 128) | dP^T [128, 256) | operand boxes [256, 512).  One thread per key row writes
+// P^T and dS'^T rows: [B*H, k_pad, q_pad] bf16 (the GEMMs read them in this layout).
 template <int D, int DV, bool kShared>
 __global__ void __launch_bounds__(320, 1)
     mla_bwd_scores_kernel(const __grid_constant__ CUtensorMap tm_q,
@@ -84,19 +101,24 @@ __global__ void __launch_bounds__(320, 1)
   using L = MlaScoresSmem<D, DV, kShared>;
   constexpr int kStages = L::kStages;
   constexpr int kKB = L::kKB, kVB = L::kVB, kPerTile = kKB + kVB;
+  constexpr int kKT = L::kKT, kStg = L::kStg, kStgBase = L::kStgBase;
+  constexpr uint32_t kColS = 0, kColDP = 128, kColOp = 256;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* sK = smem + L::kKOff;
-  uint8_t* sV = kShared ? sK : smem + L::kVOff;
+  uint8_t* sKs = smem + L::kKsOff;
   uint8_t* sRing = smem + L::kRingOff;
   float* sStat = reinterpret_cast<float*>(smem + L::kStatOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   uint64_t* k_full = bars;
-  uint64_t* full = bars + 1;
+  uint64_t* k_ready = bars + 1;
+  uint64_t* full = bars + 2;
   uint64_t* empty = full + kStages;
+  constexpr int kSS = L::kStatSlots;
   uint64_t* stat_full = empty + kStages;
-  uint64_t* stat_empty = stat_full + 2;
-  uint64_t* s_full = stat_empty + 2;
-  uint64_t* acc_empty = s_full + 2;
+  uint64_t* stat_empty = stat_full + kSS;
+  uint64_t* s_full = stat_empty + kSS;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* dp_full = s_free + 1;
+  uint64_t* dp_free = dp_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -115,16 +137,19 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == 8 && lane_id() == 0) {
     mbar_init(k_full, 1);
+    mbar_init(k_ready, 8);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < kSS; ++t) {
       mbar_init(&stat_full[t], 1);
       mbar_init(&stat_empty[t], 8);
-      mbar_init(&s_full[t], 1);
-      mbar_init(&acc_empty[t], 8);
     }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 8);
+    mbar_init(dp_full, 1);
+    mbar_init(dp_free, 8);
     fence_barrier_init();
   }
   if (warp == 9) tmem_alloc<512>(tmem_slot);
@@ -132,21 +157,37 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (nq <= 0) {  // no visible query tile (cannot happen for a top-left causal band)
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+      tc_fence_after();
+      tmem_dealloc<512>(tmem);
+    }
+    return;
+  }
 
   if (warp == 8) {
     // ───────────── TMA producer ─────────────
-    if (elect_one() && nq > 0) {
-      mbar_expect_tx(k_full, (kKB + (kShared ? 0 : kVB)) * L::kBox);
-      for (int c = 0; c < kKB; ++c) tma_load_4d(sK + c * L::kBox, &tm_k, k_full, c * 64, k0, hk, b);
-      if constexpr (!kShared)
-        for (int c = 0; c < kVB; ++c)
-          tma_load_4d(sV + c * L::kBox, &tm_v, k_full, c * 64, k0, hk, b);
+    if (elect_one()) {
+      // the key tile: smem-resident K boxes and the boxes staged (top ring slots) for TMEM
+      mbar_expect_tx(k_full, (L::kKS + kStg) * L::kBox);
+      for (int c = kKT; c < kKB; ++c)
+        tma_load_4d(sKs + (c - kKT) * L::kBox, &tm_k, k_full, c * 64, k0, hk, b);
+      for (int x = 0; x < kStg; ++x) {
+        uint8_t* dst = sRing + (kStgBase + x) * L::kBox;
+        if (x < kKT)
+          tma_load_4d(dst, &tm_k, k_full, x * 64, k0, hk, b);
+        else
+          tma_load_4d(dst, &tm_v, k_full, (x - kKT) * 64, k0, hk, b);
+      }
+      bool staged = true;  // the top slots still hold the staged boxes
       int slot = 0;
       uint32_t ph = 0;
       for (int n = 0; n < nq; ++n) {
         const int q0 = (q_tiles - 1 - n) * 128;
-        const int t = n & 1;
-        mbar_wait(&stat_empty[t], ((n >> 1) & 1) ^ 1);
+        const int t = n % kSS;
+        mbar_wait(&stat_empty[t], ((n / kSS) & 1) ^ 1);
         mbar_expect_tx(&stat_full[t], 2 * 128 * 4);
         const int64_t row = static_cast<int64_t>(bh) * p.q_pad + q0;
         asm volatile(
@@ -160,6 +201,10 @@ __global__ void __launch_bounds__(320, 1)
             "l"(p.delta + row), "r"(128 * 4), "r"(smem_u32(&stat_full[t]))
             : "memory");
         for (int c = 0; c < kPerTile; ++c) {
+          if (staged && slot >= kStgBase) {
+            mbar_wait(k_ready, 0);  // the row warps have copied the staged boxes into TMEM
+            staged = false;
+          }
           mbar_wait(&empty[slot], ph ^ 1);
           mbar_expect_tx(&full[slot], L::kBox);
           if (c < kKB)
@@ -175,97 +220,168 @@ __global__ void __launch_bounds__(320, 1)
     }
   } else if (warp == 9) {
     // ───────────── MMA issuer ─────────────
-    if (elect_one() && nq > 0) {
+    if (elect_one()) {
       constexpr uint32_t id = make_idesc_bf16(128, 128, false, false);
-      const uint32_t aR = smem_u32(sRing), aK = smem_u32(sK), aV = smem_u32(sV);
-      mbar_wait(k_full, 0);
+      const uint32_t aR = smem_u32(sRing), aKs = smem_u32(sKs);
+      mbar_wait(k_full, 0);   // the smem-resident K boxes
+      mbar_wait(k_ready, 0);  // the TMEM operand boxes
+      tc_fence_after();
       int slot = 0;
       uint32_t ph = 0;
       for (int n = 0; n < nq; ++n) {
-        const int t = n & 1;
-        mbar_wait(&acc_empty[t], ((n >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d_s = tmem + t * 256, d_dp = tmem + t * 256 + 128;
-        for (int c = 0; c < kPerTile; ++c) {
+        // S^T = K Q^T once the row warps have read S^T(n-1)
+        if (n > 0) {
+          mbar_wait(s_free, (n - 1) & 1);
+          tc_fence_after();
+        }
+        for (int c = 0; c < kKB; ++c) {
           mbar_wait(&full[slot], ph);
           tc_fence_after();
-          const bool is_s = c < kKB;
-          // S += Q_c K_c^T ; dP += dO_c V_c^T (MLA: V = K boxes 0 .. Dv/64 - 1)
-          const uint32_t bb = is_s ? aK + c * L::kBox : aV + (c - kKB) * L::kBox;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_ss(is_s ? d_s : d_dp, make_sdesc(aR + slot * L::kBox + kk * 32, 0, 1024),
-                   make_sdesc(bb + kk * 32, 0, 1024), id,
-                   (c == 0 || c == kKB) && kk == 0 ? 0u : 1u);
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t bd = make_sdesc(aR + slot * L::kBox + kk * 32, 0, 1024);
+            const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+            if (c < kKT)
+              mma_ts(tmem + kColS, tmem + kColOp + c * 32 + kk * 8, bd, id, acc);
+            else
+              mma_ss(tmem + kColS, make_sdesc(aKs + (c - kKT) * L::kBox + kk * 32, 0, 1024), bd,
+                     id, acc);
+          }
           mma_commit(&empty[slot]);
           if (++slot == kStages) {
             slot = 0;
             ph ^= 1;
           }
         }
-        mma_commit(&s_full[t]);
+        mma_commit(s_full);
+        // dP^T = V dO^T once the row warps have read dP^T(n-1)  (MLA: V = K boxes 0 .. Dv/64-1)
+        if (n > 0) {
+          mbar_wait(dp_free, (n - 1) & 1);
+          tc_fence_after();
+        }
+        for (int c = 0; c < kVB; ++c) {
+          mbar_wait(&full[slot], ph);
+          tc_fence_after();
+          const uint32_t a = tmem + kColOp + (kShared ? c : kKT + c) * 32;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ts(tmem + kColDP, a + kk * 8, make_sdesc(aR + slot * L::kBox + kk * 32, 0, 1024),
+                   id, (c > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&empty[slot]);
+          if (++slot == kStages) {
+            slot = 0;
+            ph ^= 1;
+          }
+        }
+        mma_commit(dp_full);
       }
     }
   } else {
-    // ───────────── query-row warps: P and dS' rows ─────────────
-    const int wq = warp % 4, half = warp / 4;
-    const int row = wq * 32 + static_cast<int>(lane_id());
+    // ───────────── key-row warps: P^T and dS'^T rows ─────────────
+    const int wq = warp % 4, half = warp / 4;  // TMEM lane quarter, 64-query column half
+    const int jr = wq * 32 + static_cast<int>(lane_id());
+    const int j = k0 + jr;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const int cb = half * 64;
+    // stage the key tile's operand boxes into TMEM: row jr of box x -> columns [32 x, +32)
+    mbar_wait(k_full, 0);
+    for (int x = half; x < kStg; x += 2) {
+      const uint8_t* box = sRing + (kStgBase + x) * L::kBox;
+      uint32_t v[32];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const uint4 q = *reinterpret_cast<const uint4*>(box + jr * 128 + ((g ^ (jr & 7)) << 4));
+        v[g * 4 + 0] = q.x;
+        v[g * 4 + 1] = q.y;
+        v[g * 4 + 2] = q.z;
+        v[g * 4 + 3] = q.w;
+      }
+      tmem_st32(tmem + lane_base + kColOp + x * 32, v);
+    }
+    tmem_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane_id() == 0) mbar_arrive(k_ready);
+
+    const float sc = p.scale;
     for (int n = 0; n < nq; ++n) {
-      const int t = n & 1;
+      const int t = n % kSS;
       const int q0 = (q_tiles - 1 - n) * 128;
-      const int i = q0 + row;
-      mbar_wait(&stat_full[t], (n >> 1) & 1);
-      const float l2 = sStat[t * 256 + row];
-      const float dl = sStat[t * 256 + 128 + row];
-      mbar_wait(&s_full[t], (n >> 1) & 1);
-      tc_fence_after();
-      // two 32-column halves (S and dP of one half live at a time: all 64 + 64 columns plus
-      // the packed outputs at once needed ~190 registers and spilled at the 168 cap)
+      const int ib = q0 + half * 64;  // first query column of this warp
       const bool full_blk = block_fully_kept(p.mask, q0, k0, p.seq_k) && q0 + 128 <= p.seq_q;
-      const int64_t off = (static_cast<int64_t>(bh) * p.q_pad + i) * p.k_pad + k0 + cb;
-#pragma unroll 1
+      const float* l2s = sStat + t * 256 + half * 64;
+      const float* dls = l2s + 128;
+      const int64_t off = (static_cast<int64_t>(bh) * p.k_pad + j) * p.q_pad + ib;
+      mbar_wait(&stat_full[t], (n / kSS) & 1);
+      mbar_wait(s_full, n & 1);
+      tc_fence_after();
+      uint32_t pr[64];  // S^T row, then P^T (fp32 bits)
+      tmem_ld32(tmem + lane_base + kColS + half * 64, *reinterpret_cast<uint32_t(*)[32]>(&pr[0]));
+      tmem_ld32(tmem + lane_base + kColS + half * 64 + 32,
+                *reinterpret_cast<uint32_t(*)[32]>(&pr[32]));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(s_free);
+      {
+        uint32_t pw[32];
+#pragma unroll
+        for (int e = 0; e < 64; e += 4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(l2s + e);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const bool keep = full_blk | kept(p.mask, ib + e + x, j, p.seq_k);
+            // ex2(-inf) = 0: masked scores without a branch around the MUFU op
+            const float pe = ex2(keep ? fmaf(__uint_as_float(pr[e + x]), p.scale_log2, -lv[x])
+                                      : -INFINITY);
+            pr[e + x] = __float_as_uint(pe);
+          }
+          pw[e / 2] = pack_bf16(__uint_as_float(pr[e]), __uint_as_float(pr[e + 1]));
+          pw[e / 2 + 1] = pack_bf16(__uint_as_float(pr[e + 2]), __uint_as_float(pr[e + 3]));
+        }
+        uint4* pd = reinterpret_cast<uint4*>(p.p + off);
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          pd[v] = make_uint4(pw[v * 4], pw[v * 4 + 1], pw[v * 4 + 2], pw[v * 4 + 3]);
+      }
+      mbar_wait(dp_full, n & 1);
+      tc_fence_after();
+#pragma unroll  // (P^T is indexed by hf: a rolled loop would put it in local memory)
       for (int hf = 0; hf < 2; ++hf) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(tmem + lane_base + t * 256 + cb + hf * 32, sr);
-        tmem_ld32(tmem + lane_base + t * 256 + 128 + cb + hf * 32, dr);
+        uint32_t dr[32];
+        tmem_ld32(tmem + lane_base + kColDP + half * 64 + hf * 32, dr);
         tmem_ld_wait();
         if (hf == 1) {
           tc_fence_before();
           __syncwarp();
-          if (lane_id() == 0) mbar_arrive(&acc_empty[t]);
+          if (lane_id() == 0) mbar_arrive(dp_free);
         }
-        uint32_t pw[16], dw[16];
+        uint32_t dw[16];
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float pv[2], dv[2];
+        for (int e = 0; e < 32; e += 4) {
+          const float4 d4 = *reinterpret_cast<const float4*>(dls + hf * 32 + e);
+          const float dl[4] = {d4.x, d4.y, d4.z, d4.w};
+          float dv[4];
 #pragma unroll
-          for (int x = 0; x < 2; ++x) {
-            const int j = k0 + cb + hf * 32 + e + x;
-            const bool keep = full_blk | kept(p.mask, i, j, p.seq_k);
-            // ex2(-inf) = 0: masked scores without a branch around the MUFU op; dS' is selected
-            // (not multiplied by the zero) since dP of a masked position need not be finite
-            const float pe =
-                ex2(keep ? fmaf(__uint_as_float(sr[e + x]), p.scale_log2, -l2) : -INFINITY);
-            pv[x] = pe;
-            dv[x] = keep ? pe * (__uint_as_float(dr[e + x]) - dl) * p.scale : 0.0f;
+          for (int x = 0; x < 4; ++x) {
+            const bool keep = full_blk | kept(p.mask, ib + hf * 32 + e + x, j, p.seq_k);
+            // dS' is selected (not multiplied by P's zero): dP of a masked position need not be
+            // finite
+            dv[x] = keep ? __uint_as_float(pr[hf * 32 + e + x]) *
+                               (__uint_as_float(dr[e + x]) - dl[x]) * sc
+                         : 0.0f;
           }
-          pw[e / 2] = pack_bf16(pv[0], pv[1]);
           dw[e / 2] = pack_bf16(dv[0], dv[1]);
+          dw[e / 2 + 1] = pack_bf16(dv[2], dv[3]);
         }
-        uint4* pd = reinterpret_cast<uint4*>(p.p + off + hf * 32);
         uint4* dd = reinterpret_cast<uint4*>(p.ds + off + hf * 32);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          pd[v] = make_uint4(pw[v * 4], pw[v * 4 + 1], pw[v * 4 + 2], pw[v * 4 + 3]);
+        for (int v = 0; v < 4; ++v)
           dd[v] = make_uint4(dw[v * 4], dw[v * 4 + 1], dw[v * 4 + 2], dw[v * 4 + 3]);
-        }
       }
-      // release the statistics slot only after l2 / dl have been consumed (the stores above
-      // depend on them): an arrive right after the shared loads does not wait for them to
-      // return, and the producer's next bulk copy (async proxy) into this slot could land first
-      // — measured at cfg4a as whole 32 x 64 P / dS' blocks computed with the LSE of tile n+2
+      // the statistics slot is released after its values have been consumed (see the race
+      // note in the round-2 DESIGN: an arrive right after the shared loads does not wait for
+      // them, and the producer's next bulk copy into the slot could land first)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&stat_empty[t]);
     }
@@ -283,10 +399,11 @@ __global__ void __launch_bounds__(320, 1)
 // One accumulator tile of 128 rows x N columns in TMEM, fed by a ring of stages:
 //   stage = A (16 KB: one [128][64] K-major box, or two [64][64] boxes MN-major)
 //         + B (N/64 boxes [64 K-rows][64 cols], MN-major)
-// kGemmDQ : rows = queries of (b, h, q tile); items = visible key tiles; A = dS' (K-major),
-//           B = K[hk][:, n0:n0+N].
+// The scores are stored transposed, [B*H, k_pad, q_pad] (the scores kernel writes key rows):
+// kGemmDQ : rows = queries of (b, h, q tile); items = visible key tiles; A = dS' (MN-major from
+//           the key-row layout), B = K[hk][:, n0:n0+N].
 // key side: rows = keys of (b, hk, key tile); items = (h in the head chunk, visible q tile); per
-//           64-query chunk one or two products: A = dS'^T (MN-major), B = Q[:, n0:] (dK, and MLA's
+//           64-query chunk one or two products: A = dS'^T (K-major), B = Q[:, n0:] (dK, and MLA's
 //           latent dKV) and A = P^T, B = dO[:, n0:] (dV, and MLA's dKV for n0 < 512).
 enum GemmMode : int { kGemmDQ = 0, kGemmDKV = 1, kGemmDK = 2, kGemmDV = 3 };
 
@@ -384,15 +501,21 @@ __global__ void __launch_bounds__(192, 1)
         if constexpr (!kKey) {
           const int kt = it_lo + item;
           const int c = sub;  // 64-key chunk
-          tma_load_4d(sa, &tm_a1, &full[slot], kt * 128 + c * 64, tile * 128, bh, 0);
+          // dS'^T rows [kt*128 + 64c, +64) x query columns of this tile: A MN-major, two boxes
+          tma_load_4d(sa, &tm_a1, &full[slot], tile * 128, kt * 128 + c * 64, bh, 0);
+          tma_load_4d(sa + 8192, &tm_a1, &full[slot], tile * 128 + 64, kt * 128 + c * 64, bh, 0);
           for (int nb = 0; nb < N / 64; ++nb)
             tma_load_4d_hint(sb + nb * 8192, &tm_b1, &full[slot], n0 + nb * 64,
                              kt * 128 + c * 64, hk, b, kEvictLast);
         } else {
-          // query tiles from the last one down: CTAs of different key tiles then stream the same
-          // Q / dO tiles concurrently (L2 reuse)
-          const int hh = h_lo + item / (it_hi - it_lo);
-          const int qt = it_hi - 1 - item % (it_hi - it_lo);
+          // query tiles from the last one down, the heads of the chunk inside each: the CTAs of
+          // every key tile start at the last query tile and step down at the same pace (a key
+          // tile just stops earlier), so they stream the same (q tile, head) Q / dO tile at the
+          // same time and it is read from HBM once (head-outer, the CTAs drifted apart after the
+          // first head — their per-head lengths differ — and re-read Q / dO ~10x from HBM)
+          const int nh = h_hi - h_lo;
+          const int qt = it_hi - 1 - item / nh;
+          const int hh = h_lo + item % nh;
           // chunk, product (0: dS'/Q, 1: P/dO)
           const int c = per_item == 4 ? sub / 2 : sub;
           const int prod = per_item == 4 ? sub % 2 : (kMode == kGemmDV ? 1 : 0);
@@ -400,8 +523,8 @@ __global__ void __launch_bounds__(192, 1)
           const int r0 = qt * 128 + c * 64;
           const CUtensorMap* ta = prod == 0 ? &tm_a1 : &tm_a2;
           const CUtensorMap* tb = prod == 0 ? &tm_b1 : &tm_b2;
-          tma_load_4d(sa, ta, &full[slot], tile * 128, r0, bhh, 0);
-          tma_load_4d(sa + 8192, ta, &full[slot], tile * 128 + 64, r0, bhh, 0);
+          // dS'^T / P^T rows of this key tile x 64 query columns: A K-major, one box
+          tma_load_4d(sa, ta, &full[slot], r0, tile * 128, bhh, 0);
           for (int nb = 0; nb < N / 64; ++nb)
             tma_load_4d(sb + nb * 8192, tb, &full[slot], n0 + nb * 64, r0, hh, b);
         }
@@ -415,7 +538,7 @@ __global__ void __launch_bounds__(192, 1)
     // ───────────── MMA issuer ─────────────
     if (elect_one()) {
       constexpr int kN = N >= 256 ? 256 : N;  // per-instruction N
-      constexpr uint32_t id = make_idesc_bf16(128, kN, kKey, true);
+      constexpr uint32_t id = make_idesc_bf16(128, kN, !kKey, true);
       int slot = 0;
       uint32_t ph = 0;
       for (int st = 0; st < n_stages_total; ++st) {
@@ -425,8 +548,8 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t sb = sa + L::kABytes;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = kKey ? make_sdesc(sa + kk * 2048, 8192, 1024)
-                                   : make_sdesc(sa + kk * 32, 0, 1024);
+          const uint64_t ad = kKey ? make_sdesc(sa + kk * 32, 0, 1024)
+                                   : make_sdesc(sa + kk * 2048, 8192, 1024);
 #pragma unroll
           for (int nh = 0; nh < N / kN; ++nh)
             mma_ss(tmem + nh * kN, ad,

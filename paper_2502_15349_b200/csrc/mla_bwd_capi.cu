@@ -147,9 +147,11 @@ int run_materialized(const af_parallel_desc* d, const void* q, const void* k, co
 
   // maps shared by the GEMMs
   CUtensorMap tds_q, tds_k, tp_k, tkb, tqb, tdob;
-  if (!tmap_3d(&tds_q, dsbuf, l.k_pad, l.q_pad, bhs, 64, 128) ||
-      !tmap_3d(&tds_k, dsbuf, l.k_pad, l.q_pad, bhs, 64, 64) ||
-      !tmap_3d(&tp_k, pbuf, l.k_pad, l.q_pad, bhs, 64, 64) ||
+  // P^T / dS'^T are [b*H, k_pad, q_pad]: the dQ GEMM reads [64 keys][64 queries] boxes
+  // (MN-major A), the key-side GEMMs [128 keys][64 queries] boxes (K-major A)
+  if (!tmap_3d(&tds_q, dsbuf, l.q_pad, l.k_pad, bhs, 64, 64) ||
+      !tmap_3d(&tds_k, dsbuf, l.q_pad, l.k_pad, bhs, 64, 128) ||
+      !tmap_3d(&tp_k, pbuf, l.q_pad, l.k_pad, bhs, 64, 128) ||
       !make_tmap_4d(&tkb, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_k, d->heads_kv,
                     d->batch, d->k_stride, 64, 64, true) ||
       !make_tmap_4d(&tqb, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_q, d->heads_q,
