@@ -49,10 +49,34 @@ struct MlaBwdParams {
 };
 
 // ═══════════════════════════════ 1. scores ═══════════════════════════════
+// Developer wait accounting (-DAF_SCORES_TRACE): per CTA (the first 256), SM cycles the MMA thread
+// spends in its waits and in total, and the same for key-row warp 0; read with
+// af_debug_scores_trace (tools/trace_scores.py).
+#ifdef AF_SCORES_TRACE
+__device__ long long g_scores_trace[256][8];
+#define SC_T0() long long sc_t = clock64()
+#define SC_ACC(slot, expr)                                                   \
+  do {                                                                       \
+    const long long sc_a = clock64();                                        \
+    expr;                                                                    \
+    if (blockIdx.x < 256) g_scores_trace[blockIdx.x][slot] += clock64() - sc_a; \
+  } while (0)
+#define SC_TOTAL(slot) \
+  if (blockIdx.x < 256) g_scores_trace[blockIdx.x][slot] = clock64() - sc_t
+#else
+#define SC_T0() \
+  do {          \
+  } while (0)
+#define SC_ACC(slot, expr) expr
+#define SC_TOTAL(slot) \
+  do {                 \
+  } while (0)
+#endif
 
 template <int D, int DV, bool kShared>
 struct MlaScoresSmem {
-  static constexpr int kBox = 128 * 128;              // [128 rows][64 bf16]
+  static constexpr int kBox = 128 * 128;              // [128 rows][64 bf16] key-tile box
+  static constexpr int kSlot = 64 * 128;              // [64 rows][64 bf16] half Q / dO box
   static constexpr int kKB = D / 64, kVB = DV / 64;   // boxes per K / V row tile
   // The key tile's operand boxes live in TMEM (A of tcgen05.mma from TMEM: 32 columns per 64-wide
   // box, eight slots over columns [256, 512)) — K boxes first, then (separate V) the V boxes.
@@ -61,18 +85,21 @@ struct MlaScoresSmem {
   static constexpr int kKS = kKB - kKT;                             // K boxes in smem
   static constexpr int kStg = kKT + (kShared ? 0 : kVB);            // boxes staged into TMEM
   static_assert(kStg <= 8 && (!kShared || kVB <= kKT), "operand boxes must fit the TMEM slots");
-  // ring depth: all the shared memory the resident boxes leave (the streamed Q / dO boxes are
-  // consumed one per ~256 cycles, so the ring depth sets the bytes in flight)
-  static constexpr int kStagesFit = (225 * 1024 - kKS * kBox - 4608) / kBox;
-  static constexpr int kStages = kStagesFit > 12 ? 12 : kStagesFit;
-  static_assert(kStages >= kStg + 2, "the staged operand boxes occupy the top ring slots");
-  static constexpr int kStgBase = kStages - kStg;     // first ring slot holding a staged box
+  // ring of half boxes (this CTA's 64 of a Q / dO box's 128 query rows): all the shared memory
+  // the resident boxes leave — the ring depth sets the bytes in flight
+  // + one 4 KB staging box per key-row warp for the TMA stores of its P^T / dS'^T rows
+  static constexpr int kOutBytes = 8 * 4096;
+  static constexpr int kStagesFit = (225 * 1024 - kKS * kBox - kOutBytes - 4608) / kSlot;
+  static constexpr int kStages = kStagesFit > 24 ? 24 : kStagesFit;
+  static_assert(kStages >= 2 * kStg + 2, "the staged operand boxes occupy the top ring slots");
+  static constexpr int kStgBase = kStages - 2 * kStg;  // first ring slot holding a staged box
   static constexpr int kKsOff = 0;
-  static constexpr int kRingOff = kKsOff + kKS * kBox;
+  static constexpr int kOutOff = kKsOff + kKS * kBox;
+  static constexpr int kRingOff = kOutOff + kOutBytes;
   // row statistics (LSE*log2e, D) of a query tile: a ring of 4 — the producer loads tile n+2's
   // while the rows may still be on tile n (with 2 slots it stalled the Q / dO stream behind them)
   static constexpr int kStatSlots = 4;
-  static constexpr int kStatOff = kRingOff + kStages * kBox;  // [kStatSlots][2][128] fp32
+  static constexpr int kStatOff = kRingOff + kStages * kSlot;  // [kStatSlots][2][128] fp32
   static constexpr int kBarOff = kStatOff + kStatSlots * 2 * 128 * 4;
   // k_full, k_ready, full[S], empty[S], stat_full[4], stat_empty[4], s_full, s_free, dp_full,
   // dp_free
@@ -86,22 +113,30 @@ __host__ __device__ inline int mla_q_tile_lo(const MaskParams& m, int k0) {
   return m.causal ? max(0, k0 - m.diag_offset) / 128 : 0;
 }
 
-// Key-tile stationary, transposed: S^T = K Q^T and dP^T = V dO^T with the key tile as the A
-// operand read from TMEM, so shared memory holds (almost) only the ring of streamed Q / dO boxes —
-// twelve 16 KB stages in flight instead of four behind a 147 KB resident K tile (ncu at cfg4a:
-// the MMA warp waited on the ring 35x longer than it issued; tensor pipe 31 % active).
-// TMEM: S^T [0, 128) | dP^T [128, 256) | operand boxes [256, 512).  One thread per key row writes
-// P^T and dS'^T rows: [B*H, k_pad, q_pad] bf16 (the GEMMs read them in this layout).
+// Key-tile stationary, transposed, on a CTA pair: S^T = K Q^T and dP^T = V dO^T as M = 256
+// tcgen05.mma over two key tiles (the pair's leader issues; each CTA's key tile is its A operand,
+// read from its own TMEM), N = 128 query rows of which each CTA streams 64 — so every Q / dO byte
+// is fetched from L2 once per two key tiles, and a 24-slot ring of half boxes is in flight per SM
+// (the single-CTA form streamed whole boxes per key tile: L2-throughput and latency bound, ncu
+// tensor pipe 31 -> 40 % active).
+// TMEM (each CTA): S^T [0, 128) | dP^T [128, 256) | operand boxes [256, 512).  One thread per key
+// row writes P^T and dS'^T rows: [B*H, k_pad, q_pad] bf16 (the GEMMs read them in this layout).
+// Both CTAs walk the leader's query tiles; the second key tile's extra (diagonal-below) tile is
+// fully masked and written as zeros — the paired GEMMs read that block.
 template <int D, int DV, bool kShared>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
     mla_bwd_scores_kernel(const __grid_constant__ CUtensorMap tm_q,
                           const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_k,
-                          const __grid_constant__ CUtensorMap tm_v, const MlaBwdParams p) {
+                          const __grid_constant__ CUtensorMap tm_v,
+                          const __grid_constant__ CUtensorMap tm_pst,   // P^T store, [32][64] boxes
+                          const __grid_constant__ CUtensorMap tm_dsst,  // dS'^T store
+                          const MlaBwdParams p) {
   using L = MlaScoresSmem<D, DV, kShared>;
   constexpr int kStages = L::kStages;
   constexpr int kKB = L::kKB, kVB = L::kVB, kPerTile = kKB + kVB;
   constexpr int kKT = L::kKT, kStg = L::kStg, kStgBase = L::kStgBase;
+  constexpr int kSS = L::kStatSlots;
   constexpr uint32_t kColS = 0, kColDP = 128, kColOp = 256;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sKs = smem + L::kKsOff;
@@ -112,7 +147,6 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* k_ready = bars + 1;
   uint64_t* full = bars + 2;
   uint64_t* empty = full + kStages;
-  constexpr int kSS = L::kStatSlots;
   uint64_t* stat_full = empty + kStages;
   uint64_t* stat_empty = stat_full + kSS;
   uint64_t* s_full = stat_empty + kSS;
@@ -122,22 +156,23 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
-  // CTA order (b, h)-major with the key tiles of one head adjacent, and every CTA walks its query
-  // tiles from the last one down: the CTAs of one head stream the same Q / dO tiles at the same
-  // time, so each is read from HBM once and served to the other key tiles from L2.
-  const int k_tiles = p.k_pad / 128;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  // CTA order (b, h)-major with the key tiles of one head adjacent (pairs = even / odd key tile),
+  // and every CTA walks its query tiles from the last one down: the CTAs of one head stream the
+  // same Q / dO tiles at the same time (one HBM read, L2 for the other key tiles).
+  const int k_tiles = p.k_pad / 128;  // even (k_pad is padded to 256)
   const int kt = static_cast<int>(blockIdx.x) % k_tiles;
   const int bh = static_cast<int>(blockIdx.x) / k_tiles;
   const int b = bh / p.heads, h = bh % p.heads;
   const int hk = h / (p.heads / p.heads_kv);
   const int k0 = kt * 128;
   const int q_tiles = p.q_pad / 128;
-  const int qt_lo = mla_q_tile_lo(p.mask, k0);
-  const int nq = q_tiles - qt_lo;
+  const int nq = q_tiles - mla_q_tile_lo(p.mask, (kt & ~1) * 128);  // the leader's tiles
 
   if (warp == 8 && lane_id() == 0) {
     mbar_init(k_full, 1);
-    mbar_init(k_ready, 8);
+    mbar_init(k_ready, leader ? 16 : 8);  // the leader's MMA needs both CTAs' operand boxes
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -147,35 +182,27 @@ __global__ void __launch_bounds__(320, 1)
       mbar_init(&stat_empty[t], 8);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_free, 8);
+    mbar_init(s_free, 16);  // (leader's: both CTAs' row warps)
     mbar_init(dp_full, 1);
-    mbar_init(dp_free, 8);
+    mbar_init(dp_free, 16);
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(tmem_slot);
+  if (warp == 9) tmem_alloc_pair<512>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // barriers of both CTAs initialised before any cross-CTA arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (nq <= 0) {  // no visible query tile (cannot happen for a top-left causal band)
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 9) {
-      tc_fence_after();
-      tmem_dealloc<512>(tmem);
-    }
-    return;
-  }
+  const uint32_t k_ready_l = peer_addr(k_ready, 0), s_free_l = peer_addr(s_free, 0),
+                 dp_free_l = peer_addr(dp_free, 0);
 
   if (warp == 8) {
-    // ───────────── TMA producer ─────────────
-    if (elect_one()) {
-      // the key tile: smem-resident K boxes and the boxes staged (top ring slots) for TMEM
+    // ───────────── TMA producer (each CTA: its key tile, its half of every Q / dO box) ─────────────
+    if (elect_one() && nq > 0) {
       mbar_expect_tx(k_full, (L::kKS + kStg) * L::kBox);
       for (int c = kKT; c < kKB; ++c)
         tma_load_4d(sKs + (c - kKT) * L::kBox, &tm_k, k_full, c * 64, k0, hk, b);
       for (int x = 0; x < kStg; ++x) {
-        uint8_t* dst = sRing + (kStgBase + x) * L::kBox;
+        uint8_t* dst = sRing + (kStgBase + 2 * x) * L::kSlot;
         if (x < kKT)
           tma_load_4d(dst, &tm_k, k_full, x * 64, k0, hk, b);
         else
@@ -200,17 +227,19 @@ __global__ void __launch_bounds__(320, 1)
             "[%3];" ::"r"(smem_u32(sStat + t * 256 + 128)),
             "l"(p.delta + row), "r"(128 * 4), "r"(smem_u32(&stat_full[t]))
             : "memory");
+        const int r0 = q0 + static_cast<int>(rank) * 64;  // this CTA's 64 query rows
         for (int c = 0; c < kPerTile; ++c) {
           if (staged && slot >= kStgBase) {
             mbar_wait(k_ready, 0);  // the row warps have copied the staged boxes into TMEM
             staged = false;
           }
-          mbar_wait(&empty[slot], ph ^ 1);
-          mbar_expect_tx(&full[slot], L::kBox);
+          mbar_wait(&empty[slot], ph ^ 1);  // the pair's MMA has read this slot in both CTAs
+          if (leader) mbar_expect_tx(&full[slot], 2 * L::kSlot);
+          const uint32_t fl = peer_addr(&full[slot], 0);
           if (c < kKB)
-            tma_load_4d(sRing + slot * L::kBox, &tm_q, &full[slot], c * 64, q0, h, b);
+            tma_load_4d_pair(sRing + slot * L::kSlot, &tm_q, fl, c * 64, r0, h, b);
           else
-            tma_load_4d(sRing + slot * L::kBox, &tm_do, &full[slot], (c - kKB) * 64, q0, h, b);
+            tma_load_4d_pair(sRing + slot * L::kSlot, &tm_do, fl, (c - kKB) * 64, r0, h, b);
           if (++slot == kStages) {
             slot = 0;
             ph ^= 1;
@@ -219,64 +248,71 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 9) {
-    // ───────────── MMA issuer ─────────────
-    if (elect_one()) {
-      constexpr uint32_t id = make_idesc_bf16(128, 128, false, false);
+    // ───────────── MMA issuer (the leader, for both CTAs) ─────────────
+    if (leader && nq > 0 && elect_one()) {
+      constexpr uint32_t id = make_idesc_bf16(256, 128, false, false);
       const uint32_t aR = smem_u32(sRing), aKs = smem_u32(sKs);
-      mbar_wait(k_full, 0);   // the smem-resident K boxes
-      mbar_wait(k_ready, 0);  // the TMEM operand boxes
+      SC_T0();
+      mbar_wait(k_full, 0);   // the smem-resident K boxes (the peer's: behind its k_ready)
+      SC_ACC(0, mbar_wait(k_ready, 0));  // both CTAs' TMEM operand boxes
       tc_fence_after();
       int slot = 0;
       uint32_t ph = 0;
       for (int n = 0; n < nq; ++n) {
-        // S^T = K Q^T once the row warps have read S^T(n-1)
+        // S^T = K Q^T once both CTAs' row warps have read S^T(n-1)
         if (n > 0) {
-          mbar_wait(s_free, (n - 1) & 1);
+          SC_ACC(1, mbar_wait(s_free, (n - 1) & 1));
           tc_fence_after();
         }
+        // (box loops fully unrolled: with the TS / SS choice a runtime branch, the compiler
+        // wrapped every MMA in an ELECT waterfall and the single issuing thread fell behind)
+#pragma unroll
         for (int c = 0; c < kKB; ++c) {
-          mbar_wait(&full[slot], ph);
+          SC_ACC(2, mbar_wait(&full[slot], ph));
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t bd = make_sdesc(aR + slot * L::kBox + kk * 32, 0, 1024);
+            const uint64_t bd = make_sdesc(aR + slot * L::kSlot + kk * 32, 0, 1024);
             const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
             if (c < kKT)
-              mma_ts(tmem + kColS, tmem + kColOp + c * 32 + kk * 8, bd, id, acc);
+              mma_ts_pair(tmem + kColS, tmem + kColOp + c * 32 + kk * 8, bd, id, acc);
             else
-              mma_ss(tmem + kColS, make_sdesc(aKs + (c - kKT) * L::kBox + kk * 32, 0, 1024), bd,
-                     id, acc);
+              mma_ss_pair(tmem + kColS, make_sdesc(aKs + (c - kKT) * L::kBox + kk * 32, 0, 1024),
+                          bd, id, acc);
           }
-          mma_commit(&empty[slot]);
+          mma_commit_pair(&empty[slot]);
           if (++slot == kStages) {
             slot = 0;
             ph ^= 1;
           }
         }
-        mma_commit(s_full);
-        // dP^T = V dO^T once the row warps have read dP^T(n-1)  (MLA: V = K boxes 0 .. Dv/64-1)
+        mma_commit_pair(s_full);
+        // dP^T = V dO^T once both CTAs have read dP^T(n-1)  (MLA: V = K boxes 0 .. Dv/64-1)
         if (n > 0) {
-          mbar_wait(dp_free, (n - 1) & 1);
+          SC_ACC(3, mbar_wait(dp_free, (n - 1) & 1));
           tc_fence_after();
         }
+#pragma unroll
         for (int c = 0; c < kVB; ++c) {
-          mbar_wait(&full[slot], ph);
+          SC_ACC(2, mbar_wait(&full[slot], ph));
           tc_fence_after();
           const uint32_t a = tmem + kColOp + (kShared ? c : kKT + c) * 32;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_ts(tmem + kColDP, a + kk * 8, make_sdesc(aR + slot * L::kBox + kk * 32, 0, 1024),
-                   id, (c > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&empty[slot]);
+            mma_ts_pair(tmem + kColDP, a + kk * 8,
+                        make_sdesc(aR + slot * L::kSlot + kk * 32, 0, 1024), id,
+                        (c > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_pair(&empty[slot]);
           if (++slot == kStages) {
             slot = 0;
             ph ^= 1;
           }
         }
-        mma_commit(dp_full);
+        mma_commit_pair(dp_full);
       }
+      SC_TOTAL(4);
     }
-  } else {
+  } else if (nq > 0) {
     // ───────────── key-row warps: P^T and dS'^T rows ─────────────
     const int wq = warp % 4, half = warp / 4;  // TMEM lane quarter, 64-query column half
     const int jr = wq * 32 + static_cast<int>(lane_id());
@@ -285,7 +321,7 @@ __global__ void __launch_bounds__(320, 1)
     // stage the key tile's operand boxes into TMEM: row jr of box x -> columns [32 x, +32)
     mbar_wait(k_full, 0);
     for (int x = half; x < kStg; x += 2) {
-      const uint8_t* box = sRing + (kStgBase + x) * L::kBox;
+      const uint8_t* box = sRing + (kStgBase + 2 * x) * L::kSlot;
       uint32_t v[32];
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
@@ -300,9 +336,21 @@ __global__ void __launch_bounds__(320, 1)
     tmem_st_wait();
     tc_fence_before();
     __syncwarp();
-    if (lane_id() == 0) mbar_arrive(k_ready);
+    if (lane_id() == 0) {
+      if (!leader) mbar_arrive(k_ready);  // this CTA's producer may reuse the staging slots
+      mbar_arrive_cluster(k_ready_l);     // the leader's MMA may read this CTA's boxes
+    }
 
     const float sc = p.scale;
+    // this warp's 32 key rows x 64 query columns go out through a swizzled 4 KB box and a TMA
+    // store (per-thread 16-byte stores to 32 different rows cost ~0.7 ms of LSU / L2 sector work
+    // at cfg4a)
+    uint8_t* sOut = smem + L::kOutOff + warp * 4096;
+    const int lr = static_cast<int>(lane_id());
+    auto out_chunk = [&](int g) {
+      return reinterpret_cast<uint4*>(sOut + lr * 128 + ((g ^ (lr & 7)) << 4));
+    };
+    SC_T0();
     for (int n = 0; n < nq; ++n) {
       const int t = n % kSS;
       const int q0 = (q_tiles - 1 - n) * 128;
@@ -310,7 +358,11 @@ __global__ void __launch_bounds__(320, 1)
       const bool full_blk = block_fully_kept(p.mask, q0, k0, p.seq_k) && q0 + 128 <= p.seq_q;
       const float* l2s = sStat + t * 256 + half * 64;
       const float* dls = l2s + 128;
-      const int64_t off = (static_cast<int64_t>(bh) * p.k_pad + j) * p.q_pad + ib;
+      if (warp == 0 && lane_id() == 0) {
+        SC_ACC(5, mbar_wait(&stat_full[t], (n / kSS) & 1));
+        SC_ACC(6, mbar_wait(s_full, n & 1));
+      }
+      __syncwarp();
       mbar_wait(&stat_full[t], (n / kSS) & 1);
       mbar_wait(s_full, n & 1);
       tc_fence_after();
@@ -321,7 +373,12 @@ __global__ void __launch_bounds__(320, 1)
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive(s_free);
+      if (lane_id() == 0) {  // S^T read (tcgen05.wait::ld returned): the pair's MMA may reuse it
+        if (leader)
+          mbar_arrive(s_free);
+        else
+          mbar_arrive_cluster_relaxed(s_free_l);
+      }
       {
         uint32_t pw[32];
 #pragma unroll
@@ -339,11 +396,20 @@ __global__ void __launch_bounds__(320, 1)
           pw[e / 2] = pack_bf16(__uint_as_float(pr[e]), __uint_as_float(pr[e + 1]));
           pw[e / 2 + 1] = pack_bf16(__uint_as_float(pr[e + 2]), __uint_as_float(pr[e + 3]));
         }
-        uint4* pd = reinterpret_cast<uint4*>(p.p + off);
+        if (lr == 0) bulk_wait_read<0>();  // the previous dS'^T store has read the box
+        __syncwarp();
 #pragma unroll
         for (int v = 0; v < 8; ++v)
-          pd[v] = make_uint4(pw[v * 4], pw[v * 4 + 1], pw[v * 4 + 2], pw[v * 4 + 3]);
+          *out_chunk(v) = make_uint4(pw[v * 4], pw[v * 4 + 1], pw[v * 4 + 2], pw[v * 4 + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lr == 0) {
+          tma_store_4d(&tm_pst, sOut, ib, k0 + wq * 32, bh, 0);
+          bulk_commit();
+        }
       }
+      if (warp == 0 && lane_id() == 0) SC_ACC(7, mbar_wait(dp_full, n & 1));
+      __syncwarp();
       mbar_wait(dp_full, n & 1);
       tc_fence_after();
 #pragma unroll  // (P^T is indexed by hf: a rolled loop would put it in local memory)
@@ -354,7 +420,12 @@ __global__ void __launch_bounds__(320, 1)
         if (hf == 1) {
           tc_fence_before();
           __syncwarp();
-          if (lane_id() == 0) mbar_arrive(dp_free);
+          if (lane_id() == 0) {
+            if (leader)
+              mbar_arrive(dp_free);
+            else
+              mbar_arrive_cluster_relaxed(dp_free_l);
+          }
         }
         uint32_t dw[16];
 #pragma unroll
@@ -374,24 +445,34 @@ __global__ void __launch_bounds__(320, 1)
           dw[e / 2] = pack_bf16(dv[0], dv[1]);
           dw[e / 2 + 1] = pack_bf16(dv[2], dv[3]);
         }
-        uint4* dd = reinterpret_cast<uint4*>(p.ds + off + hf * 32);
+        if (hf == 0) {
+          if (lr == 0) bulk_wait_read<0>();  // the P^T store has read the box
+          __syncwarp();
+        }
 #pragma unroll
         for (int v = 0; v < 4; ++v)
-          dd[v] = make_uint4(dw[v * 4], dw[v * 4 + 1], dw[v * 4 + 2], dw[v * 4 + 3]);
+          *out_chunk(hf * 4 + v) = make_uint4(dw[v * 4], dw[v * 4 + 1], dw[v * 4 + 2], dw[v * 4 + 3]);
       }
-      // the statistics slot is released after its values have been consumed (see the race
-      // note in the round-2 DESIGN: an arrive right after the shared loads does not wait for
-      // them, and the producer's next bulk copy into the slot could land first)
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lr == 0) {
+        tma_store_4d(&tm_dsst, sOut, ib, k0 + wq * 32, bh, 0);
+        bulk_commit();
+      }
+      // the statistics slot is released after its values have been consumed (an arrive right
+      // after the shared loads does not wait for them, and the producer's next bulk copy into
+      // the slot could land first)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive(&stat_empty[t]);
     }
+    if (lr == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // the leader's last commits land in the peer's barriers before it exits
   if (warp == 9) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc_pair<512>(tmem);
   }
 }
 

@@ -11,7 +11,8 @@
 namespace af {
 namespace {
 
-constexpr int64_t pad128(int64_t x) { return ((x + 127) / 128) * 128; }
+// query / key tiles come in pairs (the CTA-pair kernels): both axes padded to 256
+constexpr int64_t pad256(int64_t x) { return ((x + 255) / 256) * 256; }
 
 struct MatLayout {
   int64_t q_pad, k_pad, rows, groups, part_width;
@@ -20,8 +21,8 @@ struct MatLayout {
 
 MatLayout mat_layout(const af_parallel_desc* d, bool shared) {
   MatLayout l{};
-  l.q_pad = pad128(d->seq_q);
-  l.k_pad = pad128(d->seq_k);
+  l.q_pad = pad256(d->seq_q);
+  l.k_pad = pad256(d->seq_k);
   l.rows = static_cast<int64_t>(d->batch) * d->heads_q * l.q_pad;
   // head chunks of the key-side GEMMs: enough CTAs for ~4 waves, at most one chunk per head
   const int64_t k_tiles = l.k_pad / 128;
@@ -128,20 +129,26 @@ int run_materialized(const af_parallel_desc* d, const void* q, const void* k, co
   {  // 1. scores: P and dS' = tau P (dP - D) for the visible blocks
     using SL = MlaScoresSmem<D, DV, kShared>;
     CUtensorMap tq, tdo, tk, tv;
+    // Q / dO in half boxes: each CTA of a pair streams 64 of a tile's 128 query rows
     if (!make_tmap_4d(&tq, q, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_q, d->heads_q,
-                      d->batch, d->q_stride, 64, 128, true) ||
+                      d->batch, d->q_stride, 64, 64, true) ||
         !make_tmap_4d(&tdo, dout, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, DV, d->seq_q, d->heads_q,
-                      d->batch, d->o_stride, 64, 128, true) ||
+                      d->batch, d->o_stride, 64, 64, true) ||
         !make_tmap_4d(&tk, k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_k, d->heads_kv,
                       d->batch, d->k_stride, 64, 128, true) ||
         !make_tmap_4d(&tv, kShared ? k : v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                       kShared ? D : DV, d->seq_k, d->heads_kv, d->batch,
                       kShared ? d->k_stride : d->v_stride, 64, 128, true))
       return AF_ERR_INPUT;
+    CUtensorMap tpst, tdsst;  // P^T / dS'^T stores: [32 key rows][64 query columns] boxes
+    if (!tmap_3d(&tpst, pbuf, l.q_pad, l.k_pad, bhs, 64, 32) ||
+        !tmap_3d(&tdsst, dsbuf, l.q_pad, l.k_pad, bhs, 64, 32))
+      return AF_ERR_INPUT;
     auto kern = mla_bwd_scores_kernel<D, DV, kShared>;
     AF_SMEM_ATTR(kern, SL::kTotal);
     ::af::note_launch();
-    kern<<<static_cast<unsigned>(k_tiles * bhs), 320, SL::kTotal, s>>>(tq, tdo, tk, tv, p);
+    kern<<<static_cast<unsigned>(k_tiles * bhs), 320, SL::kTotal, s>>>(tq, tdo, tk, tv, tpst,
+                                                                         tdsst, p);
     AF_CUDA_CHECK(cudaGetLastError());
   }
 
@@ -265,3 +272,14 @@ int mla_bwd(const af_parallel_desc* d, const void* q, const void* k, const void*
 }
 
 }  // namespace af
+
+#ifdef AF_SCORES_TRACE
+extern "C" int af_debug_scores_trace(void* host, int reset) {
+  if (reset) {
+    static long long zero[256][8];
+    return static_cast<int>(cudaMemcpyToSymbol(af::g_scores_trace, zero, sizeof(zero)));
+  }
+  return static_cast<int>(cudaMemcpyFromSymbol(host, af::g_scores_trace,
+                                               sizeof(af::g_scores_trace)));
+}
+#endif

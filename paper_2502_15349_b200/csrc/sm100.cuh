@@ -237,6 +237,83 @@ AF_DEVICE void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
 }
 AF_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// ───────────────────────────── CTA pairs (cluster of 2, cta_group::2) ─────────────────────────────
+// A pair of CTAs on one TPC runs one M = 256 tcgen05.mma issued by the leader (rank 0): A split by
+// rows (each CTA's own 128 rows, smem or TMEM at the same address), B split by N (each CTA's smem
+// holds N/2 of its rows / columns at the same address).  Checked in tools/micro/pair_mma.cu.
+// (the builtin, not inline asm: the compiler then knows the rank is CTA-uniform — branching on an
+// asm-read rank made it wrap every tcgen05.mma of the leader's issue loop in an ELECT waterfall)
+AF_DEVICE uint32_t cluster_rank() { return __clusterRelativeBlockRank(); }
+AF_DEVICE void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+AF_DEVICE uint32_t peer_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+AF_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// Relaxed remote arrive: no release fence (a release at cluster scope waits for every earlier
+// global store of the thread — measured as the top stall of the paired scores kernel).  For
+// signalling that this thread's tcgen05.ld reads are complete (tcgen05.wait::ld has returned).
+AF_DEVICE void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA tile into this CTA's shared memory whose bytes complete on the leader's barrier
+AF_DEVICE void tma_load_4d_pair(void* smem_dst, const void* tmap, uint32_t leader_bar, int c0,
+                                int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(leader_bar)
+      : "memory");
+}
+template <uint32_t kCols>
+AF_DEVICE void tmem_alloc_pair(uint32_t* smem_dst) {  // one warp in each CTA of the pair
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(smem_dst)),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+AF_DEVICE void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+               : "memory");
+}
+AF_DEVICE void mma_ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+AF_DEVICE void mma_ts_pair(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the barrier at this offset in both CTAs once the leader's prior MMAs complete
+AF_DEVICE void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
 // ───────────────────────────── descriptors ─────────────────────────────
 // Shared-memory matrix descriptor, SWIZZLE_128B, sm100 version bits.
 //   K-major  : atoms of 8 rows x 128 B; SBO = byte stride between 8-row groups (1024 for a dense
