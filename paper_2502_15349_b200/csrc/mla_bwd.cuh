@@ -700,6 +700,239 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ── the same GEMMs on a CTA pair (N = 128, 256, 512) ──
+// M = 256 tcgen05.mma.cta_group::2: the pair's two row tiles (query tiles 2p, 2p+1 for dQ; key
+// tiles 2p, 2p+1 key-side) are the A rows, each CTA loading its own; B (K / Q / dO columns) is
+// split by N, each CTA loading half of every instruction's 256 (or N) columns — so every B byte is
+// fetched from L2 once per two row tiles (the single-CTA GEMMs re-streamed B per row tile and were
+// L2-throughput bound).  The pair walks the union of its tiles' contraction ranges; the extra
+// causal block (key tile 2p+1 x query tile 2p) is the zero block the scores kernel writes.
+template <int N>
+struct MlaPairGemmSmem {
+  static constexpr int kNI = N > 256 ? 256 : N;        // N per instruction
+  static constexpr int kHalfBoxes = kNI / 2 / 64;      // this CTA's 64-col B blocks per instr.
+  static constexpr int kABytes = 16384;
+  static constexpr int kBBytes = (N / kNI) * kHalfBoxes * 8192;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kStagesFit = (224 * 1024) / kStage;
+  static constexpr int kStages = kStagesFit > 8 ? 8 : kStagesFit;
+  static constexpr int kBarOff = kStages * kStage;
+  static constexpr int kNumBars = 2 * kStages + 1;
+  static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
+  static constexpr int kTotal = kTmemSlotOff + 16;
+  static constexpr int kTmemCols = N > 256 ? 512 : (N > 128 ? 256 : 128);
+  static_assert(kNI % 128 == 0, "each CTA's half of an instruction's N is whole 64-col blocks");
+};
+
+template <int kMode, int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    mla_bwd_gemm_pair_kernel(const __grid_constant__ CUtensorMap tm_a1,   // dS'
+                             const __grid_constant__ CUtensorMap tm_a2,   // P (key side)
+                             const __grid_constant__ CUtensorMap tm_b1,   // K (dQ) / Q (key side)
+                             const __grid_constant__ CUtensorMap tm_b2,   // dO (key side)
+                             const MlaBwdParams p, int n0) {
+  using L = MlaPairGemmSmem<N>;
+  constexpr int kStages = L::kStages, kNI = L::kNI, kHB = L::kHalfBoxes;
+  constexpr bool kKey = kMode != kGemmDQ;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* full = bars;
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
+  const int warp = static_cast<int>(warp_id());
+  const int group = p.heads / p.heads_kv;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pairx = static_cast<int>(blockIdx.x) / 2;
+
+  // ── work decomposition (per pair; the rank picks the row tile) ──
+  int b, hk, tile, h_lo = 0, h_hi = 0, bh = 0, g = 0, bk = 0;
+  int it_lo = 0, it_hi = 0;  // contraction tile range (key tiles for dQ, q tiles key-side)
+  const int q_tiles = p.q_pad / 128;
+  if constexpr (!kKey) {
+    // pair = (q tile pair, b*H + h), heaviest (last) query tiles first under a causal mask
+    const int bhs = p.batch * p.heads;
+    const int raw = pairx / bhs;
+    bh = pairx % bhs;
+    b = bh / p.heads;
+    hk = (bh % p.heads) / group;
+    const int t0 = p.mask.causal ? q_tiles - 2 - 2 * raw : 2 * raw;
+    tile = t0 + static_cast<int>(rank);
+    const TileBand band = key_band(p.mask, t0 * 128, min(p.seq_q, t0 * 128 + 256), p.seq_k);
+    it_lo = band.jb_lo;
+    it_hi = band.jb_hi;
+  } else {
+    // pair = (key tile pair, b*Hkv + hk, head chunk), heaviest (first) key tiles first
+    const int per = p.batch * p.heads_kv * p.groups;
+    const int tp = pairx / per;
+    const int rest = pairx % per;
+    tile = 2 * tp + static_cast<int>(rank);
+    bk = rest / p.groups;
+    g = rest % p.groups;
+    b = bk / p.heads_kv;
+    hk = bk % p.heads_kv;
+    h_lo = hk * group + g * group / p.groups;
+    h_hi = hk * group + (g + 1) * group / p.groups;
+    it_lo = mla_q_tile_lo(p.mask, 2 * tp * 128);
+    it_hi = q_tiles;
+  }
+  const int per_item = (kMode == kGemmDKV && n0 < kMbDv) ? 4 : 2;
+  const int n_items = kKey ? (h_hi - h_lo) * max(0, it_hi - it_lo) : max(0, it_hi - it_lo);
+  const int n_stages_total = n_items * per_item;
+
+  if (warp == 4 && lane_id() == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc_pair<L::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ───────────── TMA producer (each CTA: its A rows, its half of B) ─────────────
+    if (elect_one()) {
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int st = 0; st < n_stages_total; ++st) {
+        const int item = st / per_item, sub = st % per_item;
+        mbar_wait(&empty[slot], ph ^ 1);
+        if (leader) mbar_expect_tx(&full[slot], 2 * L::kStage);
+        const uint32_t fl = peer_addr(&full[slot], 0);
+        uint8_t* sa = smem + slot * L::kStage;
+        uint8_t* sb = sa + L::kABytes;
+        const CUtensorMap* tb;
+        int brow, bc2, bc3;  // B tile coordinates: rows (contraction), head, batch
+        if constexpr (!kKey) {
+          const int kt = it_lo + item;
+          const int c = sub;  // 64-key chunk
+          // dS'^T rows [kt*128 + 64c, +64) x this CTA's query tile: A MN-major, two boxes
+          tma_load_4d_pair(sa, &tm_a1, fl, tile * 128, kt * 128 + c * 64, bh, 0);
+          tma_load_4d_pair(sa + 8192, &tm_a1, fl, tile * 128 + 64, kt * 128 + c * 64, bh, 0);
+          tb = &tm_b1;
+          brow = kt * 128 + c * 64;
+          bc2 = hk;
+          bc3 = b;
+        } else {
+          // query tiles from the last one down, the heads of the chunk inside each (the CTAs of
+          // every key tile pair stream the same (q tile, head) tile at the same time)
+          const int nh = h_hi - h_lo;
+          const int qt = it_hi - 1 - item / nh;
+          const int hh = h_lo + item % nh;
+          const int c = per_item == 4 ? sub / 2 : sub;
+          const int prod = per_item == 4 ? sub % 2 : (kMode == kGemmDV ? 1 : 0);
+          const int r0 = qt * 128 + c * 64;
+          // dS'^T / P^T rows of this CTA's key tile x 64 query columns: A K-major, one box
+          tma_load_4d_pair(sa, prod == 0 ? &tm_a1 : &tm_a2, fl, r0, tile * 128,
+                           b * p.heads + hh, 0);
+          tb = prod == 0 ? &tm_b1 : &tm_b2;
+          brow = r0;
+          bc2 = hh;
+          bc3 = b;
+        }
+        // this CTA's half of each instruction's kNI columns: [nh*kNI + rank*kNI/2, +kNI/2)
+#pragma unroll
+        for (int nh = 0; nh < N / kNI; ++nh)
+#pragma unroll
+          for (int x = 0; x < kHB; ++x)
+            tma_load_4d_pair(sb + (nh * kHB + x) * 8192, tb, fl,
+                             n0 + nh * kNI + static_cast<int>(rank) * (kNI / 2) + x * 64, brow,
+                             bc2, bc3);
+        if (++slot == kStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ───────────── MMA issuer (the leader, for both CTAs) ─────────────
+    if (leader && n_stages_total > 0 && elect_one()) {
+      constexpr uint32_t id = make_idesc_bf16(256, kNI, !kKey, true);
+      int slot = 0;
+      uint32_t ph = 0;
+      for (int st = 0; st < n_stages_total; ++st) {
+        mbar_wait(&full[slot], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + slot * L::kStage);
+        const uint32_t sb = sa + L::kABytes;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ad = kKey ? make_sdesc(sa + kk * 32, 0, 1024)
+                                   : make_sdesc(sa + kk * 2048, 8192, 1024);
+#pragma unroll
+          for (int nh = 0; nh < N / kNI; ++nh)
+            mma_ss_pair(tmem + nh * kNI, ad, make_sdesc(sb + nh * kHB * 8192 + kk * 2048, 8192, 1024),
+                        id, (st > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit_pair(&empty[slot]);
+        if (++slot == kStages) {
+          slot = 0;
+          ph ^= 1;
+        }
+      }
+      mma_commit_pair(acc_full);
+    }
+  } else {
+    // ───────────── epilogue warps 0-3: one accumulator row per thread (this CTA's rows) ─────────────
+    const int row = warp * 32 + static_cast<int>(lane_id());
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    if (n_stages_total > 0) {
+      mbar_wait(acc_full, 0);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c = 0; c < N / 32; ++c) {
+      uint32_t r[32];
+      if (n_stages_total > 0) {
+        tmem_ld32(tmem + lane_base + c * 32, r);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) r[e] = 0u;
+      }
+      if constexpr (!kKey) {
+        const int i = tile * 128 + row;
+        if (i < p.seq_q) {
+          const int h = bh % p.heads;
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.dq) + b * p.dq_sb +
+                               h * p.dq_sh + static_cast<int64_t>(i) * p.dq_ss + n0 + c * 32;
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            d4[v] = make_uint4(pack_bf16(__uint_as_float(r[v * 8]), __uint_as_float(r[v * 8 + 1])),
+                               pack_bf16(__uint_as_float(r[v * 8 + 2]), __uint_as_float(r[v * 8 + 3])),
+                               pack_bf16(__uint_as_float(r[v * 8 + 4]), __uint_as_float(r[v * 8 + 5])),
+                               pack_bf16(__uint_as_float(r[v * 8 + 6]), __uint_as_float(r[v * 8 + 7])));
+        }
+      } else {
+        const int j = tile * 128 + row;
+        float* dst = p.dkv_part +
+                     ((static_cast<int64_t>(g) * p.batch * p.heads_kv + bk) * p.k_pad + j) *
+                         p.part_width +
+                     n0 + c * 32;
+        float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          d4[v] = make_float4(__uint_as_float(r[v * 4]), __uint_as_float(r[v * 4 + 1]),
+                              __uint_as_float(r[v * 4 + 2]), __uint_as_float(r[v * 4 + 3]));
+      }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc_pair<L::kTmemCols>(tmem);
+  }
+}
+
 // out[b, hk, j, :] = bf16( sum_g part[g, b*Hkv + hk, j, :] )  (group order fixed: deterministic)
 __global__ void mla_bwd_reduce_kernel(const float* __restrict__ part, int groups, int bhk,
                                       int heads_kv, int seq_k, int k_pad, int width, int pitch,

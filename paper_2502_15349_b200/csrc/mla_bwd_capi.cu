@@ -49,14 +49,21 @@ bool tmap_3d(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64
                       true);
 }
 
+// N a multiple of 128: the CTA-pair GEMM (each CTA streams half of B); else one CTA per tile
 template <int kMode, int N>
 int launch_gemm(const CUtensorMap& a1, const CUtensorMap& a2, const CUtensorMap& b1,
                 const CUtensorMap& b2, const MlaBwdParams& p, int n0, unsigned grid,
                 cudaStream_t s) {
-  auto kern = mla_bwd_gemm_kernel<kMode, N>;
-  AF_SMEM_ATTR(kern, MlaGemmSmem<N>::kTotal);
   ::af::note_launch();
-  kern<<<grid, 192, MlaGemmSmem<N>::kTotal, s>>>(a1, a2, b1, b2, p, n0);
+  if constexpr (N % 128 == 0) {
+    auto kern = mla_bwd_gemm_pair_kernel<kMode, N>;
+    AF_SMEM_ATTR(kern, MlaPairGemmSmem<N>::kTotal);
+    kern<<<grid, 192, MlaPairGemmSmem<N>::kTotal, s>>>(a1, a2, b1, b2, p, n0);
+  } else {
+    auto kern = mla_bwd_gemm_kernel<kMode, N>;
+    AF_SMEM_ATTR(kern, MlaGemmSmem<N>::kTotal);
+    kern<<<grid, 192, MlaGemmSmem<N>::kTotal, s>>>(a1, a2, b1, b2, p, n0);
+  }
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
 }
