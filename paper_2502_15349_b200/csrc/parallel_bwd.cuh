@@ -1005,7 +1005,8 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
     const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
     const float* __restrict__ lse, int64_t o_sb, int64_t o_sh, int64_t o_ss, int64_t do_sb,
     int64_t do_sh, int64_t do_ss, int heads, int seq_q, int seq_q_pad, int family,
-    float* __restrict__ lse2, float* __restrict__ delta, int64_t total_rows) {
+    float* __restrict__ lse2, float* __restrict__ delta, int64_t total_rows,
+    float* __restrict__ dq_zero = nullptr) {
   constexpr int kTpr = DV / 32;  // threads per row
   static_assert(kTpr >= 1 && kTpr <= 32 && (kTpr & (kTpr - 1)) == 0, "DV");
   const int64_t gt = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1038,6 +1039,15 @@ __global__ void __launch_bounds__(256) bwd_preprocess_kernel(
       for (int e = 0; e < 4; ++e)
         acc += bf16_lo_(oe[e]) * bf16_lo_(de[e]) + bf16_hi_(oe[e]) * bf16_hi_(de[e]);
     }
+  }
+  // the fused backward's fp32 dQ accumulator (dq_accum_offset layout, Dqk = DV = 128: one 32-col
+  // chunk per thread) is zeroed here rather than by a separate memset pass
+  // (a 256-thread block covers 64 rows = one 64-row query tile of one head, whose accumulator
+  // tile is 32 KB contiguous: written as coalesced float4 sweeps)
+  if (kTpr == 4 && dq_zero != nullptr && static_cast<int64_t>(blockIdx.x) * 64 < total_rows) {
+    float4* z = reinterpret_cast<float4*>(dq_zero) + static_cast<int64_t>(blockIdx.x) * 2048;
+#pragma unroll
+    for (int v = 0; v < 8; ++v) z[v * 256 + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 #pragma unroll
   for (int off = kTpr / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);

@@ -38,9 +38,7 @@ template <int D, int DV, int kFamily, int kAct>
 int launch_bwd(const BwdLaunch& a) {
   if constexpr (D == 128 && DV == 128) {
     if (a.fused) {
-      using L = BwdFusedSmem<D, DV>;
-      const int64_t acc_bytes = static_cast<int64_t>(a.d->batch) * a.d->heads_q * a.pad * D * 4;
-      AF_CUDA_CHECK(cudaMemsetAsync(a.dq_accum, 0, acc_bytes, a.s));
+      using L = BwdFusedSmem<D, DV>;  // (the dQ accumulator was zeroed by bwd_preprocess)
       auto kern = parallel_bwd_fused_kernel<D, DV, kFamily, kAct>;
       AF_SMEM_ATTR(kern, L::kTotal);
       dim3 grid((a.d->seq_k + kBlockN - 1) / kBlockN, a.d->batch * a.d->heads_kv);
@@ -197,7 +195,7 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
                                      d->o_stride[1], d->o_stride[2], d->heads_q, d->seq_q, a.pad,
                                      (d->family == AF_FAMILY_ABSSUM && d->cap_a == 0.0f)
                                          ? 3 : d->family,
-                                     lse2, delta, rows);
+                                     lse2, delta, rows, a.fused ? a.dq_accum : nullptr);
     AF_CUDA_CHECK(cudaGetLastError());
   }
   ParallelBwdParams& p = a.p;
