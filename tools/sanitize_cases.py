@@ -20,6 +20,9 @@ cases = {
     "K4/K5 Mamba2 128": configs.cfg5b(batch=1, heads=2, seq=300),
     "materialised tier (256/512)": af.builtin("retention-parallel", batch=1, heads=1, seq=64),
     "K2a/K2b split (deterministic) backward": configs.cfg2(batch=1, heads=4, heads_kv=2, seq=384),
+    # the materialised backward's separate-K/V form on CTA pairs (dK pair GEMM N = 128, dV 256)
+    "K3b softmax-diff 128/256": af.with_causal_mask(af.builtin(
+        "softmax-diff", batch=1, heads=2, seq=300, d_qk=128, d_v=256)),
 }
 only = sys.argv[1:]  # case indices (default: all)
 for idx, (name, spec) in enumerate(cases.items()):
