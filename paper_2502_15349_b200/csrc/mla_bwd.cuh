@@ -403,10 +403,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           *out_chunk(v) = make_uint4(pw[v * 4], pw[v * 4 + 1], pw[v * 4 + 2], pw[v * 4 + 3]);
         fence_proxy_async_smem();
         __syncwarp();
+#ifndef AF_SCORES_NO_STORE  // developer ablation (results are wrong without the stores)
         if (lr == 0) {
           tma_store_4d(&tm_pst, sOut, ib, k0 + wq * 32, bh, 0);
           bulk_commit();
         }
+#endif
       }
       if (warp == 0 && lane_id() == 0) SC_ACC(7, mbar_wait(dp_full, n & 1));
       __syncwarp();
@@ -455,10 +457,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       }
       fence_proxy_async_smem();
       __syncwarp();
+#ifndef AF_SCORES_NO_STORE
       if (lr == 0) {
         tma_store_4d(&tm_dsst, sOut, ib, k0 + wq * 32, bh, 0);
         bulk_commit();
       }
+#endif
       // the statistics slot is released after its values have been consumed (an arrive right
       // after the shared loads does not wait for them, and the producer's next bulk copy into
       // the slot could land first)
