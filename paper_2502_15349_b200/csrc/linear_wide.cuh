@@ -43,8 +43,12 @@ struct LinWideSmem {
   // qh_full, pk_ready, o_scaled, h_full, hb_ready, h_scaled, oi_full[2], o_empty[2]
   static constexpr int kNumBars = 6 * kStages + 7 + 4;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
-  static constexpr int kTotal = kTmemSlotOff + 16;
+  // separable decay: per-chunk column factors b_u and the row warps' deviation maxima
+  static constexpr int kBOff = (kTmemSlotOff + 16 + 15) / 16 * 16;  // [128] fp32, 16-B aligned
+  static constexpr int kDevOff = kBOff + kLinChunk * 4;      // [4] fp32
+  static constexpr int kTotal = kDevOff + 16;
 };
+static_assert(LinWideSmem::kTotal <= 232448, "wide linear kernel: shared memory");
 
 constexpr int kLinWideThreads = 18 * 32;
 
@@ -62,6 +66,8 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
   uint8_t* sHb = smem + L::kHbOff;
   float* sL = reinterpret_cast<float*>(smem + L::kLOff);
   float* sU = reinterpret_cast<float*>(smem + L::kUOff);
+  float* sB = reinterpret_cast<float*>(smem + L::kBOff);
+  float* sDev = reinterpret_cast<float*>(smem + L::kDevOff);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
   // Q, K and V rings with their own barriers, each slot released by its last reader (Q after
   // Q Hb, K after the state update, V after P V) so the next loads start as early as possible
@@ -376,7 +382,29 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
       const float l_r = l[r];
       const float l_last = l[kLinChunk - 1];
       const float cp = kReverse ? exp2f(l_last - l_r) : exp2f(l_r);
-      const float wgt = (gated ? u[r] : 1.0f) * (kReverse ? exp2f(l_r) : exp2f(l_last - l_r));
+      const float g_r = gated ? u[r] : 1.0f;
+      const float wgt = g_r * (kReverse ? exp2f(l_r) : exp2f(l_last - l_r));
+      // Separable decay: 2^(l_r - l_u) = 2^(l_r - base) 2^(base - l_u) (reverse: the mirror), so
+      // P = S a_r b_u with one exponential per row and per column instead of one per element —
+      // whenever every l of the chunk is within 2^100 of base (else the per-element form)
+      const float base = l[0];
+      {
+        float dev = fabsf(l_r - base);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dev = fmaxf(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+        if (half == 0 && lane_id() == 0) sDev[wq] = dev;
+      }
+      constexpr uint32_t kRowBar = 1;  // the 8 row warps
+      named_bar_sync(kRowBar, 256);
+      const bool fac = fmaxf(fmaxf(sDev[0], sDev[1]), fmaxf(sDev[2], sDev[3])) <= 100.0f;
+      float a_r = 0.0f;
+      if (fac) {
+        a_r = kReverse ? ex2(base - l_r) : ex2(l_r - base);
+        if (half == 0) sB[r] = (kReverse ? ex2(l_r - base) : ex2(base - l_r)) * g_r;
+      }
+      // (also orders every warp's sDev read before the next chunk's sDev writes, and the next
+      // chunk's sB writes after this chunk's P — a warp reaches them only past this barrier)
+      named_bar_sync(kRowBar, 256);
       // (a) P = S o D over this half's 64 key columns
       mbar_wait(s_full, n & 1);
       if (threadIdx.x == 0) AF_LT(7, n);
@@ -397,6 +425,23 @@ __global__ void __launch_bounds__(kLinWideThreads, 1)
           uint32_t sr[32];
           tmem_ld32(tmem + lane_base + kColS + u0, sr);
           tmem_ld_wait();
+          if (fac) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              const int uu0 = u0 + e;
+              const float4 b4 = *reinterpret_cast<const float4*>(sB + uu0);
+              const float bu[4] = {b4.x, b4.y, b4.z, b4.w};
+              float pv[4];
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {
+                const bool keep = all || (kReverse ? (uu0 + x >= r) : (uu0 + x <= r));
+                pv[x] = keep ? (__uint_as_float(sr[e + x]) * a_r) * bu[x] : 0.0f;
+              }
+              pk[cc * 16 + e / 2] = pack_bf16(pv[0], pv[1]);
+              pk[cc * 16 + e / 2 + 1] = pack_bf16(pv[2], pv[3]);
+            }
+            continue;
+          }
 #pragma unroll
           for (int e = 0; e < 32; e += 4) {
             const int uu0 = u0 + e;
