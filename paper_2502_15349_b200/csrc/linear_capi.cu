@@ -264,7 +264,7 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
     __nv_bfloat16* kmb = reinterpret_cast<__nv_bfloat16*>(
         static_cast<char*>(workspace) +
         (static_cast<size_t>(n) * (3 * slots + 2) * sizeof(float) + 255) / 256 * 256);
-    const int64_t thr = n * (d->d_k / 8);
+    const int64_t thr = n * (d->d_k >= 8 * kGkVec ? d->d_k / (8 * kGkVec) : 1);
     ::af::note_launch();
     gate_keys_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, s>>>(
         static_cast<const __nv_bfloat16*>(k), d->k_stride[0], d->k_stride[1], d->k_stride[2],
