@@ -323,25 +323,35 @@ extern "C" int af_linear_bwd(const af_linear_desc* d, const void* q, const void*
         dq_dot, dk_dot, raw_gate_dot ? kdot_raw : nullptr, slots, p, step_dloga,
         d_key_gate != nullptr ? step_dkdot : nullptr);
     AF_CUDA_CHECK(cudaGetLastError());
-    auto reduce = [&](const float* val, StepTensor div, StepTensor out) -> int {
-      const int nb = out.sb == 0 ? 1 : d->batch, nh = out.sh == 0 ? 1 : d->heads;
-      const int64_t total = static_cast<int64_t>(nb) * nh * d->seq;
-      ::af::note_launch();
-      step_grad_reduce_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
-          val, div, out, d->batch, d->heads, d->seq);
-      AF_CUDA_CHECK(cudaGetLastError());
-      return AF_OK;
-    };
+    // the per-step reductions: decay factors, then the gate (one launch when their outputs share
+    // a broadcast pattern)
+    StepReduceJobs jobs{};
     for (int f = 0; f < d->n_decay_factors; ++f)
       if (d_decay_factor != nullptr && d_decay_factor[f] != nullptr)
-        if ((st = reduce(step_dloga, p.fac[f],
-                         step_tensor(d_decay_factor[f], d->decay_factor_stride[f]))) != AF_OK)
-          return st;
+        jobs.job[jobs.n++] = {step_dloga, p.fac[f],
+                              step_tensor(d_decay_factor[f], d->decay_factor_stride[f])};
     if (d_key_gate != nullptr)
-      if ((st = reduce(step_dkdot, raw_gate_dot ? StepTensor{nullptr, 0, 0, 0} : p.u_scale,
-                       step_tensor(d_key_gate, d->key_gate_stride))) !=
-          AF_OK)
-        return st;
+      jobs.job[jobs.n++] = {step_dkdot,
+                            raw_gate_dot ? StepTensor{nullptr, 0, 0, 0} : p.u_scale,
+                            step_tensor(d_key_gate, d->key_gate_stride)};
+    bool same = true;
+    for (int j = 1; j < jobs.n; ++j)
+      same &= (jobs.job[j].out.sb == 0) == (jobs.job[0].out.sb == 0) &&
+              (jobs.job[j].out.sh == 0) == (jobs.job[0].out.sh == 0);
+    for (int j0 = 0; j0 < jobs.n;) {
+      StepReduceJobs one{};
+      const int cnt = same ? jobs.n : 1;
+      for (int j = 0; j < cnt; ++j) one.job[j] = jobs.job[j0 + j];
+      one.n = cnt;
+      const StepTensor& o = one.job[0].out;
+      const int nb = o.sb == 0 ? 1 : d->batch, nh = o.sh == 0 ? 1 : d->heads;
+      const int64_t total = static_cast<int64_t>(nb) * nh * d->seq;
+      ::af::note_launch();
+      step_grad_reduce_multi_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+          one, d->batch, d->heads, d->seq);
+      AF_CUDA_CHECK(cudaGetLastError());
+      j0 += cnt;
+    }
   }
   return AF_OK;
 }

@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(lin_threads(DK), 1)
 // two sums nearly cancel; a dot over u k instead of bf16(u k) measured 5 % off the oracle), and
 // kdot_raw = k . dKm over the raw keys (when the key gate is not also a decay factor).  One block
 // per (b, h) sequence writes d log a_t and the gate's dot (both [B, H, S] fp32);
-// step_grad_reduce_kernel then forms d fac_f = d log a / fac_f and d gate = kdot_raw (k_mod =
+// step_grad_reduce_multi_kernel then forms d fac_f = d log a / fac_f and d gate = kdot_raw (k_mod =
 // k * gate: dL/dgate = k . dKm, no division — finite at gate = 0; else dk_dot / gate) and sums
 // broadcast axes in a fixed order — no atomics, bitwise deterministic.  A decay factor of exactly
 // 0 gives a non-finite d fac at that step (d log a / 0; the unrolled reference differentiates
@@ -800,23 +800,38 @@ __global__ void __launch_bounds__(kStepGradThreads)
 // out[b', h', t] += sum over the broadcast axes of out (stride 0) of val[b, h, t] / div(b, h, t)
 // (div.ptr null: val itself),
 // in ascending (b, h) order.  val is [B, H, S] fp32; one thread per output element.
-__global__ void step_grad_reduce_kernel(const float* __restrict__ val, StepTensor div,
-                                        StepTensor out, int batch, int heads, int seq) {
-  const int nb = out.sb == 0 ? 1 : batch, nh = out.sh == 0 ? 1 : heads;
+// The per-step reductions (out[b, h, t] += sum over broadcast axes of val / div, fixed order) — up
+// to three in one launch (decay factors and the gate of one call; a
+// gate that is also a decay factor writes the same tensor twice — in the same thread, in job
+// order).  Every job's output must share one broadcast pattern (else separate launches).
+struct StepReduceJob {
+  const float* val;
+  StepTensor div, out;
+};
+struct StepReduceJobs {
+  StepReduceJob job[3];
+  int n;
+};
+__global__ void step_grad_reduce_multi_kernel(StepReduceJobs jobs, int batch, int heads, int seq) {
+  const StepTensor& o0 = jobs.job[0].out;
+  const int nb = o0.sb == 0 ? 1 : batch, nh = o0.sh == 0 ? 1 : heads;
   const int64_t total = static_cast<int64_t>(nb) * nh * seq;
   const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (gid >= total) return;
   const int t = static_cast<int>(gid % seq);
   const int hh = static_cast<int>((gid / seq) % nh);
   const int bb = static_cast<int>(gid / (static_cast<int64_t>(seq) * nh));
-  float acc = 0.0f;
-  for (int b = (out.sb == 0 ? 0 : bb); b < (out.sb == 0 ? batch : bb + 1); ++b)
-    for (int h = (out.sh == 0 ? 0 : hh); h < (out.sh == 0 ? heads : hh + 1); ++h)
-      acc += div.ptr != nullptr ? val[(static_cast<int64_t>(b) * heads + h) * seq + t] /
-                                      div.at(b, h, t)
-                                : val[(static_cast<int64_t>(b) * heads + h) * seq + t];
-  float* dst = const_cast<float*>(out.ptr) + bb * out.sb + hh * out.sh + t * out.ss;
-  *dst += acc;
+  for (int j = 0; j < jobs.n; ++j) {
+    const StepReduceJob& jb = jobs.job[j];
+    float acc = 0.0f;
+    for (int b = (o0.sb == 0 ? 0 : bb); b < (o0.sb == 0 ? batch : bb + 1); ++b)
+      for (int h = (o0.sh == 0 ? 0 : hh); h < (o0.sh == 0 ? heads : hh + 1); ++h)
+        acc += jb.div.ptr != nullptr
+                   ? jb.val[(static_cast<int64_t>(b) * heads + h) * seq + t] / jb.div.at(b, h, t)
+                   : jb.val[(static_cast<int64_t>(b) * heads + h) * seq + t];
+    float* dst = const_cast<float*>(jb.out.ptr) + bb * jb.out.sb + hh * jb.out.sh + t * jb.out.ss;
+    *dst += acc;
+  }
 }
 
 // Km = bf16(k * gate): the backward uses one rounded copy of the gated keys in every pass so the
