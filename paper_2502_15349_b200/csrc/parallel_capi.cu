@@ -9,45 +9,48 @@ namespace {
 
 template <int D, int DV, int kFamily, int kAct, int kStages>
 int launch_fwd_stages(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
-                      const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t stream) {
+                      const CUtensorMap& tv, const CUtensorMap& to, const ParallelFwdParams& p,
+                      cudaStream_t stream) {
   using L = FwdSmem<D, DV, kStages>;
   auto kern = parallel_fwd_kernel<D, DV, kFamily, kAct, kStages>;
   AF_SMEM_ATTR(kern, L::kTotal);
   dim3 grid((d->seq_q + 2 * kBlockM - 1) / (2 * kBlockM), d->batch * d->heads_q);
   ::af::note_launch();
-  kern<<<grid, fwd_threads(kFamily), L::kTotal, stream>>>(tq, tk, tv, p);
+  kern<<<grid, fwd_threads(kFamily), L::kTotal, stream>>>(tq, tk, tv, to, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
 }
 
 template <int D, int DV, int kFamily, int kAct>
 int launch_fwd(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
-               const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t stream) {
+               const CUtensorMap& tv, const CUtensorMap& to, const ParallelFwdParams& p,
+               cudaStream_t stream) {
   // D = 192: two 48 KB Q tiles leave room for one stage; D <= 128 runs two unless the measured
   // scheduler picked one (desc->kv_stages)
   constexpr bool kTunable = (kFamily == kFamilySoftmax && kAct == kActIdentity) ||
                             (kFamily == kFamilyElementwise && kAct == kActSigmoid);
   if constexpr (D <= 128) {
-    if (kTunable && d->kv_stages == 1) return launch_fwd_stages<D, DV, kFamily, kAct, 1>(d, tq, tk, tv, p, stream);
-    return launch_fwd_stages<D, DV, kFamily, kAct, 2>(d, tq, tk, tv, p, stream);
+    if (kTunable && d->kv_stages == 1) return launch_fwd_stages<D, DV, kFamily, kAct, 1>(d, tq, tk, tv, to, p, stream);
+    return launch_fwd_stages<D, DV, kFamily, kAct, 2>(d, tq, tk, tv, to, p, stream);
   } else {
-    return launch_fwd_stages<D, DV, kFamily, kAct, 1>(d, tq, tk, tv, p, stream);
+    return launch_fwd_stages<D, DV, kFamily, kAct, 1>(d, tq, tk, tv, to, p, stream);
   }
 }
 
 template <int D, int DV>
 int dispatch_family(const af_parallel_desc* d, const CUtensorMap& tq, const CUtensorMap& tk,
-                    const CUtensorMap& tv, const ParallelFwdParams& p, cudaStream_t s) {
+                    const CUtensorMap& tv, const CUtensorMap& to, const ParallelFwdParams& p,
+                    cudaStream_t s) {
   if (d->family == AF_FAMILY_SOFTMAX) {
-    if (d->cap_b != 0.0f) return launch_fwd<D, DV, kFamilySoftmax, kActSoftcap>(d, tq, tk, tv, p, s);
-    return launch_fwd<D, DV, kFamilySoftmax, kActIdentity>(d, tq, tk, tv, p, s);
+    if (d->cap_b != 0.0f) return launch_fwd<D, DV, kFamilySoftmax, kActSoftcap>(d, tq, tk, tv, to, p, s);
+    return launch_fwd<D, DV, kFamilySoftmax, kActIdentity>(d, tq, tk, tv, to, p, s);
   }
-  if (d->family == AF_FAMILY_ABSSUM) return launch_fwd<D, DV, kFamilyAbssum, kActIdentity>(d, tq, tk, tv, p, s);
+  if (d->family == AF_FAMILY_ABSSUM) return launch_fwd<D, DV, kFamilyAbssum, kActIdentity>(d, tq, tk, tv, to, p, s);
   switch (d->act) {
-    case AF_ACT_SIGMOID: return launch_fwd<D, DV, kFamilyElementwise, kActSigmoid>(d, tq, tk, tv, p, s);
-    case AF_ACT_RELU: return launch_fwd<D, DV, kFamilyElementwise, kActRelu>(d, tq, tk, tv, p, s);
-    case AF_ACT_RELU2: return launch_fwd<D, DV, kFamilyElementwise, kActRelu2>(d, tq, tk, tv, p, s);
-    case AF_ACT_IDENTITY: return launch_fwd<D, DV, kFamilyElementwise, kActIdentity>(d, tq, tk, tv, p, s);
+    case AF_ACT_SIGMOID: return launch_fwd<D, DV, kFamilyElementwise, kActSigmoid>(d, tq, tk, tv, to, p, s);
+    case AF_ACT_RELU: return launch_fwd<D, DV, kFamilyElementwise, kActRelu>(d, tq, tk, tv, to, p, s);
+    case AF_ACT_RELU2: return launch_fwd<D, DV, kFamilyElementwise, kActRelu2>(d, tq, tk, tv, to, p, s);
+    case AF_ACT_IDENTITY: return launch_fwd<D, DV, kFamilyElementwise, kActIdentity>(d, tq, tk, tv, to, p, s);
     default: break;
   }
   set_error("unknown activation %d", d->act);
@@ -133,10 +136,17 @@ extern "C" int af_parallel_fwd(const af_parallel_desc* d, const void* q, const v
                     d->batch, d->v_stride, 64, kBlockN, true))
     return AF_ERR_INPUT;
   ParallelFwdParams p = make_fwd_params(d, o, lse);
+  // O through TMA stores of staged [32 rows][64 cols] boxes when its strides allow a tensor map
+  // (16-byte multiples, feature stride 1); else per-thread row stores
+  CUtensorMap to{};
+  p.o_tma = (d->o_stride[3] == 1 && d->d_v % 64 == 0 &&
+             make_tmap_4d(&to, o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d->d_v, d->seq_q,
+                          d->heads_q, d->batch, d->o_stride, 64, 32, true))
+                ? 1 : 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (d->d_qk == 128 && d->d_v == 128) return dispatch_family<128, 128>(d, tq, tk, tv, p, s);
-  if (d->d_qk == 64 && d->d_v == 64) return dispatch_family<64, 64>(d, tq, tk, tv, p, s);
-  if (d->d_qk == 192 && d->d_v == 128) return dispatch_family<192, 128>(d, tq, tk, tv, p, s);
+  if (d->d_qk == 128 && d->d_v == 128) return dispatch_family<128, 128>(d, tq, tk, tv, to, p, s);
+  if (d->d_qk == 64 && d->d_v == 64) return dispatch_family<64, 64>(d, tq, tk, tv, to, p, s);
+  if (d->d_qk == 192 && d->d_v == 128) return dispatch_family<192, 128>(d, tq, tk, tv, to, p, s);
   set_error("bf16 parallel forward: head dims (%d, %d) not instantiated", d->d_qk, d->d_v);
   return AF_ERR_UNSUPPORTED;
 }

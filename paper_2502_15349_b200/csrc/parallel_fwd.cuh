@@ -151,7 +151,8 @@ template <int D, int DV, int kFamily, int kAct, int kStages>
 __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
     parallel_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                         const __grid_constant__ CUtensorMap tm_k,
-                        const __grid_constant__ CUtensorMap tm_v, const ParallelFwdParams p) {
+                        const __grid_constant__ CUtensorMap tm_v,
+                        const __grid_constant__ CUtensorMap tm_o, const ParallelFwdParams p) {
   using L = FwdSmem<D, DV, kStages>;
   static_assert(D % 64 == 0 && DV % 64 == 0 && D <= 256 && DV <= 128, "tile dims");
   extern __shared__ uint8_t smem_raw[];
@@ -523,6 +524,12 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
     __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_stride_b +
                           h * p.o_stride_h + static_cast<int64_t>(i) * p.o_stride_s +
                           ch * (DV / 2);
+    // O through the tile's Q buffer (free: every S MMA of this tile has completed) as SW128
+    // [rows][64] boxes and TMA stores — per-thread 16-byte stores to 32 different rows per
+    // instruction cost LSU / L2 sector work at the end of every CTA
+    constexpr bool kStageO = DV / 2 == 64;
+    const bool stage_o = kStageO && p.o_tma != 0;
+    uint8_t* sO = sQ + t * L::kQBytes;
 #pragma unroll
     for (int c = 0; c < DV / 64; ++c) {
       uint32_t orr[32];
@@ -533,7 +540,18 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) orr[e] = 0u;
       }
-      if (i < p.seq_q) {
+      if (stage_o) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int g = c * 4 + v;  // 16-byte chunk of the 64-column box (box = ch)
+          *reinterpret_cast<uint4*>(sO + ch * (kBlockM * 128) + row * 128 +
+                                    ((g ^ (row & 7)) << 4)) = make_uint4(
+              pack_bf16(__uint_as_float(orr[v * 8 + 0]) * inv, __uint_as_float(orr[v * 8 + 1]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 2]) * inv, __uint_as_float(orr[v * 8 + 3]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 4]) * inv, __uint_as_float(orr[v * 8 + 5]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv));
+        }
+      } else if (i < p.seq_q) {
         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
         for (int v = 0; v < 4; ++v)
@@ -542,6 +560,16 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
               pack_bf16(__uint_as_float(orr[v * 8 + 2]) * inv, __uint_as_float(orr[v * 8 + 3]) * inv),
               pack_bf16(__uint_as_float(orr[v * 8 + 4]) * inv, __uint_as_float(orr[v * 8 + 5]) * inv),
               pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv));
+      }
+    }
+    if (stage_o) {  // this warp's 32 rows of box ch (rows past seq_q are clipped by the map)
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane_id() == 0) {
+        tma_store_4d(&tm_o, sO + ch * (kBlockM * 128) + wq * 32 * 128, ch * 64,
+                     r0 + wq * 32, h, b);
+        bulk_commit();
+        bulk_wait<0>();
       }
     }
   } else {
@@ -738,6 +766,9 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
     }
     __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_stride_b +
                           h * p.o_stride_h + static_cast<int64_t>(i) * p.o_stride_s;
+    // O through the tile's Q buffer (see the two-warp path above) when the map exists
+    const bool stage_o = p.o_tma != 0;
+    uint8_t* sO = sQ + t * L::kQBytes;
 #pragma unroll
     for (int c = 0; c < DV / 32; ++c) {
       uint32_t orr[32];
@@ -747,6 +778,19 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
       } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e) orr[e] = 0u;
+      }
+      if (stage_o) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int g = (c % 2) * 4 + v;  // 16-byte chunk of 64-column box c / 2
+          *reinterpret_cast<uint4*>(sO + (c / 2) * (kBlockM * 128) + row * 128 +
+                                    ((g ^ (row & 7)) << 4)) = make_uint4(
+              pack_bf16(__uint_as_float(orr[v * 8 + 0]) * inv, __uint_as_float(orr[v * 8 + 1]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 2]) * inv, __uint_as_float(orr[v * 8 + 3]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 4]) * inv, __uint_as_float(orr[v * 8 + 5]) * inv),
+              pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv));
+        }
+        continue;
       }
       if (i < p.seq_q) {
         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
@@ -759,6 +803,17 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
           w.w = pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv);
           dst[v] = w;
         }
+      }
+    }
+    if (stage_o) {  // this warp's 32 rows of every 64-column box (rows past seq_q are clipped)
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane_id() == 0) {
+#pragma unroll
+        for (int x = 0; x < DV / 64; ++x)
+          tma_store_4d(&tm_o, sO + x * (kBlockM * 128) + wq * 32 * 128, x * 64, r0 + wq * 32, h, b);
+        bulk_commit();
+        bulk_wait<0>();
       }
     }
     if constexpr (kFamily == kFamilySoftmax) {

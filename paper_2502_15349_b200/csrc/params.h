@@ -46,6 +46,7 @@ struct ParallelFwdParams {
   void* o;
   int64_t o_stride_b, o_stride_h, o_stride_s;
   float* lse;
+  int o_tma;  // 1: O leaves through the kernel's O tensor map (TMA stores of staged boxes)
 };
 
 struct ParallelBwdParams {
