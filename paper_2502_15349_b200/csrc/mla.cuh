@@ -85,6 +85,7 @@ struct MlaParams {
   void* o;
   int64_t o_sb, o_sh, o_ss;
   float* lse;
+  int o_tma;  // prefill: O leaves through tm_o (TMA stores of staged boxes)
   // decode partials: fp32 [B, splits, H, 512] and lse [B, splits, H]
   float* part_o;
   float* part_lse;
@@ -111,7 +112,9 @@ struct MlaSmem {
 template <bool kDecode>
 __global__ void __launch_bounds__(192, 1)
     mla_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
-                   const __grid_constant__ CUtensorMap tm_kv, const MlaParams p) {
+                   const __grid_constant__ CUtensorMap tm_kv,
+                   const __grid_constant__ CUtensorMap tm_o,  // prefill O, [32 rows][64] boxes
+                   const MlaParams p) {
   constexpr int kN = MlaTile<kDecode>::kN;
   constexpr int kSt = MlaTile<kDecode>::kStages;
   constexpr int kQT = MlaTile<kDecode>::kQT;
@@ -377,6 +380,9 @@ __global__ void __launch_bounds__(192, 1)
       const bool live = i < p.seq_q;
       __nv_bfloat16* orow = reinterpret_cast<__nv_bfloat16*>(p.o) + b * p.o_sb + h * p.o_sh +
                             static_cast<int64_t>(live ? i : 0) * p.o_ss + half * kMlaHalf;
+      // O through the (drained) latent ring as four SW128 [128][64] boxes and TMA stores
+      const bool stage_o = p.o_tma != 0;
+      static_assert(kSt * L::kKBytes >= 4 * 128 * 128, "O staging fits the latent ring");
 #pragma unroll 1
       for (int c = 0; c < kMlaHalf / 32; ++c) {
         uint32_t orr[32];
@@ -387,6 +393,19 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) orr[e] = 0u;
         }
+        if (stage_o) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int g = (c % 2) * 4 + v;
+            *reinterpret_cast<uint4*>(sK + (c / 2) * (128 * 128) + row * 128 +
+                                      ((g ^ (row & 7)) << 4)) = make_uint4(
+                pack_bf16(__uint_as_float(orr[v * 8 + 0]) * inv, __uint_as_float(orr[v * 8 + 1]) * inv),
+                pack_bf16(__uint_as_float(orr[v * 8 + 2]) * inv, __uint_as_float(orr[v * 8 + 3]) * inv),
+                pack_bf16(__uint_as_float(orr[v * 8 + 4]) * inv, __uint_as_float(orr[v * 8 + 5]) * inv),
+                pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv));
+          }
+          continue;
+        }
         if (live) {
           uint4* d4 = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
@@ -396,6 +415,18 @@ __global__ void __launch_bounds__(192, 1)
                 pack_bf16(__uint_as_float(orr[v * 8 + 2]) * inv, __uint_as_float(orr[v * 8 + 3]) * inv),
                 pack_bf16(__uint_as_float(orr[v * 8 + 4]) * inv, __uint_as_float(orr[v * 8 + 5]) * inv),
                 pack_bf16(__uint_as_float(orr[v * 8 + 6]) * inv, __uint_as_float(orr[v * 8 + 7]) * inv));
+        }
+      }
+      if (stage_o) {  // this warp's 32 rows of the four boxes (rows past seq_q are clipped)
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane_id() == 0) {
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+            tma_store_4d(&tm_o, sK + x * (128 * 128) + warp * 32 * 128, half * kMlaHalf + x * 64,
+                         q0 + warp * 32, h, b);
+          bulk_commit();
+          bulk_wait<0>();
         }
       }
       if (half == 0 && live && p.lse != nullptr)

@@ -29,11 +29,16 @@ int mla_prefill(const af_parallel_desc* d, const void* q, const void* k, void* o
   p.q_sb = d->q_stride[0]; p.q_sh = d->q_stride[1]; p.q_ss = d->q_stride[2];
   p.o = o; p.o_sb = d->o_stride[0]; p.o_sh = d->o_stride[1]; p.o_ss = d->o_stride[2];
   p.lse = lse;
+  CUtensorMap to{};
+  p.o_tma = (d->o_stride[3] == 1 &&
+             make_tmap_4d(&to, o, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, kMlaDv, d->seq_q,
+                          d->heads_q, d->batch, d->o_stride, 64, 32, true))
+                ? 1 : 0;
   auto kern = mla_fwd_kernel<false>;
   AF_SMEM_ATTR(kern, PrefillSmem::kTotal);
   const int q_tiles = (d->seq_q + 127) / 128;
   ::af::note_launch();
-  kern<<<q_tiles * d->batch * d->heads_q * 2, 192, PrefillSmem::kTotal, s>>>(tq, tkv, p);
+  kern<<<q_tiles * d->batch * d->heads_q * 2, 192, PrefillSmem::kTotal, s>>>(tq, tkv, to, p);
   AF_CUDA_CHECK(cudaGetLastError());
   return AF_OK;
 }
@@ -110,7 +115,7 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
     auto kern = mla_fwd_kernel<true>;
     AF_SMEM_ATTR(kern, DecodeSmem::kTotal);
     ::af::note_launch();
-    kern<<<d->batch * splits * 2, 192, DecodeSmem::kTotal, s>>>(tq, tkv, p);
+    kern<<<d->batch * splits * 2, 192, DecodeSmem::kTotal, s>>>(tq, tkv, tkv, p);
   }
   AF_CUDA_CHECK(cudaGetLastError());
   ::af::note_launch();
