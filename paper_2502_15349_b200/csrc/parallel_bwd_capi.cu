@@ -22,6 +22,7 @@ struct BwdLaunch {
   const af_parallel_desc* d;
   CUtensorMap tq, tk, tv, tdo;
   CUtensorMap tq64, tdo64;  // 64-row query boxes (fused kernel)
+  CUtensorMap tdk, tdv;     // dK / dV stores (fused kernel): [32 rows][64 cols] boxes
   bool fused;
   float* dq_accum;
   ParallelBwdParams p;
@@ -43,8 +44,8 @@ int launch_bwd(const BwdLaunch& a) {
       AF_SMEM_ATTR(kern, L::kTotal);
       dim3 grid((a.d->seq_k + kBlockN - 1) / kBlockN, a.d->batch * a.d->heads_kv);
       ::af::note_launch();
-      kern<<<grid, kFusedThreads, L::kTotal, a.s>>>(a.tq64, a.tk, a.tv, a.tdo64, a.p, a.lse2,
-                                                    a.delta, a.pad, a.dq_accum);
+      kern<<<grid, kFusedThreads, L::kTotal, a.s>>>(a.tq64, a.tk, a.tv, a.tdo64, a.tdk, a.tdv,
+                                                    a.p, a.lse2, a.delta, a.pad, a.dq_accum);
       AF_CUDA_CHECK(cudaGetLastError());
       const int64_t rows = static_cast<int64_t>(a.d->batch) * a.d->heads_q * a.d->seq_q;
       const int64_t threads = rows * (D / 8);
@@ -199,6 +200,12 @@ extern "C" int af_parallel_bwd(const af_parallel_desc* d, const void* q, const v
     AF_CUDA_CHECK(cudaGetLastError());
   }
   ParallelBwdParams& p = a.p;
+  p.dkv_tma = (a.fused && d->k_stride[3] == 1 && d->v_stride[3] == 1 &&
+               make_tmap_4d(&a.tdk, dk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d->d_qk, d->seq_k,
+                            d->heads_kv, d->batch, d->k_stride, 64, 32, true) &&
+               make_tmap_4d(&a.tdv, dv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, d->d_v, d->seq_k,
+                            d->heads_kv, d->batch, d->v_stride, 64, 32, true))
+                  ? 1 : 0;
   p.batch = d->batch; p.heads_q = d->heads_q; p.heads_kv = d->heads_kv;
   p.seq_q = d->seq_q; p.seq_k = d->seq_k; p.d_qk = d->d_qk; p.d_v = d->d_v;
   p.scale = d->scale; p.scale_log2 = d->scale * kLog2e;

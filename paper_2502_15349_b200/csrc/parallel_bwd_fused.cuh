@@ -64,6 +64,7 @@ struct BwdFusedSmem {
   static constexpr int kVOff = kKOff + kKBytes;
   static constexpr int kQOff = kVOff + kVBytes;
   static constexpr int kOOff = kQOff + kStages * kQBytes;
+  // (the epilogue stages dK / dV boxes, 4 KB per row warp, over the drained Q and dO rings)
   static constexpr int kDsOff = kOOff + kStages * kOBytes;
   static constexpr int kStgOff = kDsOff + 2 * kDsBytes;
   static constexpr int kLseOff = kStgOff + kStgBytes;
@@ -104,6 +105,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
                               const __grid_constant__ CUtensorMap tm_k,
                               const __grid_constant__ CUtensorMap tm_v,
                               const __grid_constant__ CUtensorMap tm_do,
+                              const __grid_constant__ CUtensorMap tm_dk,  // [32 rows][64] boxes
+                              const __grid_constant__ CUtensorMap tm_dv,
                               const ParallelBwdParams p, const float* __restrict__ lse2,
                               const float* __restrict__ delta, int seq_q_pad,
                               float* __restrict__ dq_accum) {
@@ -451,6 +454,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
               : reinterpret_cast<__nv_bfloat16*>(p.dk) + b * p.dk_stride_b + hk * p.dk_stride_h +
                     static_cast<int64_t>(live ? j : 0) * p.dk_stride_s) +
         part * ncol;
+    // dK / dV through a 4 KB SW128 [32 rows][64 cols] box per warp in the drained Q / dO rings
+    // and a TMA store (per-thread 16-byte row stores otherwise)
+    static_assert(16 * 4096 <= kStages * (L::kQBytes + L::kOBytes), "dK / dV staging");
+    const bool stage = p.dkv_tma != 0 && ncol == 64;
+    uint8_t* box = sQ + warp * 4096;
+    const int lr = static_cast<int>(lane_id());
 #pragma unroll 1
     for (int c = 0; c < ncol / 32; ++c) {
       uint32_t r[32];
@@ -461,7 +470,28 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) r[e] = 0u;
       }
-      if (live) store_row_bf16<32>(dst + c * 32, r, mul);
+      if (stage) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int g = c * 4 + v;
+          *reinterpret_cast<uint4*>(box + lr * 128 + ((g ^ (lr & 7)) << 4)) = make_uint4(
+              pack_bf16(__uint_as_float(r[v * 8 + 0]) * mul, __uint_as_float(r[v * 8 + 1]) * mul),
+              pack_bf16(__uint_as_float(r[v * 8 + 2]) * mul, __uint_as_float(r[v * 8 + 3]) * mul),
+              pack_bf16(__uint_as_float(r[v * 8 + 4]) * mul, __uint_as_float(r[v * 8 + 5]) * mul),
+              pack_bf16(__uint_as_float(r[v * 8 + 6]) * mul, __uint_as_float(r[v * 8 + 7]) * mul));
+        }
+      } else if (live) {
+        store_row_bf16<32>(dst + c * 32, r, mul);
+      }
+    }
+    if (stage) {  // rows past seq_k are clipped by the map
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lr == 0) {
+        tma_store_4d(is_v ? &tm_dv : &tm_dk, box, part * ncol, k0 + wq * 32, hk, b);
+        bulk_commit();
+        bulk_wait<0>();
+      }
     }
   }
 

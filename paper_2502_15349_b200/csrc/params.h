@@ -64,6 +64,7 @@ struct ParallelBwdParams {
   void* dv;            // [B, Hkv, Sk, Dv] bf16 (group-summed)
   int64_t dk_stride_b, dk_stride_h, dk_stride_s;
   int64_t dv_stride_b, dv_stride_h, dv_stride_s;
+  int dkv_tma;  // fused kernel: dK / dV leave through its tensor maps (TMA stores)
 };
 
 }  // namespace af
