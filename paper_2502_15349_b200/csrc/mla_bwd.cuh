@@ -46,6 +46,7 @@ struct MlaBwdParams {
   float* dkv_part;   // fp32 partials [G, B*Hkv, k_pad, width] of the key-side GEMM
   int groups;        // head chunks per KV head (partials summed in chunk order)
   int part_width;    // columns of one partial row (576 for MLA, Dqk for dK, Dv for dV)
+  int dq_tma;        // pair dQ GEMM: dQ leaves through its store map (TMA stores)
 };
 
 // ═══════════════════════════════ 1. scores ═══════════════════════════════
@@ -726,6 +727,7 @@ struct MlaPairGemmSmem {
   static constexpr int kTotal = kTmemSlotOff + 16;
   static constexpr int kTmemCols = N > 256 ? 512 : (N > 128 ? 256 : 128);
   static_assert(kNI % 128 == 0, "each CTA's half of an instruction's N is whole 64-col blocks");
+  static_assert(4 * (N / 64) * 4096 <= kStages * kStage, "dQ staging fits the drained ring");
 };
 
 template <int kMode, int N>
@@ -734,6 +736,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                              const __grid_constant__ CUtensorMap tm_a2,   // P (key side)
                              const __grid_constant__ CUtensorMap tm_b1,   // K (dQ) / Q (key side)
                              const __grid_constant__ CUtensorMap tm_b2,   // dO (key side)
+                             const __grid_constant__ CUtensorMap tm_out,  // dQ store (dQ side)
                              const MlaBwdParams p, int n0) {
   using L = MlaPairGemmSmem<N>;
   constexpr int kStages = L::kStages, kNI = L::kNI, kHB = L::kHalfBoxes;
@@ -902,7 +905,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       }
       if constexpr (!kKey) {
         const int i = tile * 128 + row;
-        if (i < p.seq_q) {
+        if (p.dq_tma) {  // this warp's rows into its 64-column boxes of the drained ring
+          uint8_t* bx = smem + (warp * (N / 64) + c / 2) * 4096;
+          const int lr = static_cast<int>(lane_id());
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int gq = (c % 2) * 4 + v;
+            *reinterpret_cast<uint4*>(bx + lr * 128 + ((gq ^ (lr & 7)) << 4)) =
+                make_uint4(pack_bf16(__uint_as_float(r[v * 8]), __uint_as_float(r[v * 8 + 1])),
+                           pack_bf16(__uint_as_float(r[v * 8 + 2]), __uint_as_float(r[v * 8 + 3])),
+                           pack_bf16(__uint_as_float(r[v * 8 + 4]), __uint_as_float(r[v * 8 + 5])),
+                           pack_bf16(__uint_as_float(r[v * 8 + 6]), __uint_as_float(r[v * 8 + 7])));
+          }
+        } else if (i < p.seq_q) {
           const int h = bh % p.heads;
           __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.dq) + b * p.dq_sb +
                                h * p.dq_sh + static_cast<int64_t>(i) * p.dq_ss + n0 + c * 32;
@@ -925,6 +940,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         for (int v = 0; v < 8; ++v)
           d4[v] = make_float4(__uint_as_float(r[v * 4]), __uint_as_float(r[v * 4 + 1]),
                               __uint_as_float(r[v * 4 + 2]), __uint_as_float(r[v * 4 + 3]));
+      }
+    }
+    if constexpr (!kKey) {
+      if (p.dq_tma) {  // N / 64 boxes of [32 rows][64 cols]; rows past seq_q are clipped
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane_id() == 0) {
+          const int h = bh % p.heads;
+          for (int x = 0; x < N / 64; ++x)
+            tma_store_4d(&tm_out, smem + (warp * (N / 64) + x) * 4096, n0 + x * 64,
+                         tile * 128 + warp * 32, h, b);
+          bulk_commit();
+          bulk_wait<0>();
+        }
       }
     }
   }

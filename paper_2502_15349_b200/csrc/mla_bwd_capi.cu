@@ -53,12 +53,15 @@ bool tmap_3d(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64
 template <int kMode, int N>
 int launch_gemm(const CUtensorMap& a1, const CUtensorMap& a2, const CUtensorMap& b1,
                 const CUtensorMap& b2, const MlaBwdParams& p, int n0, unsigned grid,
-                cudaStream_t s) {
+                cudaStream_t s, const CUtensorMap* out = nullptr) {
   ::af::note_launch();
   if constexpr (N % 128 == 0) {
     auto kern = mla_bwd_gemm_pair_kernel<kMode, N>;
     AF_SMEM_ATTR(kern, MlaPairGemmSmem<N>::kTotal);
-    kern<<<grid, 192, MlaPairGemmSmem<N>::kTotal, s>>>(a1, a2, b1, b2, p, n0);
+    MlaBwdParams q = p;
+    q.dq_tma = (kMode == kGemmDQ && out != nullptr) ? p.dq_tma : 0;
+    kern<<<grid, 192, MlaPairGemmSmem<N>::kTotal, s>>>(a1, a2, b1, b2, out != nullptr ? *out : a1,
+                                                       q, n0);
   } else {
     auto kern = mla_bwd_gemm_kernel<kMode, N>;
     AF_SMEM_ATTR(kern, MlaGemmSmem<N>::kTotal);
@@ -176,14 +179,22 @@ int run_materialized(const af_parallel_desc* d, const void* q, const void* k, co
   const unsigned gq = static_cast<unsigned>(q_tiles * bhs);
   const unsigned gk = static_cast<unsigned>(k_tiles * d->batch * d->heads_kv * l.groups);
   int st;
+  // dQ leaves the pair GEMM through TMA stores of [32 rows][64 cols] boxes when it can be mapped
+  CUtensorMap tdq;
+  p.dq_tma = (d->q_stride[3] == 1 &&
+              make_tmap_4d(&tdq, dq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_q,
+                           d->heads_q, d->batch, d->q_stride, 64, 32, true))
+                 ? 1 : 0;
   if constexpr (kShared) {  // MLA: dQ in 512 + 64 columns, one latent dKV accumulator
-    if ((st = launch_gemm<kGemmDQ, 512>(tds_q, tds_q, tkb, tkb, p, 0, gq, s)) != AF_OK) return st;
+    if ((st = launch_gemm<kGemmDQ, 512>(tds_q, tds_q, tkb, tkb, p, 0, gq, s, &tdq)) != AF_OK)
+      return st;
     if ((st = launch_gemm<kGemmDQ, 64>(tds_q, tds_q, tkb, tkb, p, 512, gq, s)) != AF_OK) return st;
     if ((st = launch_gemm<kGemmDKV, 512>(tds_k, tp_k, tqb, tdob, p, 0, gk, s)) != AF_OK) return st;
     if ((st = launch_gemm<kGemmDKV, 64>(tds_k, tp_k, tqb, tdob, p, 512, gk, s)) != AF_OK) return st;
     return launch_reduce(p, l, d, D, dk, d->k_stride, s);
   } else {
-    if ((st = launch_gemm<kGemmDQ, D>(tds_q, tds_q, tkb, tkb, p, 0, gq, s)) != AF_OK) return st;
+    if ((st = launch_gemm<kGemmDQ, D>(tds_q, tds_q, tkb, tkb, p, 0, gq, s, &tdq)) != AF_OK)
+      return st;
     if ((st = launch_gemm<kGemmDK, D>(tds_k, tp_k, tqb, tdob, p, 0, gk, s)) != AF_OK) return st;
     if ((st = launch_reduce(p, l, d, D, dk, d->k_stride, s)) != AF_OK) return st;
     if ((st = launch_gemm<kGemmDV, DV>(tds_k, tp_k, tqb, tdob, p, 0, gk, s)) != AF_OK) return st;
