@@ -85,7 +85,7 @@ struct MlaParams {
   void* o;
   int64_t o_sb, o_sh, o_ss;
   float* lse;
-  int o_tma;  // prefill: O leaves through tm_o (TMA stores of staged boxes)
+  int o_tma;  // O (prefill) / partial O (decode) leaves through tm_o (TMA stores of staged boxes)
   // decode partials: fp32 [B, splits, H, 512] and lse [B, splits, H]
   float* part_o;
   float* part_lse;
@@ -113,7 +113,7 @@ template <bool kDecode>
 __global__ void __launch_bounds__(192, 1)
     mla_fwd_kernel(const __grid_constant__ CUtensorMap tm_q,
                    const __grid_constant__ CUtensorMap tm_kv,
-                   const __grid_constant__ CUtensorMap tm_o,  // prefill O, [32 rows][64] boxes
+                   const __grid_constant__ CUtensorMap tm_o,  // prefill O / decode partial O
                    const MlaParams p) {
   constexpr int kN = MlaTile<kDecode>::kN;
   constexpr int kSt = MlaTile<kDecode>::kStages;
@@ -356,6 +356,10 @@ __global__ void __launch_bounds__(192, 1)
       const int hh = row;
       float* dst = p.part_o + ((static_cast<int64_t>(b) * p.splits + split) * p.heads + hh) * kMlaDv +
                    half * kMlaHalf;
+      // fp32 partial rows through the drained latent ring as SW128 [32 rows][32 cols] boxes and
+      // TMA stores (eight per warp)
+      const bool stage_o = p.o_tma != 0;
+      static_assert(kSt * L::kKBytes >= 4 * 8 * 4096, "partial-O staging fits the latent ring");
 #pragma unroll 1
       for (int c = 0; c < kMlaHalf / 32; ++c) {
         uint32_t orr[32];
@@ -366,12 +370,34 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) orr[e] = 0u;
         }
+        if (stage_o) {
+          uint8_t* bx = sK + (warp * 8 + c) * 4096;
+          const int lr = static_cast<int>(lane_id());
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            *reinterpret_cast<float4*>(bx + lr * 128 + ((v ^ (lr & 7)) << 4)) =
+                make_float4(__uint_as_float(orr[v * 4]) * inv, __uint_as_float(orr[v * 4 + 1]) * inv,
+                            __uint_as_float(orr[v * 4 + 2]) * inv,
+                            __uint_as_float(orr[v * 4 + 3]) * inv);
+          continue;
+        }
         if (hh < p.heads) {
           float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
 #pragma unroll
           for (int v = 0; v < 8; ++v)
             d4[v] = make_float4(__uint_as_float(orr[v * 4]) * inv, __uint_as_float(orr[v * 4 + 1]) * inv,
                                 __uint_as_float(orr[v * 4 + 2]) * inv, __uint_as_float(orr[v * 4 + 3]) * inv);
+        }
+      }
+      if (stage_o) {  // heads past p.heads are clipped by the map
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane_id() == 0) {
+          for (int x = 0; x < 8; ++x)
+            tma_store_4d(&tm_o, sK + (warp * 8 + x) * 4096, half * kMlaHalf + x * 32, warp * 32,
+                         split, b);
+          bulk_commit();
+          bulk_wait<0>();
         }
       }
       if (half == 0 && hh < p.heads)

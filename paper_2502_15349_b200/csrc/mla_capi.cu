@@ -115,7 +115,14 @@ extern "C" int af_mla_decode(const af_mla_desc* d, const void* q, const void* kv
     auto kern = mla_fwd_kernel<true>;
     AF_SMEM_ATTR(kern, DecodeSmem::kTotal);
     ::af::note_launch();
-    kern<<<d->batch * splits * 2, 192, DecodeSmem::kTotal, s>>>(tq, tkv, tkv, p);
+    // partial O [B, splits, H, 512] fp32 as (512, H, splits, B) with [32 heads][32 cols] boxes
+    CUtensorMap tpo;
+    const int64_t po_st[4] = {static_cast<int64_t>(splits) * d->heads * kMlaDv,
+                              static_cast<int64_t>(d->heads) * kMlaDv, kMlaDv, 1};
+    p.o_tma = make_tmap_4d(&tpo, part_o, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, kMlaDv, d->heads,
+                           splits, d->batch, po_st, 32, 32, true)
+                  ? 1 : 0;
+    kern<<<d->batch * splits * 2, 192, DecodeSmem::kTotal, s>>>(tq, tkv, p.o_tma ? tpo : tkv, p);
   }
   AF_CUDA_CHECK(cudaGetLastError());
   ::af::note_launch();
