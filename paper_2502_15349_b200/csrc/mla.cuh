@@ -180,18 +180,29 @@ __global__ void __launch_bounds__(192, 1)
   // TMEM column of the packed Q chunk c (64 Q columns = 32 packed TMEM columns)
   auto q_tcol = [](int c) -> uint32_t { return c < 4 ? kColQ + c * 32 : 64 + (c - 4) * 32; };
 
+  // Q columns [0, kQT) (bound for TMEM) are staged by TMA at the tail of the latent ring: the row
+  // warps copy them into TMEM before the ring reaches those stages (per-thread row loads of
+  // 768 bytes each were uncoalesced global reads at the start of every CTA)
+  constexpr int kStgOff = kSt * L::kKBytes - (kQT / 64) * L::kQBox;
+  static_assert(kStgOff >= 0, "Q staging fits the latent ring");
   if (warp == 4) {
     if (elect_one() && nk > 0) {
-      mbar_expect_tx(q_full, L::kQBytes);
-      for (int c = 0; c < kQB; ++c) {
-        const int col = kQT + c * 64;
+      mbar_expect_tx(q_full, L::kQBytes + (kQT / 64) * L::kQBox);
+      for (int c = 0; c < kQB + kQT / 64; ++c) {
+        const int col = c < kQB ? kQT + c * 64 : (c - kQB) * 64;
+        uint8_t* dst = c < kQB ? sQ + c * L::kQBox : sK + kStgOff + (c - kQB) * L::kQBox;
         if constexpr (kDecode)
-          tma_load_4d(sQ + c * L::kQBox, &tm_q, q_full, col, 0, b, 0);
+          tma_load_4d(dst, &tm_q, q_full, col, 0, b, 0);
         else
-          tma_load_4d(sQ + c * L::kQBox, &tm_q, q_full, col, q0, h, b);
+          tma_load_4d(dst, &tm_q, q_full, col, q0, h, b);
       }
+      bool staged = true;
       for (int n = 0; n < nk; ++n) {
         const int s = n % kSt;
+        if (staged && (s + 1) * L::kKBytes > kStgOff) {
+          mbar_wait(q_ready, 0);  // the staged Q columns are in TMEM
+          staged = false;
+        }
         mbar_wait(&k_empty[s], ((n / kSt) & 1) ^ 1);
         MLA_TRACE(0, n);
         mbar_expect_tx(&k_full[s], L::kKBytes);
@@ -250,18 +261,16 @@ __global__ void __launch_bounds__(192, 1)
     const int row = warp * 32 + static_cast<int>(lane_id());
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
     const int i = kDecode ? 0 : q0 + row;  // query position (prefill)
-    {  // Q columns [0, 256) of this row -> TMEM (packed bf16 pairs, A-operand layout)
-      const bool live = kDecode ? row < p.heads : i < p.seq_q;
-      const __nv_bfloat16* qrow =
-          kDecode ? p.q + b * p.q_sb + static_cast<int64_t>(live ? row : 0) * p.q_ss
-                  : p.q + b * p.q_sb + h * p.q_sh + static_cast<int64_t>(live ? i : 0) * p.q_ss;
+    {  // Q columns [0, kQT) of this row -> TMEM (packed bf16 pairs, A-operand layout), from the
+       // staged SW128 boxes (rows past the tensor were zero-filled by TMA)
+      if (nk > 0) mbar_wait(q_full, 0);
 #pragma unroll
       for (int c = 0; c < kQT / 64; ++c) {
         uint32_t w[32];
+        const uint8_t* bx = sK + kStgOff + c * L::kQBox;
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
-          const uint4 x = live ? *reinterpret_cast<const uint4*>(qrow + c * 64 + v * 8)
-                               : make_uint4(0u, 0u, 0u, 0u);
+          const uint4 x = *reinterpret_cast<const uint4*>(bx + row * 128 + ((v ^ (row & 7)) << 4));
           w[v * 4 + 0] = x.x;
           w[v * 4 + 1] = x.y;
           w[v * 4 + 2] = x.z;
