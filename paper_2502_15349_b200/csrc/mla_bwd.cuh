@@ -356,7 +356,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
       const int t = n % kSS;
       const int q0 = (q_tiles - 1 - n) * 128;
       const int ib = q0 + half * 64;  // first query column of this warp
-      const bool full_blk = block_fully_kept(p.mask, q0, k0, p.seq_k) && q0 + 128 <= p.seq_q;
+      // kept(i = ib + c, j) as one column range per thread: c in [c_lo, c_hi) (the band's lower
+      // and upper query bounds for this key row; an out-of-range key keeps nothing)
+      int c_lo = p.mask.causal ? j - p.mask.diag_offset - ib : INT_MIN / 2;
+      int c_hi = p.mask.window > 0 ? j - p.mask.diag_offset + p.mask.window - ib : INT_MAX / 2;
+      if (j >= p.seq_k) c_lo = INT_MAX / 2;
       const float* l2s = sStat + t * 256 + half * 64;
       const float* dls = l2s + 128;
       if (warp == 0 && lane_id() == 0) {
@@ -388,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
           for (int x = 0; x < 4; ++x) {
-            const bool keep = full_blk | kept(p.mask, ib + e + x, j, p.seq_k);
+            const bool keep = (e + x >= c_lo) & (e + x < c_hi);
             // ex2(-inf) = 0: masked scores without a branch around the MUFU op
             const float pe = ex2(keep ? fmaf(__uint_as_float(pr[e + x]), p.scale_log2, -lv[x])
                                       : -INFINITY);
@@ -438,7 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(320, 1)
           float dv[4];
 #pragma unroll
           for (int x = 0; x < 4; ++x) {
-            const bool keep = full_blk | kept(p.mask, ib + hf * 32 + e + x, j, p.seq_k);
+            const bool keep = (hf * 32 + e + x >= c_lo) & (hf * 32 + e + x < c_hi);
             // dS' is selected (not multiplied by P's zero): dP of a masked position need not be
             // finite
             dv[x] = keep ? __uint_as_float(pr[hf * 32 + e + x]) *
