@@ -149,6 +149,16 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t* sr, i
                                bool fullblk, float slope, const float* ls, uint32_t* pk,
                                uint32_t* gk) {
   uint32_t bits = 0u;
+  // kept(i0 + c, j) & (i0 + c < seq_q) as one column range c in [c_lo, c_hi) for this key row:
+  // two compares per element instead of kept()'s clamps (a key past seq_k keeps nothing);
+  // evaluated only where a block is partial
+  auto keep_at = [&](int c) {
+    int c_lo = p.mask.causal ? j - p.mask.diag_offset - i0 : INT_MIN / 2;
+    int c_hi = p.seq_q - i0;
+    if (p.mask.window > 0) c_hi = min(c_hi, j - p.mask.diag_offset + p.mask.window - i0);
+    if (j >= p.seq_k) c_lo = INT_MAX / 2;
+    return fullblk | ((c >= c_lo) & (c < c_hi));
+  };
   if constexpr (kFamily == kFamilySoftmax && kAct == kActSoftcap) {
     const float cap_in = p.cap_b * p.scale, cap_out = p.cap_a * kLog2e;
     const float cap_g = p.cap_a * p.cap_b;
@@ -158,7 +168,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t* sr, i
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
         const int i = i0 + e + x;
-        const bool keep = fullblk | (kept(p.mask, i, j, p.seq_k) & (i < p.seq_q));
+        const bool keep = keep_at(e + x);
         const float t = tanh_precise(cap_in * __uint_as_float(sr[e + x]));
         pv[x] = keep ? ex2(fmaf(cap_out, t, -ls[e + x])) : 0.0f;
         gv[x] = cap_g * fmaf(-t, t, 1.0f);
@@ -174,7 +184,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t* sr, i
 #pragma unroll
       for (int x = 0; x < 2; ++x) {
         const int i = i0 + e + x;
-        const bool keep = fullblk | (kept(p.mask, i, j, p.seq_k) & (i < p.seq_q));
+        const bool keep = keep_at(e + x);
         const float rc = norm ? rcp_approx(fmaxf(ls[e + x], 1.0f)) : 1.0f;
         const float m = ex2(static_cast<float>(i - j) * slope);
         const float z = __uint_as_float(sr[e + x]) * p.scale * m;
@@ -208,7 +218,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t* sr, i
 #pragma unroll
         for (int x = 0; x < 2; ++x) {
           const int i = i0 + e + x;
-          const bool keep = kept(p.mask, i, j, p.seq_k) & (i < p.seq_q);
+          const bool keep = keep_at(e + x);
           pv[x] = keep ? ex2(fmaf(__uint_as_float(sr[e + x]), p.scale_log2,
                                   -ls[e + x]))
                        : 0.0f;
@@ -240,7 +250,7 @@ AF_DEVICE uint32_t kv_rows_p32(const ParallelBwdParams& p, const uint32_t* sr, i
           const int i = i0 + e + x;
           const float z = fmaf(__uint_as_float(sr[e + x]), p.scale,
                                zb - slope * static_cast<float>(e + x));
-          const bool keep = kept(p.mask, i, j, p.seq_k) & (i < p.seq_q);
+          const bool keep = keep_at(e + x);
           const bool g = (kAct == kActRelu) ? (z >= 0.0f) : true;
           bits |= (keep && g) ? (1u << (e + x)) : 0u;
           pv[x] = keep ? apply_act<kAct>(z) : 0.0f;
