@@ -117,6 +117,11 @@ class HostPipeline:
         self.d2h = torch.cuda.Stream(self.device)
         self._slots: list[dict] = [{}, {}]
         self._obufs: list[dict] = [{}, {}]  # per-slot output / workspace buffers (api reuse)
+        # the last call's final use of each slot: the next call's first chunks wait on these
+        # rather than on the caller stream, so consecutive calls overlap (call N+1's H2D runs
+        # under call N's last kernels and D2H copies instead of after them)
+        self._prev_comp_done: list = [None, None]
+        self._prev_out_read: list = [None, None]
 
     # device slot tensor for one host slice (reused across calls of the same shape)
     def _slot(self, s: int, name: str, like: torch.Tensor) -> torch.Tensor:
@@ -167,10 +172,8 @@ class HostPipeline:
             if not isinstance(t, torch.Tensor) or t.is_cuda:
                 raise InputError("HostPipeline takes host tensors", name=name)
         caller = torch.cuda.current_stream(self.device)
-        start = torch.cuda.Event()
-        start.record(caller)
-        for s in (self.h2d, self.comp, self.d2h):
-            s.wait_event(start)
+        # (no wait on the caller stream: the inputs are host memory, and the device buffers this
+        # call reuses are guarded by the previous call's per-slot events below)
         kv_names = {"k", "v"}
         in_ready = [torch.cuda.Event() for _ in self.units]
         comp_done = [torch.cuda.Event() for _ in self.units]
@@ -181,6 +184,8 @@ class HostPipeline:
             self._unit_spec = _sub_spec(self.spec, unit)
             if c >= 2:
                 self.h2d.wait_event(comp_done[c - 2])  # slot s inputs no longer read
+            elif self._prev_comp_done[s] is not None:
+                self.h2d.wait_event(self._prev_comp_done[s])
             dev = {}
             with torch.cuda.stream(self.h2d):
                 for name, t in host_arrays.items():
@@ -199,6 +204,8 @@ class HostPipeline:
             self.comp.wait_event(in_ready[c])
             if c >= 2:
                 self.comp.wait_event(out_read[c - 2])  # slot s outputs copied out
+            elif self._prev_out_read[s] is not None:
+                self.comp.wait_event(self._prev_out_read[s])
             # outputs and workspaces come from the slot's persistent buffers: no per-chunk
             # allocation on the host path (fresh 100 MB-class allocations per chunk made the
             # enqueue, not the copies, the bound)
@@ -235,6 +242,10 @@ class HostPipeline:
                 for n, t in summed.items():
                     t.record_stream(self.d2h)
                     host_out[n].copy_(t, non_blocking=True)
+        n = len(self.units)
+        for c in range(max(0, n - 2), n):
+            self._prev_comp_done[c % 2] = comp_done[c]
+            self._prev_out_read[c % 2] = out_read[c]
         end = torch.cuda.Event()
         end.record(self.d2h)
         caller.wait_event(end)

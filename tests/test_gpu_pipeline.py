@@ -87,3 +87,30 @@ def test_mla_pipeline_head_chunks():
     err = (out["k"].float() - ref).norm() / ref.norm()
     assert err < 1e-2, err
     assert torch.equal(out2["k"], out["k"])
+
+
+def test_pipeline_back_to_back_calls(deterministic):
+    """Consecutive calls overlap (the next call's copies start under the previous call's last
+    kernels, guarded by per-slot events): three calls on different inputs, issued without
+    synchronisation, each bitwise equal to the device-resident API."""
+    b, h, hkv, s = 2, 4, 2, 384
+    spec = S.with_causal_mask(S.builtin("softmax", batch=b, heads=h, heads_kv=hkv, seq=s,
+                                        d_qk=128, d_v=128))
+    pipe = HostPipeline(spec, max_chunks=4)
+    assert len(pipe.units) > 2
+    calls = []
+    for seed in range(3):
+        g = torch.Generator().manual_seed(100 + seed)
+        host = {n: (torch.rand(b, hh, s, 128, generator=g) * 2 - 1).bfloat16().pin_memory()
+                for n, hh in (("q", h), ("k", hkv), ("v", hkv))}
+        hdo = (torch.rand(b, h, s, 128, generator=g) * 2 - 1).bfloat16().pin_memory()
+        calls.append((host, hdo))
+    outs = [pipe(*c) for c in calls]  # no synchronisation between the calls
+    torch.cuda.synchronize()
+    for (host, hdo), out in zip(calls, outs):
+        dev = {k: v.cuda() for k, v in host.items()}
+        o, lse = af.parallel_forward(spec, dev)
+        gr = af.parallel_backward(spec, dev, o, lse, hdo.cuda())
+        assert torch.equal(out["o"], o.cpu()) and torch.equal(out["lse"], lse.cpu())
+        for n in ("q", "k", "v"):
+            assert torch.equal(out[n], gr[n].cpu()), n
