@@ -100,7 +100,8 @@ class HostPipeline:
     return them.  ``out`` may pass preallocated pinned host tensors (same keys) to avoid
     allocating pinned memory per call."""
 
-    def __init__(self, spec, device=None, max_chunks: int = 16, precision: str = "bf16"):
+    def __init__(self, spec, device=None, max_chunks: int = 16, precision: str = "bf16",
+                 overlap_calls: bool = True):
         self.spec = api._spec(spec)
         self.precision = precision
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
@@ -122,6 +123,7 @@ class HostPipeline:
         # under call N's last kernels and D2H copies instead of after them)
         self._prev_comp_done: list = [None, None]
         self._prev_out_read: list = [None, None]
+        self.overlap_calls = overlap_calls  # False: every call starts after the caller's work
 
     # device slot tensor for one host slice (reused across calls of the same shape)
     def _slot(self, s: int, name: str, like: torch.Tensor) -> torch.Tensor:
@@ -174,6 +176,11 @@ class HostPipeline:
         caller = torch.cuda.current_stream(self.device)
         # (no wait on the caller stream: the inputs are host memory, and the device buffers this
         # call reuses are guarded by the previous call's per-slot events below)
+        if not self.overlap_calls:
+            start = torch.cuda.Event()
+            start.record(caller)
+            for st in (self.h2d, self.comp, self.d2h):
+                st.wait_event(start)
         kv_names = {"k", "v"}
         in_ready = [torch.cuda.Event() for _ in self.units]
         comp_done = [torch.cuda.Event() for _ in self.units]
