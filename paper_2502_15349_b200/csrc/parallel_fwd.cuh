@@ -42,6 +42,9 @@ __device__ unsigned long long g_fwd_trace[9 * 64 * 6 + 1];
 #ifndef AF_FWD_EARLY_P
 #define AF_FWD_EARLY_P 1
 #endif
+#ifndef AF_FWD_ALTERNATE
+#define AF_FWD_ALTERNATE 1  // softmax rows: the two tiles take turns through the exponentials
+#endif
 #ifndef AF_SIGMOID_TANH
 #define AF_SIGMOID_TANH 1
 #endif
@@ -674,6 +677,18 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
             AF_TRACE(t * 4 + wq, n, 3);
           }
         };
+        // The two query tiles' row warps of a lane quarter share a scheduler and its MUFU lanes:
+        // they take turns through the exponential phase (tile 0 block n, tile 1 block n, tile 0
+        // block n+1, ...; a named-barrier token per direction) instead of contending in it —
+        // traced: both phases overlapping ran each at half the MUFU rate (≈2.1k clk softmax per
+        // tile, 3.4k clk period).
+        if constexpr (AF_FWD_ALTERNATE) {
+          if (t == 0) {
+            if (n > 0) named_bar_sync(5 + wq, 64);  // tile 1 is through block n-1
+          } else {
+            named_bar_sync(1 + wq, 64);  // tile 0 is through block n
+          }
+        }
         float2 ls2[2] = {splat2(0.0f), splat2(0.0f)};
         if (fast) {
           // packed pairs: one FFMA2 for the scale/max fold, FADD2 row sums (two chains); an
@@ -706,6 +721,7 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
           }
         }
         l_run = l_run * factor + ((ls2[0].x + ls2[1].x) + (ls2[0].y + ls2[1].y));
+        if constexpr (AF_FWD_ALTERNATE) named_bar_arrive(t == 0 ? 1 + wq : 5 + wq, 64);
         AF_TRACE(t * 4 + wq, n, 4);
       } else if constexpr (kFamily == kFamilyAbssum) {
         // s = tau q.k gamma^(i-j) on the kept band (slope = log2 gamma); l_run = sum |s|
@@ -755,6 +771,9 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
     }
 
     // ───────────── epilogue: O / l, LSE ─────────────
+    if constexpr (kFamily == kFamilySoftmax && AF_FWD_ALTERNATE) {
+      if (t == 0 && nk > 0) named_bar_sync(5 + wq, 64);  // tile 1's last token
+    }
     float inv = 1.0f;
     if constexpr (kFamily == kFamilySoftmax) inv = (l_run == 0.0f) ? 0.0f : 1.0f / l_run;
     if constexpr (kFamily == kFamilyAbssum) {
