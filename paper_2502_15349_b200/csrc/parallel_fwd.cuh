@@ -116,6 +116,15 @@ AF_DEVICE bool block_fully_kept(const MaskParams& m, int r0, int c0, int seq_k) 
   if (m.window > 0 && (r0 + kBlockM - 1) + m.diag_offset - c0 >= m.window) return false;
   return true;
 }
+// True when no (i, j) of the tile's block is kept: a two-tile CTA walks the union of its tiles'
+// key bands, so the first / last block of a sliding-window or causal sweep can be empty for one
+// tile (its P is zero; the row warps skip the epilogue math).
+AF_DEVICE bool block_fully_masked(const MaskParams& m, int r0, int c0, int seq_k) {
+  if (c0 >= seq_k) return true;
+  if (m.causal && c0 > r0 + kBlockM - 1 + m.diag_offset) return true;
+  if (m.window > 0 && c0 + kBlockN - 1 < r0 + m.diag_offset - m.window + 1) return true;
+  return false;
+}
 // Branch-free band test: keep iff lo <= j < hi, with the row's bounds loop-invariant so unrolled
 // callers hoist them (short-circuit forms compiled to a branch + reconvergence per score).
 AF_DEVICE bool kept(const MaskParams& m, int i, int j, int seq_k) {
@@ -451,6 +460,17 @@ __global__ void __launch_bounds__(fwd_threads(kFamily), 1)
       const int cb = c0 + ch * 64;
       mbar_wait(&s_full[t], n & 1);
       tc_fence_after();
+      if (block_fully_masked(p.mask, r0, c0, p.seq_k)) {  // P = 0 without the epilogue math
+        uint32_t z[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) z[e] = 0u;
+        tmem_st32(s_tmem, z);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&p_full[t]);
+        continue;
+      }
       uint32_t sr[64];
       tmem_ld32(s_tmem, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
       tmem_ld32(s_tmem + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
