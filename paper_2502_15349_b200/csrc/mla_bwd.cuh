@@ -47,6 +47,7 @@ struct MlaBwdParams {
   int groups;        // head chunks per KV head (partials summed in chunk order)
   int part_width;    // columns of one partial row (576 for MLA, Dqk for dK, Dv for dV)
   int dq_tma;        // pair dQ GEMM: dQ leaves through its store map (TMA stores)
+  int part_tma;      // pair key-side GEMMs: fp32 partials leave through their store map
 };
 
 // ═══════════════════════════════ 1. scores ═══════════════════════════════
@@ -732,6 +733,7 @@ struct MlaPairGemmSmem {
   static constexpr int kTmemCols = N > 256 ? 512 : (N > 128 ? 256 : 128);
   static_assert(kNI % 128 == 0, "each CTA's half of an instruction's N is whole 64-col blocks");
   static_assert(4 * (N / 64) * 4096 <= kStages * kStage, "dQ staging fits the drained ring");
+  static_assert(4 * 8 * 4096 <= kStages * kStage, "partial staging (one column half) fits");
 };
 
 template <int kMode, int N>
@@ -740,7 +742,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                              const __grid_constant__ CUtensorMap tm_a2,   // P (key side)
                              const __grid_constant__ CUtensorMap tm_b1,   // K (dQ) / Q (key side)
                              const __grid_constant__ CUtensorMap tm_b2,   // dO (key side)
-                             const __grid_constant__ CUtensorMap tm_out,  // dQ store (dQ side)
+                             const __grid_constant__ CUtensorMap tm_out,  // dQ / partials store
                              const MlaBwdParams p, int n0) {
   using L = MlaPairGemmSmem<N>;
   constexpr int kStages = L::kStages, kNI = L::kNI, kHB = L::kHalfBoxes;
@@ -933,6 +935,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                                pack_bf16(__uint_as_float(r[v * 8 + 4]), __uint_as_float(r[v * 8 + 5])),
                                pack_bf16(__uint_as_float(r[v * 8 + 6]), __uint_as_float(r[v * 8 + 7])));
         }
+      } else if (p.part_tma) {
+        // fp32 partial rows into [32 rows][32 cols] SW128 boxes of the drained ring, in two
+        // column halves (256 columns = 8 boxes per warp per half)
+        const int hc = c / 8;  // column half of N = 512 (c counts 32-column chunks)
+        if (c % 8 == 0 && hc > 0) {  // the first half's stores have read the boxes
+          if (lane_id() == 0) bulk_wait_read<0>();
+          __syncwarp();
+        }
+        uint8_t* bx = smem + (warp * 8 + c % 8) * 4096;
+        const int lr = static_cast<int>(lane_id());
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<float4*>(bx + lr * 128 + ((v ^ (lr & 7)) << 4)) =
+              make_float4(__uint_as_float(r[v * 4]), __uint_as_float(r[v * 4 + 1]),
+                          __uint_as_float(r[v * 4 + 2]), __uint_as_float(r[v * 4 + 3]));
+        if (c % 8 == 7 || c == N / 32 - 1) {
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane_id() == 0) {
+            for (int x = 0; x <= c % 8; ++x)
+              tma_store_4d(&tm_out, smem + (warp * 8 + x) * 4096, n0 + (hc * 8 + x) * 32,
+                           tile * 128 + warp * 32, bk, g);
+            bulk_commit();
+          }
+        }
       } else {
         const int j = tile * 128 + row;
         float* dst = p.dkv_part +
@@ -945,6 +972,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           d4[v] = make_float4(__uint_as_float(r[v * 4]), __uint_as_float(r[v * 4 + 1]),
                               __uint_as_float(r[v * 4 + 2]), __uint_as_float(r[v * 4 + 3]));
       }
+    }
+    if constexpr (kKey) {
+      if (p.part_tma && lane_id() == 0) bulk_wait<0>();
     }
     if constexpr (!kKey) {
       if (p.dq_tma) {  // N / 64 boxes of [32 rows][64 cols]; rows past seq_q are clipped

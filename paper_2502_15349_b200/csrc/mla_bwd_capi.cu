@@ -60,6 +60,7 @@ int launch_gemm(const CUtensorMap& a1, const CUtensorMap& a2, const CUtensorMap&
     AF_SMEM_ATTR(kern, MlaPairGemmSmem<N>::kTotal);
     MlaBwdParams q = p;
     q.dq_tma = (kMode == kGemmDQ && out != nullptr) ? p.dq_tma : 0;
+    q.part_tma = (kMode != kGemmDQ && out != nullptr && N == 512) ? p.part_tma : 0;
     kern<<<grid, 192, MlaPairGemmSmem<N>::kTotal, s>>>(a1, a2, b1, b2, out != nullptr ? *out : a1,
                                                        q, n0);
   } else {
@@ -185,11 +186,24 @@ int run_materialized(const af_parallel_desc* d, const void* q, const void* k, co
               make_tmap_4d(&tdq, dq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, D, d->seq_q,
                            d->heads_q, d->batch, d->q_stride, 64, 32, true))
                  ? 1 : 0;
+  // the key-side partials [G, B*Hkv, k_pad, width] fp32 through [32 rows][32 cols] boxes
+  CUtensorMap tpart;
+  const int64_t part_st[4] = {static_cast<int64_t>(d->batch) * d->heads_kv * l.k_pad * l.part_width,
+                              l.k_pad * l.part_width, l.part_width, 1};
+  p.part_tma = make_tmap_4d(&tpart, part, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                            static_cast<int>(l.part_width), static_cast<int>(l.k_pad),
+                            d->batch * d->heads_kv, static_cast<int>(l.groups), part_st, 32, 32,
+                            true)
+                   ? 1 : 0;
+#ifdef AF_MLA_PART_ROWSTORES  // developer ablation: per-thread row stores of the partials
+  p.part_tma = 0;
+#endif
   if constexpr (kShared) {  // MLA: dQ in 512 + 64 columns, one latent dKV accumulator
     if ((st = launch_gemm<kGemmDQ, 512>(tds_q, tds_q, tkb, tkb, p, 0, gq, s, &tdq)) != AF_OK)
       return st;
     if ((st = launch_gemm<kGemmDQ, 64>(tds_q, tds_q, tkb, tkb, p, 512, gq, s)) != AF_OK) return st;
-    if ((st = launch_gemm<kGemmDKV, 512>(tds_k, tp_k, tqb, tdob, p, 0, gk, s)) != AF_OK) return st;
+    if ((st = launch_gemm<kGemmDKV, 512>(tds_k, tp_k, tqb, tdob, p, 0, gk, s, &tpart)) != AF_OK)
+      return st;
     if ((st = launch_gemm<kGemmDKV, 64>(tds_k, tp_k, tqb, tdob, p, 512, gk, s)) != AF_OK) return st;
     return launch_reduce(p, l, d, D, dk, d->k_stride, s);
   } else {
