@@ -103,8 +103,8 @@ struct MlaSmem {
   static constexpr int kQOff = 0;
   static constexpr int kKOff = kQBytes;
   static constexpr int kBarOff = kKOff + kSt * kKBytes;
-  // q_full, q_ready, k_full[kSt], k_empty[kSt], s_full[2], p_ready, o_done
-  static constexpr int kNumBars = 6 + 2 * kSt;
+  // q_full, q_ready, k_full[kSt], k_empty[kSt], s_full[2], p_ready[2], o_done[2]
+  static constexpr int kNumBars = 8 + 2 * kSt;
   static constexpr int kTmemSlotOff = kBarOff + kNumBars * 8;
   static constexpr int kTotal = kTmemSlotOff + 16;
 };
@@ -130,8 +130,11 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* k_full = bars + 2;
   uint64_t* k_empty = bars + 2 + kSt;
   uint64_t* s_full = bars + 2 + 2 * kSt;
+  // p_ready[n % 2]: a softmax warp may start tile n+1 (S(n+1) is issued before PV(n)) before
+  // the slowest warp has published P(n); one barrier would count its arrival toward tile n
   uint64_t* p_ready = s_full + 2;
-  uint64_t* o_done = p_ready + 1;
+  // o_done[n % 2]: PV(n) done; exact parity waits need PV(n - 2) done, which S(n + 1) implies
+  uint64_t* o_done = p_ready + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L::kTmemSlotOff);
 
   const int warp = static_cast<int>(warp_id());
@@ -167,8 +170,10 @@ __global__ void __launch_bounds__(192, 1)
     }
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
-    mbar_init(p_ready, 4);
-    mbar_init(o_done, 1);
+    mbar_init(&p_ready[0], 4);
+    mbar_init(&p_ready[1], 4);
+    mbar_init(&o_done[0], 1);
+    mbar_init(&o_done[1], 1);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(tmem_slot);
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(192, 1)
         const int s = n & 1;
         const int st = n % kSt;
         if (n + 1 < nk) issue_s(n + 1);
-        mbar_wait(p_ready, n & 1);
+        mbar_wait(&p_ready[n & 1], (n >> 1) & 1);
         MLA_TRACE(2, n);
         tc_fence_after();
         // V = latent columns [256*half, +256): boxes 4*half .. 4*half+3 of the tile, MN-major
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int kk = 0; kk < kN / 16; ++kk)
           mma_ts(tmem + kColO, tmem + s * kN + kk * 8,
                  make_sdesc(vbase + kk * 2048, L::kKBox, 1024), id_o, (n > 0 || kk > 0));
-        mma_commit(o_done);
+        mma_commit(&o_done[n & 1]);
         mma_commit(&k_empty[st]);
       }
     }
@@ -335,7 +340,7 @@ __global__ void __launch_bounds__(192, 1)
       tmem_st_wait();
       MLA_TRACE(8, n);
       if (n > 0 && __any_sync(0xffffffffu, need)) {
-        mbar_wait(o_done, (n - 1) & 1);
+        mbar_wait(&o_done[(n - 1) & 1], ((n - 1) >> 1) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < kMlaHalf / 32; ++c) {
@@ -350,12 +355,12 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive(p_ready);
+      if (lane_id() == 0) mbar_arrive(&p_ready[n & 1]);
       MLA_TRACE(4, n);
     }
     // ───────────── epilogue ─────────────
     if (nk > 0) {
-      mbar_wait(o_done, (nk - 1) & 1);
+      mbar_wait(&o_done[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
       tc_fence_after();
     }
     const float inv = (l_run == 0.0f) ? 0.0f : 1.0f / l_run;

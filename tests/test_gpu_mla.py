@@ -44,7 +44,9 @@ def test_mla_prefill_matches_oracle(b, h, sq, sk, causal):
             assert np.max(np.abs(lse[bb, hh].double().cpu().numpy() - wl[0, 0])) <= 1e-3
 
 
-@pytest.mark.parametrize("b,h,sk", [(2, 128, 5000), (1, 128, 64), (3, 16, 1000)])
+# odd tile counts (the CTA pair's last tile pair has one tile), one key, split tails
+@pytest.mark.parametrize("b,h,sk", [(2, 128, 5000), (1, 128, 64), (3, 16, 1000), (1, 128, 1),
+                                    (2, 128, 97), (4, 64, 4133), (1, 128, 32)])
 def test_mla_decode_matches_oracle(b, h, sk):
     q, k = inputs(b, h, 1, sk, 1)
     o, lse = af.parallel_forward(mla_spec(b, h, 1, sk, False), {"q": q, "k": k})
